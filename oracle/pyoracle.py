@@ -1,0 +1,75 @@
+"""ORACLE — test infrastructure only. ctypes front-ends for the two CPU oracles:
+
+  RefOracle   oracle/_ref/libloratwin_ref.so: the UNMODIFIED reference TUs
+              (built from /root/reference by oracle/Makefile) behind the same
+              C-ABI, symbols `ltref_*` (oracle/ref_capi.cpp).
+  PortOracle  oracle/_ref/libloratwin_oracle.so: the C restatement
+              oracle/restate.c, symbols `ltor_*`.
+
+Both drive the same Runner as the GPU library, so parity tests diff identical
+POD outputs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+from paper_2508_08343_b200 import _abi as A
+from paper_2508_08343_b200.batch import Runner
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_LIB = os.path.join(HERE, "_ref", "libloratwin_ref.so")
+PORT_LIB = os.path.join(HERE, "_ref", "libloratwin_oracle.so")
+REFERENCE_SRC = "/root/reference/proj/core"
+
+
+def build(target: str = "all") -> None:
+    """Builds the oracle libraries (the reference one only where /root/reference exists)."""
+    targets = ["restate"] if target == "all" else [target]
+    if "restate" in targets and not os.path.exists(os.path.join(HERE, "restate.c")):
+        targets.remove("restate")
+    if target == "all" and os.path.isdir(REFERENCE_SRC):
+        targets.append("ref")
+    if targets:
+        subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
+
+
+class _Oracle(Runner):
+    prefix = ""
+    path = ""
+
+    def __init__(self, threads: int = 1):
+        if not os.path.exists(self.path):
+            build("ref" if self.prefix == "ltref_" else "restate")
+        lib = A.Lib(self.path, self.prefix, A.ORACLE_SYMBOLS)
+        self._set_threads = getattr(lib.dll, self.prefix + "set_threads")
+        self._set_threads.argtypes = [C.c_int32]
+        self._msg = getattr(lib.dll, self.prefix + "message")
+        self._msg.argtypes = [C.c_int64, C.c_char_p, C.c_size_t]
+        self._msg.restype = C.c_int32
+        super().__init__(lib, None, self.message)
+        self.set_threads(threads)
+
+    def set_threads(self, n: int):
+        self.threads = n
+        self._set_threads(n)
+
+    def message(self, i: int) -> str:
+        buf = C.create_string_buffer(512)
+        self._msg(i, buf, 512)
+        return buf.value.decode()
+
+
+class RefOracle(_Oracle):
+    prefix = "ltref_"
+    path = REF_LIB
+
+
+class PortOracle(_Oracle):
+    prefix = "ltor_"
+    path = PORT_LIB
+
+
+def available(kind: str = "ref") -> bool:
+    return os.path.exists(REF_LIB if kind == "ref" else PORT_LIB)

@@ -1,0 +1,377 @@
+// ORACLE / TEST INFRASTRUCTURE ONLY.
+//
+// The loratwin_gpu.h C-ABI implemented on top of the UNMODIFIED reference
+// (compiled from /root/reference/proj/core/src by oracle/Makefile into
+// oracle/_ref/libloratwin_ref.so; symbols carry the `ltref_` prefix). It lets
+// the parity tests and bench.py's reference arm drive the reference's own
+// public API -- run_simulation / run_scripted + compute_metrics
+// (engine.cpp:198-211, metrics.cpp:70-113), generate_arrivals
+// (workload.cpp:170-211), sweep_optimal (placement.cpp:185-264) -- with the
+// same POD inputs the GPU library takes. Parallelism follows the reference's
+// run_parallel pattern (placement.cpp:65-96): an atomic work counter over a
+// std::thread pool, per-task error capture.
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <functional>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "loratwin/engine.hpp"
+#include "loratwin/errors.hpp"
+#include "loratwin/metrics.hpp"
+#include "loratwin/placement.hpp"
+#include "loratwin/workload.hpp"
+#include "loratwin_gpu.h"
+
+using namespace loratwin;
+
+namespace {
+
+int g_threads = 1;
+std::vector<std::string> g_messages;  // per-scenario / per-condition what() of the last call
+
+void set_status(lt_status* st, int32_t code, int64_t index, const std::string& msg) {
+  if (!st) return;
+  st->code = code;
+  st->kind = LT_K_MESSAGE;
+  st->index = index;
+  st->detail_a = st->detail_b = 0;
+  std::snprintf(st->message, sizeof(st->message), "%s", msg.c_str());
+}
+
+int32_t classify(const std::exception_ptr& e, std::string* msg) {
+  try {
+    std::rethrow_exception(e);
+  } catch (const ValidationError& x) {
+    *msg = x.what();
+    return LT_ERR_VALIDATION;
+  } catch (const ConfigError& x) {
+    *msg = x.what();
+    return LT_ERR_CONFIG;
+  } catch (const SimulationError& x) {
+    *msg = x.what();
+    return LT_ERR_SIMULATION;
+  } catch (const InternalError& x) {
+    *msg = x.what();
+    return LT_ERR_INTERNAL;
+  } catch (const std::exception& x) {
+    *msg = x.what();
+    return LT_ERR_INTERNAL;
+  }
+}
+
+void run_pool(std::size_t count, const std::function<void(std::size_t)>& task) {
+  const int workers = std::max(1, std::min<int>(g_threads, static_cast<int>(count)));
+  if (workers == 1) {
+    for (std::size_t i = 0; i < count; ++i) task(i);
+    return;
+  }
+  std::atomic<std::size_t> next{0};
+  std::vector<std::thread> pool;
+  for (int w = 0; w < workers; ++w)
+    pool.emplace_back([&] {
+      for (std::size_t i; (i = next.fetch_add(1)) < count;) task(i);
+    });
+  for (auto& t : pool) t.join();
+}
+
+ServerConfig to_config(const lt_server_config& c) {
+  ServerConfig s;
+  s.slots = c.slots;
+  s.loaded_adapter_priority = c.loaded_adapter_priority != 0;
+  s.iteration_cap = c.iteration_cap;
+  s.ideal_includes_input = c.ideal_includes_input != 0;
+  s.latency.k1 = c.k1;
+  s.latency.k2 = c.k2;
+  s.latency.k3 = c.k3;
+  s.latency.k4 = c.k4;
+  s.latency.k5 = c.k5;
+  s.latency.k6 = c.k6;
+  s.latency.k7 = c.k7;
+  s.memory.total_kv_budget = c.total_kv_budget;
+  s.memory.kv_bytes_per_token = c.kv_bytes_per_token;
+  for (int i = 0; i < c.n_slot_cost; ++i) s.memory.slot_cost_table[c.slot_cost_rank[i]] = c.slot_cost_tokens[i];
+  if (c.has_slot_cost_base_rank8) s.memory.slot_cost_base_rank8 = c.slot_cost_base_rank8;
+  for (int i = 0; i < c.n_load; ++i) s.load.cpu_load_seconds[c.load_rank[i]] = c.load_seconds[i];
+  s.load.disk_multiplier = c.disk_multiplier;
+  s.load.default_source = c.load_source == LT_SOURCE_DISK ? LoadSource::Disk : LoadSource::Cpu;
+  return s;
+}
+
+LengthSpec to_lengths(const lt_length_spec& l, const int32_t* full) {
+  if (l.mode == LT_MODE_FULL) {
+    std::vector<std::pair<int, int>> pairs;
+    for (int64_t i = 0; i < l.full_count; ++i)
+      pairs.emplace_back(full[2 * (l.full_offset + i)], full[2 * (l.full_offset + i) + 1]);
+    return LengthSpec::full(std::move(pairs));
+  }
+  return LengthSpec::mean(l.mean_input, l.std_input, l.mean_output, l.std_output);
+}
+
+WorkloadSpec to_workload(const lt_workload_batch& b, const lt_scenario& s) {
+  WorkloadSpec w;
+  w.lengths = to_lengths(b.lengths[s.length_index], b.full_lengths);
+  w.duration_s = s.duration_s;
+  w.seed = s.seed;
+  for (int32_t i = 0; i < s.n_adapters; ++i) {
+    const lt_adapter& a = b.adapters[s.adapter_offset + i];
+    AdapterSpec spec;
+    spec.adapter_id = a.adapter_id;
+    spec.rank = a.rank;
+    spec.rate = a.rate;
+    if (a.length_index >= 0) spec.lengths = to_lengths(b.lengths[a.length_index], b.full_lengths);
+    w.adapters.push_back(spec);
+  }
+  return w;
+}
+
+uint64_t fold(uint64_t h, uint64_t w) {
+  h ^= w;
+  h *= 0x100000001b3ULL;
+  return h;
+}
+
+uint64_t digest_of(const SimulationResult& r) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  for (const IterationTraceRow& t : r.iteration_trace) {
+    uint64_t lat;
+    std::memcpy(&lat, &t.lat_step_s, 8);
+    h = fold(h, static_cast<uint32_t>(t.r_running) | (static_cast<uint64_t>(static_cast<uint32_t>(t.r_waiting)) << 32));
+    h = fold(h, static_cast<uint32_t>(t.a_running) | (static_cast<uint64_t>(static_cast<uint32_t>(t.loads)) << 32));
+    h = fold(h, lat);
+  }
+  return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+void ltref_set_threads(int32_t n) { g_threads = n < 1 ? 1 : n; }
+int32_t ltref_threads(void) { return g_threads; }
+
+int32_t ltref_message(int64_t index, char* buf, size_t len) {
+  if (index < 0 || static_cast<std::size_t>(index) >= g_messages.size()) return -1;
+  std::snprintf(buf, len, "%s", g_messages[static_cast<std::size_t>(index)].c_str());
+  return 0;
+}
+
+int32_t ltref_generate_arrivals_batch(void*, const lt_workload_batch* batch, const lt_sim_options*,
+                                      lt_request* out, int64_t capacity, int64_t* offsets,
+                                      int64_t* counts, lt_status* status) {
+  const std::size_t n = static_cast<std::size_t>(batch->n_scenarios);
+  std::vector<std::vector<Request>> lists(n);
+  std::vector<std::exception_ptr> errors(n);
+  g_messages.assign(n, std::string());
+  run_pool(n, [&](std::size_t i) {
+    try {
+      const lt_scenario& s = batch->scenarios[i];
+      WorkloadSpec w = to_workload(*batch, s);
+      lists[i] = generate_arrivals(w, static_cast<LengthMode>(s.mode));
+    } catch (...) {
+      errors[i] = std::current_exception();
+    }
+  });
+  int64_t off = 0;
+  if (status) status->code = LT_OK;
+  for (std::size_t i = 0; i < n; ++i) {
+    offsets[i] = off;
+    counts[i] = static_cast<int64_t>(lists[i].size());
+    if (errors[i]) {
+      std::string msg;
+      const int32_t code = classify(errors[i], &msg);
+      g_messages[i] = msg;
+      if (status && status->code == LT_OK) set_status(status, code, static_cast<int64_t>(i), msg);
+    }
+    for (const Request& r : lists[i]) {
+      if (off < capacity) {
+        lt_request& o = out[off];
+        o.request_id = r.request_id;
+        o.adapter_id = r.adapter_id;
+        o.input_tokens = r.input_tokens;
+        o.output_tokens = r.output_tokens;
+        o._pad = 0;
+        o.arrival_time_s = r.arrival_time_s;
+      }
+      ++off;
+    }
+  }
+  return status ? status->code : 0;
+}
+
+int32_t ltref_simulate_batch(void*, const lt_workload_batch* batch, const lt_server_config* config,
+                             const lt_sim_options* options, lt_sim_summary* out,
+                             lt_request_states* states, lt_status* status) {
+  const std::size_t n = static_cast<std::size_t>(batch->n_scenarios);
+  const ServerConfig base = to_config(*config);
+  std::vector<std::exception_ptr> errors(n);
+  std::vector<SimulationResult> keep(states ? n : 0);
+  g_messages.assign(n, std::string());
+  run_pool(n, [&](std::size_t i) {
+    lt_sim_summary& o = out[i];
+    std::memset(&o, 0, sizeof(o));
+    try {
+      const lt_scenario& s = batch->scenarios[i];
+      ServerConfig cfg = base;
+      if (s.slots > 0) cfg.slots = s.slots;
+      SimOptions opt;
+      opt.record_iteration_trace = options && options->want_digest;
+      opt.check_invariants = options && options->check_invariants;
+      if (options && options->iteration_cap_override > 0) opt.iteration_cap_override = options->iteration_cap_override;
+      WorkloadSpec w = to_workload(*batch, s);
+      SimulationResult r;
+      if (s.n_requests >= 0) {
+        std::vector<Request> rr;
+        rr.reserve(static_cast<std::size_t>(s.n_requests));
+        for (int64_t k = 0; k < s.n_requests; ++k) {
+          const lt_request& q = batch->requests[s.request_offset + k];
+          Request x;
+          x.request_id = q.request_id;
+          x.adapter_id = q.adapter_id;
+          x.arrival_time_s = q.arrival_time_s;
+          x.input_tokens = q.input_tokens;
+          x.output_tokens = q.output_tokens;
+          rr.push_back(x);
+        }
+        r = run_scripted(rr, w.adapters, w.duration_s, cfg, opt);
+      } else {
+        r = run_simulation(w, cfg, static_cast<LengthMode>(s.mode), opt);
+      }
+      const MetricsSummary m = compute_metrics(r, w, cfg.ideal_includes_input);
+      o.n_requests = static_cast<int64_t>(r.requests.size());
+      o.iterations = r.iterations;
+      o.final_clock_s = r.final_clock_s;
+      o.duration_s = r.duration_s;
+      o.truncated = r.truncated;
+      o.slots = r.slots;
+      o.served_adapters = r.served_adapters;
+      o.kv_capacity_tokens = r.kv_capacity_tokens;
+      o.starved = m.starved;
+      o.finished_count = m.finished_count;
+      o.rejected_count = m.rejected_count;
+      o.load_events = static_cast<int64_t>(r.load_events.size());
+      o.throughput_tok_s = m.throughput_tok_s;
+      o.ideal_throughput_tok_s = m.ideal_throughput_tok_s;
+      o.ttft_mean_s = m.ttft_mean_s;
+      o.itl_mean_s = m.itl_mean_s;
+      o.degenerate = m.degenerate;
+      int64_t pre = 0, tot = 0, win = 0;
+      for (const RequestState& q : r.requests) {
+        pre += q.preemption_count;
+        tot += q.tokens_generated;
+        for (double t : q.token_emit_times_s) win += t <= r.duration_s;
+      }
+      o.preemptions = pre;
+      o.tokens_total = tot;
+      o.tokens_in_window = win;
+      if (opt.record_iteration_trace) {
+        o.digest = digest_of(r);
+        for (const IterationTraceRow& t : r.iteration_trace) o.sum_running += t.r_running;
+      }
+      if (states) keep[i] = std::move(r);
+    } catch (...) {
+      errors[i] = std::current_exception();
+    }
+  });
+  if (status) status->code = LT_OK;
+  for (std::size_t i = 0; i < n; ++i) {
+    if (!errors[i]) continue;
+    std::string msg;
+    const int32_t code = classify(errors[i], &msg);
+    g_messages[i] = msg;
+    out[i].status = code;
+    out[i].status_kind = LT_K_MESSAGE;
+    if (status && status->code == LT_OK) set_status(status, code, static_cast<int64_t>(i), msg);
+  }
+  if (states) {
+    int64_t off = 0;
+    for (std::size_t i = 0; i < n; ++i) {
+      if (states->req_offset) states->req_offset[i] = off;
+      for (const RequestState& q : keep[i].requests) {
+        if (off < states->capacity) {
+          if (states->phase) states->phase[off] = static_cast<int8_t>(q.phase);
+          if (states->tokens_generated) states->tokens_generated[off] = q.tokens_generated;
+          if (states->first_token_time_s)
+            states->first_token_time_s[off] = q.first_token_time_s ? *q.first_token_time_s : NAN;
+          if (states->completion_time_s) states->completion_time_s[off] = q.completion_time_s;
+          if (states->preemption_count) states->preemption_count[off] = q.preemption_count;
+          if (states->adapter_id) states->adapter_id[off] = q.request.adapter_id;
+          if (states->input_tokens) states->input_tokens[off] = q.request.input_tokens;
+          if (states->output_tokens) states->output_tokens[off] = q.request.output_tokens;
+          if (states->arrival_time_s) states->arrival_time_s[off] = q.request.arrival_time_s;
+        }
+        ++off;
+      }
+    }
+  }
+  return status ? status->code : 0;
+}
+
+int32_t ltref_sweep_batch(void*, const lt_condition_batch* batch, const lt_server_config* config,
+                          const lt_sweep_grid* grid, double duration_s, uint64_t seed,
+                          const lt_sweep_options* options, const lt_sim_options*,
+                          lt_placement* out, lt_frontier_point* frontier, int32_t max_frontier,
+                          lt_status* status) {
+  const std::size_t n = static_cast<std::size_t>(batch->n_conditions);
+  const ServerConfig cfg = to_config(*config);
+  SweepGrid g;
+  g.n_values.assign(grid->n_values, grid->n_values + grid->n_count);
+  g.g_mode = grid->g_mode == LT_G_EXPLICIT ? SweepGrid::GMode::Explicit : SweepGrid::GMode::Geometric;
+  if (grid->g_values) g.g_values.assign(grid->g_values, grid->g_values + grid->g_count);
+  SweepOptions so;
+  so.early_exit = options->early_exit != 0;
+  so.early_exit_k = options->early_exit_k;
+  so.jobs = 1;  // parallelism lives at the condition level, as in generate_dataset
+  so.mode = static_cast<LengthMode>(options->mode);
+  std::vector<std::exception_ptr> errors(n);
+  g_messages.assign(n, std::string());
+  run_pool(n, [&](std::size_t i) {
+    lt_placement& o = out[i];
+    std::memset(&o, 0, sizeof(o));
+    try {
+      const lt_condition& c = batch->conditions[i];
+      Condition cond;
+      cond.lengths = to_lengths(batch->lengths[c.length_index], batch->full_lengths);
+      for (int32_t j = 0; j < c.mix_count; ++j) {
+        AdapterTemplate t;
+        t.rank = batch->templates[c.mix_offset + j].rank;
+        t.rate = batch->templates[c.mix_offset + j].rate;
+        cond.mix.push_back(t);
+      }
+      const PlacementResult p = sweep_optimal(cond, cfg, g, duration_s, seed, so);
+      o.max_throughput_tok_s = p.max_throughput_tok_s;
+      o.n_star = p.n_star;
+      o.g_star = p.g_star;
+      o.all_starved = p.all_starved;
+      o.frontier_open = p.frontier_open;
+      o.frontier_count = static_cast<int32_t>(p.frontier.size());
+      for (std::size_t k = 0; k < p.frontier.size() && static_cast<int32_t>(k) < max_frontier; ++k) {
+        lt_frontier_point& f = frontier[i * static_cast<std::size_t>(max_frontier) + k];
+        f.n = p.frontier[k].n;
+        f.g = p.frontier[k].g;
+        f.throughput_tok_s = p.frontier[k].throughput_tok_s;
+        f.starved = p.frontier[k].starved;
+        f.skipped = p.frontier[k].skipped;
+        if (!f.skipped) ++o.points_simulated;
+      }
+    } catch (...) {
+      errors[i] = std::current_exception();
+    }
+  });
+  if (status) status->code = LT_OK;
+  for (std::size_t i = 0; i < n; ++i) {
+    if (!errors[i]) continue;
+    std::string msg;
+    const int32_t code = classify(errors[i], &msg);
+    g_messages[i] = msg;
+    out[i].status = code;
+    out[i].status_kind = LT_K_MESSAGE;
+    if (status && status->code == LT_OK) set_status(status, code, static_cast<int64_t>(i), msg);
+  }
+  return status ? status->code : 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,254 @@
+"""Public API: the reference's hot-path functions, executed on a B200.
+
+Mirrors run_simulation / run_scripted (engine.hpp:70-78), compute_metrics
+(metrics.hpp:49-50), generate_arrivals (workload.hpp:111-113) and
+sweep_optimal (placement.hpp:100-102), plus their batched forms, which are the
+product: one call simulates thousands of independent engines. Everything runs
+through libloratwin_gpu.so (include/loratwin_gpu.h); there is no CPU path —
+without the built library or a B200 these calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi as A
+from .batch import (ConditionBatch, PackedConfig, Runner, WorkloadBatch, sim_options)
+from .types import (AdapterSpec, Condition, DeviceError, ERROR_CLASSES, FrontierPoint, LengthMode,
+                    LoratwinError, MetricsSummary, Phase, PlacementResult, Request, RequestState,
+                    ServerConfig, SimOptions, SimulationResult, SweepGrid, SweepOptions, WorkloadSpec)
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "lib", "libloratwin_gpu.so")
+
+_lib: Optional[A.Lib] = None
+_devices = {}
+
+
+def load_library() -> A.Lib:
+    """Loads the in-tree CUDA library; raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        _lib = A.Lib(LIB_PATH, "lt_")
+        if _lib.abi_version() != A.ABI_VERSION:
+            raise DeviceError("libloratwin_gpu.so ABI version mismatch")
+    return _lib
+
+
+class Device:
+    """One lt_ctx (one B200, one CUDA stream)."""
+
+    def __init__(self, index: int = 0):
+        self.lib = load_library()
+        st = A.lt_status()
+        self.ctx = self.lib.create(index, C.byref(st))
+        if not self.ctx:
+            raise DeviceError(st.message.decode())
+        self.index = index
+        self.runner = Runner(self.lib, self.ctx, self.message)
+
+    def message(self, i: int) -> str:
+        buf = C.create_string_buffer(512)
+        self.lib.last_message(self.ctx, i, buf, 512)
+        return buf.value.decode()
+
+    def stream(self) -> int:
+        return self.lib.stream(self.ctx) or 0
+
+    def timing(self) -> dict:
+        t = A.lt_timing()
+        self.lib.last_timing(self.ctx, C.byref(t))
+        return {name: getattr(t, name) for name, _ in A.lt_timing._fields_}
+
+    def close(self):
+        if self.ctx:
+            self.lib.destroy(self.ctx)
+            self.ctx = None
+
+    # --- batched entry points (the product) -----------------------------------
+    def simulate_batch(self, batch: WorkloadBatch, config: ServerConfig, options: Optional[SimOptions] = None,
+                       want_states: bool = False, want_digest: bool = False, libm_variant: int = -1):
+        return self.runner.simulate(batch, config, sim_options(options, want_digest, libm_variant), want_states)
+
+    def generate_arrivals_batch(self, batch: WorkloadBatch, libm_variant: int = -1):
+        return self.runner.generate_arrivals(batch, sim_options(None, False, libm_variant))
+
+    def sweep_batch(self, conds: ConditionBatch, config: ServerConfig, grid: SweepGrid, duration_s: float,
+                    seed: int, options: Optional[SweepOptions] = None, libm_variant: int = -1):
+        return self.runner.sweep(conds, config, grid, duration_s, seed, options or SweepOptions(),
+                                 sim_options(None, False, libm_variant))
+
+    def plan(self, batch: WorkloadBatch, config: ServerConfig, options: Optional[SimOptions] = None,
+             want_digest: bool = False) -> "Plan":
+        return Plan(self, batch, config, sim_options(options, want_digest))
+
+
+class Plan:
+    """Inputs uploaded once and kept in HBM (lt_plan_*): run() re-simulates
+    the whole batch on device; results() copies the summaries back."""
+
+    def __init__(self, dev: Device, batch: WorkloadBatch, config: ServerConfig, opts: A.lt_sim_options):
+        self.dev = dev
+        self._keep = (batch, PackedConfig(config), opts)
+        self.n = len(batch.scenarios)
+        st = A.lt_status()
+        cb = batch.c_struct()
+        self.h = dev.lib.plan_simulate(dev.ctx, C.byref(cb), C.byref(self._keep[1].c), C.byref(opts), C.byref(st))
+        if not self.h:
+            raise DeviceError(st.message.decode())
+
+    def run(self):
+        st = A.lt_status()
+        if self.dev.lib.plan_run(self.h, C.byref(st)) != A.LT_OK:
+            raise DeviceError(st.message.decode())
+
+    def results(self) -> np.ndarray:
+        out = np.zeros(max(self.n, 1), dtype=A.SUMMARY_DT)
+        st = A.lt_status()
+        self.dev.lib.plan_results(self.h, out.ctypes.data, None, C.byref(st))
+        if st.code == A.LT_ERR_DEVICE:
+            raise DeviceError(st.message.decode())
+        return out[:self.n]
+
+    def close(self):
+        if self.h:
+            self.dev.lib.plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def device(index: int = 0) -> Device:
+    if index not in _devices:
+        _devices[index] = Device(index)
+    return _devices[index]
+
+
+# --- conversions ----------------------------------------------------------------
+
+def raise_for(row, message: str):
+    code = int(row["status"])
+    if code != A.LT_OK:
+        raise ERROR_CLASSES.get(code, LoratwinError)(message)
+
+
+def metrics_of(row) -> MetricsSummary:
+    return MetricsSummary(throughput_tok_s=float(row["throughput_tok_s"]), itl_mean_s=float(row["itl_mean_s"]),
+                          ttft_mean_s=float(row["ttft_mean_s"]),
+                          ideal_throughput_tok_s=float(row["ideal_throughput_tok_s"]),
+                          starved=bool(row["starved"]), finished_count=int(row["finished_count"]),
+                          rejected_count=int(row["rejected_count"]), degenerate=bool(row["degenerate"]))
+
+
+def result_of(row, states, i: int) -> SimulationResult:
+    reqs: List[RequestState] = []
+    if states is not None:
+        off = int(states["req_offset"][i])
+        for k in range(int(row["n_requests"])):
+            j = off + k
+            first = float(states["first_token_time_s"][j])
+            reqs.append(RequestState(
+                request=Request(request_id=k, adapter_id=int(states["adapter_id"][j]),
+                                arrival_time_s=float(states["arrival_time_s"][j]),
+                                input_tokens=int(states["input_tokens"][j]),
+                                output_tokens=int(states["output_tokens"][j])),
+                phase=Phase(int(states["phase"][j])), tokens_generated=int(states["tokens_generated"][j]),
+                first_token_time_s=None if math.isnan(first) else first,
+                completion_time_s=float(states["completion_time_s"][j]),
+                preemption_count=int(states["preemption_count"][j])))
+    return SimulationResult(requests=reqs, iterations=int(row["iterations"]), final_clock_s=float(row["final_clock_s"]),
+                            duration_s=float(row["duration_s"]), truncated=bool(row["truncated"]),
+                            slots=int(row["slots"]), served_adapters=int(row["served_adapters"]),
+                            kv_capacity_tokens=int(row["kv_capacity_tokens"]), load_events=int(row["load_events"]),
+                            preemptions=int(row["preemptions"]), tokens_in_window=int(row["tokens_in_window"]),
+                            digest=int(row["digest"]), metrics=metrics_of(row))
+
+
+def placement_of(row, frontier_rows) -> PlacementResult:
+    fr = [FrontierPoint(n=int(f["n"]), g=int(f["g"]), throughput_tok_s=float(f["throughput_tok_s"]),
+                        starved=bool(f["starved"]), skipped=bool(f["skipped"]))
+          for f in frontier_rows[:int(row["frontier_count"])]]
+    return PlacementResult(max_throughput_tok_s=float(row["max_throughput_tok_s"]), n_star=int(row["n_star"]),
+                           g_star=int(row["g_star"]), frontier=fr, all_starved=bool(row["all_starved"]),
+                           frontier_open=bool(row["frontier_open"]))
+
+
+# --- reference-shaped single calls ---------------------------------------------
+
+def run_simulation(workload: WorkloadSpec, config: ServerConfig, mode: LengthMode = LengthMode.Mean,
+                   options: Optional[SimOptions] = None, dev: Optional[Device] = None) -> SimulationResult:
+    """engine.hpp:70-71 — one engine on the B200 (result + device-computed metrics)."""
+    dev = dev or device()
+    batch = WorkloadBatch.from_workloads([workload], mode=mode)
+    out, states = dev.simulate_batch(batch, config, options, want_states=True)
+    raise_for(out[0], dev.message(0))
+    return result_of(out[0], states, 0)
+
+
+def run_scripted(requests: Sequence[Request], adapters: Sequence[AdapterSpec], duration_s: float,
+                 config: ServerConfig, options: Optional[SimOptions] = None,
+                 dev: Optional[Device] = None) -> SimulationResult:
+    """engine.hpp:76-78 — the same loop over an explicit request list."""
+    dev = dev or device()
+    w = WorkloadSpec(adapters=list(adapters), duration_s=duration_s)
+    w.lengths.mean_input = w.lengths.mean_output = 1.0  # unused by scripted runs
+    batch = WorkloadBatch.from_workloads([w], scripted=[list(requests)])
+    out, states = dev.simulate_batch(batch, config, options, want_states=True)
+    raise_for(out[0], dev.message(0))
+    return result_of(out[0], states, 0)
+
+
+def compute_metrics(result: SimulationResult, workload: WorkloadSpec = None,
+                    ideal_includes_input: bool = False) -> MetricsSummary:
+    """metrics.hpp:49-50 — computed on device in the engine epilogue (K2)."""
+    return result.metrics
+
+
+def generate_arrivals(workload: WorkloadSpec, mode_override: Optional[LengthMode] = None,
+                      dev: Optional[Device] = None) -> List[Request]:
+    """workload.hpp:111-113 — arrivals generated on device (K0 + merge)."""
+    dev = dev or device()
+    mode = workload.lengths.mode if mode_override is None else mode_override
+    batch = WorkloadBatch.from_workloads([workload], mode=mode)
+    reqs, counts = dev.generate_arrivals_batch(batch)
+    code, idx, msg = dev.runner.last_arrivals_status
+    if code != A.LT_OK:
+        raise ERROR_CLASSES.get(code, LoratwinError)(msg)
+    return [Request(int(r["request_id"]), int(r["adapter_id"]), float(r["arrival_time_s"]),
+                    int(r["input_tokens"]), int(r["output_tokens"])) for r in reqs]
+
+
+def sweep_optimal(condition: Condition, config: ServerConfig, grid: SweepGrid, duration_s: float, seed: int,
+                  options: Optional[SweepOptions] = None, dev: Optional[Device] = None) -> PlacementResult:
+    """placement.hpp:100-102 — every grid point simulated on device, reduced on device (K3)."""
+    dev = dev or device()
+    out, fr = dev.sweep_batch(ConditionBatch.from_conditions([condition]), config, grid, duration_s, seed, options)
+    raise_for(out[0], dev.message(0))
+    return placement_of(out[0], fr[0])
+
+
+def sweep_conditions(conditions: Sequence[Condition], config: ServerConfig, grid: SweepGrid, duration_s: float,
+                     seed: int, options: Optional[SweepOptions] = None,
+                     dev: Optional[Device] = None) -> List[PlacementResult]:
+    """Batched sweep_optimal (generate_dataset's loop, placement.cpp:492-522).
+    Failed conditions are returned as the exception object, like
+    generate_dataset records failures and continues."""
+    dev = dev or device()
+    out, fr = dev.sweep_batch(ConditionBatch.from_conditions(conditions), config, grid, duration_s, seed, options)
+    res = []
+    for i in range(len(conditions)):
+        if int(out[i]["status"]) != A.LT_OK:
+            res.append(ERROR_CLASSES.get(int(out[i]["status"]), LoratwinError)(dev.message(i)))
+        else:
+            res.append(placement_of(out[i], fr[i]))
+    return res

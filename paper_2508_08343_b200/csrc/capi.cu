@@ -1,0 +1,1295 @@
+// loratwin_gpu.h implementation: host orchestration of the B200 DT sweep.
+//
+// Host work is limited to what the reference does before its hot loop and
+// that cannot differ per device: input validation with the reference's exact
+// messages (workload.cpp:97-141, server_config.cpp:21-27,
+// estimators.cpp:38-98, engine.cpp:32-71), ideal throughput
+// (metrics.cpp:36-45), and packing POD inputs into the device SoA layout
+// (lt_device.cuh). Arrival generation, merging, every engine iteration, the
+// metrics epilogue and the placement reduction run on the GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <random>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "k_engine.cuh"
+#include "k_sweep.cuh"
+#include "k_workload.cuh"
+#include "loratwin_gpu.h"
+#include "lt_device.cuh"
+
+using namespace lt;
+
+namespace {
+
+struct CudaError {
+  std::string what;
+};
+
+#define LT_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t err_ = (call);                                                             \
+    if (err_ != cudaSuccess)                                                               \
+      throw CudaError{std::string(#call) + ": " + cudaGetErrorString(err_)};               \
+  } while (0)
+
+void set_status(lt_status* st, int32_t code, int32_t kind, int64_t index, int64_t a, int64_t b,
+                const std::string& msg) {
+  if (!st) return;
+  st->code = code;
+  st->kind = kind;
+  st->index = index;
+  st->detail_a = a;
+  st->detail_b = b;
+  std::snprintf(st->message, sizeof(st->message), "%s", msg.c_str());
+}
+
+void ok_status(lt_status* st) {
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->index = -1;
+  }
+}
+
+// Host-side error of one scenario: code + reference message.
+struct HostErr {
+  int32_t code = LT_OK;
+  int32_t kind = LT_K_NONE;
+  int64_t a = 0, b = 0;
+  std::string msg;
+  bool set(int32_t c, const std::string& m, int32_t k = LT_K_VALIDATION_MSG, int64_t aa = 0,
+           int64_t bb = 0) {
+    code = c;
+    kind = k;
+    msg = m;
+    a = aa;
+    b = bb;
+    return false;
+  }
+};
+
+std::string render(int32_t code, int32_t kind, int64_t a, int64_t b) {
+  char buf[320];
+  lt_format_status(code, kind, a, b, buf, sizeof(buf));
+  return buf;
+}
+
+// ----------------------------------------------------------------------------
+// Reference validation (exact messages).
+
+bool validate_lengths(const lt_length_spec& l, const int32_t* full, const std::string& path,
+                      HostErr* e) {
+  if (l.mode == LT_MODE_FULL) {
+    if (l.full_count <= 0)
+      return e->set(LT_ERR_VALIDATION, path + ".full_lengths: Full mode requires a non-empty length list");
+    for (int64_t i = 0; i < l.full_count; ++i) {
+      if (full[2 * (l.full_offset + i)] < 1 || full[2 * (l.full_offset + i) + 1] < 1)
+        return e->set(LT_ERR_VALIDATION, path + ".full_lengths[" + std::to_string(i) +
+                                              "]: token counts must be >= 1");
+    }
+    return true;
+  }
+  if (l.mean_input <= 0.0)
+    return e->set(LT_ERR_VALIDATION, path + ".mean_input: must be > 0, got " + std::to_string(l.mean_input));
+  if (l.mean_output <= 0.0)
+    return e->set(LT_ERR_VALIDATION, path + ".mean_output: must be > 0, got " + std::to_string(l.mean_output));
+  if (l.std_input < 0.0)
+    return e->set(LT_ERR_VALIDATION, path + ".std_input: must be >= 0, got " + std::to_string(l.std_input));
+  if (l.std_output < 0.0)
+    return e->set(LT_ERR_VALIDATION, path + ".std_output: must be >= 0, got " + std::to_string(l.std_output));
+  return true;
+}
+
+// ServerConfig::validate (server_config.cpp:21-27) without the slots check.
+bool validate_config_body(const lt_server_config& c, HostErr* e) {
+  if (c.iteration_cap < 1) return e->set(LT_ERR_VALIDATION, "config.iteration_cap: must be >= 1");
+  if (c.k4 < 0.0) return e->set(LT_ERR_VALIDATION, "estimators.latency.k4: must be >= 0");
+  if (c.k5 <= 0.0)
+    return e->set(LT_ERR_VALIDATION, "estimators.latency.k5: must be > 0 (a forward pass takes time)");
+  if (c.k6 < 0.0) return e->set(LT_ERR_VALIDATION, "estimators.latency.k6: must be >= 0");
+  if (c.k7 < 1.0)
+    return e->set(LT_ERR_VALIDATION, "estimators.latency.k7: must be >= 1 (adapters never speed up the model)");
+  if (c.total_kv_budget <= 0)
+    return e->set(LT_ERR_VALIDATION, "estimators.memory.total_kv_budget: must be > 0");
+  if (c.n_slot_cost == 0 && !c.has_slot_cost_base_rank8)
+    return e->set(LT_ERR_VALIDATION,
+                  "estimators.memory: one of slot_cost_tokens or slot_cost_base_rank8 is required");
+  if (c.has_slot_cost_base_rank8 && c.slot_cost_base_rank8 <= 0.0)
+    return e->set(LT_ERR_VALIDATION, "estimators.memory.slot_cost_base_rank8: must be > 0");
+  {
+    std::map<int, int64_t> t;
+    for (int i = 0; i < c.n_slot_cost; ++i) t[c.slot_cost_rank[i]] = c.slot_cost_tokens[i];
+    int64_t prev = 0;
+    int prev_rank = 0;
+    for (const auto& [rank, cost] : t) {
+      if (rank <= 0) return e->set(LT_ERR_VALIDATION, "estimators.memory.slot_cost_tokens: ranks must be > 0");
+      if (cost <= prev)
+        return e->set(LT_ERR_VALIDATION,
+                      "estimators.memory.slot_cost_tokens: cost must increase with rank (rank " +
+                          std::to_string(rank) + " vs rank " + std::to_string(prev_rank) + ")");
+      prev = cost;
+      prev_rank = rank;
+    }
+  }
+  if (c.disk_multiplier < 1.0) return e->set(LT_ERR_VALIDATION, "estimators.load.disk_multiplier: must be >= 1");
+  {
+    std::map<int, double> t;
+    for (int i = 0; i < c.n_load; ++i) t[c.load_rank[i]] = c.load_seconds[i];
+    double prev = 0.0;
+    int prev_rank = 0;
+    for (const auto& [rank, seconds] : t) {
+      if (rank <= 0) return e->set(LT_ERR_VALIDATION, "estimators.load.cpu_load_seconds: ranks must be > 0");
+      if (seconds < prev)
+        return e->set(LT_ERR_VALIDATION,
+                      "estimators.load.cpu_load_seconds: latency must not decrease with rank (rank " +
+                          std::to_string(rank) + " vs rank " + std::to_string(prev_rank) + ")");
+      prev = seconds;
+      prev_rank = rank;
+    }
+  }
+  return true;
+}
+
+// Parsed config tables.
+struct Config {
+  lt_server_config raw;
+  std::map<int, int64_t> slot_cost;
+  std::map<int, double> load;
+  HostErr body_err;  // config.validate() failure other than slots
+  bool body_ok = true;
+  int variant = 1;
+};
+
+// MemoryModel::slot_cost_tokens (estimators.cpp:46-55).
+bool slot_cost(const Config& c, int rank, int64_t* out, HostErr* e) {
+  if (rank == 0) {
+    *out = 0;
+    return true;
+  }
+  if (rank < 0) return e->set(LT_ERR_VALIDATION, "slot rank must be >= 0, got " + std::to_string(rank));
+  auto it = c.slot_cost.find(rank);
+  if (it != c.slot_cost.end()) {
+    *out = it->second;
+    return true;
+  }
+  if (c.raw.has_slot_cost_base_rank8) {
+    *out = static_cast<int64_t>(std::llround(c.raw.slot_cost_base_rank8 * rank / 8.0));
+    return true;
+  }
+  return e->set(LT_ERR_CONFIG, render(LT_ERR_CONFIG, LT_K_NO_SLOT_COST, rank, 0), LT_K_NO_SLOT_COST, rank);
+}
+
+// LoadLatencyTable::load_latency (estimators.cpp:78-83); NaN when missing
+// (the reference raises lazily, at the first load of that rank).
+double load_latency(const Config& c, int rank) {
+  auto it = c.load.find(rank);
+  if (it == c.load.end()) return NAN;
+  return c.raw.load_source == LT_SOURCE_CPU ? it->second : it->second * c.raw.disk_multiplier;
+}
+
+struct Stats {
+  double max, min, mean, std;
+};
+
+// list_stats (workload.cpp:31-50).
+Stats list_stats(const int32_t* full, int64_t off, int64_t n, bool input) {
+  Stats s{0.0, 0.0, 0.0, 0.0};
+  if (n == 0) return s;
+  s.max = -1.79769313486231570815e+308;
+  s.min = 1.79769313486231570815e+308;
+  double sum = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double v = full[2 * (off + i) + (input ? 0 : 1)];
+    s.max = std::max(s.max, v);
+    s.min = std::min(s.min, v);
+    sum += v;
+  }
+  s.mean = sum / static_cast<double>(n);
+  double sq = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double v = full[2 * (off + i) + (input ? 0 : 1)];
+    sq += (v - s.mean) * (v - s.mean);
+  }
+  s.std = std::sqrt(sq / static_cast<double>(n));
+  return s;
+}
+
+double output_mean(const lt_length_spec& l, const int32_t* full) {
+  if (l.mode == LT_MODE_FULL) return list_stats(full, l.full_offset, l.full_count, false).mean;
+  return l.mean_output;
+}
+double input_mean(const lt_length_spec& l, const int32_t* full) {
+  if (l.mode == LT_MODE_FULL) return list_stats(full, l.full_offset, l.full_count, true).mean;
+  return l.mean_input;
+}
+
+// LengthSpec::as_mean (workload.cpp:91-95) for Mean-mode sampling.
+DLen as_dlen(const lt_length_spec& l, const int32_t* full) {
+  if (l.mode == LT_MODE_FULL) {
+    const Stats in = list_stats(full, l.full_offset, l.full_count, true);
+    const Stats out = list_stats(full, l.full_offset, l.full_count, false);
+    return DLen{in.mean, in.std, out.mean, out.std};
+  }
+  return DLen{l.mean_input, l.std_input, l.mean_output, l.std_output};
+}
+
+// ----------------------------------------------------------------------------
+// Device buffers
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) LT_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    alloc(v.size());
+    if (!v.empty()) LT_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+}  // namespace
+
+struct lt_ctx {
+  std::vector<std::string> messages;  // per scenario / condition of the last call
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 0;
+  lt_timing timing{};
+  cudaEvent_t ev[8]{};
+};
+
+// A prepared batch: everything the kernels need, resident in HBM.
+struct lt_plan {
+  lt_ctx* ctx = nullptr;
+  Config cfg;
+  int64_t n_scen = 0;
+  int max_adapters = 32;
+  int64_t max_req = 0;
+  int64_t total_req = 0;
+  std::vector<DScen> h_scen;
+  std::vector<HostErr> errs;
+  std::vector<int32_t> h_order;
+  std::vector<int32_t> adapter_ids;  // dense -> adapter_id, per scenario segment
+  DBuf<DScen> scen;
+  DBuf<DAdapter> adapters;
+  DBuf<DLen> lens;
+  DBuf<DKey> keys;
+  DBuf<double> E;
+  DBuf<double2> Z;
+  DBuf<int32_t> order;
+  DBuf<int32_t> counter;
+  DBuf<double> r_arr, r_first, r_last;
+  DBuf<int32_t> r_in, r_out, r_adp, r_gen, r_pre;
+  DBuf<int8_t> r_phase;
+  DBuf<int4> ws_run;
+  DBuf<int2> ws_pq, ws_fq;
+  DBuf<lt_sim_summary> out;
+  int64_t ws_stride = 0;
+  int grid = 0;
+  int block = 256;
+  size_t smem = 0;
+  int want_digest = 0;
+  double tables_ms = 0, merge_ms = 0, h2d_ms = 0;
+  int64_t h2d_bytes = 0;
+  int64_t launches_prep = 0;
+};
+
+namespace {
+
+// ----------------------------------------------------------------------------
+// Batch preparation
+
+struct Prep {
+  std::vector<DAdapter> adapters;
+  std::vector<DLen> lens;
+  std::vector<DKey> keys;
+  std::vector<int32_t> pair_scen, pair_adp;
+  std::vector<int64_t> pair_begin;
+  std::unordered_map<std::string, int> len_index;
+  std::map<std::pair<uint64_t, int64_t>, int> key_index;
+  std::vector<double> cost;
+};
+
+int intern_len(Prep& p, const DLen& d) {
+  std::string k(reinterpret_cast<const char*>(&d), sizeof(d));
+  auto it = p.len_index.find(k);
+  if (it != p.len_index.end()) return it->second;
+  const int idx = static_cast<int>(p.lens.size());
+  p.lens.push_back(d);
+  p.len_index.emplace(k, idx);
+  return idx;
+}
+
+int libm_variant_for(const lt_sim_options* o) {
+  if (o && o->libm_variant >= 0) return o->libm_variant ? 1 : 0;
+  return lt_host_libm_variant();
+}
+
+// Validates scenario `i` in reference order and fills its device record.
+void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t i) {
+  const lt_scenario& s = b.scenarios[i];
+  DScen& d = P.h_scen[i];
+  std::memset(&d, 0, sizeof(d));
+  HostErr& e = P.errs[i];
+  const int G = s.slots > 0 ? s.slots : P.cfg.raw.slots;
+  d.G = G;
+  d.duration = s.duration_s;
+  d.n_adapters = s.n_adapters;
+  d.adapter_begin = static_cast<int64_t>(pr.adapters.size());
+  d.generated = s.n_requests < 0;
+  d.iter_cap = P.cfg.raw.iteration_cap;
+  const bool scripted = s.n_requests >= 0;
+  const lt_adapter* ad = b.adapters + s.adapter_offset;
+  const int32_t* full = b.full_lengths;
+  auto fail = [&]() {
+    d.status = e.code;
+    d.status_kind = e.kind;
+    d.status_a = e.a;
+    d.status_b = e.b;
+    d.n_adapters = 0;
+  };
+  auto lengths_of = [&](const lt_adapter& a) -> const lt_length_spec& {
+    return a.length_index >= 0 ? b.lengths[a.length_index] : b.lengths[s.length_index];
+  };
+  if (!scripted) {
+    // WorkloadSpec::validate(for_simulation=true) (workload.cpp:118-141)
+    if (s.n_adapters <= 0) return e.set(LT_ERR_VALIDATION, "workload.adapters: must be non-empty"), fail();
+    if (s.duration_s <= 0.0)
+      return e.set(LT_ERR_VALIDATION, "workload.duration_s: must be > 0, got " + std::to_string(s.duration_s)), fail();
+    std::set<int> seen;
+    for (int k = 0; k < s.n_adapters; ++k) {
+      const std::string path = "workload.adapters[" + std::to_string(k) + "]";
+      if (ad[k].rank < 0)
+        return e.set(LT_ERR_VALIDATION, path + ".rank: must be >= 0, got " + std::to_string(ad[k].rank)), fail();
+      if (ad[k].rate <= 0.0)
+        return e.set(LT_ERR_VALIDATION, path + ".rate: must be > 0, got " + std::to_string(ad[k].rate)), fail();
+      if (!seen.insert(ad[k].adapter_id).second)
+        return e.set(LT_ERR_VALIDATION, path + ".adapter_id: duplicate id " + std::to_string(ad[k].adapter_id)), fail();
+      if (ad[k].length_index >= 0 &&
+          !validate_lengths(b.lengths[ad[k].length_index], full, path + ".lengths", &e))
+        return fail();
+    }
+    if (!validate_lengths(b.lengths[s.length_index], full, "workload.lengths", &e)) return fail();
+    // generate_arrivals mode handling (workload.cpp:185-192)
+    for (int k = 0; k < s.n_adapters; ++k) {
+      const lt_length_spec& l = lengths_of(ad[k]);
+      if (s.mode != l.mode && s.mode == LT_MODE_FULL)
+        return e.set(LT_ERR_VALIDATION, "workload.lengths: cannot force Full mode without a length list"), fail();
+      if (s.mode == LT_MODE_FULL && l.mode == LT_MODE_FULL)
+        return e.set(LT_ERR_UNSUPPORTED, "Full-mode length sampling is not implemented on the device path",
+                     LT_K_MESSAGE),
+               fail();
+    }
+  }
+  // Engine::Engine (engine.cpp:32-71)
+  if (G < 1) return e.set(LT_ERR_VALIDATION, "config.slots: must be >= 1, got " + std::to_string(G)), fail();
+  if (!P.cfg.body_ok) return (e = P.cfg.body_err), fail();
+  if (s.n_adapters <= 0) return e.set(LT_ERR_VALIDATION, "workload.adapters: must be non-empty"), fail();
+  if (s.duration_s <= 0.0) return e.set(LT_ERR_VALIDATION, "workload.duration_s: must be > 0"), fail();
+  if (s.n_adapters > kMaxAdapters)
+    return e.set(LT_ERR_UNSUPPORTED, render(LT_ERR_UNSUPPORTED, LT_K_TOO_MANY_ADAPTERS, s.n_adapters, kMaxAdapters),
+                 LT_K_TOO_MANY_ADAPTERS, s.n_adapters, kMaxAdapters),
+           fail();
+  int max_rank = 0;
+  std::vector<int> perm(s.n_adapters);
+  for (int k = 0; k < s.n_adapters; ++k) {
+    perm[k] = k;
+    max_rank = std::max(max_rank, ad[k].rank);
+  }
+  std::sort(perm.begin(), perm.end(), [&](int x, int y) { return ad[x].adapter_id < ad[y].adapter_id; });
+  for (int k = 1; k < s.n_adapters; ++k)
+    if (ad[perm[k]].adapter_id == ad[perm[k - 1]].adapter_id)
+      return e.set(LT_ERR_VALIDATION, "workload.adapters: duplicate adapter_id"), fail();
+  int64_t capacity = P.cfg.raw.total_kv_budget;
+  for (int g = 0; g < G; ++g) {
+    int64_t c;
+    if (!slot_cost(P.cfg, max_rank, &c, &e)) return fail();
+    capacity -= c;
+  }
+  capacity = std::max<int64_t>(capacity, 0);
+  if (capacity <= 0)
+    return e.set(LT_ERR_CONFIG, render(LT_ERR_CONFIG, LT_K_INFEASIBLE_SLOTS, G, 0), LT_K_INFEASIBLE_SLOTS, G), fail();
+  d.capacity = capacity;
+  // ideal_throughput (metrics.cpp:36-45), spec order
+  double ideal = 0.0;
+  for (int k = 0; k < s.n_adapters; ++k) {
+    const lt_length_spec& l = lengths_of(ad[k]);
+    double tokens = output_mean(l, full);
+    if (P.cfg.raw.ideal_includes_input) tokens += input_mean(l, full);
+    ideal += ad[k].rate * tokens;
+  }
+  d.ideal = ideal;
+  d.length_param = intern_len(pr, as_dlen(b.lengths[s.length_index], full));
+  double cost = 0.0;
+  for (int k = 0; k < s.n_adapters; ++k) {
+    const lt_adapter& a = ad[perm[k]];
+    DAdapter x{};
+    x.id = a.adapter_id;
+    x.rank = a.rank;
+    x.rate = a.rate;
+    x.load_lat = load_latency(P.cfg, a.rank);
+    x.length_param = a.length_index >= 0 ? intern_len(pr, as_dlen(b.lengths[a.length_index], full)) : -1;
+    x.key = -1;
+    if (!scripted) {
+      auto key = std::make_pair(s.seed, static_cast<int64_t>(a.adapter_id));
+      auto it = pr.key_index.find(key);
+      int kidx;
+      if (it == pr.key_index.end()) {
+        kidx = static_cast<int>(pr.keys.size());
+        DKey k{};
+        k.seed = s.seed;
+        k.id = a.adapter_id;
+        k.rate_max = a.rate;
+        k.dur_max = s.duration_s;
+        pr.keys.push_back(k);
+        pr.key_index.emplace(key, kidx);
+      } else {
+        kidx = it->second;
+        DKey& k = pr.keys[kidx];
+        k.rate_max = std::max(k.rate_max, a.rate);
+        k.dur_max = std::max(k.dur_max, s.duration_s);
+      }
+      x.key = kidx;
+      pr.pair_scen.push_back(static_cast<int32_t>(i));
+      pr.pair_adp.push_back(k);
+      const lt_length_spec& l = lengths_of(a);
+      cost += a.rate * s.duration_s * (output_mean(l, full) + 1.0);
+    }
+    pr.adapters.push_back(x);
+    P.adapter_ids.push_back(a.adapter_id);
+  }
+  if (scripted) {
+    const lt_request* rq = b.requests + s.request_offset;
+    std::unordered_map<int, int> dense;
+    for (int k = 0; k < s.n_adapters; ++k) dense[ad[perm[k]].adapter_id] = k;
+    for (int64_t r = 0; r < s.n_requests; ++r) {
+      if (rq[r].request_id != r)
+        return e.set(LT_ERR_VALIDATION, "requests must be sorted with request_id = position, got id " +
+                                            std::to_string(rq[r].request_id) + " at position " + std::to_string(r)),
+               fail();
+      if (!dense.count(rq[r].adapter_id))
+        return e.set(LT_ERR_VALIDATION, "request " + std::to_string(rq[r].request_id) +
+                                            " references unknown adapter " + std::to_string(rq[r].adapter_id)),
+               fail();
+      cost += rq[r].output_tokens + 1.0;
+    }
+    d.n_req = static_cast<int32_t>(s.n_requests);
+  }
+  pr.cost[i] = cost;
+  P.max_adapters = std::max(P.max_adapters, s.n_adapters);
+}
+
+void load_config(Config& c, const lt_server_config* cfg, const lt_sim_options* opts) {
+  c.raw = *cfg;
+  for (int i = 0; i < cfg->n_slot_cost; ++i) c.slot_cost[cfg->slot_cost_rank[i]] = cfg->slot_cost_tokens[i];
+  for (int i = 0; i < cfg->n_load; ++i) c.load[cfg->load_rank[i]] = cfg->load_seconds[i];
+  c.body_ok = validate_config_body(*cfg, &c.body_err);
+  if (opts && opts->iteration_cap_override > 0) c.raw.iteration_cap = opts->iteration_cap_override;
+  c.variant = libm_variant_for(opts);
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// Builds a plan: validation, RNG tables, counting, merge, request arrays,
+// workspace. Leaves everything resident; returns nullptr + status on error.
+lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_config* cfg,
+                    const lt_sim_options* opts) {
+  auto plan = std::make_unique<lt_plan>();
+  lt_plan& P = *plan;
+  P.ctx = ctx;
+  cudaStream_t st = ctx->stream;
+  load_config(P.cfg, cfg, opts);
+  P.want_digest = opts ? opts->want_digest : 0;
+  P.n_scen = b->n_scenarios;
+  P.h_scen.resize(P.n_scen);
+  P.errs.resize(P.n_scen);
+  Prep pr;
+  pr.cost.assign(P.n_scen, 0.0);
+  pr.pair_begin.resize(P.n_scen);
+  for (int64_t i = 0; i < P.n_scen; ++i) {
+    pr.pair_begin[i] = static_cast<int64_t>(pr.pair_scen.size());
+    prepare_scenario(P, pr, *b, i);
+    if (P.errs[i].code != LT_OK) {
+      // drop partially appended pairs of a failed scenario
+      pr.pair_scen.resize(pr.pair_begin[i]);
+      pr.pair_adp.resize(pr.pair_begin[i]);
+    }
+  }
+  P.max_adapters = (P.max_adapters + 31) / 32 * 32;
+  if (pr.lens.empty()) pr.lens.push_back(DLen{1, 0, 1, 0});
+  cudaEventRecord(ctx->ev[0], st);
+  // keys: reserve rate_max * dur_max + 8 sigma + slack draws
+  int64_t e_total = 0;
+  for (DKey& k : pr.keys) {
+    const double lam = k.rate_max * k.dur_max;
+    const double capd = lam + 8.0 * std::sqrt(lam) + 32.0;
+    k.cap = static_cast<int32_t>(std::min(capd, 2.0e9));
+    k.e_off = e_total;
+    k.z_off = e_total;
+    e_total += k.cap;
+  }
+  std::vector<int64_t> scen_begin(P.n_scen, 0);
+  std::vector<int32_t> adp_count;
+  for (int attempt = 0;; ++attempt) {
+    P.keys.upload(pr.keys, st);
+    P.E.alloc(std::max<int64_t>(e_total, 1));
+    P.Z.alloc(std::max<int64_t>(e_total, 1));
+    P.h2d_bytes += pr.keys.size() * sizeof(DKey);
+    if (!pr.keys.empty()) {
+      const int nk = static_cast<int>(pr.keys.size());
+      if (P.cfg.variant)
+        tables_kernel<true><<<(nk + 127) / 128, 128, 0, st>>>(P.keys.p, nk, P.E.p, P.Z.p);
+      else
+        tables_kernel<false><<<(nk + 127) / 128, 128, 0, st>>>(P.keys.p, nk, P.E.p, P.Z.p);
+      LT_CUDA(cudaGetLastError());
+      ++P.launches_prep;
+    }
+    std::vector<DKey> back(pr.keys.size());
+    if (!back.empty())
+      LT_CUDA(cudaMemcpyAsync(back.data(), P.keys.p, back.size() * sizeof(DKey), cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    bool overflow = false;
+    for (size_t k = 0; k < back.size(); ++k) {
+      if (back[k].overflow) overflow = true;
+    }
+    if (!overflow) {
+      pr.keys = back;
+      break;
+    }
+    if (attempt > 4) throw CudaError{"RNG table sizing failed"};
+    e_total = 0;
+    for (size_t k = 0; k < pr.keys.size(); ++k) {
+      DKey& key = pr.keys[k];
+      if (back[k].overflow) key.cap = static_cast<int32_t>(std::min<int64_t>(int64_t(key.cap) * 4, 2000000000));
+      key.e_off = key.z_off = e_total;
+      e_total += key.cap;
+    }
+  }
+  cudaEventRecord(ctx->ev[1], st);
+  // count arrivals per (scenario, adapter)
+  const int64_t n_pairs = static_cast<int64_t>(pr.pair_scen.size());
+  P.scen.upload(P.h_scen, st);
+  P.adapters.upload(pr.adapters, st);
+  P.lens.upload(pr.lens, st);
+  P.h2d_bytes += P.h_scen.size() * sizeof(DScen) + pr.adapters.size() * sizeof(DAdapter);
+  DBuf<int32_t> d_pair_scen, d_pair_adp, d_adp_count, d_overflow;
+  DBuf<int64_t> d_pair_begin;
+  DBuf<unsigned long long> d_scen_count;
+  if (n_pairs > 0) {
+    d_pair_scen.upload(pr.pair_scen, st);
+    d_pair_adp.upload(pr.pair_adp, st);
+    d_adp_count.alloc(n_pairs);
+    d_scen_count.alloc(P.n_scen);
+    d_overflow.alloc(1);
+    LT_CUDA(cudaMemsetAsync(d_scen_count.p, 0, P.n_scen * sizeof(unsigned long long), st));
+    LT_CUDA(cudaMemsetAsync(d_overflow.p, 0, sizeof(int32_t), st));
+    count_kernel<<<static_cast<unsigned>((n_pairs + 255) / 256), 256, 0, st>>>(
+        P.scen.p, d_pair_scen.p, d_pair_adp.p, n_pairs, P.adapters.p, P.keys.p, P.E.p, d_adp_count.p,
+        d_scen_count.p, d_overflow.p);
+    LT_CUDA(cudaGetLastError());
+    ++P.launches_prep;
+    std::vector<unsigned long long> counts(P.n_scen);
+    int32_t ovf = 0;
+    LT_CUDA(cudaMemcpyAsync(counts.data(), d_scen_count.p, P.n_scen * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaMemcpyAsync(&ovf, d_overflow.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    if (ovf) throw CudaError{"internal: RNG table shorter than an arrival stream"};
+    for (int64_t i = 0; i < P.n_scen; ++i)
+      if (P.h_scen[i].generated && P.h_scen[i].status == LT_OK) P.h_scen[i].n_req = static_cast<int32_t>(counts[i]);
+  }
+  int64_t off = 0;
+  for (int64_t i = 0; i < P.n_scen; ++i) {
+    P.h_scen[i].req_begin = off;
+    off += P.h_scen[i].n_req;
+    P.max_req = std::max<int64_t>(P.max_req, P.h_scen[i].n_req);
+  }
+  P.total_req = off;
+  P.scen.upload(P.h_scen, st);
+  const int64_t nr = std::max<int64_t>(P.total_req, 1);
+  P.r_arr.alloc(nr);
+  P.r_in.alloc(nr);
+  P.r_out.alloc(nr);
+  P.r_adp.alloc(nr);
+  P.r_phase.alloc(nr);
+  P.r_gen.alloc(nr);
+  P.r_first.alloc(nr);
+  P.r_last.alloc(nr);
+  P.r_pre.alloc(nr);
+  // scripted requests
+  {
+    std::vector<double> arr;
+    std::vector<int32_t> in, outv, adp;
+    std::vector<int64_t> where;
+    for (int64_t i = 0; i < P.n_scen; ++i) {
+      const lt_scenario& s = b->scenarios[i];
+      if (s.n_requests < 0 || P.h_scen[i].status != LT_OK) continue;
+      std::unordered_map<int, int> dense;
+      const int64_t ab = P.h_scen[i].adapter_begin;
+      for (int k = 0; k < s.n_adapters; ++k) dense[P.adapter_ids[ab + k]] = k;
+      for (int64_t r = 0; r < s.n_requests; ++r) {
+        const lt_request& q = b->requests[s.request_offset + r];
+        arr.push_back(q.arrival_time_s);
+        in.push_back(q.input_tokens);
+        outv.push_back(q.output_tokens);
+        adp.push_back(dense[q.adapter_id]);
+      }
+      where.push_back(i);
+    }
+    int64_t cursor = 0;
+    for (int64_t i : where) {
+      const int64_t n = P.h_scen[i].n_req;
+      const int64_t at = P.h_scen[i].req_begin;
+      LT_CUDA(cudaMemcpyAsync(P.r_arr.p + at, arr.data() + cursor, n * sizeof(double), cudaMemcpyHostToDevice, st));
+      LT_CUDA(cudaMemcpyAsync(P.r_in.p + at, in.data() + cursor, n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      LT_CUDA(cudaMemcpyAsync(P.r_out.p + at, outv.data() + cursor, n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      LT_CUDA(cudaMemcpyAsync(P.r_adp.p + at, adp.data() + cursor, n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      cursor += n;
+    }
+    P.h2d_bytes += cursor * 20;
+    LT_CUDA(cudaStreamSynchronize(st));
+  }
+  cudaEventRecord(ctx->ev[2], st);
+  if (n_pairs > 0) {
+    d_pair_begin.upload(pr.pair_begin, st);
+    const int wpb = 4;
+    const size_t smem = static_cast<size_t>(wpb) * P.max_adapters * 16;
+    LT_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    merge_kernel<<<static_cast<unsigned>((P.n_scen + wpb - 1) / wpb), wpb * 32, smem, st>>>(
+        P.scen.p, static_cast<int>(P.n_scen), P.adapters.p, P.keys.p, P.lens.p, P.E.p, P.Z.p,
+        d_pair_begin.p, d_adp_count.p, P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p, P.max_adapters);
+    LT_CUDA(cudaGetLastError());
+    ++P.launches_prep;
+  }
+  cudaEventRecord(ctx->ev[3], st);
+  // engine order: most expensive first
+  P.h_order.resize(P.n_scen);
+  for (int64_t i = 0; i < P.n_scen; ++i) P.h_order[i] = static_cast<int32_t>(i);
+  std::stable_sort(P.h_order.begin(), P.h_order.end(),
+                   [&](int32_t x, int32_t y) { return pr.cost[x] > pr.cost[y]; });
+  P.order.upload(P.h_order, st);
+  P.counter.alloc(1);
+  P.out.alloc(std::max<int64_t>(P.n_scen, 1));
+  // occupancy-sized persistent grid
+  P.block = 256;
+  P.smem = static_cast<size_t>(P.block / 32) * P.max_adapters * 12;
+  LT_CUDA(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(P.smem)));
+  int per_sm = 0;
+  LT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, engine_kernel, P.block, P.smem));
+  per_sm = std::max(per_sm, 1);
+  const int64_t want = (P.n_scen + P.block / 32 - 1) / (P.block / 32);
+  P.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(ctx->sm_count) * per_sm)));
+  P.ws_stride = std::max<int64_t>(P.max_req, 1);
+  const int64_t slots = int64_t(P.grid) * (P.block / 32);
+  P.ws_run.alloc(slots * P.ws_stride);
+  P.ws_pq.alloc(slots * P.ws_stride);
+  P.ws_fq.alloc(slots * P.ws_stride);
+  LT_CUDA(cudaStreamSynchronize(st));
+  P.tables_ms = elapsed(ctx->ev[0], ctx->ev[1]);
+  P.merge_ms = elapsed(ctx->ev[2], ctx->ev[3]);
+  return plan.release();
+}
+
+void run_plan(lt_plan& P) {
+  lt_ctx* ctx = P.ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t nr = std::max<int64_t>(P.total_req, 1);
+  LT_CUDA(cudaMemsetAsync(P.r_phase.p, 0, nr, st));
+  LT_CUDA(cudaMemsetAsync(P.r_gen.p, 0, nr * sizeof(int32_t), st));
+  LT_CUDA(cudaMemsetAsync(P.r_pre.p, 0, nr * sizeof(int32_t), st));
+  LT_CUDA(cudaMemsetAsync(P.r_first.p, 0xff, nr * sizeof(double), st));  // NaN: no first token
+  LT_CUDA(cudaMemsetAsync(P.r_last.p, 0, nr * sizeof(double), st));
+  LT_CUDA(cudaMemsetAsync(P.counter.p, 0, sizeof(int32_t), st));
+  EngineParams E{};
+  E.scen = P.scen.p;
+  E.order = P.order.p;
+  E.n_scen = static_cast<int32_t>(P.n_scen);
+  E.max_adapters = P.max_adapters;
+  E.counter = P.counter.p;
+  E.adapters = P.adapters.p;
+  E.r_arr = P.r_arr.p;
+  E.r_in = P.r_in.p;
+  E.r_out = P.r_out.p;
+  E.r_adp = P.r_adp.p;
+  E.r_phase = P.r_phase.p;
+  E.r_gen = P.r_gen.p;
+  E.r_first = P.r_first.p;
+  E.r_last = P.r_last.p;
+  E.r_pre = P.r_pre.p;
+  E.ws_run = P.ws_run.p;
+  E.ws_pq = P.ws_pq.p;
+  E.ws_fq = P.ws_fq.p;
+  E.ws_stride = P.ws_stride;
+  E.k1 = P.cfg.raw.k1;
+  E.k2 = P.cfg.raw.k2;
+  E.k3 = P.cfg.raw.k3;
+  E.k4 = P.cfg.raw.k4;
+  E.k5 = P.cfg.raw.k5;
+  E.k6 = P.cfg.raw.k6;
+  E.k7 = P.cfg.raw.k7;
+  E.priority = P.cfg.raw.loaded_adapter_priority;
+  E.want_digest = P.want_digest;
+  E.out = P.out.p;
+  cudaEventRecord(ctx->ev[4], st);
+  if (P.n_scen > 0) {
+    engine_kernel<<<P.grid, P.block, P.smem, st>>>(E);
+    LT_CUDA(cudaGetLastError());
+  }
+  cudaEventRecord(ctx->ev[5], st);
+}
+
+void fetch_results(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {
+  lt_ctx* ctx = P.ctx;
+  cudaStream_t st = ctx->stream;
+  if (P.n_scen > 0)
+    LT_CUDA(cudaMemcpyAsync(out, P.out.p, P.n_scen * sizeof(lt_sim_summary), cudaMemcpyDeviceToHost, st));
+  int64_t d2h = P.n_scen * sizeof(lt_sim_summary);
+  std::vector<int8_t> phase;
+  std::vector<int32_t> gen, pre, in, outv, adp;
+  std::vector<double> first, last, arr;
+  if (states) {
+    const int64_t n = P.total_req;
+    phase.resize(n);
+    gen.resize(n);
+    pre.resize(n);
+    in.resize(n);
+    outv.resize(n);
+    adp.resize(n);
+    first.resize(n);
+    last.resize(n);
+    arr.resize(n);
+    if (n) {
+      LT_CUDA(cudaMemcpyAsync(phase.data(), P.r_phase.p, n, cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(gen.data(), P.r_gen.p, n * 4, cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(pre.data(), P.r_pre.p, n * 4, cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(in.data(), P.r_in.p, n * 4, cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(outv.data(), P.r_out.p, n * 4, cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(adp.data(), P.r_adp.p, n * 4, cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(first.data(), P.r_first.p, n * 8, cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(last.data(), P.r_last.p, n * 8, cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(arr.data(), P.r_arr.p, n * 8, cudaMemcpyDeviceToHost, st));
+    }
+    d2h += n * 45;
+  }
+  cudaEventRecord(ctx->ev[6], st);
+  LT_CUDA(cudaStreamSynchronize(st));
+  ctx->messages.assign(P.n_scen, std::string());
+  for (int64_t i = 0; i < P.n_scen; ++i) {
+    const HostErr& e = P.errs[i];
+    if (e.code != LT_OK) {
+      out[i].status = e.code;
+      out[i].status_kind = e.kind;
+      out[i].status_a = e.a;
+      out[i].status_b = e.b;
+      ctx->messages[i] = e.msg;
+    } else if (out[i].status != LT_OK) {
+      ctx->messages[i] = render(out[i].status, out[i].status_kind, out[i].status_a, out[i].status_b);
+    }
+  }
+  if (states) {
+    int64_t off = 0;
+    for (int64_t i = 0; i < P.n_scen; ++i) {
+      if (states->req_offset) states->req_offset[i] = off;
+      const DScen& d = P.h_scen[i];
+      for (int64_t r = 0; r < d.n_req; ++r, ++off) {
+        if (off >= states->capacity) continue;
+        const int64_t g = d.req_begin + r;
+        const int8_t ph = phase[g];
+        int32_t tg = gen[g];
+        if (ph == kFinished) tg = outv[g];
+        if (states->phase) states->phase[off] = ph;
+        if (states->tokens_generated) states->tokens_generated[off] = tg;
+        if (states->first_token_time_s) states->first_token_time_s[off] = first[g];
+        if (states->completion_time_s)
+          states->completion_time_s[off] =
+              (ph == kFinished || (ph == kRunning && tg == outv[g])) ? last[g] : 0.0;
+        if (states->preemption_count) states->preemption_count[off] = pre[g];
+        if (states->adapter_id) states->adapter_id[off] = P.adapter_ids[d.adapter_begin + adp[g]];
+        if (states->input_tokens) states->input_tokens[off] = in[g];
+        if (states->output_tokens) states->output_tokens[off] = outv[g];
+        if (states->arrival_time_s) states->arrival_time_s[off] = arr[g];
+      }
+    }
+  }
+  lt_timing& t = ctx->timing;
+  t.tables_ms = P.tables_ms;
+  t.merge_ms = P.merge_ms;
+  t.engine_ms = elapsed(ctx->ev[4], ctx->ev[5]);
+  t.d2h_ms = elapsed(ctx->ev[5], ctx->ev[6]);
+  t.d2h_bytes = d2h;
+  t.h2d_bytes = P.h2d_bytes;
+  t.engine_launches = 1 + P.launches_prep;
+  int64_t bytes = 0;
+  for (int64_t i = 0; i < P.n_scen; ++i) {
+    const lt_sim_summary& o = out[i];
+    bytes += 20 * o.sum_running + 16 * o.sum_visited + 24 * o.sum_arrivals + 16 * o.sum_moves + 64 * o.iterations;
+  }
+  t.algorithmic_bytes = bytes;
+}
+
+int32_t first_error(lt_ctx* ctx, const lt_sim_summary* out, int64_t n, lt_status* st) {
+  for (int64_t i = 0; i < n; ++i) {
+    if (out[i].status != LT_OK) {
+      set_status(st, out[i].status, out[i].status_kind, i, out[i].status_a, out[i].status_b,
+                 ctx->messages[i]);
+      return out[i].status;
+    }
+  }
+  return LT_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+// C-ABI
+
+extern "C" {
+
+int32_t lt_abi_version(void) { return LT_ABI_VERSION; }
+
+int32_t lt_host_libm_variant(void) {
+  static int cached = -1;
+  if (cached >= 0) return cached;
+  std::mt19937_64 g(12345);
+  for (int i = 0; i < 1000000; ++i) {
+    const double x = -static_cast<double>(g() >> 11) * 0x1.0p-53;
+    const double a = glibc_log1p<true>(x), b = glibc_log1p<false>(x);
+    if (as_u64(a) != as_u64(b)) {
+      volatile double xv = x;
+      const double w = std::log1p(xv);
+      cached = as_u64(w) == as_u64(a) ? 1 : 0;
+      return cached;
+    }
+  }
+  cached = 1;
+  return cached;
+}
+
+void lt_format_status(int32_t code, int32_t kind, int64_t a, int64_t b, char* buf, size_t len) {
+  if (!buf || !len) return;
+  switch (kind) {
+    case LT_K_INFEASIBLE_SLOTS:
+      std::snprintf(buf, len, "infeasible configuration: %lld slots consume the entire KV budget (mem_max = 0)",
+                    static_cast<long long>(a));
+      return;
+    case LT_K_NO_LOAD_ENTRY:
+      std::snprintf(buf, len, "estimators.load.cpu_load_seconds: no entry for rank %lld", static_cast<long long>(a));
+      return;
+    case LT_K_SOLE_SURVIVOR:
+      std::snprintf(buf, len, "single request exceeds KV capacity: request %lld", static_cast<long long>(a));
+      return;
+    case LT_K_NO_SLOT_COST:
+      std::snprintf(buf, len,
+                    "estimators.memory: no slot cost for rank %lld (add a slot_cost_tokens entry or "
+                    "slot_cost_base_rank8)",
+                    static_cast<long long>(a));
+      return;
+    case LT_K_ADMISSION_STUCK:
+      std::snprintf(buf, len, "empty batch with a non-empty waiting queue: admission stuck");
+      return;
+    case LT_K_TOO_MANY_ADAPTERS:
+      std::snprintf(buf, len, "device path supports at most %lld adapters per scenario, got %lld",
+                    static_cast<long long>(b), static_cast<long long>(a));
+      return;
+    case LT_K_ITERATION_RANGE:
+      std::snprintf(buf, len, "device path iteration index limit reached at %lld", static_cast<long long>(a));
+      return;
+    case LT_K_TABLE_EXHAUSTED:
+      std::snprintf(buf, len, "internal: RNG table exhausted");
+      return;
+    case LT_K_SLOT_OVERFLOW:
+      std::snprintf(buf, len, "SlotCache: running batch needs %lld adapters but only %lld slots exist (admission bug)",
+                    static_cast<long long>(a), static_cast<long long>(b));
+      return;
+    case LT_K_NO_EVICTABLE:
+      std::snprintf(buf, len, "SlotCache: no evictable slot for adapter %lld (admission bug)",
+                    static_cast<long long>(a));
+      return;
+    default:
+      buf[0] = 0;
+      if (code == LT_OK) std::snprintf(buf, len, "ok");
+      return;
+  }
+}
+
+lt_ctx* lt_create(int32_t device, lt_status* status) {
+  ok_status(status);
+  try {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device || device < 0) {
+      set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, "no CUDA device available for the B200 path");
+      return nullptr;
+    }
+    auto ctx = std::make_unique<lt_ctx>();
+    ctx->device = device;
+    LT_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    LT_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+      set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, prop.major, prop.minor,
+                 std::string("device is not sm_100 (B200): ") + prop.name);
+      return nullptr;
+    }
+    ctx->sm_count = prop.multiProcessorCount;
+    LT_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->ev) LT_CUDA(cudaEventCreate(&e));
+    return ctx.release();
+  } catch (const CudaError& e) {
+    set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
+    return nullptr;
+  }
+}
+
+void lt_destroy(lt_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+void* lt_stream(lt_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int32_t lt_last_message(lt_ctx* ctx, int64_t index, char* buf, size_t len) {
+  if (!ctx || !buf || !len) return LT_ERR_VALIDATION;
+  if (index < 0 || static_cast<size_t>(index) >= ctx->messages.size()) {
+    buf[0] = 0;
+    return LT_ERR_VALIDATION;
+  }
+  std::snprintf(buf, len, "%s", ctx->messages[static_cast<size_t>(index)].c_str());
+  return LT_OK;
+}
+
+int32_t lt_last_timing(lt_ctx* ctx, lt_timing* out) {
+  if (!ctx || !out) return LT_ERR_VALIDATION;
+  *out = ctx->timing;
+  return LT_OK;
+}
+
+lt_plan* lt_plan_simulate(lt_ctx* ctx, const lt_workload_batch* batch, const lt_server_config* config,
+                          const lt_sim_options* options, lt_status* status) {
+  ok_status(status);
+  try {
+    cudaSetDevice(ctx->device);
+    return build_plan(ctx, batch, config, options);
+  } catch (const CudaError& e) {
+    set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
+    return nullptr;
+  }
+}
+
+int32_t lt_plan_run(lt_plan* plan, lt_status* status) {
+  ok_status(status);
+  try {
+    cudaSetDevice(plan->ctx->device);
+    run_plan(*plan);
+    return LT_OK;
+  } catch (const CudaError& e) {
+    set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
+    return LT_ERR_DEVICE;
+  }
+}
+
+int32_t lt_plan_results(lt_plan* plan, lt_sim_summary* out, lt_request_states* states, lt_status* status) {
+  ok_status(status);
+  try {
+    cudaSetDevice(plan->ctx->device);
+    fetch_results(*plan, out, states);
+    return first_error(plan->ctx, out, plan->n_scen, status);
+  } catch (const CudaError& e) {
+    set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
+    return LT_ERR_DEVICE;
+  }
+}
+
+void lt_plan_destroy(lt_plan* plan) {
+  if (!plan) return;
+  cudaSetDevice(plan->ctx->device);
+  delete plan;
+}
+
+int32_t lt_simulate_batch(lt_ctx* ctx, const lt_workload_batch* batch, const lt_server_config* config,
+                          const lt_sim_options* options, lt_sim_summary* out, lt_request_states* states,
+                          lt_status* status) {
+  const auto t0 = std::chrono::steady_clock::now();
+  lt_plan* plan = lt_plan_simulate(ctx, batch, config, options, status);
+  if (!plan) return status ? status->code : LT_ERR_DEVICE;
+  int32_t rc = lt_plan_run(plan, status);
+  if (rc == LT_OK) rc = lt_plan_results(plan, out, states, status);
+  lt_plan_destroy(plan);
+  ctx->timing.total_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return rc;
+}
+
+int32_t lt_generate_arrivals_batch(lt_ctx* ctx, const lt_workload_batch* batch, const lt_sim_options* options,
+                                   lt_request* out, int64_t capacity, int64_t* offsets, int64_t* counts,
+                                   lt_status* status) {
+  ok_status(status);
+  lt_server_config cfg{};
+  // generate_arrivals needs no server config; a permissive one keeps the
+  // engine-level checks out of the way.
+  cfg.slots = 1;
+  cfg.iteration_cap = 1;
+  cfg.k5 = 1.0;
+  cfg.k7 = 1.0;
+  cfg.total_kv_budget = INT64_MAX / 4;
+  cfg.has_slot_cost_base_rank8 = 1;
+  cfg.slot_cost_base_rank8 = 1.0;
+  cfg.disk_multiplier = 1.0;
+  std::unique_ptr<lt_plan> plan;
+  try {
+    cudaSetDevice(ctx->device);
+    plan.reset(build_plan(ctx, batch, &cfg, options));
+    cudaStream_t st = ctx->stream;
+    const int64_t n = plan->total_req;
+    std::vector<double> arr(n);
+    std::vector<int32_t> in(n), outv(n), adp(n);
+    if (n) {
+      LT_CUDA(cudaMemcpyAsync(arr.data(), plan->r_arr.p, n * 8, cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(in.data(), plan->r_in.p, n * 4, cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(outv.data(), plan->r_out.p, n * 4, cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(adp.data(), plan->r_adp.p, n * 4, cudaMemcpyDeviceToHost, st));
+    }
+    LT_CUDA(cudaStreamSynchronize(st));
+    int64_t off = 0;
+    int32_t rc = LT_OK;
+    for (int64_t i = 0; i < plan->n_scen; ++i) {
+      const DScen& d = plan->h_scen[i];
+      const HostErr& e = plan->errs[i];
+      offsets[i] = off;
+      counts[i] = d.n_req;
+      if (e.code != LT_OK && rc == LT_OK) {
+        rc = e.code;
+        set_status(status, e.code, e.kind, i, e.a, e.b, e.msg);
+      }
+      for (int64_t r = 0; r < d.n_req; ++r, ++off) {
+        if (off >= capacity) continue;
+        const int64_t g = d.req_begin + r;
+        lt_request& q = out[off];
+        q.request_id = r;
+        q.adapter_id = plan->adapter_ids[d.adapter_begin + adp[g]];
+        q.input_tokens = in[g];
+        q.output_tokens = outv[g];
+        q._pad = 0;
+        q.arrival_time_s = arr[g];
+      }
+    }
+    return rc;
+  } catch (const CudaError& e) {
+    set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
+    return LT_ERR_DEVICE;
+  }
+}
+
+
+int32_t lt_sweep_frontier_capacity(const lt_sweep_grid* grid) {
+  if (!grid) return 0;
+  int32_t cap = 0;
+  for (int i = 0; i < grid->n_count; ++i) cap += std::max<int32_t>(4, grid->g_count);
+  return std::max<int32_t>(cap, 1);
+}
+
+int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_server_config* config,
+                       const lt_sweep_grid* grid, double duration_s, uint64_t seed,
+                       const lt_sweep_options* options, const lt_sim_options* sim_options,
+                       lt_placement* out, lt_frontier_point* frontier, int32_t max_frontier,
+                       lt_status* status) {
+  ok_status(status);
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t n_cond = batch->n_conditions;
+  ctx->messages.assign(n_cond, std::string());
+  try {
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    // SweepGrid::validate (placement.cpp:169-183)
+    HostErr grid_err;
+    bool grid_ok = true;
+    if (grid->n_count <= 0) {
+      grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.n_values: must be non-empty");
+    } else {
+      for (int i = 0; i < grid->n_count && grid_ok; ++i) {
+        if (grid->n_values[i] < 1)
+          grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.n_values: entries must be >= 1");
+        else if (i > 0 && grid->n_values[i] <= grid->n_values[i - 1])
+          grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.n_values: must be strictly ascending");
+      }
+      if (grid_ok && grid->g_mode == LT_G_EXPLICIT) {
+        if (grid->g_count <= 0)
+          grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.g_values: must be non-empty in explicit mode");
+        for (int i = 0; i < grid->g_count && grid_ok; ++i)
+          if (grid->g_values[i] < 1) grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.g_values: entries must be >= 1");
+      }
+    }
+    // rows: SweepGrid::g_candidates (placement.cpp:159-167)
+    std::vector<SweepRow> rows;
+    std::vector<int32_t> g_list;
+    int32_t per_cond = 0;
+    int n_max = 1;
+    if (grid_ok) {
+      for (int i = 0; i < grid->n_count; ++i) {
+        const int n = grid->n_values[i];
+        n_max = std::max(n_max, n);
+        std::set<int> gs;
+        if (grid->g_mode == LT_G_GEOMETRIC) {
+          for (int g : {8, n / 4, n / 2, n}) gs.insert(std::clamp(g, 1, n));
+        } else {
+          for (int k = 0; k < grid->g_count; ++k) gs.insert(std::clamp(grid->g_values[k], 1, n));
+        }
+        SweepRow r{n, static_cast<int32_t>(gs.size()), static_cast<int32_t>(g_list.size()), per_cond};
+        for (int g : gs) g_list.push_back(g);
+        per_cond += r.g_count;
+        rows.push_back(r);
+      }
+    }
+    // Conditions -> grid-point scenarios (instantiate_condition, placement.cpp:139-157):
+    // adapter ids 1..N with (rank, rate) = mix[(id-1) % |mix|]; every point of a
+    // condition reads a prefix of the condition's n_max-adapter block.
+    std::vector<lt_adapter> adapters;
+    std::vector<lt_scenario> scen;
+    std::vector<int64_t> cond_base(n_cond, -1);
+    std::vector<HostErr> cond_err(n_cond);
+    for (int64_t c = 0; c < n_cond; ++c) {
+      const lt_condition& cd = batch->conditions[c];
+      HostErr& e = cond_err[c];
+      if (!grid_ok) {
+        e = grid_err;
+        continue;
+      }
+      if (!validate_lengths(batch->lengths[cd.length_index], batch->full_lengths, "condition.lengths", &e)) continue;
+      if (cd.mix_count <= 0) {
+        e.set(LT_ERR_VALIDATION, "condition.mix: must be non-empty");
+        continue;
+      }
+      const int64_t ab = static_cast<int64_t>(adapters.size());
+      for (int i = 0; i < n_max; ++i) {
+        const lt_template& t = batch->templates[cd.mix_offset + (i % cd.mix_count)];
+        lt_adapter a{};
+        a.adapter_id = i + 1;
+        a.rank = t.rank;
+        a.rate = t.rate;
+        a.length_index = -1;
+        adapters.push_back(a);
+      }
+      cond_base[c] = static_cast<int64_t>(scen.size());
+      for (const SweepRow& r : rows) {
+        for (int gi = 0; gi < r.g_count; ++gi) {
+          lt_scenario s{};
+          s.adapter_offset = ab;
+          s.n_adapters = r.n;
+          s.length_index = cd.length_index;
+          s.duration_s = duration_s;
+          s.seed = seed;
+          s.slots = g_list[r.g_offset + gi];
+          s.mode = options->mode;
+          s.n_requests = -1;
+          scen.push_back(s);
+        }
+      }
+    }
+    lt_workload_batch wb{};
+    wb.scenarios = scen.data();
+    wb.n_scenarios = static_cast<int64_t>(scen.size());
+    wb.adapters = adapters.data();
+    wb.n_adapters = static_cast<int64_t>(adapters.size());
+    wb.lengths = batch->lengths;
+    wb.n_lengths = batch->n_lengths;
+    wb.full_lengths = batch->full_lengths;
+    wb.n_full_pairs = batch->n_full_pairs;
+    lt_sim_options so{};
+    if (sim_options) so = *sim_options;
+    so.want_digest = 0;
+    std::unique_ptr<lt_plan> plan(build_plan(ctx, &wb, config, &so));
+    run_plan(*plan);
+    DBuf<SweepRow> d_rows;
+    DBuf<int32_t> d_g;
+    DBuf<int64_t> d_base;
+    DBuf<lt_placement> d_out;
+    DBuf<lt_frontier_point> d_front;
+    d_rows.upload(rows, st);
+    d_g.upload(g_list, st);
+    d_base.upload(cond_base, st);
+    d_out.alloc(std::max<int64_t>(n_cond, 1));
+    d_front.alloc(std::max<int64_t>(n_cond * max_frontier, 1));
+    if (n_cond > 0 && !rows.empty()) {
+      sweep_reduce_kernel<<<static_cast<unsigned>((n_cond + 127) / 128), 128, 0, st>>>(
+          static_cast<int>(n_cond), d_rows.p, static_cast<int>(rows.size()), d_g.p, per_cond, d_base.p,
+          plan->out.p, options->early_exit, options->early_exit_k, max_frontier, d_out.p, d_front.p);
+      LT_CUDA(cudaGetLastError());
+    }
+    cudaEventRecord(ctx->ev[6], st);
+    if (n_cond > 0) {
+      LT_CUDA(cudaMemcpyAsync(out, d_out.p, n_cond * sizeof(lt_placement), cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(frontier, d_front.p, n_cond * max_frontier * sizeof(lt_frontier_point),
+                              cudaMemcpyDeviceToHost, st));
+    }
+    cudaEventRecord(ctx->ev[7], st);
+    LT_CUDA(cudaStreamSynchronize(st));
+    int32_t rc = LT_OK;
+    for (int64_t c = 0; c < n_cond; ++c) {
+      lt_placement& p = out[c];
+      std::string msg;
+      if (cond_base[c] < 0) {
+        std::memset(&p, 0, sizeof(p));
+        p.status_point = -1;
+        p.status = cond_err[c].code;
+        p.status_kind = cond_err[c].kind;
+        p.status_a = cond_err[c].a;
+        p.status_b = cond_err[c].b;
+        msg = cond_err[c].msg;
+      } else if (p.status != LT_OK) {
+        const HostErr& pe = plan->errs[p.status_point];
+        msg = pe.code != LT_OK ? pe.msg : render(p.status, p.status_kind, p.status_a, p.status_b);
+      }
+      ctx->messages[c] = msg;
+      if (p.status != LT_OK && rc == LT_OK) {
+        rc = p.status;
+        set_status(status, p.status, p.status_kind, c, p.status_a, p.status_b, msg);
+      }
+    }
+    lt_timing& t = ctx->timing;
+    t.tables_ms = plan->tables_ms;
+    t.merge_ms = plan->merge_ms;
+    t.engine_ms = elapsed(ctx->ev[4], ctx->ev[5]);
+    t.reduce_ms = elapsed(ctx->ev[5], ctx->ev[6]);
+    t.d2h_ms = elapsed(ctx->ev[6], ctx->ev[7]);
+    t.engine_launches = plan->launches_prep + 2;
+    t.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return rc;
+  } catch (const CudaError& e) {
+    set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
+    return LT_ERR_DEVICE;
+  }
+}
+
+}  // extern "C"

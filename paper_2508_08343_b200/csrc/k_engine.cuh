@@ -1,0 +1,687 @@
+// K1 engine_step + K2 metrics epilogue: one warp simulates one engine.
+//
+// Reference semantics (Appendix A of SURVEY.md), per iteration of
+// Engine::run (engine.cpp:80-150):
+//   idle jump (82-85) -> ingest arrivals <= clock (88-92) ->
+//   complete_finished (kv_scheduler.cpp:238-259) -> decode_step_alloc
+//   (:183-236) -> admit (:170-181, SlotPlan :49-98, scan_queue :109-166) ->
+//   SlotCache::ensure_loaded (adapter_cache.cpp:40-78) -> lat_step
+//   (estimators.cpp:110-139) -> emit one token per running request
+//   (engine.cpp:128-135) -> advance clock, iteration cap (144-149).
+//
+// Warp mapping: every scalar of the engine is warp-uniform (held by all 32
+// lanes); adapter sets (resident, claimed/needed, evicted, blocked, slotful)
+// are 1024-bit masks with lane L owning adapters [32L, 32L+32); queues are
+// scanned 32 entries per step with ballots, prefix popcounts and
+// __match_any_sync; only slot claims/blocks and the memory stop are resolved
+// one lane at a time, in queue order.
+//
+// Event-driven state: a running request never stores its token count. Its
+// running entry keeps the iteration at which it retires (admission iteration
+// + out - gen), so the per-iteration "+1 KV / +1 token for every running
+// request" of the reference is O(1): the ledger grows by R, tokens by R, and
+// a request's KV = in + gen is recovered from (fin - iteration) when it
+// leaves. LIFO preemption is running.back() because running stays in
+// admission order (kv_scheduler.cpp:159, :242-257).
+#pragma once
+#include <float.h>
+#include <limits.h>
+
+#include "lt_device.cuh"
+
+namespace lt {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Bit `a` of a lane-distributed 1024-bit mask (a may differ per lane).
+__device__ __forceinline__ bool mask_bit(uint32_t w, int a) {
+  return (__shfl_sync(kFull, w, (a >> 5) & 31) >> (a & 31)) & 1u;
+}
+__device__ __forceinline__ void mask_set(uint32_t& w, int a, int lane) {
+  if (lane == (a >> 5)) w |= 1u << (a & 31);
+}
+__device__ __forceinline__ void mask_clear(uint32_t& w, int a, int lane) {
+  if (lane == (a >> 5)) w &= ~(1u << (a & 31));
+}
+// Lowest set adapter index of a mask, or -1.
+__device__ __forceinline__ int mask_lowest(uint32_t w) {
+  const unsigned nz = __ballot_sync(kFull, w != 0);
+  if (!nz) return -1;
+  const int src = __ffs(nz) - 1;
+  const uint32_t ws = __shfl_sync(kFull, w, src);
+  return src * 32 + __ffs(ws) - 1;
+}
+
+__device__ __forceinline__ int warp_min_i(int v) {
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// LRU victim: argmin over set bits of `cand` of (last_used, adapter_id);
+// dense index order == adapter_id order. Adapters needed by the previous
+// ensure_loaded call still carry last_used == prev_now (lazy refresh).
+__device__ __forceinline__ int lru_victim(uint32_t cand, uint32_t prev_needed, double prev_now,
+                                          const double* last_used, int lane) {
+  double best = DBL_MAX;
+  int best_a = INT_MAX;
+  uint32_t w = cand;
+  while (w) {
+    const int b = __ffs(w) - 1;
+    w &= w - 1;
+    const int a = lane * 32 + b;
+    const double key = ((prev_needed >> b) & 1u) ? prev_now : last_used[a];
+    if (key < best || (key == best && a < best_a)) {
+      best = key;
+      best_a = a;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(kFull, best, o);
+    const int oa = __shfl_xor_sync(kFull, best_a, o);
+    if (ob < best || (ob == best && oa < best_a)) {
+      best = ob;
+      best_a = oa;
+    }
+  }
+  return best_a == INT_MAX ? -1 : best_a;
+}
+
+__device__ __forceinline__ uint64_t fold64(uint64_t h, uint64_t w) {
+  h ^= w;
+  h *= 0x100000001b3ULL;
+  return h;
+}
+
+struct WarpEngine {
+  // --- warp-uniform scalars
+  double clock = 0.0, prev_now = 0.0, duration = 0.0;
+  int64_t used = 0, cap = 0;
+  int32_t iter = 0, iter_cap = 0;
+  int32_t R = 0, Wp = 0, Wf = 0, ingest = 0, n_req = 0;
+  int32_t resident_count = 0, G = 1, N = 1;
+  int32_t min_fin = INT_MAX;
+  int32_t waived = -1;
+  int32_t status = LT_OK, status_kind = LT_K_NONE;
+  int64_t status_a = 0, status_b = 0;
+  int32_t truncated = 0;
+  long long finished = 0, preempts = 0, loads_n = 0, tok_win = 0, tok_tot = 0;
+  long long sum_r = 0, sum_v = 0, sum_a = 0, sum_m = 0;
+  uint64_t digest = 0xcbf29ce484222325ULL;
+  // --- per-lane words of adapter masks
+  uint32_t slotful_w = 0, resident_w = 0, claimed_w = 0, prev_needed_w = 0;
+  // --- scan-local SlotPlan state
+  uint32_t evicted_w = 0, blocked_w = 0;
+  int32_t free_slots = 0;
+  // --- pointers
+  int64_t rb = 0, ab = 0;
+  int lane = 0;
+  double* last_used = nullptr;
+  int32_t* run_cnt = nullptr;
+  int4* run = nullptr;
+  int2* pq = nullptr;
+  int2* fq = nullptr;
+
+  __device__ __forceinline__ void fail(int32_t code, int32_t kind, int64_t a, int64_t b) {
+    status = code;
+    status_kind = kind;
+    status_a = a;
+    status_b = b;
+  }
+
+  __device__ __forceinline__ bool claimed(int a) const { return mask_bit(claimed_w, a); }
+
+  // An adapter left the running batch: its slot is no longer claimed.
+  __device__ __forceinline__ void release_adapter(int a, bool dec_to_zero) {
+    if (dec_to_zero) mask_clear(claimed_w, a, lane);
+  }
+
+  // SlotPlan::can_claim (kv_scheduler.cpp:68-72), warp-uniform a.
+  __device__ __forceinline__ bool can_claim(int a) const {
+    const uint32_t pool = resident_w & ~claimed_w & ~evicted_w;
+    if (mask_bit(claimed_w, a) || mask_bit(pool, a)) return true;
+    if (free_slots > 0) return true;
+    return __any_sync(kFull, pool != 0);
+  }
+
+  // SlotPlan::claim (kv_scheduler.cpp:74-88).
+  __device__ __forceinline__ void claim(int a) {
+    if (mask_bit(claimed_w, a)) return;
+    const uint32_t pool = resident_w & ~claimed_w & ~evicted_w;
+    if (!mask_bit(pool, a)) {
+      if (free_slots > 0) {
+        --free_slots;
+      } else {
+        const int v = lru_victim(pool, prev_needed_w, prev_now, last_used, lane);
+        if (v >= 0) mask_set(evicted_w, v, lane);
+      }
+    }
+    mask_set(claimed_w, a, lane);
+  }
+
+  // complete_finished (kv_scheduler.cpp:238-259): stable compaction of running.
+  __device__ __forceinline__ void retire(const EngineParams& P) {
+    int w = 0;
+    int new_min = INT_MAX;
+    long long released = 0, nfin = 0;
+    for (int base = 0; base < R; base += 32) {
+      const int i = base + lane;
+      const bool v = i < R;
+      int4 e = make_int4(0, INT_MAX, 0, 0);
+      if (v) e = run[i];
+      const bool fin = v && e.y <= iter;
+      const unsigned keepm = __ballot_sync(kFull, v && !fin);
+      const unsigned finm = __ballot_sync(kFull, fin);
+      if (v && !fin) {
+        run[w + __popc(keepm & lanemask_lt())] = e;
+        new_min = min(new_min, e.y);
+      }
+      if (finm) {
+        int a = -1;
+        bool zero = false;
+        if (fin) {
+          const int idx = e.x;
+          released += static_cast<long long>(e.w) - (idx == waived ? 1 : 0);
+          P.r_phase[rb + idx] = kFinished;
+          P.r_last[rb + idx] = clock;  // completion == the final emit (engine.cpp:134)
+          a = e.z & kAdapterMask;
+          zero = atomicSub(&run_cnt[a], 1) == 1;
+        }
+        nfin += fin;
+        unsigned zm = __ballot_sync(kFull, zero);
+        while (zm) {
+          const int src = __ffs(zm) - 1;
+          zm &= zm - 1;
+          release_adapter(__shfl_sync(kFull, a, src), true);
+        }
+      }
+      w += __popc(keepm);
+      __syncwarp();
+    }
+    const long long rel = warp_sum_ll(released);
+    const long long nf = warp_sum_ll(nfin);
+    used -= rel;
+    finished += nf;
+    sum_m += nf;
+    if (nf) waived = -1;
+    R = w;
+    min_fin = warp_min_i(new_min);
+  }
+
+  // Insert a preempted request into waiting_preempted ordered by
+  // (arrival, request_id) (kv_scheduler.cpp:206-215).
+  __device__ __forceinline__ void pq_insert(const EngineParams& P, int idx, int adapter_word) {
+    const double arr = P.r_arr[rb + idx];
+    // Victims are the latest admissions, so their slot is near the back:
+    // scan backwards for the first entry that is not greater.
+    int pos = 0;
+    for (int hi = Wp; hi > 0; hi -= 32) {
+      const int i = hi - 32 + lane;
+      bool greater = false;  // entry i sorts after the victim
+      if (i >= 0) {
+        const int j = pq[i].x;
+        const double aj = P.r_arr[rb + j];
+        greater = (arr < aj) || (arr == aj && idx < j);
+      }
+      const unsigned notg = __ballot_sync(kFull, i >= 0 && !greater);
+      if (notg) {
+        pos = hi - 32 + (31 - __clz(notg)) + 1;
+        break;
+      }
+    }
+    // shift [pos, Wp) right by one, back to front
+    for (int hi = Wp; hi > pos; hi -= 32) {
+      const int lo = max(pos, hi - 32);
+      const int i = lo + lane;
+      int2 e;
+      if (i < hi) e = pq[i];
+      __syncwarp();
+      if (i < hi) pq[i + 1] = e;
+      __syncwarp();
+    }
+    if (lane == 0) pq[pos] = make_int2(idx, adapter_word);
+    __syncwarp();
+    ++Wp;
+  }
+
+  // decode_step_alloc (kv_scheduler.cpp:183-236).
+  __device__ __forceinline__ bool alloc(const EngineParams& P) {
+    if (R == 0) return true;
+    int64_t demand = R;
+    while (used + demand > cap && R > 1) {
+      const int4 e = run[R - 1];
+      --R;
+      const int idx = e.x;
+      const int a = e.z & kAdapterMask;
+      const int outv = P.r_out[rb + idx];
+      const int rem = e.y - iter;
+      const int gen = outv - rem;
+      const int in = e.w - outv;
+      used -= static_cast<int64_t>(in) + gen;
+      bool zero = false;
+      if (lane == 0) {
+        P.r_phase[rb + idx] = kPreempted;
+        P.r_pre[rb + idx] += 1;
+        P.r_gen[rb + idx] = gen;
+        P.r_last[rb + idx] = clock;
+        zero = atomicSub(&run_cnt[a], 1) == 1;
+      }
+      zero = __shfl_sync(kFull, zero, 0);
+      release_adapter(a, zero);
+      const bool over = static_cast<int64_t>(in) + gen + 1 > cap;
+      pq_insert(P, idx, a | (over ? kOverBit : 0));
+      ++preempts;
+      ++sum_m;
+      --demand;
+    }
+    if (used + demand > cap) {
+      const int4 e = run[0];
+      const int rem = e.y - iter;
+      if (rem > 1 || used + demand - 1 > cap) {
+        fail(LT_ERR_SIMULATION, LT_K_SOLE_SURVIVOR, e.x, 0);
+        return false;
+      }
+      waived = e.x;  // the final token needs no new reservation
+      return true;
+    }
+    used += R;
+    return true;
+  }
+
+  // scan_queue (kv_scheduler.cpp:109-166) over one waiting queue, in place.
+  // Returns false if the scan stopped.
+  __device__ __forceinline__ int scan(const EngineParams& P, int2* q, const int W, bool is_pq,
+                                      bool* keep_scanning) {
+    int read = 0, write = 0;
+    bool stopped = false;
+    const unsigned lt_mask = lanemask_lt();
+    while (read < W) {
+      const int i = read + lane;
+      const bool v = i < W;
+      int2 e = make_int2(0, 0);
+      if (v) e = q[i];
+      const int a = e.y & kAdapterMask;
+      const bool over = v && (e.y & kOverBit);
+      const bool sf = v && mask_bit(slotful_w, a);
+      const bool kb = sf && mask_bit(blocked_w, a);
+      const unsigned vm = __ballot_sync(kFull, v);
+      const unsigned rejm = __ballot_sync(kFull, over);
+      const unsigned kbm = __ballot_sync(kFull, v && !over && kb);
+      unsigned cand = __ballot_sync(kFull, v && !over && !kb);
+      int stop = 32;
+      if (!P.priority && kbm) stop = __ffs(kbm) - 1;
+      cand &= (stop >= 32) ? kFull : ((1u << stop) - 1);
+      int64_t demand = 0;
+      int gen = 0;
+      if ((cand >> lane) & 1u) {
+        gen = is_pq ? P.r_gen[rb + e.x] : 0;
+        demand = static_cast<int64_t>(P.r_in[rb + e.x]) + gen + 1;
+      }
+      const unsigned same = __match_any_sync(kFull, v ? a : -1);
+      const unsigned sfm = __ballot_sync(kFull, sf);
+      unsigned admitted = 0;
+      while (cand) {
+        const int c = __ffs(cand) - 1;
+        const int ac = __shfl_sync(kFull, a, c);
+        const bool sfc = (sfm >> c) & 1u;
+        if (sfc && !can_claim(ac)) {
+          mask_set(blocked_w, ac, lane);
+          cand &= ~__shfl_sync(kFull, same, c);
+          if (!P.priority) {
+            stop = c;
+            break;
+          }
+          continue;
+        }
+        const int64_t dc = __shfl_sync(kFull, demand, c);
+        if (used + dc > cap) {
+          stop = c;  // strict FCFS on memory
+          break;
+        }
+        used += dc;
+        if (sfc) claim(ac);
+        if (lane == 0) run_cnt[ac] += 1;
+        __syncwarp();
+        admitted |= 1u << c;
+        cand &= ~(1u << c);
+      }
+      const unsigned processed = (stop >= 32) ? kFull : ((1u << stop) - 1);
+      const unsigned rejected = rejm & processed;
+      const unsigned removed = rejected | admitted;
+      if ((admitted >> lane) & 1u) {
+        const int p = R + __popc(admitted & lt_mask);
+        const int outv = P.r_out[rb + e.x];
+        const int fin = iter + (outv - gen);
+        run[p] = make_int4(e.x, fin, a | (is_pq ? 0 : kFreshBit),
+                           P.r_in[rb + e.x] + outv);
+        P.r_phase[rb + e.x] = kRunning;
+        min_fin = min(min_fin, fin);
+      }
+      if ((rejected >> lane) & 1u) P.r_phase[rb + e.x] = kRejected;
+      const int na = __popc(admitted);
+      R += na;
+      sum_m += na;
+      const unsigned keep = vm & ~removed;
+      __syncwarp();
+      if ((keep >> lane) & 1u) q[write + __popc(keep & lt_mask)] = e;
+      write += __popc(keep);
+      sum_v += (stop < 32) ? stop + 1 : __popc(vm);
+      read += 32;
+      __syncwarp();
+      if (stop < 32) {
+        stopped = true;
+        break;
+      }
+    }
+    min_fin = warp_min_i(min_fin);
+    if (stopped && read < W) {
+      if (write < read) {
+        for (int base = read; base < W; base += 32) {
+          const int i = base + lane;
+          int2 e;
+          if (i < W) e = q[i];
+          __syncwarp();
+          if (i < W) q[write + (i - read)] = e;
+          __syncwarp();
+        }
+      }
+      write += W - read;
+    }
+    *keep_scanning = !stopped;
+    return write;
+  }
+
+  // admit (kv_scheduler.cpp:170-181).
+  __device__ __forceinline__ void admit(const EngineParams& P) {
+    free_slots = G - resident_count;
+    evicted_w = 0;
+    blocked_w = 0;
+    bool go = true;
+    Wp = scan(P, pq, Wp, true, &go);
+    if (go) Wf = scan(P, fq, Wf, false, &go);
+  }
+
+  // SlotCache::ensure_loaded (adapter_cache.cpp:40-78) with needed = the
+  // running batch's adapters (engine.cpp:108-114). Returns Σ load latency.
+  __device__ __forceinline__ bool ensure_loaded(const EngineParams& P, double* loads_sum, int* loads_cnt) {
+    const uint32_t needed_w = claimed_w;
+    const int n_needed = __reduce_add_sync(kFull, __popc(needed_w));
+    if (n_needed > G) {
+      fail(LT_ERR_INTERNAL, LT_K_SLOT_OVERFLOW, n_needed, G);
+      return false;
+    }
+    uint32_t missing_w = needed_w & ~resident_w;
+    double sum = 0.0;
+    int cnt = 0;
+    for (;;) {
+      const int a = mask_lowest(missing_w);
+      if (a < 0) break;
+      if (resident_count >= G) {
+        const int v = lru_victim(resident_w & ~needed_w, prev_needed_w, prev_now, last_used, lane);
+        if (v < 0) {
+          fail(LT_ERR_INTERNAL, LT_K_NO_EVICTABLE, P.adapters[ab + a].id, 0);
+          return false;
+        }
+        mask_clear(resident_w, v, lane);
+        --resident_count;
+      }
+      mask_set(resident_w, a, lane);
+      ++resident_count;
+      const DAdapter& ad = P.adapters[ab + a];
+      const double ll = ad.load_lat;
+      if (ll != ll) {
+        fail(LT_ERR_CONFIG, LT_K_NO_LOAD_ENTRY, ad.rank, 0);
+        return false;
+      }
+      sum = sum + ll;
+      ++cnt;
+      mask_clear(missing_w, a, lane);
+    }
+    // last_used refresh (adapter_cache.cpp:74-77), applied lazily: adapters
+    // that just left the needed set keep the clock of their last use.
+    uint32_t dropped = prev_needed_w & ~needed_w;
+    while (dropped) {
+      const int b = __ffs(dropped) - 1;
+      dropped &= dropped - 1;
+      last_used[lane * 32 + b] = prev_now;
+    }
+    __syncwarp();
+    prev_needed_w = needed_w;
+    prev_now = clock;
+    *loads_sum = sum;
+    *loads_cnt = cnt;
+    return true;
+  }
+};
+
+// Ordered (sequential) FP sum of up to 32 per-lane values with flags.
+__device__ __forceinline__ double ordered_add(double acc, double v, bool f) {
+  unsigned m = __ballot_sync(kFull, f);
+  while (m) {
+    const int src = __ffs(m) - 1;
+    m &= m - 1;
+    acc = acc + __shfl_sync(kFull, v, src);
+  }
+  return acc;
+}
+
+__device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_warp) {
+  WarpEngine E;
+  E.lane = threadIdx.x & 31;
+  const int lane = E.lane;
+  const DScen sc = P.scen[s];
+  lt_sim_summary o;
+  memset(&o, 0, sizeof(o));
+  o.n_requests = sc.n_req;
+  o.duration_s = sc.duration;
+  o.slots = sc.G;
+  o.served_adapters = sc.n_adapters;
+  o.kv_capacity_tokens = sc.capacity;
+  o.ideal_throughput_tok_s = sc.ideal;
+  if (sc.status != LT_OK) {
+    o.status = sc.status;
+    o.status_kind = sc.status_kind;
+    o.status_a = sc.status_a;
+    o.status_b = sc.status_b;
+    if (lane == 0) P.out[s] = o;
+    return;
+  }
+  E.rb = sc.req_begin;
+  E.ab = sc.adapter_begin;
+  E.n_req = sc.n_req;
+  E.N = sc.n_adapters;
+  E.G = sc.G;
+  E.cap = sc.capacity;
+  E.duration = sc.duration;
+  E.iter_cap = static_cast<int32_t>(sc.iter_cap > 0x7ff00000LL ? 0x7ff00000LL : sc.iter_cap);
+  E.last_used = reinterpret_cast<double*>(smem_warp);
+  E.run_cnt = reinterpret_cast<int32_t*>(E.last_used + P.max_adapters);
+  E.run = P.ws_run + static_cast<int64_t>(slot) * P.ws_stride;
+  E.pq = P.ws_pq + static_cast<int64_t>(slot) * P.ws_stride;
+  E.fq = P.ws_fq + static_cast<int64_t>(slot) * P.ws_stride;
+  for (int a = lane; a < E.N; a += 32) {
+    E.last_used[a] = 0.0;
+    E.run_cnt[a] = 0;
+  }
+  for (int b = 0; b < 32; ++b) {
+    const int a = lane * 32 + b;
+    if (a < E.N && P.adapters[E.ab + a].rank > 0) E.slotful_w |= 1u << b;
+  }
+  __syncwarp();
+  const bool capped_by_range = sc.iter_cap > 0x7ff00000LL;
+
+  while (true) {
+    if (E.R == 0 && E.Wp + E.Wf == 0) {
+      if (E.ingest >= E.n_req) break;  // fully drained
+      const double t = P.r_arr[E.rb + E.ingest];
+      E.clock = E.clock < t ? t : E.clock;  // std::max(clock_, arrival)
+    }
+    // ingest arrivals <= clock (engine.cpp:88-92)
+    while (E.ingest < E.n_req) {
+      const int i = E.ingest + lane;
+      const bool ok = i < E.n_req && P.r_arr[E.rb + i] <= E.clock;
+      const unsigned b = __ballot_sync(kFull, ok);
+      const int n = (b == kFull) ? 32 : __ffs(~b) - 1;
+      if (lane < n) {
+        const int a = P.r_adp[E.rb + i];
+        const bool over = static_cast<int64_t>(P.r_in[E.rb + i]) + 1 > E.cap;
+        E.fq[E.Wf + lane] = make_int2(i, a | (over ? kOverBit : 0));
+      }
+      E.Wf += n;
+      E.ingest += n;
+      E.sum_a += n;
+      if (n < 32) break;
+    }
+    __syncwarp();
+    if (E.R > 0 && E.iter >= E.min_fin) E.retire(P);
+    if (!E.alloc(P)) break;
+    const int r_before = E.R;
+    E.admit(P);
+    __syncwarp();
+    if (E.R == 0) {
+      if (E.Wp + E.Wf != 0) {
+        E.fail(LT_ERR_INTERNAL, LT_K_ADMISSION_STUCK, 0, 0);
+        break;
+      }
+      continue;
+    }
+    double loads = 0.0;
+    int nl = 0;
+    if (!E.ensure_loaded(P, &loads, &nl)) break;
+    E.loads_n += nl;
+    // lat_step (estimators.cpp:110-139), no contraction (--fmad=false).
+    const int W = E.Wp + E.Wf;
+    const int A = __reduce_add_sync(kFull, __popc(E.claimed_w));
+    const double rr = static_cast<double>(E.R), ww = static_cast<double>(W);
+    const double ratio_raw = static_cast<double>(E.G) / static_cast<double>(E.N);
+    const double ratio = (1.0 < ratio_raw) ? 1.0 : ratio_raw;
+    const double v = P.k1 * rr + P.k2 * ww + P.k3 * ww * ratio;
+    const double sched = (v < 0.0) ? 0.0 : v;
+    const double model = P.k4 * rr + P.k5;
+    const double adapters = (A == 0) ? 1.0 : P.k6 * static_cast<double>(A) + P.k7;
+    const double lat = sched + loads + model * adapters;
+    const double emit = E.clock + lat;
+    // first tokens of this iteration's fresh admissions (engine.cpp:131)
+    for (int i = r_before + lane; i < E.R; i += 32) {
+      const int4 e = E.run[i];
+      if (e.z & kFreshBit) P.r_first[E.rb + e.x] = emit;
+    }
+    E.tok_tot += E.R;
+    if (emit <= E.duration) E.tok_win += E.R;
+    E.sum_r += E.R;
+    if (P.want_digest) {
+      E.digest = fold64(E.digest, static_cast<uint32_t>(E.R) | (static_cast<uint64_t>(static_cast<uint32_t>(W)) << 32));
+      E.digest = fold64(E.digest, static_cast<uint32_t>(A) | (static_cast<uint64_t>(static_cast<uint32_t>(nl)) << 32));
+      E.digest = fold64(E.digest, static_cast<uint64_t>(__double_as_longlong(lat)));
+    }
+    E.clock = emit;
+    ++E.iter;
+    if (E.iter >= E.iter_cap) {
+      if (capped_by_range) {
+        E.fail(LT_ERR_UNSUPPORTED, LT_K_ITERATION_RANGE, E.iter, 0);
+      } else {
+        E.truncated = 1;
+      }
+      break;
+    }
+  }
+  __syncwarp();
+  // Requests still running keep their emitted tokens (truncation / error).
+  for (int i = lane; i < E.R; i += 32) {
+    const int4 e = E.run[i];
+    const int outv = P.r_out[E.rb + e.x];
+    P.r_gen[E.rb + e.x] = outv - (e.y - E.iter);
+    P.r_last[E.rb + e.x] = E.clock;
+  }
+  __syncwarp();
+
+  o.status = E.status;
+  o.status_kind = E.status_kind;
+  o.status_a = E.status_a;
+  o.status_b = E.status_b;
+  o.iterations = E.iter;
+  o.final_clock_s = E.clock;
+  o.truncated = E.truncated;
+  o.preemptions = E.preempts;
+  o.load_events = E.loads_n;
+  o.tokens_in_window = E.tok_win;
+  o.tokens_total = E.tok_tot;
+  o.digest = P.want_digest ? E.digest : 0;
+  o.sum_running = E.sum_r;
+  o.sum_visited = E.sum_v;
+  o.sum_arrivals = E.sum_a;
+  o.sum_moves = E.sum_m;
+
+  // K2: compute_metrics (metrics.cpp:70-113), sums in request_id order.
+  if (E.status == LT_OK) {
+    if (E.n_req == 0) {
+      o.degenerate = 1;
+    } else {
+      const double window = E.duration;
+      double rej_demand = 0.0, ttft_sum = 0.0, itl_sum = 0.0;
+      long long nrej = 0, nfin = 0, nttft = 0, nitl = 0;
+      for (int base = 0; base < E.n_req; base += 32) {
+        const int i = base + lane;
+        const bool v = i < E.n_req;
+        int8_t ph = kWaiting;
+        double first = 0.0, arr = 0.0, last = 0.0;
+        int outv = 0, gen = 0;
+        if (v) {
+          ph = P.r_phase[E.rb + i];
+          first = P.r_first[E.rb + i];
+          arr = P.r_arr[E.rb + i];
+          last = P.r_last[E.rb + i];
+          outv = P.r_out[E.rb + i];
+          gen = (ph == kFinished) ? outv : P.r_gen[E.rb + i];
+          if (ph == kFinished) P.r_gen[E.rb + i] = outv;
+        }
+        const bool is_rej = v && ph == kRejected;
+        const bool has_first = v && first == first;
+        const bool has_itl = v && gen >= 2;
+        nrej += __popc(__ballot_sync(kFull, is_rej));
+        nfin += __popc(__ballot_sync(kFull, v && ph == kFinished));
+        nttft += __popc(__ballot_sync(kFull, has_first));
+        rej_demand = ordered_add(rej_demand, static_cast<double>(outv) / window, is_rej);
+        ttft_sum = ordered_add(ttft_sum, first - arr, has_first);
+        itl_sum = ordered_add(itl_sum, last - first, has_itl);
+        nitl += warp_sum_ll(has_itl ? gen - 1 : 0);
+      }
+      o.rejected_count = nrej;
+      o.finished_count = nfin;
+      o.throughput_tok_s = static_cast<double>(E.tok_win) / window;
+      o.ttft_mean_s = nttft ? ttft_sum / static_cast<double>(nttft) : 0.0;
+      o.itl_mean_s = nitl ? itl_sum / static_cast<double>(nitl) : 0.0;
+      const double eff_raw = sc.ideal - rej_demand;
+      const double eff = (eff_raw < 0.0) ? 0.0 : eff_raw;
+      o.starved = o.throughput_tok_s < 0.9 * eff;
+    }
+  }
+  if (lane == 0) P.out[s] = o;
+}
+
+// Persistent kernel: each warp pulls scenarios (cost-descending order) from a
+// global counter until the batch is drained.
+__global__ void __launch_bounds__(256) engine_kernel(EngineParams P) {
+  extern __shared__ __align__(16) char smem[];
+  const int warp = threadIdx.x >> 5;
+  const int slot = blockIdx.x * (blockDim.x >> 5) + warp;
+  char* mine = smem + static_cast<size_t>(warp) * P.max_adapters * 12;
+  for (;;) {
+    int k = 0;
+    if ((threadIdx.x & 31) == 0) k = atomicAdd(P.counter, 1);
+    k = __shfl_sync(kFull, k, 0);
+    if (k >= P.n_scen) break;
+    engine_run(P, P.order[k], slot, mine);
+  }
+}
+
+}  // namespace lt

@@ -1,0 +1,104 @@
+// Device-side data layout of the DT sweep (shared by all kernels).
+//
+// HBM layout (SoA, one segment per scenario, all sized by the host):
+//   scenarios  DScen[n]                     per-engine scalars
+//   adapters   DAdapter[sum N]              per scenario, sorted by adapter_id
+//   requests   arrival f64 / in / out / adapter i32   [sum n_req]   (inputs)
+//              phase u8 / gen i32 / first f64 / last f64 / preempt i32  (state + outputs)
+//   workspace  per persistent warp slot: running int4[cap], preempted int2[cap],
+//              fresh int2[cap] (cap = max n_req of the batch)
+//   smem       per warp: last_used f64[NA], run_count i32[NA] (NA = max adapters)
+#pragma once
+#include <stdint.h>
+
+#include "loratwin_gpu.h"
+
+namespace lt {
+
+constexpr int kMaxAdapters = 1024;  // 32 lanes x 32-bit adapter bitmask words
+
+enum Phase : int8_t { kWaiting = 0, kRunning = 1, kPreempted = 2, kFinished = 3, kRejected = 4 };
+
+// Queue entry (int2): x = request index within the scenario,
+// y = dense adapter index | kOverBit (demand can never fit: reject on visit).
+constexpr int kOverBit = 1 << 30;
+constexpr int kAdapterMask = (1 << 20) - 1;
+// Running entry (int4): x = request index, y = retire iteration (iteration at
+// whose start gen >= out), z = dense adapter | kFreshBit (first admission this
+// iteration), w = input + output tokens.
+constexpr int kFreshBit = 1 << 30;
+
+struct DScen {
+  int64_t req_begin;
+  int32_t n_req;
+  int32_t n_adapters;
+  int64_t adapter_begin;
+  int32_t G;
+  int32_t generated;
+  int64_t capacity;
+  double duration;
+  double ideal;
+  int64_t iter_cap;
+  int32_t status;
+  int32_t status_kind;
+  int64_t status_a;
+  int64_t status_b;
+  int32_t length_param;  // scenario-level Mean parameters (index into DLen)
+  int32_t _pad;
+};
+
+struct DAdapter {
+  int32_t id;
+  int32_t rank;
+  double rate;
+  double load_lat;  // NaN: rank missing from cpu_load_seconds (lazy ConfigError)
+  int32_t key;      // RNG table key (generated scenarios)
+  int32_t length_param;
+};
+
+struct DLen {
+  double mean_in, std_in, mean_out, std_out;
+};
+
+// One (seed, adapter_id) RNG key: E table (arrivals stream {1, id}) and Z
+// table (lengths stream {2, id}), shared by every scenario using the key.
+struct DKey {
+  uint64_t seed;
+  int64_t id;
+  double rate_max;
+  double dur_max;
+  int64_t e_off;
+  int64_t z_off;
+  int32_t cap;    // entries reserved in E (and Z)
+  int32_t e_len;  // E entries written (arrivals + the terminating draw)
+  int32_t z_len;  // Z pairs written
+  int32_t overflow;
+};
+
+struct EngineParams {
+  const DScen* scen;
+  const int32_t* order;
+  int32_t n_scen;
+  int32_t max_adapters;  // smem stride per warp
+  int32_t* counter;
+  const DAdapter* adapters;
+  const double* r_arr;
+  const int32_t* r_in;
+  const int32_t* r_out;
+  const int32_t* r_adp;
+  int8_t* r_phase;
+  int32_t* r_gen;
+  double* r_first;
+  double* r_last;
+  int32_t* r_pre;
+  int4* ws_run;
+  int2* ws_pq;
+  int2* ws_fq;
+  int64_t ws_stride;  // entries per warp slot
+  double k1, k2, k3, k4, k5, k6, k7;
+  int32_t priority;
+  int32_t want_digest;
+  lt_sim_summary* out;
+};
+
+}  // namespace lt

@@ -1,0 +1,272 @@
+"""GPU parity: the B200 path (libloratwin_gpu.so via the C-ABI) against the
+reference — the compiled reference behind oracle/_ref (live) and the golden
+vectors it produced (tests/golden, usable without /root/reference).
+
+Bar (BASELINE.json north_star): integer outputs, scheduler decisions
+(per-iteration digest) and placement decisions bit-exact; FP64 metrics within
+1e-9 relative (final clock, throughput, ideal and TTFT come out bit-identical;
+the ITL mean is a telescoped sum, SURVEY 7 hard part 8).
+"""
+import json
+import math
+import os
+import struct
+
+import numpy as np
+import pytest
+
+import paper_2508_08343_b200 as lt
+from paper_2508_08343_b200 import _abi as A
+from paper_2508_08343_b200.batch import ConditionBatch, WorkloadBatch, sim_options
+from tests import workloads as W
+from tests.conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+INT_FIELDS = ["status", "n_requests", "iterations", "truncated", "slots", "served_adapters", "starved",
+              "kv_capacity_tokens", "finished_count", "rejected_count", "preemptions", "load_events",
+              "tokens_in_window", "tokens_total", "degenerate"]
+EXACT_FP = ["final_clock_s", "throughput_tok_s", "ideal_throughput_tok_s", "ttft_mean_s"]
+ITL_RTOL = 1e-9
+
+
+def unhex(h):
+    return struct.unpack("<d", bytes.fromhex(h))[0]
+
+
+def assert_summaries(gpu, ref, digest=True, where=""):
+    assert len(gpu) == len(ref)
+    for f in INT_FIELDS + (["digest"] if digest else []):
+        bad = np.nonzero(gpu[f] != ref[f])[0]
+        assert bad.size == 0, f"{where}{f} differs at scenarios {bad[:10]}: gpu={gpu[f][bad[:5]]} ref={ref[f][bad[:5]]}"
+    ok = gpu["status"] == 0
+    for f in EXACT_FP:
+        bad = np.nonzero(ok & (gpu[f] != ref[f]))[0]
+        assert bad.size == 0, f"{where}{f} differs at {bad[:10]}: gpu={gpu[f][bad[:3]]} ref={ref[f][bad[:3]]}"
+    np.testing.assert_allclose(gpu["itl_mean_s"][ok], ref["itl_mean_s"][ok], rtol=ITL_RTOL, atol=0)
+
+
+# --- hand-traced fixture (proj/tests/fixtures/hand_traced_two_adapter.json) -----------------
+
+def test_hand_traced_fixture(dev):
+    fx = json.load(open(os.path.join(GOLDEN, "hand_traced_two_adapter.json")))
+    cfg = W.fixture_config(fx)
+    ads, reqs = W.fixture_scripted(fx)
+    res = lt.run_scripted(reqs, ads, fx["duration_s"], cfg, dev=dev)
+    exp = fx["expected"]
+    tol = fx["tolerance"]
+    assert res.iterations == exp["iterations"]
+    assert abs(res.final_clock_s - exp["final_clock_s"]) <= tol
+    assert res.load_events == len(exp["load_events"])
+    for r, e in zip(res.requests, exp["requests"]):
+        assert abs(r.first_token_time_s - r.request.arrival_time_s - e["ttft_s"]) <= tol
+        assert abs(r.completion_time_s - e["completion_s"]) <= tol
+        assert r.tokens_generated == len(e["emit_times_s"])
+        assert r.preemption_count == e["preemptions"]
+        assert r.phase == lt.Phase.Finished
+
+
+def test_hand_traced_matches_reference_bits(dev, ref):
+    fx = json.load(open(os.path.join(GOLDEN, "hand_traced_two_adapter.json")))
+    cfg = W.fixture_config(fx)
+    ads, reqs = W.fixture_scripted(fx)
+    b = WorkloadBatch.from_workloads([W.scripted_workload(ads, fx["duration_s"])], scripted=[reqs])
+    g, gs = dev.simulate_batch(b, cfg, want_states=True, want_digest=True)
+    r, rs = ref.simulate(b, cfg, sim_options(None, True), want_states=True)
+    assert_summaries(g, r)
+    for k in gs:
+        np.testing.assert_array_equal(gs[k], rs[k], err_msg=k)
+
+
+# --- scripted fuzz (AC2, acceptance.cpp:212-318): scheduler + cache + ledger --------------------
+
+@pytest.mark.parametrize("block", range(4))
+def test_scripted_fuzz(dev, ref, block):
+    for seed in range(block * 50, block * 50 + 50):
+        ads, reqs, cfg = W.scripted_fuzz(seed, n_requests=40 + seed % 50, n_adapters=1 + seed % 6,
+                                         tight=seed % 5 != 4)
+        b = WorkloadBatch.from_workloads([W.scripted_workload(ads, 6.0)], scripted=[reqs])
+        g, gs = dev.simulate_batch(b, cfg, want_states=True, want_digest=True)
+        r, rs = ref.simulate(b, cfg, sim_options(None, True), want_states=True)
+        assert_summaries(g, r, where=f"seed {seed}: ")
+        if g[0]["status"] == 0:
+            for k in gs:
+                np.testing.assert_array_equal(gs[k], rs[k], err_msg=f"seed {seed} {k}")
+        else:
+            assert dev.message(0) == ref.message(0), f"seed {seed}"
+
+
+def test_scripted_fuzz_batched(dev, ref):
+    """Many fuzz scenarios in ONE batch (different configs are not batchable,
+    so one shared tight config)."""
+    rng = np.random.default_rng(3)
+    wls, scripted = [], []
+    for s in range(300):
+        ads, reqs, _ = W.scripted_fuzz(1000 + s, n_requests=int(rng.integers(1, 120)), n_adapters=int(rng.integers(1, 9)))
+        wls.append(W.scripted_workload(ads, 5.0))
+        scripted.append(reqs)
+    cfg = W.scripted_fuzz(7)[2]
+    cfg.memory.total_kv_budget = 300
+    b = WorkloadBatch.from_workloads(wls, slots=[1 + i % 4 for i in range(len(wls))], scripted=scripted)
+    g, _ = dev.simulate_batch(b, cfg, want_digest=True)
+    r, _ = ref.simulate(b, cfg, sim_options(None, True))
+    assert_summaries(g, r)
+    for i in np.nonzero(g["status"])[0]:
+        assert dev.message(int(i)) == ref.message(int(i))
+
+
+# --- K0: generated arrivals are bit-identical --------------------------------------------------
+
+def test_generate_arrivals_golden(dev):
+    gold = json.load(open(os.path.join(GOLDEN, "arrivals.json")))
+    wls = W.arrival_cases()
+    variant = 1 if gold["libm_variant"] == "fma" else 0
+    reqs, counts = dev.generate_arrivals_batch(WorkloadBatch.from_workloads(wls), libm_variant=variant)
+    offs = np.concatenate([[0], np.cumsum(counts)])
+    for c in gold["cases"]:
+        rr = reqs[offs[c["case"]]:offs[c["case"] + 1]]
+        assert len(rr) == c["n"]
+        np.testing.assert_array_equal(rr["adapter_id"], c["adapter_id"])
+        np.testing.assert_array_equal(rr["input_tokens"], c["input_tokens"])
+        np.testing.assert_array_equal(rr["output_tokens"], c["output_tokens"])
+        assert [struct.pack("<d", x).hex() for x in rr["arrival_time_s"]] == c["arrival_hex"]
+
+
+def test_generate_arrivals_live(dev, ref):
+    wls, _ = W.c2_workloads(duration_s=120.0, stride=37)
+    b = WorkloadBatch.from_workloads(wls)
+    g, gc = dev.generate_arrivals_batch(b)
+    r, rc = ref.generate_arrivals(b, sim_options())
+    np.testing.assert_array_equal(gc, rc)
+    for f in ("request_id", "adapter_id", "input_tokens", "output_tokens", "arrival_time_s"):
+        np.testing.assert_array_equal(g[f], r[f], err_msg=f)
+
+
+# --- run_simulation + compute_metrics ------------------------------------------------------------
+
+def test_summaries_golden(dev):
+    gold = json.load(open(os.path.join(GOLDEN, "summaries.json")))["records"]
+    b, cfg = W.summary_cases()
+    g, _ = dev.simulate_batch(b, cfg, want_digest=True)
+    for i, rec in enumerate(gold):
+        for k, v in rec.items():
+            got = g[i][k]
+            if isinstance(v, str):
+                want = unhex(v)
+                if k == "itl_mean_s":
+                    assert math.isclose(got, want, rel_tol=ITL_RTOL, abs_tol=0), (i, k)
+                else:
+                    assert got == want or (math.isnan(got) and math.isnan(want)), (i, k, got, want)
+            else:
+                assert int(got) == v, (i, k, int(got), v)
+
+
+def test_summaries_live_with_states(dev, ref):
+    b, cfg = W.summary_cases()
+    g, gs = dev.simulate_batch(b, cfg, want_states=True, want_digest=True)
+    r, rs = ref.simulate(b, cfg, sim_options(None, True), want_states=True)
+    assert_summaries(g, r)
+    for k in gs:
+        np.testing.assert_array_equal(gs[k], rs[k], err_msg=k)
+
+
+def test_c2_grid_subset(dev, ref):
+    """Every 8th scenario of C2 at full 600 s duration."""
+    b = W.c2_batch(duration_s=600.0, stride=8)
+    cfg = lt.h100_like_config(1)
+    g, _ = dev.simulate_batch(b, cfg, want_digest=True)
+    r, _ = ref.simulate(b, cfg, sim_options(None, True))
+    assert_summaries(g, r)
+
+
+def test_priority_off_and_disk_source(dev, ref):
+    b, cfg = W.summary_cases()
+    cfg.loaded_adapter_priority = False
+    cfg.load.default_source = lt.LoadSource.Disk
+    g, _ = dev.simulate_batch(b, cfg, want_digest=True)
+    r, _ = ref.simulate(b, cfg, sim_options(None, True))
+    assert_summaries(g, r)
+
+
+def test_iteration_cap_truncation(dev, ref):
+    b, cfg = W.summary_cases()
+    opts = lt.SimOptions(iteration_cap_override=500)
+    g, gs = dev.simulate_batch(b, cfg, options=opts, want_states=True, want_digest=True)
+    r, rs = ref.simulate(b, cfg, sim_options(opts, True), want_states=True)
+    assert_summaries(g, r)
+    assert g["truncated"].sum() > 0
+    for k in gs:
+        np.testing.assert_array_equal(gs[k], rs[k], err_msg=k)
+
+
+def test_errors_match_reference(dev, ref):
+    """ConfigError (infeasible G, missing load rank -- lazily), SimulationError
+    (oversized sole survivor), ValidationError texts."""
+    cfg = lt.h100_like_config(8)
+    cfg.load.cpu_load_seconds.pop(32)
+    wls, slots = [], []
+    wls.append(lt.WorkloadSpec([lt.AdapterSpec(1, 32, 0.5)], lt.LengthSpec.mean(100, 10, 50, 5), 60.0, 1)); slots.append(2)
+    wls.append(lt.WorkloadSpec([lt.AdapterSpec(1, 128, 0.5)], lt.LengthSpec.mean(100, 10, 50, 5), 60.0, 1)); slots.append(64)
+    wls.append(lt.WorkloadSpec([lt.AdapterSpec(1, 8, -1.0)], lt.LengthSpec.mean(100, 10, 50, 5), 60.0, 1)); slots.append(1)
+    wls.append(lt.WorkloadSpec([lt.AdapterSpec(1, 8, 1.0), lt.AdapterSpec(1, 8, 1.0)], lt.LengthSpec.mean(100, 10, 50, 5), 60.0, 1)); slots.append(1)
+    wls.append(lt.WorkloadSpec([lt.AdapterSpec(1, 8, 1.0)], lt.LengthSpec.mean(-1, 10, 50, 5), 60.0, 1)); slots.append(1)
+    wls.append(lt.WorkloadSpec([lt.AdapterSpec(1, 16, 0.2)], lt.LengthSpec.mean(100, 10, 50, 5), 60.0, 1)); slots.append(0)
+    # a sole request whose context outgrows the KV capacity mid-generation
+    wls.append(lt.WorkloadSpec([lt.AdapterSpec(1, 8, 0.01)], lt.LengthSpec.mean(310000, 0, 20000, 0), 400.0, 3)); slots.append(1)
+    b = WorkloadBatch.from_workloads(wls, slots=slots)
+    g, _ = dev.simulate_batch(b, cfg)
+    r, _ = ref.simulate(b, cfg, sim_options())
+    np.testing.assert_array_equal(g["status"], r["status"])
+    for i in range(len(wls)):
+        assert dev.message(i) == ref.message(i), i
+    assert set(g["status"]) >= {1, 2}
+
+
+# --- sweep_optimal (K3) --------------------------------------------------------------------------
+
+def test_sweep_golden(dev):
+    gold = json.load(open(os.path.join(GOLDEN, "sweeps.json")))["records"]
+    conds, cfg, grid, dur, seed, opts = W.sweep_cases()
+    res = lt.sweep_conditions(conds, cfg, grid, dur, seed, opts, dev=dev)
+    for p, rec in zip(res, gold):
+        assert not isinstance(p, Exception) or rec["status"] != 0
+        if rec["status"] != 0:
+            assert str(p) == rec["message"]
+            continue
+        assert (p.n_star, p.g_star, int(p.all_starved), int(p.frontier_open)) == \
+            (rec["n_star"], rec["g_star"], rec["all_starved"], rec["frontier_open"])
+        assert p.max_throughput_tok_s == unhex(rec["max_throughput_hex"])
+        assert [[f.n, f.g, struct.pack("<d", f.throughput_tok_s).hex(), int(f.starved), int(f.skipped)]
+                for f in p.frontier] == rec["frontier"]
+
+
+@pytest.mark.parametrize("g_mode", [lt.GMode.Geometric, lt.GMode.Explicit])
+def test_sweep_live(dev, ref, g_mode):
+    conds = lt.enumerate_conditions(W.PAPER_RATES[:6], [8, 16, 32], lt.LengthSpec.mean(250, 50, 231, 50),
+                                    triple_size=3, condition_stride=23)
+    grid = lt.SweepGrid(n_values=[1, 2, 4, 8, 16, 32, 64, 128], g_mode=g_mode, g_values=[2, 4, 8, 16, 32, 64])
+    cfg = lt.h100_like_config(1)
+    opts = lt.SweepOptions(early_exit=True, early_exit_k=3)
+    cb = ConditionBatch.from_conditions(conds)
+    gp, gf = dev.sweep_batch(cb, cfg, grid, 120.0, 5, opts)
+    rp, rf = ref.sweep(cb, cfg, grid, 120.0, 5, opts, sim_options())
+    for f in ("status", "n_star", "g_star", "all_starved", "frontier_open", "frontier_count",
+              "max_throughput_tok_s"):
+        np.testing.assert_array_equal(gp[f], rp[f], err_msg=f)
+    for i in range(len(conds)):
+        n = int(gp[i]["frontier_count"])
+        if gp[i]["status"] == 0:
+            np.testing.assert_array_equal(gf[i][:n], rf[i][:n])
+        else:
+            assert dev.message(i) == ref.message(i)
+
+
+def test_plan_rerun_is_deterministic(dev):
+    b = W.c2_batch(duration_s=120.0, stride=16)
+    plan = dev.plan(b, lt.h100_like_config(1), want_digest=True)
+    plan.run()
+    a = plan.results()
+    plan.run()
+    c = plan.results()
+    plan.close()
+    np.testing.assert_array_equal(a, c)

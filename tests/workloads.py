@@ -1,0 +1,178 @@
+"""Workload builders shared by the tests, tools/make_golden.py and bench.py.
+
+The BASELINE.md configs (C1-C5) are built exactly as SURVEY.md 8(d) specifies;
+the *_cases helpers are smaller seeded sets used for parity.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import paper_2508_08343_b200 as lt
+from paper_2508_08343_b200 import _abi as A
+from paper_2508_08343_b200.batch import WorkloadBatch
+
+PAPER_RATES = [3.2, 1.6, 0.8, 0.4, 0.1, 0.05, 0.025, 0.0125, 0.00625, 0.003125]
+
+
+def fixture_config(fx) -> lt.ServerConfig:
+    """ServerConfig of a reference JSON fixture (json_io.cpp:188-235 field names)."""
+    c = fx["config"]
+    e = c["estimators"]
+    mem = e["memory"]
+    return lt.ServerConfig(
+        slots=c["slots"], loaded_adapter_priority=c.get("loaded_adapter_priority", True),
+        iteration_cap=c.get("iteration_cap", 100_000_000), ideal_includes_input=c.get("ideal_includes_input", False),
+        latency=lt.LatencyCoefficients(**e["latency"]),
+        memory=lt.MemoryModel(total_kv_budget=mem["total_kv_budget"], kv_bytes_per_token=mem.get("kv_bytes_per_token", 0.0),
+                              slot_cost_table={int(k): v for k, v in mem.get("slot_cost_tokens", {}).items()},
+                              slot_cost_base_rank8=mem.get("slot_cost_base_rank8")),
+        load=lt.LoadLatencyTable(cpu_load_seconds={int(k): v for k, v in e["load"]["cpu_load_seconds"].items()},
+                                 disk_multiplier=e["load"].get("disk_multiplier", 1.7),
+                                 default_source=lt.LoadSource.Disk if e["load"].get("source") == "disk" else lt.LoadSource.Cpu))
+
+
+def fixture_scripted(fx):
+    ads = [lt.AdapterSpec(a["adapter_id"], a["rank"], 1.0) for a in fx["adapters"]]
+    reqs = [lt.Request(r["request_id"], r["adapter_id"], r["arrival_time_s"], r["input_tokens"], r["output_tokens"])
+            for r in fx["requests"]]
+    return ads, reqs
+
+
+def scripted_workload(adapters, duration_s):
+    w = lt.WorkloadSpec(adapters=list(adapters), duration_s=duration_s)
+    w.lengths = lt.LengthSpec.mean(1.0, 0.0, 1.0, 0.0)
+    return w
+
+
+def arrival_cases():
+    cases = []
+    rng = np.random.default_rng(11)
+    for i in range(24):
+        n = int(rng.choice([1, 3, 8, 17, 40]))
+        ids = list(range(1, n + 1))
+        if i % 4 == 1:
+            ids = [int(x) for x in rng.permutation(np.arange(1000, 1000 + 7 * n, 7))]
+        ads = []
+        for k, aid in enumerate(ids):
+            rank = int(rng.choice([0, 8, 16, 32]))
+            rate = float(rng.choice([0.01, 0.1, 0.5, 2.0]))
+            ad = lt.AdapterSpec(aid, rank, rate)
+            if i % 5 == 2 and k % 3 == 0:
+                ad.lengths = lt.LengthSpec.mean(40.0, 30.0, 12.0, 9.0)
+            ads.append(ad)
+        lengths = [lt.LengthSpec.mean(250, 50, 231, 50), lt.LengthSpec.mean(23, 5, 27, 5),
+                   lt.LengthSpec.mean(2048, 512, 1024, 256), lt.LengthSpec.mean(3.0, 4.0, 2.0, 3.0),
+                   lt.LengthSpec.mean(64, 0, 128, 0)][i % 5]
+        seed = [0, 1, 17, 2 ** 32 + 5, 2 ** 63 + 12345, 987654321][i % 6]
+        cases.append(lt.WorkloadSpec(adapters=ads, lengths=lengths, duration_s=float(rng.choice([30.0, 90.0, 200.0])),
+                                     seed=seed))
+    return cases
+
+
+def c2_workloads(duration_s: float = 600.0, stride: int = 1):
+    """C2: N in {8..256 step 8} x rank mode {8,16,32,mixed} x r in
+    {3.2,...,0.0125}; per-adapter rate 8r/N; Mean(250,80,231,80); G=min(N,32);
+    seed 1234+i; loop order N, rank, r."""
+    rs = [3.2, 1.6, 0.8, 0.4, 0.1, 0.05, 0.025, 0.0125]
+    wls, slots = [], []
+    i = 0
+    for n in range(8, 257, 8):
+        for rank_mode in (8, 16, 32, "mixed"):
+            for r in rs:
+                if i % stride == 0:
+                    ads = []
+                    for aid in range(1, n + 1):
+                        rank = (8, 16, 32)[(aid - 1) % 3] if rank_mode == "mixed" else rank_mode
+                        ads.append(lt.AdapterSpec(aid, rank, 8.0 * r / n))
+                    wls.append(lt.WorkloadSpec(adapters=ads, lengths=lt.LengthSpec.mean(250, 80, 231, 80),
+                                               duration_s=duration_s, seed=1234 + i))
+                    slots.append(min(n, 32))
+                i += 1
+    return wls, slots
+
+
+def c2_batch(duration_s: float = 600.0, stride: int = 1) -> WorkloadBatch:
+    """Vectorised C2 packing (same content as c2_workloads)."""
+    rs = np.array([3.2, 1.6, 0.8, 0.4, 0.1, 0.05, 0.025, 0.0125])
+    ns, modes, rr, seeds = [], [], [], []
+    i = 0
+    for n in range(8, 257, 8):
+        for m in range(4):
+            for r in rs:
+                if i % stride == 0:
+                    ns.append(n)
+                    modes.append(m)
+                    rr.append(r)
+                    seeds.append(1234 + i)
+                i += 1
+    ns = np.array(ns)
+    scen = np.zeros(len(ns), dtype=A.SCENARIO_DT)
+    offs = np.concatenate([[0], np.cumsum(ns)[:-1]])
+    scen["adapter_offset"] = offs
+    scen["n_adapters"] = ns
+    scen["length_index"] = 0
+    scen["duration_s"] = duration_s
+    scen["seed"] = np.array(seeds, dtype=np.uint64)
+    scen["slots"] = np.minimum(ns, 32)
+    scen["mode"] = A.MODE_MEAN
+    scen["n_requests"] = -1
+    ads = np.zeros(int(ns.sum()), dtype=A.ADAPTER_DT)
+    ids = np.concatenate([np.arange(1, n + 1) for n in ns])
+    mode_rep = np.repeat(np.array(modes), ns)
+    ranks = np.where(mode_rep == 3, np.array([8, 16, 32])[(ids - 1) % 3], np.array([8, 16, 32, 0])[mode_rep])
+    ads["adapter_id"] = ids
+    ads["rank"] = ranks
+    ads["rate"] = np.repeat(8.0 * np.array(rr) / ns, ns)
+    ads["length_index"] = -1
+    lens = np.zeros(1, dtype=A.LENGTH_DT)
+    lens[0] = (A.MODE_MEAN, 0, 250.0, 80.0, 231.0, 80.0, 0, 0)
+    return WorkloadBatch(scen, ads, lens, np.zeros(2, dtype=np.int32), np.zeros(0, dtype=A.REQUEST_DT))
+
+
+def summary_cases():
+    """~60 seeded engines spanning idle, saturated, slot-starved, KV-starved
+    (preemption) and oversized-request regimes, on h100_like."""
+    wls, slots = [], []
+    rng = np.random.default_rng(5)
+    for i in range(60):
+        n = int(rng.choice([1, 4, 8, 24, 64, 130]))
+        rank_mode = int(rng.integers(0, 4))
+        agg = float(rng.choice([0.05, 0.4, 2.0, 6.0, 12.0]))
+        lengths = [lt.LengthSpec.mean(250, 80, 231, 80), lt.LengthSpec.mean(2048, 512, 1024, 256),
+                   lt.LengthSpec.mean(23, 5, 27, 5), lt.LengthSpec.mean(9000, 4000, 300, 100)][i % 4]
+        ads = []
+        for aid in range(1, n + 1):
+            rank = (8, 16, 32)[(aid - 1) % 3] if rank_mode == 3 else (8, 16, 32)[rank_mode]
+            if i % 7 == 3 and aid % 5 == 0:
+                rank = 0
+            ads.append(lt.AdapterSpec(aid, rank, agg / n))
+        wls.append(lt.WorkloadSpec(adapters=ads, lengths=lengths, duration_s=float(rng.choice([60.0, 180.0])),
+                                   seed=int(rng.integers(0, 2 ** 40))))
+        slots.append(int(min(n, rng.choice([1, 2, 8, 32]))))
+    return WorkloadBatch.from_workloads(wls, slots=slots), lt.h100_like_config(8)
+
+
+def sweep_cases():
+    conds = lt.enumerate_conditions([3.2, 0.4, 0.05, 0.0125], [8, 16, 32], lt.LengthSpec.mean(250, 50, 231, 50),
+                                    triple_size=3, condition_stride=9)
+    grid = lt.SweepGrid(n_values=[1, 2, 4, 8, 16, 32, 64], g_mode=lt.GMode.Geometric)
+    return conds, lt.h100_like_config(1), grid, 120.0, 5, lt.SweepOptions(early_exit=True, early_exit_k=2)
+
+
+def scripted_fuzz(seed: int, n_requests: int = 60, n_adapters: int = 5, tight: bool = True):
+    """AC2-style randomized scripted scenario (acceptance.cpp:212-318)."""
+    rng = np.random.default_rng(seed)
+    ads = [lt.AdapterSpec(k + 1, int(rng.choice([0, 8, 16])), 1.0) for k in range(n_adapters)]
+    t = np.sort(rng.uniform(0.0, 8.0, size=n_requests))
+    if seed % 3 == 0:
+        t = np.round(t, 1)  # ties in arrival time
+    reqs = [lt.Request(i, int(rng.integers(1, n_adapters + 1)), float(t[i]), int(rng.integers(1, 40)),
+                       int(rng.integers(1, 30))) for i in range(n_requests)]
+    cfg = lt.ServerConfig(
+        slots=int(rng.integers(1, 4)),
+        latency=lt.LatencyCoefficients(1e-3, 2e-4, 5e-4, 2e-3, 0.02, 0.01, 1.1),
+        memory=lt.MemoryModel(total_kv_budget=int(rng.integers(150, 600)) if tight else 100000,
+                              slot_cost_table={8: 10, 16: 20}),
+        load=lt.LoadLatencyTable(cpu_load_seconds={8: 0.05, 16: 0.09}),
+        loaded_adapter_priority=bool(seed % 2 == 0))
+    return ads, reqs, cfg
