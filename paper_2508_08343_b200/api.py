@@ -23,7 +23,7 @@ from .types import (AdapterSpec, Condition, DeviceError, ERROR_CLASSES, Frontier
                     ServerConfig, SimOptions, SimulationResult, SweepGrid, SweepOptions, WorkloadSpec)
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libloratwin_gpu.so")
+LIB_PATH = os.environ.get("LT_GPU_LIB") or os.path.join(PKG_DIR, "lib", "libloratwin_gpu.so")
 
 _lib: Optional[A.Lib] = None
 _devices = {}

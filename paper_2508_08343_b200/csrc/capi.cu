@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -42,6 +43,21 @@ struct CudaError {
     if (err_ != cudaSuccess)                                                               \
       throw CudaError{std::string(#call) + ": " + cudaGetErrorString(err_)};               \
   } while (0)
+
+// LT_SYNC_DEBUG=1: synchronise after every launch and name the failing kernel.
+bool sync_debug() {
+  static const bool on = [] {
+    const char* v = std::getenv("LT_SYNC_DEBUG");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+void after_launch(const char* name, cudaStream_t st) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && sync_debug()) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) throw CudaError{std::string(name) + ": " + cudaGetErrorString(e)};
+}
 
 void set_status(lt_status* st, int32_t code, int32_t kind, int64_t index, int64_t a, int64_t b,
                 const std::string& msg) {
@@ -568,7 +584,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
         tables_kernel<true><<<(nk + 127) / 128, 128, 0, st>>>(P.keys.p, nk, P.E.p, P.Z.p);
       else
         tables_kernel<false><<<(nk + 127) / 128, 128, 0, st>>>(P.keys.p, nk, P.E.p, P.Z.p);
-      LT_CUDA(cudaGetLastError());
+      after_launch("tables_kernel", st);
       ++P.launches_prep;
     }
     std::vector<DKey> back(pr.keys.size());
@@ -613,7 +629,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     count_kernel<<<static_cast<unsigned>((n_pairs + 255) / 256), 256, 0, st>>>(
         P.scen.p, d_pair_scen.p, d_pair_adp.p, n_pairs, P.adapters.p, P.keys.p, P.E.p, d_adp_count.p,
         d_scen_count.p, d_overflow.p);
-    LT_CUDA(cudaGetLastError());
+    after_launch("count_kernel", st);
     ++P.launches_prep;
     std::vector<unsigned long long> counts(P.n_scen);
     int32_t ovf = 0;
@@ -686,7 +702,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     merge_kernel<<<static_cast<unsigned>((P.n_scen + wpb - 1) / wpb), wpb * 32, smem, st>>>(
         P.scen.p, static_cast<int>(P.n_scen), P.adapters.p, P.keys.p, P.lens.p, P.E.p, P.Z.p,
         d_pair_begin.p, d_adp_count.p, P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p, P.max_adapters);
-    LT_CUDA(cudaGetLastError());
+    after_launch("merge_kernel", st);
     ++P.launches_prep;
   }
   cudaEventRecord(ctx->ev[3], st);
@@ -762,7 +778,7 @@ void run_plan(lt_plan& P) {
   cudaEventRecord(ctx->ev[4], st);
   if (P.n_scen > 0) {
     engine_kernel<<<P.grid, P.block, P.smem, st>>>(E);
-    LT_CUDA(cudaGetLastError());
+    after_launch("engine_kernel", st);
   }
   cudaEventRecord(ctx->ev[5], st);
 }
@@ -1245,7 +1261,7 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
       sweep_reduce_kernel<<<static_cast<unsigned>((n_cond + 127) / 128), 128, 0, st>>>(
           static_cast<int>(n_cond), d_rows.p, static_cast<int>(rows.size()), d_g.p, per_cond, d_base.p,
           plan->out.p, options->early_exit, options->early_exit_k, max_frontier, d_out.p, d_front.p);
-      LT_CUDA(cudaGetLastError());
+      after_launch("sweep_reduce_kernel", st);
     }
     cudaEventRecord(ctx->ev[6], st);
     if (n_cond > 0) {

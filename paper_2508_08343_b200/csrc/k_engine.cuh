@@ -85,6 +85,7 @@ __device__ __forceinline__ int lru_victim(uint32_t cand, uint32_t prev_needed, d
       best_a = a;
     }
   }
+  __syncwarp();
   for (int o = 16; o > 0; o >>= 1) {
     const double ob = __shfl_xor_sync(kFull, best, o);
     const int oa = __shfl_xor_sync(kFull, best_a, o);
@@ -148,7 +149,9 @@ struct WarpEngine {
   // SlotPlan::can_claim (kv_scheduler.cpp:68-72), warp-uniform a.
   __device__ __forceinline__ bool can_claim(int a) const {
     const uint32_t pool = resident_w & ~claimed_w & ~evicted_w;
-    if (mask_bit(claimed_w, a) || mask_bit(pool, a)) return true;
+    const bool in_claimed = mask_bit(claimed_w, a);
+    const bool in_pool = mask_bit(pool, a);
+    if (in_claimed || in_pool) return true;
     if (free_slots > 0) return true;
     return __any_sync(kFull, pool != 0);
   }
@@ -197,6 +200,7 @@ struct WarpEngine {
           zero = atomicSub(&run_cnt[a], 1) == 1;
         }
         nfin += fin;
+        __syncwarp();
         unsigned zm = __ballot_sync(kFull, zero);
         while (zm) {
           const int src = __ffs(zm) - 1;
@@ -311,8 +315,11 @@ struct WarpEngine {
       if (v) e = q[i];
       const int a = e.y & kAdapterMask;
       const bool over = v && (e.y & kOverBit);
-      const bool sf = v && mask_bit(slotful_w, a);
-      const bool kb = sf && mask_bit(blocked_w, a);
+      // every lane must execute the shuffles (no short-circuit around warp intrinsics)
+      const bool sf_bit = mask_bit(slotful_w, a);
+      const bool kb_bit = mask_bit(blocked_w, a);
+      const bool sf = v && sf_bit;
+      const bool kb = sf && kb_bit;
       const unsigned vm = __ballot_sync(kFull, v);
       const unsigned rejm = __ballot_sync(kFull, over);
       const unsigned kbm = __ballot_sync(kFull, v && !over && kb);
@@ -326,7 +333,7 @@ struct WarpEngine {
         gen = is_pq ? P.r_gen[rb + e.x] : 0;
         demand = static_cast<int64_t>(P.r_in[rb + e.x]) + gen + 1;
       }
-      const unsigned same = __match_any_sync(kFull, v ? a : -1);
+      __syncwarp();
       const unsigned sfm = __ballot_sync(kFull, sf);
       unsigned admitted = 0;
       while (cand) {
@@ -335,7 +342,8 @@ struct WarpEngine {
         const bool sfc = (sfm >> c) & 1u;
         if (sfc && !can_claim(ac)) {
           mask_set(blocked_w, ac, lane);
-          cand &= ~__shfl_sync(kFull, same, c);
+          // every later entry of this adapter is now a known-blocked keep
+          cand &= ~__ballot_sync(kFull, v && a == ac);
           if (!P.priority) {
             stop = c;
             break;
@@ -367,6 +375,7 @@ struct WarpEngine {
         min_fin = min(min_fin, fin);
       }
       if ((rejected >> lane) & 1u) P.r_phase[rb + e.x] = kRejected;
+      __syncwarp();
       const int na = __popc(admitted);
       R += na;
       sum_m += na;
@@ -512,6 +521,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     E.last_used[a] = 0.0;
     E.run_cnt[a] = 0;
   }
+  __syncwarp();
   for (int b = 0; b < 32; ++b) {
     const int a = lane * 32 + b;
     if (a < E.N && P.adapters[E.ab + a].rank > 0) E.slotful_w |= 1u << b;
@@ -520,6 +530,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   const bool capped_by_range = sc.iter_cap > 0x7ff00000LL;
 
   while (true) {
+    __syncwarp();
     if (E.R == 0 && E.Wp + E.Wf == 0) {
       if (E.ingest >= E.n_req) break;  // fully drained
       const double t = P.r_arr[E.rb + E.ingest];
@@ -528,7 +539,9 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     // ingest arrivals <= clock (engine.cpp:88-92)
     while (E.ingest < E.n_req) {
       const int i = E.ingest + lane;
-      const bool ok = i < E.n_req && P.r_arr[E.rb + i] <= E.clock;
+      const int ic = i < E.n_req ? i : E.n_req - 1;  // clamped: no divergent load before the vote
+      const double ta = P.r_arr[E.rb + ic];
+      const bool ok = (i < E.n_req) & (ta <= E.clock);
       const unsigned b = __ballot_sync(kFull, ok);
       const int n = (b == kFull) ? 32 : __ffs(~b) - 1;
       if (lane < n) {
@@ -575,6 +588,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
       const int4 e = E.run[i];
       if (e.z & kFreshBit) P.r_first[E.rb + e.x] = emit;
     }
+    __syncwarp();
     E.tok_tot += E.R;
     if (emit <= E.duration) E.tok_win += E.R;
     E.sum_r += E.R;
@@ -644,6 +658,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
           gen = (ph == kFinished) ? outv : P.r_gen[E.rb + i];
           if (ph == kFinished) P.r_gen[E.rb + i] = outv;
         }
+        __syncwarp();
         const bool is_rej = v && ph == kRejected;
         const bool has_first = v && first == first;
         const bool has_itl = v && gen >= 2;

@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(256) merge_kernel(const DScen* scen, int n_sce
       head_t[ba] = (nj < adp_count[pb + ba]) ? bt + E[key.e_off + nj] / ad.rate : INFINITY;
       local_best(&mt, &ma);
     }
+    __syncwarp();
   }
 }
 
