@@ -295,6 +295,7 @@ typedef struct lt_ctx lt_ctx;
 /* Timing of the last call, from CUDA events on the context's stream. */
 typedef struct lt_timing {
   double h2d_ms, tables_ms, merge_ms, engine_ms, reduce_ms, d2h_ms, total_ms;
+  double run_ms; /* whole device pipeline of the last run (K0 tables .. engine) */
   int64_t h2d_bytes, d2h_bytes;
   int64_t engine_launches; /* kernels this library launched in the call */
   int64_t algorithmic_bytes; /* B_iter summed over the engine launches */
@@ -348,6 +349,9 @@ int32_t lt_plan_run(lt_plan* plan, lt_status* status); /* asynchronous on lt_str
 int32_t lt_plan_results(lt_plan* plan, lt_sim_summary* out, lt_request_states* states,
                         lt_status* status);
 void lt_plan_destroy(lt_plan* plan);
+/* Device address of the plan's lt_sim_summary array (for device-side
+ * collectives, e.g. an NCCL all-gather of per-scenario records). */
+int32_t lt_plan_summaries_device(lt_plan* plan, void** ptr, int64_t* bytes);
 
 #ifdef __cplusplus
 }

@@ -137,7 +137,7 @@ class lt_placement(C.Structure):
 class lt_timing(C.Structure):
     _fields_ = [("h2d_ms", C.c_double), ("tables_ms", C.c_double), ("merge_ms", C.c_double),
                 ("engine_ms", C.c_double), ("reduce_ms", C.c_double), ("d2h_ms", C.c_double),
-                ("total_ms", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("total_ms", C.c_double), ("run_ms", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("engine_launches", C.c_int64), ("algorithmic_bytes", C.c_int64)]
 
 
@@ -189,6 +189,7 @@ SIGNATURES = {
     "plan_run": (C.c_int32, [C.c_void_p, C.POINTER(lt_status)]),
     "plan_results": (C.c_int32, [C.c_void_p, C.c_void_p, C.POINTER(lt_request_states), C.POINTER(lt_status)]),
     "plan_destroy": (None, [C.c_void_p]),
+    "plan_summaries_device": (C.c_int32, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
 }
 
 # Symbols the oracle libraries must export (same meaning, other prefix).

@@ -116,6 +116,13 @@ class Plan:
             raise DeviceError(st.message.decode())
         return out[:self.n]
 
+    def device_summaries(self):
+        """(device pointer, bytes) of the lt_sim_summary array this plan writes."""
+        p = C.c_void_p()
+        n = C.c_int64()
+        self.dev.lib.plan_summaries_device(self.h, C.byref(p), C.byref(n))
+        return p.value or 0, n.value
+
     def close(self):
         if self.h:
             self.dev.lib.plan_destroy(self.h)

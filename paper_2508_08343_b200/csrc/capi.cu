@@ -9,6 +9,8 @@
 // metrics epilogue and the placement reduction run on the GPU.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -323,14 +325,24 @@ struct lt_plan {
   DBuf<int4> ws_run;
   DBuf<int2> ws_pq, ws_fq;
   DBuf<lt_sim_summary> out;
+  // re-run state (lt_plan_run recomputes K0 tables, counts, offsets, merge)
+  DBuf<int32_t> pair_scen, pair_adp, adp_count, overflow;
+  DBuf<int64_t> pair_begin;
+  DBuf<unsigned long long> scen_count, base_count, scen_off;
+  DBuf<char> scan_tmp;
+  size_t scan_tmp_bytes = 0;
+  int64_t n_pairs = 0;
+  int n_keys = 0;
+  bool fresh = true;
   int64_t ws_stride = 0;
   int grid = 0;
   int block = 256;
   size_t smem = 0;
   int want_digest = 0;
-  double tables_ms = 0, merge_ms = 0, h2d_ms = 0;
+  double tables_ms = 0, h2d_ms = 0;
   int64_t h2d_bytes = 0;
   int64_t launches_prep = 0;
+  int64_t launches_run = 0;
 };
 
 namespace {
@@ -571,8 +583,6 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     k.z_off = e_total;
     e_total += k.cap;
   }
-  std::vector<int64_t> scen_begin(P.n_scen, 0);
-  std::vector<int32_t> adp_count;
   for (int attempt = 0;; ++attempt) {
     P.keys.upload(pr.keys, st);
     P.E.alloc(std::max<int64_t>(e_total, 1));
@@ -609,38 +619,48 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     }
   }
   cudaEventRecord(ctx->ev[1], st);
-  // count arrivals per (scenario, adapter)
+  // count arrivals per (scenario, adapter): sizes the request arrays
   const int64_t n_pairs = static_cast<int64_t>(pr.pair_scen.size());
+  P.n_pairs = n_pairs;
+  P.n_keys = static_cast<int>(pr.keys.size());
   P.scen.upload(P.h_scen, st);
   P.adapters.upload(pr.adapters, st);
   P.lens.upload(pr.lens, st);
   P.h2d_bytes += P.h_scen.size() * sizeof(DScen) + pr.adapters.size() * sizeof(DAdapter);
-  DBuf<int32_t> d_pair_scen, d_pair_adp, d_adp_count, d_overflow;
-  DBuf<int64_t> d_pair_begin;
-  DBuf<unsigned long long> d_scen_count;
+  P.scen_count.alloc(std::max<int64_t>(P.n_scen, 1));
+  P.scen_off.alloc(std::max<int64_t>(P.n_scen, 1));
+  P.overflow.alloc(1);
+  {
+    std::vector<unsigned long long> base(std::max<int64_t>(P.n_scen, 1), 0ULL);
+    for (int64_t i = 0; i < P.n_scen; ++i)
+      if (!P.h_scen[i].generated && P.h_scen[i].status == LT_OK) base[i] = P.h_scen[i].n_req;
+    P.base_count.upload(base, st);
+  }
   if (n_pairs > 0) {
-    d_pair_scen.upload(pr.pair_scen, st);
-    d_pair_adp.upload(pr.pair_adp, st);
-    d_adp_count.alloc(n_pairs);
-    d_scen_count.alloc(P.n_scen);
-    d_overflow.alloc(1);
-    LT_CUDA(cudaMemsetAsync(d_scen_count.p, 0, P.n_scen * sizeof(unsigned long long), st));
-    LT_CUDA(cudaMemsetAsync(d_overflow.p, 0, sizeof(int32_t), st));
+    P.pair_scen.upload(pr.pair_scen, st);
+    P.pair_adp.upload(pr.pair_adp, st);
+    P.pair_begin.upload(pr.pair_begin, st);
+    P.adp_count.alloc(n_pairs);
+    LT_CUDA(cudaMemsetAsync(P.scen_count.p, 0, P.n_scen * sizeof(unsigned long long), st));
+    LT_CUDA(cudaMemsetAsync(P.overflow.p, 0, sizeof(int32_t), st));
     count_kernel<<<static_cast<unsigned>((n_pairs + 255) / 256), 256, 0, st>>>(
-        P.scen.p, d_pair_scen.p, d_pair_adp.p, n_pairs, P.adapters.p, P.keys.p, P.E.p, d_adp_count.p,
-        d_scen_count.p, d_overflow.p);
+        P.scen.p, P.pair_scen.p, P.pair_adp.p, n_pairs, P.adapters.p, P.keys.p, P.E.p, P.adp_count.p,
+        P.scen_count.p, P.overflow.p);
     after_launch("count_kernel", st);
     ++P.launches_prep;
     std::vector<unsigned long long> counts(P.n_scen);
     int32_t ovf = 0;
-    LT_CUDA(cudaMemcpyAsync(counts.data(), d_scen_count.p, P.n_scen * sizeof(unsigned long long),
+    LT_CUDA(cudaMemcpyAsync(counts.data(), P.scen_count.p, P.n_scen * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, st));
-    LT_CUDA(cudaMemcpyAsync(&ovf, d_overflow.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaMemcpyAsync(&ovf, P.overflow.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     LT_CUDA(cudaStreamSynchronize(st));
     if (ovf) throw CudaError{"internal: RNG table shorter than an arrival stream"};
     for (int64_t i = 0; i < P.n_scen; ++i)
       if (P.h_scen[i].generated && P.h_scen[i].status == LT_OK) P.h_scen[i].n_req = static_cast<int32_t>(counts[i]);
   }
+  LT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, P.scan_tmp_bytes, P.scen_count.p, P.scen_off.p,
+                                        static_cast<int>(std::max<int64_t>(P.n_scen, 1)), st));
+  P.scan_tmp.alloc(std::max<size_t>(P.scan_tmp_bytes, 1));
   int64_t off = 0;
   for (int64_t i = 0; i < P.n_scen; ++i) {
     P.h_scen[i].req_begin = off;
@@ -692,20 +712,8 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     P.h2d_bytes += cursor * 20;
     LT_CUDA(cudaStreamSynchronize(st));
   }
-  cudaEventRecord(ctx->ev[2], st);
-  if (n_pairs > 0) {
-    d_pair_begin.upload(pr.pair_begin, st);
-    const int wpb = 4;
-    const size_t smem = static_cast<size_t>(wpb) * P.max_adapters * 16;
-    LT_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-    merge_kernel<<<static_cast<unsigned>((P.n_scen + wpb - 1) / wpb), wpb * 32, smem, st>>>(
-        P.scen.p, static_cast<int>(P.n_scen), P.adapters.p, P.keys.p, P.lens.p, P.E.p, P.Z.p,
-        d_pair_begin.p, d_adp_count.p, P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p, P.max_adapters);
-    after_launch("merge_kernel", st);
-    ++P.launches_prep;
-  }
-  cudaEventRecord(ctx->ev[3], st);
+  LT_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(size_t(4) * P.max_adapters * 16)));
   // engine order: most expensive first
   P.h_order.resize(P.n_scen);
   for (int64_t i = 0; i < P.n_scen; ++i) P.h_order[i] = static_cast<int32_t>(i);
@@ -731,7 +739,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   P.ws_fq.alloc(slots * P.ws_stride);
   LT_CUDA(cudaStreamSynchronize(st));
   P.tables_ms = elapsed(ctx->ev[0], ctx->ev[1]);
-  P.merge_ms = elapsed(ctx->ev[2], ctx->ev[3]);
+  P.fresh = true;
   return plan.release();
 }
 
@@ -739,6 +747,50 @@ void run_plan(lt_plan& P) {
   lt_ctx* ctx = P.ctx;
   cudaStream_t st = ctx->stream;
   const int64_t nr = std::max<int64_t>(P.total_req, 1);
+  cudaEventRecord(ctx->ev[0], st);
+  // K0: RNG tables, arrival counts and request offsets are recomputed on
+  // device every run (the first run after lt_plan_simulate reuses the ones
+  // computed while sizing the buffers).
+  if (!P.fresh && P.n_keys > 0) {
+    if (P.cfg.variant)
+      tables_kernel<true><<<(P.n_keys + 127) / 128, 128, 0, st>>>(P.keys.p, P.n_keys, P.E.p, P.Z.p);
+    else
+      tables_kernel<false><<<(P.n_keys + 127) / 128, 128, 0, st>>>(P.keys.p, P.n_keys, P.E.p, P.Z.p);
+    after_launch("tables_kernel", st);
+  }
+  cudaEventRecord(ctx->ev[1], st);
+  int64_t launches = (!P.fresh && P.n_keys > 0) ? 1 : 0;
+  if (!P.fresh && P.n_scen > 0) {
+    LT_CUDA(cudaMemcpyAsync(P.scen_count.p, P.base_count.p, P.n_scen * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToDevice, st));
+    if (P.n_pairs > 0) {
+      count_kernel<<<static_cast<unsigned>((P.n_pairs + 255) / 256), 256, 0, st>>>(
+          P.scen.p, P.pair_scen.p, P.pair_adp.p, P.n_pairs, P.adapters.p, P.keys.p, P.E.p, P.adp_count.p,
+          P.scen_count.p, P.overflow.p);
+      after_launch("count_kernel", st);
+      ++launches;
+    }
+    size_t tb = P.scan_tmp_bytes;
+    LT_CUDA(cub::DeviceScan::ExclusiveSum(P.scan_tmp.p, tb, P.scen_count.p, P.scen_off.p,
+                                          static_cast<int>(P.n_scen), st));
+    set_offsets_kernel<<<static_cast<unsigned>((P.n_scen + 255) / 256), 256, 0, st>>>(
+        P.scen.p, static_cast<int>(P.n_scen), P.scen_count.p, P.scen_off.p);
+    after_launch("set_offsets_kernel", st);
+    launches += 2;
+  }
+  cudaEventRecord(ctx->ev[2], st);
+  if (P.n_pairs > 0) {
+    const int wpb = 4;
+    const size_t smem = static_cast<size_t>(wpb) * P.max_adapters * 16;
+    merge_kernel<<<static_cast<unsigned>((P.n_scen + wpb - 1) / wpb), wpb * 32, smem, st>>>(
+        P.scen.p, static_cast<int>(P.n_scen), P.adapters.p, P.keys.p, P.lens.p, P.E.p, P.Z.p,
+        P.pair_begin.p, P.adp_count.p, P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p, P.max_adapters);
+    after_launch("merge_kernel", st);
+    ++launches;
+  }
+  cudaEventRecord(ctx->ev[3], st);
+  P.fresh = false;
+  P.launches_run = launches + 1;
   LT_CUDA(cudaMemsetAsync(P.r_phase.p, 0, nr, st));
   LT_CUDA(cudaMemsetAsync(P.r_gen.p, 0, nr * sizeof(int32_t), st));
   LT_CUDA(cudaMemsetAsync(P.r_pre.p, 0, nr * sizeof(int32_t), st));
@@ -857,13 +909,14 @@ void fetch_results(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {
     }
   }
   lt_timing& t = ctx->timing;
-  t.tables_ms = P.tables_ms;
-  t.merge_ms = P.merge_ms;
+  t.tables_ms = elapsed(ctx->ev[0], ctx->ev[1]);
+  t.merge_ms = elapsed(ctx->ev[1], ctx->ev[3]);
   t.engine_ms = elapsed(ctx->ev[4], ctx->ev[5]);
   t.d2h_ms = elapsed(ctx->ev[5], ctx->ev[6]);
+  t.run_ms = elapsed(ctx->ev[0], ctx->ev[5]);
   t.d2h_bytes = d2h;
   t.h2d_bytes = P.h2d_bytes;
-  t.engine_launches = 1 + P.launches_prep;
+  t.engine_launches = P.launches_run;
   int64_t bytes = 0;
   for (int64_t i = 0; i < P.n_scen; ++i) {
     const lt_sim_summary& o = out[i];
@@ -1046,6 +1099,13 @@ int32_t lt_plan_results(lt_plan* plan, lt_sim_summary* out, lt_request_states* s
     set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
     return LT_ERR_DEVICE;
   }
+}
+
+int32_t lt_plan_summaries_device(lt_plan* plan, void** ptr, int64_t* bytes) {
+  if (!plan || !ptr || !bytes) return LT_ERR_VALIDATION;
+  *ptr = plan->out.p;
+  *bytes = plan->n_scen * static_cast<int64_t>(sizeof(lt_sim_summary));
+  return LT_OK;
 }
 
 void lt_plan_destroy(lt_plan* plan) {
@@ -1294,12 +1354,13 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
       }
     }
     lt_timing& t = ctx->timing;
-    t.tables_ms = plan->tables_ms;
-    t.merge_ms = plan->merge_ms;
+    t.tables_ms = elapsed(ctx->ev[0], ctx->ev[1]);
+    t.merge_ms = elapsed(ctx->ev[1], ctx->ev[3]);
     t.engine_ms = elapsed(ctx->ev[4], ctx->ev[5]);
     t.reduce_ms = elapsed(ctx->ev[5], ctx->ev[6]);
     t.d2h_ms = elapsed(ctx->ev[6], ctx->ev[7]);
-    t.engine_launches = plan->launches_prep + 2;
+    t.run_ms = elapsed(ctx->ev[0], ctx->ev[6]);
+    t.engine_launches = plan->launches_run + 1;
     t.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return rc;
   } catch (const CudaError& e) {

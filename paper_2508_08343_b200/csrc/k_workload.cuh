@@ -79,6 +79,15 @@ __global__ void count_kernel(const DScen* scen, const int32_t* pair_scen, const 
   atomicAdd(&scen_count[pair_scen[p]], static_cast<unsigned long long>(j));
 }
 
+// Request offsets of every scenario from the device exclusive scan.
+__global__ void set_offsets_kernel(DScen* scen, int n_scen, const unsigned long long* count,
+                                   const unsigned long long* off) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_scen) return;
+  scen[i].req_begin = static_cast<int64_t>(off[i]);
+  if (scen[i].generated && scen[i].status == LT_OK) scen[i].n_req = static_cast<int32_t>(count[i]);
+}
+
 // N-way merge of one scenario's adapter streams into request_id order.
 // Per-lane cache of the lane's best head; one warp argmin per request.
 __global__ void __launch_bounds__(256) merge_kernel(const DScen* scen, int n_scen,
