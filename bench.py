@@ -227,6 +227,7 @@ def impl_gpu(args):
         parity = {"scenarios": int(len(g)), "fields": fields, "mismatches": mism, "oracle": cpu["kind"]}
         log("cpu baseline", cpu, "parity", parity)
 
+    log(f"[{time.strftime('%X')}] building plan ({n_scen} scenarios)")
     plan = dev.plan(batch, cfg)
     stream = torch.cuda.ExternalStream(dev.stream(), device=torch.device("cuda", local))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
@@ -245,8 +246,10 @@ def impl_gpu(args):
             with torch.cuda.stream(stream):
                 dist.all_gather(gathered, mine)
 
-    for _ in range(args.warmup):
+    for i in range(args.warmup):
         step()
+        torch.cuda.synchronize()
+        log(f"[{time.strftime('%X')}] warmup {i} done: {dev.timing()['run_ms']:.1f} ms device pipeline")
     torch.cuda.synchronize()
     res = plan.results()
     iters_rank = int(res["iterations"].sum())
@@ -288,6 +291,7 @@ def impl_gpu(args):
     value = iters_all * args.steps / (total_ms / 1000.0)
     ms_per_step = total_ms / args.steps
 
+    log(f"[{time.strftime('%X')}] timed steps: {times}")
     # e2e through the public C-ABI call with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -310,6 +314,7 @@ def impl_gpu(args):
         e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": 1000 * statistics.mean(walls), "call": "lt_simulate_batch (host pinned buffers)"}
 
+    log(f"[{time.strftime('%X')}] e2e: {e2e}")
     secondary = None
     if rank == 0 and not args.no_sweeps:
         try:
@@ -361,7 +366,7 @@ def main():
     ap.add_argument("--cpu-stride", type=int, default=5)
     ap.add_argument("--ref-stride", type=int, default=9)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--sweep-conditions", type=int, default=256)
+    ap.add_argument("--sweep-conditions", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweeps", action="store_true")

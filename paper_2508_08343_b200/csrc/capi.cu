@@ -743,10 +743,10 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   return plan.release();
 }
 
-void run_plan(lt_plan& P) {
+// K0 + merge: (re)generates every request of every generated scenario.
+void prepare_requests(lt_plan& P) {
   lt_ctx* ctx = P.ctx;
   cudaStream_t st = ctx->stream;
-  const int64_t nr = std::max<int64_t>(P.total_req, 1);
   cudaEventRecord(ctx->ev[0], st);
   // K0: RNG tables, arrival counts and request offsets are recomputed on
   // device every run (the first run after lt_plan_simulate reuses the ones
@@ -791,6 +791,13 @@ void run_plan(lt_plan& P) {
   cudaEventRecord(ctx->ev[3], st);
   P.fresh = false;
   P.launches_run = launches + 1;
+}
+
+void run_plan(lt_plan& P) {
+  lt_ctx* ctx = P.ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t nr = std::max<int64_t>(P.total_req, 1);
+  prepare_requests(P);
   LT_CUDA(cudaMemsetAsync(P.r_phase.p, 0, nr, st));
   LT_CUDA(cudaMemsetAsync(P.r_gen.p, 0, nr * sizeof(int32_t), st));
   LT_CUDA(cudaMemsetAsync(P.r_pre.p, 0, nr * sizeof(int32_t), st));
@@ -1147,6 +1154,7 @@ int32_t lt_generate_arrivals_batch(lt_ctx* ctx, const lt_workload_batch* batch, 
   try {
     cudaSetDevice(ctx->device);
     plan.reset(build_plan(ctx, batch, &cfg, options));
+    prepare_requests(*plan);
     cudaStream_t st = ctx->stream;
     const int64_t n = plan->total_req;
     std::vector<double> arr(n);
@@ -1252,9 +1260,10 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
     // adapter ids 1..N with (rank, rate) = mix[(id-1) % |mix|]; every point of a
     // condition reads a prefix of the condition's n_max-adapter block.
     std::vector<lt_adapter> adapters;
-    std::vector<lt_scenario> scen;
     std::vector<int64_t> cond_base(n_cond, -1);
+    std::vector<int64_t> cond_ab(n_cond, -1);
     std::vector<HostErr> cond_err(n_cond);
+    int64_t n_points = 0;
     for (int64_t c = 0; c < n_cond; ++c) {
       const lt_condition& cd = batch->conditions[c];
       HostErr& e = cond_err[c];
@@ -1267,7 +1276,7 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
         e.set(LT_ERR_VALIDATION, "condition.mix: must be non-empty");
         continue;
       }
-      const int64_t ab = static_cast<int64_t>(adapters.size());
+      cond_ab[c] = static_cast<int64_t>(adapters.size());
       for (int i = 0; i < n_max; ++i) {
         const lt_template& t = batch->templates[cd.mix_offset + (i % cd.mix_count)];
         lt_adapter a{};
@@ -1277,51 +1286,120 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
         a.length_index = -1;
         adapters.push_back(a);
       }
-      cond_base[c] = static_cast<int64_t>(scen.size());
-      for (const SweepRow& r : rows) {
-        for (int gi = 0; gi < r.g_count; ++gi) {
-          lt_scenario s{};
-          s.adapter_offset = ab;
-          s.n_adapters = r.n;
-          s.length_index = cd.length_index;
-          s.duration_s = duration_s;
-          s.seed = seed;
-          s.slots = g_list[r.g_offset + gi];
-          s.mode = options->mode;
-          s.n_requests = -1;
-          scen.push_back(s);
-        }
-      }
+      cond_base[c] = n_points;
+      n_points += per_cond;
     }
-    lt_workload_batch wb{};
-    wb.scenarios = scen.data();
-    wb.n_scenarios = static_cast<int64_t>(scen.size());
-    wb.adapters = adapters.data();
-    wb.n_adapters = static_cast<int64_t>(adapters.size());
-    wb.lengths = batch->lengths;
-    wb.n_lengths = batch->n_lengths;
-    wb.full_lengths = batch->full_lengths;
-    wb.n_full_pairs = batch->n_full_pairs;
+    // Rows are simulated in waves, exactly as sweep_optimal consumes them
+    // (placement.cpp:204-245): wave r holds row r of every condition that has
+    // neither stopped early nor failed, so the device simulates the same grid
+    // points as the reference. Waves are chunked by estimated work.
+    std::vector<lt_sim_summary> pts(std::max<int64_t>(n_points, 1));
+    std::vector<std::string> pt_msg(std::max<int64_t>(n_points, 1));
+    std::vector<char> active(n_cond, 0);
+    std::vector<double> best(n_cond, -1.0);
+    std::vector<int> stall(n_cond, 0);
+    for (int64_t c = 0; c < n_cond; ++c) active[c] = cond_base[c] >= 0;
     lt_sim_options so{};
     if (sim_options) so = *sim_options;
     so.want_digest = 0;
-    std::unique_ptr<lt_plan> plan(build_plan(ctx, &wb, config, &so));
-    run_plan(*plan);
+    double engine_ms = 0, tables_ms = 0, merge_ms = 0, run_ms = 0;
+    int64_t launches = 0, algo = 0;
+    const double budget = 6.0e7;  // estimated requests per device batch
+    for (size_t ni = 0; ni < rows.size(); ++ni) {
+      const SweepRow& r = rows[ni];
+      std::vector<int64_t> conds;
+      for (int64_t c = 0; c < n_cond; ++c)
+        if (active[c]) conds.push_back(c);
+      size_t ci = 0;
+      while (ci < conds.size()) {
+        std::vector<lt_scenario> scen;
+        std::vector<int64_t> pidx;
+        double est = 0.0;
+        while (ci < conds.size() && (scen.empty() || est < budget)) {
+          const int64_t c = conds[ci++];
+          const lt_condition& cd = batch->conditions[c];
+          double rate_sum = 0.0;
+          for (int i = 0; i < r.n; ++i) rate_sum += batch->templates[cd.mix_offset + (i % cd.mix_count)].rate;
+          for (int gi = 0; gi < r.g_count; ++gi) {
+            lt_scenario s{};
+            s.adapter_offset = cond_ab[c];
+            s.n_adapters = r.n;
+            s.length_index = cd.length_index;
+            s.duration_s = duration_s;
+            s.seed = seed;
+            s.slots = g_list[r.g_offset + gi];
+            s.mode = options->mode;
+            s.n_requests = -1;
+            scen.push_back(s);
+            pidx.push_back(cond_base[c] + r.point_offset + gi);
+            est += rate_sum * duration_s;
+          }
+        }
+        lt_workload_batch wb{};
+        wb.scenarios = scen.data();
+        wb.n_scenarios = static_cast<int64_t>(scen.size());
+        wb.adapters = adapters.data();
+        wb.n_adapters = static_cast<int64_t>(adapters.size());
+        wb.lengths = batch->lengths;
+        wb.n_lengths = batch->n_lengths;
+        wb.full_lengths = batch->full_lengths;
+        wb.n_full_pairs = batch->n_full_pairs;
+        std::unique_ptr<lt_plan> plan(build_plan(ctx, &wb, config, &so));
+        run_plan(*plan);
+        std::vector<lt_sim_summary> part(scen.size());
+        fetch_results(*plan, part.data(), nullptr);
+        for (size_t k = 0; k < scen.size(); ++k) {
+          pts[pidx[k]] = part[k];
+          pt_msg[pidx[k]] = ctx->messages[k];
+        }
+        engine_ms += ctx->timing.engine_ms;
+        tables_ms += ctx->timing.tables_ms;
+        merge_ms += ctx->timing.merge_ms;
+        run_ms += ctx->timing.run_ms;
+        launches += ctx->timing.engine_launches;
+        algo += ctx->timing.algorithmic_bytes;
+      }
+      // mirror of the reduction's control flow: which conditions continue
+      for (int64_t c : conds) {
+        bool improved = false, err = false;
+        for (int gi = 0; gi < r.g_count; ++gi) {
+          const lt_sim_summary& p = pts[cond_base[c] + r.point_offset + gi];
+          if (p.status != LT_OK) err = true;
+          if (!p.starved && p.throughput_tok_s > best[c]) {
+            best[c] = p.throughput_tok_s;
+            improved = true;
+          }
+        }
+        if (err) {
+          active[c] = 0;
+          continue;
+        }
+        if (options->early_exit) {
+          stall[c] = improved ? 0 : stall[c] + 1;
+          if (stall[c] >= options->early_exit_k && ni + 1 < rows.size()) active[c] = 0;
+        }
+      }
+    }
+    ctx->messages.assign(n_cond, std::string());
     DBuf<SweepRow> d_rows;
     DBuf<int32_t> d_g;
     DBuf<int64_t> d_base;
+    DBuf<lt_sim_summary> d_pts;
     DBuf<lt_placement> d_out;
     DBuf<lt_frontier_point> d_front;
     d_rows.upload(rows, st);
     d_g.upload(g_list, st);
     d_base.upload(cond_base, st);
+    d_pts.upload(pts, st);
     d_out.alloc(std::max<int64_t>(n_cond, 1));
     d_front.alloc(std::max<int64_t>(n_cond * max_frontier, 1));
+    cudaEventRecord(ctx->ev[5], st);
     if (n_cond > 0 && !rows.empty()) {
       sweep_reduce_kernel<<<static_cast<unsigned>((n_cond + 127) / 128), 128, 0, st>>>(
           static_cast<int>(n_cond), d_rows.p, static_cast<int>(rows.size()), d_g.p, per_cond, d_base.p,
-          plan->out.p, options->early_exit, options->early_exit_k, max_frontier, d_out.p, d_front.p);
+          d_pts.p, options->early_exit, options->early_exit_k, max_frontier, d_out.p, d_front.p);
       after_launch("sweep_reduce_kernel", st);
+      ++launches;
     }
     cudaEventRecord(ctx->ev[6], st);
     if (n_cond > 0) {
@@ -1344,8 +1422,7 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
         p.status_b = cond_err[c].b;
         msg = cond_err[c].msg;
       } else if (p.status != LT_OK) {
-        const HostErr& pe = plan->errs[p.status_point];
-        msg = pe.code != LT_OK ? pe.msg : render(p.status, p.status_kind, p.status_a, p.status_b);
+        msg = pt_msg[p.status_point];
       }
       ctx->messages[c] = msg;
       if (p.status != LT_OK && rc == LT_OK) {
@@ -1354,13 +1431,14 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
       }
     }
     lt_timing& t = ctx->timing;
-    t.tables_ms = elapsed(ctx->ev[0], ctx->ev[1]);
-    t.merge_ms = elapsed(ctx->ev[1], ctx->ev[3]);
-    t.engine_ms = elapsed(ctx->ev[4], ctx->ev[5]);
+    t.tables_ms = tables_ms;
+    t.merge_ms = merge_ms;
+    t.engine_ms = engine_ms;
     t.reduce_ms = elapsed(ctx->ev[5], ctx->ev[6]);
     t.d2h_ms = elapsed(ctx->ev[6], ctx->ev[7]);
-    t.run_ms = elapsed(ctx->ev[0], ctx->ev[6]);
-    t.engine_launches = plan->launches_run + 1;
+    t.run_ms = run_ms;
+    t.engine_launches = launches;
+    t.algorithmic_bytes = algo;
     t.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return rc;
   } catch (const CudaError& e) {
