@@ -199,9 +199,10 @@ typedef struct lt_sim_summary {
   uint64_t digest; /* FNV-1a over per-iteration (R, W, A, loads, lat bits) */
   /* roofline counters: sums over iterations */
   int64_t sum_running;  /* R */
-  int64_t sum_visited;  /* waiting entries visited by admission scans */
+  int64_t sum_visited;  /* waiting entries the admission scans touched (device: events) */
   int64_t sum_arrivals; /* A */
   int64_t sum_moves;    /* admissions + finishes + preemptions */
+  int64_t device_cycles; /* SM clock cycles the engine warp spent on this scenario (0 on CPU) */
 } lt_sim_summary;
 
 /* Optional per-request final states (RequestState, kv_scheduler.hpp:30-41),

@@ -85,7 +85,8 @@ class lt_sim_summary(C.Structure):
                 ("throughput_tok_s", C.c_double), ("ideal_throughput_tok_s", C.c_double),
                 ("ttft_mean_s", C.c_double), ("itl_mean_s", C.c_double), ("degenerate", C.c_int32),
                 ("_pad", C.c_int32), ("digest", C.c_uint64), ("sum_running", C.c_int64),
-                ("sum_visited", C.c_int64), ("sum_arrivals", C.c_int64), ("sum_moves", C.c_int64)]
+                ("sum_visited", C.c_int64), ("sum_arrivals", C.c_int64), ("sum_moves", C.c_int64),
+                ("device_cycles", C.c_int64)]
 
 
 class lt_request_states(C.Structure):

@@ -323,7 +323,8 @@ struct lt_plan {
   DBuf<int32_t> r_in, r_out, r_adp, r_gen, r_pre;
   DBuf<int8_t> r_phase;
   DBuf<int4> ws_run;
-  DBuf<int2> ws_pq, ws_fq;
+  DBuf<int2> ws_pq;
+  DBuf<int32_t> ws_nxt, ws_ov;
   DBuf<lt_sim_summary> out;
   // re-run state (lt_plan_run recomputes K0 tables, counts, offsets, merge)
   DBuf<int32_t> pair_scen, pair_adp, adp_count, overflow;
@@ -723,8 +724,13 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   P.counter.alloc(1);
   P.out.alloc(std::max<int64_t>(P.n_scen, 1));
   // occupancy-sized persistent grid
-  P.block = 256;
-  P.smem = static_cast<size_t>(P.block / 32) * P.max_adapters * 12;
+  {
+    const size_t per_warp = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter;
+    int warps = 8;
+    while (warps > 1 && per_warp * warps > 200 * 1024) warps /= 2;
+    P.block = warps * 32;
+    P.smem = per_warp * warps;
+  }
   LT_CUDA(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(P.smem)));
   int per_sm = 0;
@@ -736,7 +742,8 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   const int64_t slots = int64_t(P.grid) * (P.block / 32);
   P.ws_run.alloc(slots * P.ws_stride);
   P.ws_pq.alloc(slots * P.ws_stride);
-  P.ws_fq.alloc(slots * P.ws_stride);
+  P.ws_nxt.alloc(slots * P.ws_stride);
+  P.ws_ov.alloc(slots * P.ws_stride);
   LT_CUDA(cudaStreamSynchronize(st));
   P.tables_ms = elapsed(ctx->ev[0], ctx->ev[1]);
   P.fresh = true;
@@ -822,7 +829,8 @@ void run_plan(lt_plan& P) {
   E.r_pre = P.r_pre.p;
   E.ws_run = P.ws_run.p;
   E.ws_pq = P.ws_pq.p;
-  E.ws_fq = P.ws_fq.p;
+  E.ws_nxt = P.ws_nxt.p;
+  E.ws_ov = P.ws_ov.p;
   E.ws_stride = P.ws_stride;
   E.k1 = P.cfg.raw.k1;
   E.k2 = P.cfg.raw.k2;

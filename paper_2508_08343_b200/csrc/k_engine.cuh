@@ -32,6 +32,9 @@
 namespace lt {
 
 constexpr unsigned kFull = 0xffffffffu;
+// per-warp shared memory per adapter: last_used f64 + run_cnt, q_head, q_tail,
+// q_cnt, blk_ep, aflag (i32)
+constexpr int kSmemPerAdapter = 8 + 6 * 4;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -128,9 +131,18 @@ struct WarpEngine {
   int lane = 0;
   double* last_used = nullptr;
   int32_t* run_cnt = nullptr;
+  // fresh queue = per-adapter FIFO chains in request-id order (+ oversized FIFO)
+  int32_t* q_head = nullptr;
+  int32_t* q_tail = nullptr;
+  int32_t* q_cnt = nullptr;
+  int32_t* blk_ep = nullptr;  // == epoch: adapter blocked in the current admission scan
+  int32_t* aflag = nullptr;   // bit0 slotful (rank > 0), bit1 claimed (mirror of claimed_w)
+  int32_t epoch = 0;
+  int32_t ov_head = 0, ov_tail = 0;
   int4* run = nullptr;
   int2* pq = nullptr;
-  int2* fq = nullptr;
+  int32_t* nxt = nullptr;
+  int32_t* ov = nullptr;
 
   __device__ __forceinline__ void fail(int32_t code, int32_t kind, int64_t a, int64_t b) {
     status = code;
@@ -143,7 +155,19 @@ struct WarpEngine {
 
   // An adapter left the running batch: its slot is no longer claimed.
   __device__ __forceinline__ void release_adapter(int a, bool dec_to_zero) {
-    if (dec_to_zero) mask_clear(claimed_w, a, lane);
+    if (dec_to_zero) {
+      mask_clear(claimed_w, a, lane);
+      if (lane == 0) aflag[a] &= ~2;
+    }
+  }
+
+  __device__ __forceinline__ bool pool_any() const {
+    return __any_sync(kFull, (resident_w & ~claimed_w & ~evicted_w) != 0);
+  }
+
+  __device__ __forceinline__ void block_adapter(int a) {
+    mask_set(blocked_w, a, lane);
+    if (lane == 0) blk_ep[a] = epoch;
   }
 
   // SlotPlan::can_claim (kv_scheduler.cpp:68-72), warp-uniform a.
@@ -169,6 +193,7 @@ struct WarpEngine {
       }
     }
     mask_set(claimed_w, a, lane);
+    if (lane == 0) aflag[a] |= 2;
   }
 
   // complete_finished (kv_scheduler.cpp:238-259): stable compaction of running.
@@ -341,7 +366,7 @@ struct WarpEngine {
         const int ac = __shfl_sync(kFull, a, c);
         const bool sfc = (sfm >> c) & 1u;
         if (sfc && !can_claim(ac)) {
-          mask_set(blocked_w, ac, lane);
+          block_adapter(ac);
           // every later entry of this adapter is now a known-blocked keep
           cand &= ~__ballot_sync(kFull, v && a == ac);
           if (!P.priority) {
@@ -414,9 +439,123 @@ struct WarpEngine {
     free_slots = G - resident_count;
     evicted_w = 0;
     blocked_w = 0;
+    ++epoch;
     bool go = true;
     Wp = scan(P, pq, Wp, true, &go);
-    if (go) Wf = scan(P, fq, Wf, false, &go);
+    if (go) scan_fresh(P);
+  }
+
+  // Lane-local earliest waiting fresh entry among this lane's adapters
+  // (a = lane + 32 m) that can still act in the current scan.
+  __device__ __forceinline__ void fresh_best(int* bkey, int* ba, bool mass) const {
+    int best = INT_MAX, bi = -1;
+    for (int a = lane; a < N; a += 32) {
+      if (q_cnt[a] <= 0 || blk_ep[a] == epoch) continue;
+      const int f = aflag[a];
+      if (mass && (f & 1) && !(f & 2)) continue;
+      const int h = q_head[a];
+      if (h < best) {
+        best = h;
+        bi = a;
+      }
+    }
+    *bkey = best;
+    *ba = bi;
+  }
+
+  // scan_queue over waiting_fresh (kv_scheduler.cpp:109-166), event-driven.
+  // The reference visits every waiting entry in order; here the fresh queue
+  // is kept as per-adapter FIFO chains (request-id order), and the scan jumps
+  // from one *acting* entry to the next in id order: an admission, the first
+  // entry of an adapter that must be claimed or blocked, or the entry that
+  // stops the scan. Entries of blocked adapters are kept without being
+  // touched. Once no free slot and no idle resident remain (with the
+  // loaded-adapter priority on), every unclaimed adapter is blocked for the
+  // rest of the scan, so only claimed adapters' chains are walked. Oversized
+  // entries (can never fit) sit in their own FIFO and are rejected up to the
+  // stop point, as the reference rejects them when the scan passes them.
+  __device__ __forceinline__ void scan_fresh(const EngineParams& P) {
+    bool mass = P.priority && free_slots == 0 && !pool_any();
+    int lk, la;
+    fresh_best(&lk, &la, mass);
+    int stop_id = INT_MAX;
+    for (;;) {
+      int k = lk, a = la;
+      for (int o = 16; o > 0; o >>= 1) {
+        const int ok = __shfl_xor_sync(kFull, k, o);
+        const int oa = __shfl_xor_sync(kFull, a, o);
+        if (ok < k) {
+          k = ok;
+          a = oa;
+        }
+      }
+      if (k == INT_MAX) break;
+      const int id = k;
+      ++sum_v;
+      const bool sf = aflag[a] & 1;
+      const bool cl = mask_bit(claimed_w, a);
+      if (sf && !cl && !can_claim(a)) {
+        block_adapter(a);
+        if (!P.priority) {
+          stop_id = id;
+          break;
+        }
+        __syncwarp();
+        if (lane == (a & 31)) fresh_best(&lk, &la, mass);
+        __syncwarp();
+        continue;
+      }
+      const int in = P.r_in[rb + id];
+      const int64_t demand = static_cast<int64_t>(in) + 1;
+      if (used + demand > cap) {
+        stop_id = id;  // strict FCFS on memory
+        break;
+      }
+      used += demand;
+      if (sf) claim(a);
+      const int outv = P.r_out[rb + id];
+      const int fin = iter + outv;
+      if (lane == 0) {
+        run_cnt[a] += 1;
+        run[R] = make_int4(id, fin, a | kFreshBit, in + outv);
+        P.r_phase[rb + id] = kRunning;
+        const int c = q_cnt[a] - 1;
+        q_cnt[a] = c;
+        if (c == 0) {
+          q_head[a] = -1;
+          q_tail[a] = -1;
+        } else {
+          q_head[a] = nxt[id];
+        }
+      }
+      ++R;
+      --Wf;
+      ++sum_m;
+      min_fin = min(min_fin, fin);
+      __syncwarp();
+      const bool mass2 = P.priority && free_slots == 0 && !pool_any();
+      if (mass2 != mass) {
+        mass = mass2;
+        fresh_best(&lk, &la, mass);
+      } else if (lane == (a & 31)) {
+        fresh_best(&lk, &la, mass);
+      }
+      __syncwarp();
+    }
+    // oversized entries in front of the stop point are rejected in place
+    while (ov_head < ov_tail) {
+      const int i = ov_head + lane;
+      const int id = i < ov_tail ? ov[i] : INT_MAX;
+      const bool rej = i < ov_tail && id < stop_id;
+      const unsigned m = __ballot_sync(kFull, rej);
+      if (rej) P.r_phase[rb + id] = kRejected;
+      const int n = __popc(m);  // ov is in id order: the rejected ones are a prefix
+      ov_head += n;
+      Wf -= n;
+      sum_v += n;
+      __syncwarp();
+      if (n < 32) break;
+    }
   }
 
   // SlotCache::ensure_loaded (adapter_cache.cpp:40-78) with needed = the
@@ -484,6 +623,7 @@ __device__ __forceinline__ double ordered_add(double acc, double v, bool f) {
 }
 
 __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_warp) {
+  const long long t_start = clock64();
   WarpEngine E;
   E.lane = threadIdx.x & 31;
   const int lane = E.lane;
@@ -512,14 +652,26 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   E.cap = sc.capacity;
   E.duration = sc.duration;
   E.iter_cap = static_cast<int32_t>(sc.iter_cap > 0x7ff00000LL ? 0x7ff00000LL : sc.iter_cap);
+  const int NA = P.max_adapters;
   E.last_used = reinterpret_cast<double*>(smem_warp);
-  E.run_cnt = reinterpret_cast<int32_t*>(E.last_used + P.max_adapters);
+  E.run_cnt = reinterpret_cast<int32_t*>(E.last_used + NA);
+  E.q_head = E.run_cnt + NA;
+  E.q_tail = E.q_head + NA;
+  E.q_cnt = E.q_tail + NA;
+  E.blk_ep = E.q_cnt + NA;
+  E.aflag = E.blk_ep + NA;
   E.run = P.ws_run + static_cast<int64_t>(slot) * P.ws_stride;
   E.pq = P.ws_pq + static_cast<int64_t>(slot) * P.ws_stride;
-  E.fq = P.ws_fq + static_cast<int64_t>(slot) * P.ws_stride;
+  E.nxt = P.ws_nxt + static_cast<int64_t>(slot) * P.ws_stride;
+  E.ov = P.ws_ov + static_cast<int64_t>(slot) * P.ws_stride;
   for (int a = lane; a < E.N; a += 32) {
     E.last_used[a] = 0.0;
     E.run_cnt[a] = 0;
+    E.q_head[a] = -1;
+    E.q_tail[a] = -1;
+    E.q_cnt[a] = 0;
+    E.blk_ep[a] = -1;
+    E.aflag[a] = P.adapters[E.ab + a].rank > 0 ? 1 : 0;
   }
   __syncwarp();
   for (int b = 0; b < 32; ++b) {
@@ -536,7 +688,8 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
       const double t = P.r_arr[E.rb + E.ingest];
       E.clock = E.clock < t ? t : E.clock;  // std::max(clock_, arrival)
     }
-    // ingest arrivals <= clock (engine.cpp:88-92)
+    // ingest arrivals <= clock (engine.cpp:88-92): append to the adapter's
+    // FIFO chain, or to the oversized FIFO when in + 1 > capacity.
     while (E.ingest < E.n_req) {
       const int i = E.ingest + lane;
       const int ic = i < E.n_req ? i : E.n_req - 1;  // clamped: no divergent load before the vote
@@ -544,14 +697,32 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
       const bool ok = (i < E.n_req) & (ta <= E.clock);
       const unsigned b = __ballot_sync(kFull, ok);
       const int n = (b == kFull) ? 32 : __ffs(~b) - 1;
-      if (lane < n) {
-        const int a = P.r_adp[E.rb + i];
-        const bool over = static_cast<int64_t>(P.r_in[E.rb + i]) + 1 > E.cap;
-        E.fq[E.Wf + lane] = make_int2(i, a | (over ? kOverBit : 0));
+      const int a_l = P.r_adp[E.rb + ic];
+      const bool over_l = static_cast<int64_t>(P.r_in[E.rb + ic]) + 1 > E.cap;
+      const unsigned live = (n >= 32) ? kFull : ((1u << n) - 1);
+      const unsigned overm = __ballot_sync(kFull, over_l) & live;
+      if ((overm >> lane) & 1u) E.ov[E.ov_tail + __popc(overm & lanemask_lt())] = i;
+      E.ov_tail += __popc(overm);
+      unsigned m = live & ~overm;
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int a = __shfl_sync(kFull, a_l, src);
+        if (lane == 0) {
+          const int id = E.ingest + src;
+          const int t = E.q_tail[a];
+          if (t < 0)
+            E.q_head[a] = id;
+          else
+            E.nxt[t] = id;
+          E.q_tail[a] = id;
+          E.q_cnt[a] += 1;
+        }
       }
       E.Wf += n;
       E.ingest += n;
       E.sum_a += n;
+      __syncwarp();
       if (n < 32) break;
     }
     __syncwarp();
@@ -680,6 +851,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
       o.starved = o.throughput_tok_s < 0.9 * eff;
     }
   }
+  o.device_cycles = clock64() - t_start;
   if (lane == 0) P.out[s] = o;
 }
 
@@ -689,7 +861,7 @@ __global__ void __launch_bounds__(256) engine_kernel(EngineParams P) {
   extern __shared__ __align__(16) char smem[];
   const int warp = threadIdx.x >> 5;
   const int slot = blockIdx.x * (blockDim.x >> 5) + warp;
-  char* mine = smem + static_cast<size_t>(warp) * P.max_adapters * 12;
+  char* mine = smem + static_cast<size_t>(warp) * P.max_adapters * kSmemPerAdapter;
   for (;;) {
     int k = 0;
     if ((threadIdx.x & 31) == 0) k = atomicAdd(P.counter, 1);
