@@ -203,6 +203,8 @@ typedef struct lt_sim_summary {
   int64_t sum_arrivals; /* A */
   int64_t sum_moves;    /* admissions + finishes + preemptions */
   int64_t device_cycles; /* SM clock cycles the engine warp spent on this scenario (0 on CPU) */
+  int64_t phase_cycles[6]; /* profiling builds only (-DLT_PHASE_PROF): ingest, retire, alloc,
+                              preempted-queue scan, fresh scan, load+price+emit; 0 otherwise */
 } lt_sim_summary;
 
 /* Optional per-request final states (RequestState, kv_scheduler.hpp:30-41),

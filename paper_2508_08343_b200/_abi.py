@@ -86,7 +86,7 @@ class lt_sim_summary(C.Structure):
                 ("ttft_mean_s", C.c_double), ("itl_mean_s", C.c_double), ("degenerate", C.c_int32),
                 ("_pad", C.c_int32), ("digest", C.c_uint64), ("sum_running", C.c_int64),
                 ("sum_visited", C.c_int64), ("sum_arrivals", C.c_int64), ("sum_moves", C.c_int64),
-                ("device_cycles", C.c_int64)]
+                ("device_cycles", C.c_int64), ("phase_cycles", C.c_int64 * 6)]
 
 
 class lt_request_states(C.Structure):

@@ -324,7 +324,8 @@ struct lt_plan {
   DBuf<int8_t> r_phase;
   DBuf<int4> ws_run;
   DBuf<int2> ws_pq;
-  DBuf<int32_t> ws_nxt, ws_ov;
+  DBuf<int4> ws_node;
+  DBuf<int32_t> ws_ov, ws_cmin;
   DBuf<lt_sim_summary> out;
   // re-run state (lt_plan_run recomputes K0 tables, counts, offsets, merge)
   DBuf<int32_t> pair_scen, pair_adp, adp_count, overflow;
@@ -742,7 +743,8 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   const int64_t slots = int64_t(P.grid) * (P.block / 32);
   P.ws_run.alloc(slots * P.ws_stride);
   P.ws_pq.alloc(slots * P.ws_stride);
-  P.ws_nxt.alloc(slots * P.ws_stride);
+  P.ws_node.alloc(slots * P.ws_stride);
+  P.ws_cmin.alloc(slots * (P.ws_stride / 32 + 2));
   P.ws_ov.alloc(slots * P.ws_stride);
   LT_CUDA(cudaStreamSynchronize(st));
   P.tables_ms = elapsed(ctx->ev[0], ctx->ev[1]);
@@ -829,7 +831,8 @@ void run_plan(lt_plan& P) {
   E.r_pre = P.r_pre.p;
   E.ws_run = P.ws_run.p;
   E.ws_pq = P.ws_pq.p;
-  E.ws_nxt = P.ws_nxt.p;
+  E.ws_node = P.ws_node.p;
+  E.ws_cmin = P.ws_cmin.p;
   E.ws_ov = P.ws_ov.p;
   E.ws_stride = P.ws_stride;
   E.k1 = P.cfg.raw.k1;

@@ -33,8 +33,8 @@ namespace lt {
 
 constexpr unsigned kFull = 0xffffffffu;
 // per-warp shared memory per adapter: last_used f64 + run_cnt, q_head, q_tail,
-// q_cnt, blk_ep, aflag (i32)
-constexpr int kSmemPerAdapter = 8 + 6 * 4;
+// q_cnt, act_key (i32)
+constexpr int kSmemPerAdapter = 8 + 5 * 4;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -113,7 +113,7 @@ struct WarpEngine {
   int32_t iter = 0, iter_cap = 0;
   int32_t R = 0, Wp = 0, Wf = 0, ingest = 0, n_req = 0;
   int32_t resident_count = 0, G = 1, N = 1;
-  int32_t min_fin = INT_MAX;
+  int32_t R_end = 0;  // running array length incl. tombstones (x = -1)
   int32_t waived = -1;
   int32_t status = LT_OK, status_kind = LT_K_NONE;
   int64_t status_a = 0, status_b = 0;
@@ -123,6 +123,7 @@ struct WarpEngine {
   uint64_t digest = 0xcbf29ce484222325ULL;
   // --- per-lane words of adapter masks
   uint32_t slotful_w = 0, resident_w = 0, claimed_w = 0, prev_needed_w = 0;
+  uint32_t nonempty_w = 0;  // adapters with a non-empty fresh chain
   // --- scan-local SlotPlan state
   uint32_t evicted_w = 0, blocked_w = 0;
   int32_t free_slots = 0;
@@ -135,13 +136,12 @@ struct WarpEngine {
   int32_t* q_head = nullptr;
   int32_t* q_tail = nullptr;
   int32_t* q_cnt = nullptr;
-  int32_t* blk_ep = nullptr;  // == epoch: adapter blocked in the current admission scan
-  int32_t* aflag = nullptr;   // bit0 slotful (rank > 0), bit1 claimed (mirror of claimed_w)
-  int32_t epoch = 0;
+  int32_t* act_key = nullptr;  // scan-local: chain head if the adapter can act, else INT_MAX
   int32_t ov_head = 0, ov_tail = 0;
   int4* run = nullptr;
+  int32_t* cmin = nullptr;  // per 32-entry chunk of run[]: lower bound of live retire iterations
   int2* pq = nullptr;
-  int32_t* nxt = nullptr;
+  int4* node = nullptr;  // per waiting fresh request: {in, out, next-in-chain, adapter}
   int32_t* ov = nullptr;
 
   __device__ __forceinline__ void fail(int32_t code, int32_t kind, int64_t a, int64_t b) {
@@ -155,10 +155,7 @@ struct WarpEngine {
 
   // An adapter left the running batch: its slot is no longer claimed.
   __device__ __forceinline__ void release_adapter(int a, bool dec_to_zero) {
-    if (dec_to_zero) {
-      mask_clear(claimed_w, a, lane);
-      if (lane == 0) aflag[a] &= ~2;
-    }
+    if (dec_to_zero) mask_clear(claimed_w, a, lane);
   }
 
   __device__ __forceinline__ bool pool_any() const {
@@ -167,7 +164,6 @@ struct WarpEngine {
 
   __device__ __forceinline__ void block_adapter(int a) {
     mask_set(blocked_w, a, lane);
-    if (lane == 0) blk_ep[a] = epoch;
   }
 
   // SlotPlan::can_claim (kv_scheduler.cpp:68-72), warp-uniform a.
@@ -193,28 +189,74 @@ struct WarpEngine {
       }
     }
     mask_set(claimed_w, a, lane);
-    if (lane == 0) aflag[a] |= 2;
   }
 
-  // complete_finished (kv_scheduler.cpp:238-259): stable compaction of running.
-  __device__ __forceinline__ void retire(const EngineParams& P) {
-    int w = 0;
-    int new_min = INT_MAX;
-    long long released = 0, nfin = 0;
-    for (int base = 0; base < R; base += 32) {
-      const int i = base + lane;
-      const bool v = i < R;
-      int4 e = make_int4(0, INT_MAX, 0, 0);
-      if (v) e = run[i];
-      const bool fin = v && e.y <= iter;
-      const unsigned keepm = __ballot_sync(kFull, v && !fin);
-      const unsigned finm = __ballot_sync(kFull, fin);
-      if (v && !fin) {
-        run[w + __popc(keepm & lanemask_lt())] = e;
-        new_min = min(new_min, e.y);
+  // Running set = run[0, R_end) in admission order with tombstones (x = -1)
+  // for retired entries; cmin[c] bounds the retire iteration of chunk c from
+  // below, so an iteration only touches the chunks that hold a retiree. The
+  // last entry is always live (trim), so LIFO preemption pops run[R_end-1].
+  __device__ __forceinline__ void run_append(int4 e) {
+    if (lane == 0) {
+      const int pos = R_end;
+      run[pos] = e;
+      const int c = pos >> 5;
+      cmin[c] = (pos & 31) ? min(cmin[c], e.y) : e.y;
+    }
+    ++R_end;
+    ++R;
+  }
+
+  __device__ __forceinline__ void trim() {
+    while (R_end > 0) {
+      const int lo = max(0, R_end - 32);
+      const int i = lo + lane;
+      const bool live = i < R_end && run[i].x >= 0;
+      const unsigned lm = __ballot_sync(kFull, live);
+      if (lm) {
+        R_end = lo + 32 - __clz(lm);
+        break;
       }
-      if (finm) {
-        int a = -1;
+      R_end = lo;
+    }
+  }
+
+  // Stable compaction of the live entries (amortised: only when tombstones
+  // outnumber live entries), then chunk bounds are rebuilt.
+  __device__ __forceinline__ void compact() {
+    int w = 0;
+    for (int base = 0; base < R_end; base += 32) {
+      const int i = base + lane;
+      const int4 e = (i < R_end) ? run[i] : make_int4(-1, INT_MAX, 0, 0);
+      const unsigned lm = __ballot_sync(kFull, e.x >= 0);
+      if (e.x >= 0) run[w + __popc(lm & lanemask_lt())] = e;
+      w += __popc(lm);
+    }
+    __syncwarp();
+    R_end = w;
+    for (int base = 0; base < R_end; base += 32) {
+      const int i = base + lane;
+      const int y = (i < R_end) ? run[i].y : INT_MAX;
+      const int m = warp_min_i(y);
+      if (lane == 0) cmin[base >> 5] = m;
+    }
+    __syncwarp();
+  }
+
+  // complete_finished (kv_scheduler.cpp:238-259).
+  __device__ __forceinline__ void retire(const EngineParams& P) {
+    long long released = 0, nfin = 0;
+    const int nch = (R_end + 31) >> 5;
+    for (int c0 = 0; c0 < nch; c0 += 32) {
+      const int c = c0 + lane;
+      const int cm = (c < nch) ? cmin[c] : INT_MAX;
+      unsigned due = __ballot_sync(kFull, cm <= iter);
+      while (due) {
+        const int cc = c0 + __ffs(due) - 1;
+        due &= due - 1;
+        const int i = cc * 32 + lane;
+        const int4 e = (i < R_end) ? run[i] : make_int4(-1, INT_MAX, 0, 0);
+        const bool fin = e.x >= 0 && e.y <= iter;
+        int a = 0;
         bool zero = false;
         if (fin) {
           const int idx = e.x;
@@ -223,9 +265,11 @@ struct WarpEngine {
           P.r_last[rb + idx] = clock;  // completion == the final emit (engine.cpp:134)
           a = e.z & kAdapterMask;
           zero = atomicSub(&run_cnt[a], 1) == 1;
+          run[i] = make_int4(-1, INT_MAX, 0, 0);
         }
         nfin += fin;
-        __syncwarp();
+        const int live_min = warp_min_i((e.x >= 0 && !fin) ? e.y : INT_MAX);
+        if (lane == 0) cmin[cc] = live_min;
         unsigned zm = __ballot_sync(kFull, zero);
         while (zm) {
           const int src = __ffs(zm) - 1;
@@ -233,17 +277,18 @@ struct WarpEngine {
           release_adapter(__shfl_sync(kFull, a, src), true);
         }
       }
-      w += __popc(keepm);
-      __syncwarp();
     }
+    __syncwarp();
     const long long rel = warp_sum_ll(released);
     const long long nf = warp_sum_ll(nfin);
+    if (nf == 0) return;
     used -= rel;
     finished += nf;
     sum_m += nf;
-    if (nf) waived = -1;
-    R = w;
-    min_fin = warp_min_i(new_min);
+    waived = -1;
+    R -= static_cast<int>(nf);
+    trim();
+    if (R_end - R > max(R, 32)) compact();
   }
 
   // Insert a preempted request into waiting_preempted ordered by
@@ -287,8 +332,10 @@ struct WarpEngine {
     if (R == 0) return true;
     int64_t demand = R;
     while (used + demand > cap && R > 1) {
-      const int4 e = run[R - 1];
+      const int4 e = run[R_end - 1];
       --R;
+      --R_end;
+      trim();
       const int idx = e.x;
       const int a = e.z & kAdapterMask;
       const int outv = P.r_out[rb + idx];
@@ -313,7 +360,7 @@ struct WarpEngine {
       --demand;
     }
     if (used + demand > cap) {
-      const int4 e = run[0];
+      const int4 e = run[R_end - 1];  // the sole survivor
       const int rem = e.y - iter;
       if (rem > 1 || used + demand - 1 > cap) {
         fail(LT_ERR_SIMULATION, LT_K_SOLE_SURVIVOR, e.x, 0);
@@ -390,20 +437,28 @@ struct WarpEngine {
       const unsigned processed = (stop >= 32) ? kFull : ((1u << stop) - 1);
       const unsigned rejected = rejm & processed;
       const unsigned removed = rejected | admitted;
-      if ((admitted >> lane) & 1u) {
-        const int p = R + __popc(admitted & lt_mask);
-        const int outv = P.r_out[rb + e.x];
-        const int fin = iter + (outv - gen);
-        run[p] = make_int4(e.x, fin, a | (is_pq ? 0 : kFreshBit),
-                           P.r_in[rb + e.x] + outv);
-        P.r_phase[rb + e.x] = kRunning;
-        min_fin = min(min_fin, fin);
+      {
+        int fin_l = 0, s_l = 0;
+        if ((admitted >> lane) & 1u) {
+          const int outv = P.r_out[rb + e.x];
+          fin_l = iter + (outv - gen);
+          s_l = P.r_in[rb + e.x] + outv;
+          P.r_phase[rb + e.x] = kRunning;
+        }
+        unsigned am = admitted;
+        while (am) {
+          const int src = __ffs(am) - 1;
+          am &= am - 1;
+          const int idx = __shfl_sync(kFull, e.x, src);
+          const int ad = __shfl_sync(kFull, a, src);
+          const int f = __shfl_sync(kFull, fin_l, src);
+          const int sv = __shfl_sync(kFull, s_l, src);
+          run_append(make_int4(idx, f, ad | (is_pq ? 0 : kFreshBit), sv));
+        }
       }
       if ((rejected >> lane) & 1u) P.r_phase[rb + e.x] = kRejected;
       __syncwarp();
-      const int na = __popc(admitted);
-      R += na;
-      sum_m += na;
+      sum_m += __popc(admitted);
       const unsigned keep = vm & ~removed;
       __syncwarp();
       if ((keep >> lane) & 1u) q[write + __popc(keep & lt_mask)] = e;
@@ -416,7 +471,6 @@ struct WarpEngine {
         break;
       }
     }
-    min_fin = warp_min_i(min_fin);
     if (stopped && read < W) {
       if (write < read) {
         for (int base = read; base < W; base += 32) {
@@ -439,28 +493,44 @@ struct WarpEngine {
     free_slots = G - resident_count;
     evicted_w = 0;
     blocked_w = 0;
-    ++epoch;
     bool go = true;
     Wp = scan(P, pq, Wp, true, &go);
     if (go) scan_fresh(P);
   }
 
-  // Lane-local earliest waiting fresh entry among this lane's adapters
-  // (a = lane + 32 m) that can still act in the current scan.
-  __device__ __forceinline__ void fresh_best(int* bkey, int* ba, bool mass) const {
+  // Lane-local minimum of act_key over this lane's adapters a = lane + 32 m.
+  __device__ __forceinline__ void local_best(int* bkey, int* ba) const {
     int best = INT_MAX, bi = -1;
     for (int a = lane; a < N; a += 32) {
-      if (q_cnt[a] <= 0 || blk_ep[a] == epoch) continue;
-      const int f = aflag[a];
-      if (mass && (f & 1) && !(f & 2)) continue;
-      const int h = q_head[a];
-      if (h < best) {
-        best = h;
+      const int k = act_key[a];
+      if (k < best) {
+        best = k;
         bi = a;
       }
     }
     *bkey = best;
     *ba = bi;
+  }
+
+  // act_key for every adapter (round-robin layout: lane owns a = lane + 32 m,
+  // whose mask bit is bit `lane` of word m).
+  __device__ __forceinline__ void build_act_keys(bool mass, bool only_mass_exclusion) {
+    for (int m = 0; m * 32 < N; ++m) {
+      const uint32_t wb = __shfl_sync(kFull, blocked_w, m);
+      const uint32_t ws = __shfl_sync(kFull, slotful_w, m);
+      const uint32_t wc = __shfl_sync(kFull, claimed_w, m);
+      const uint32_t wn = __shfl_sync(kFull, nonempty_w, m);
+      const int a = lane + 32 * m;
+      if (a < N) {
+        const bool excl = mass && ((ws >> lane) & 1u) && !((wc >> lane) & 1u);
+        if (only_mass_exclusion) {
+          if (excl) act_key[a] = INT_MAX;
+        } else {
+          const bool acting = ((wn >> lane) & 1u) && !((wb >> lane) & 1u) && !excl;
+          act_key[a] = acting ? q_head[a] : INT_MAX;
+        }
+      }
+    }
   }
 
   // scan_queue over waiting_fresh (kv_scheduler.cpp:109-166), event-driven.
@@ -476,8 +546,39 @@ struct WarpEngine {
   // stop point, as the reference rejects them when the scan passes them.
   __device__ __forceinline__ void scan_fresh(const EngineParams& P) {
     bool mass = P.priority && free_slots == 0 && !pool_any();
-    int lk, la;
-    fresh_best(&lk, &la, mass);
+    // Acting adapters of this scan. When at most 32 can act (always for
+    // N <= 32; and in the slot-starved steady state, where only the <= G
+    // claimed adapters act), each lane holds one of them and an event is a
+    // single warp argmin; otherwise act_key[] holds the candidate heads.
+    const uint32_t act_w = nonempty_w & ~blocked_w & ~(mass ? (slotful_w & ~claimed_w) : 0u);
+    const int cnt_w = __popc(act_w);
+    int pre = cnt_w;  // inclusive prefix over lanes
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(kFull, pre, o);
+      if (lane >= o) pre += t;
+    }
+    const int n_act = __shfl_sync(kFull, pre, 31);
+    const bool lane_mode = n_act <= 32;
+    int lk = INT_MAX, la = -1;
+    int4 my_nd = make_int4(0, 0, -1, 0);  // lane mode: node of this lane's head, prefetched
+    if (lane_mode) {
+      const int excl = pre - cnt_w;  // exclusive prefix of this lane's word
+      for (int m = 0; m * 32 < N; ++m) {
+        const uint32_t wm = __shfl_sync(kFull, act_w, m);
+        const int base = __shfl_sync(kFull, excl, m);
+        const int k = lane - base;
+        if (wm && k >= 0 && k < __popc(wm)) {
+          const int a = m * 32 + static_cast<int>(__fns(wm, 0, k + 1));
+          la = a;
+          lk = q_head[a];
+        }
+      }
+      if (lk != INT_MAX) my_nd = node[lk];
+    } else {
+      build_act_keys(mass, false);
+      __syncwarp();
+      local_best(&lk, &la);
+    }
     int stop_id = INT_MAX;
     for (;;) {
       int k = lk, a = la;
@@ -491,8 +592,19 @@ struct WarpEngine {
       }
       if (k == INT_MAX) break;
       const int id = k;
+      const bool mine = lane_mode ? (la == a) : (lane == (a & 31));  // the lane that owns a
       ++sum_v;
-      const bool sf = aflag[a] & 1;
+      int4 nd;  // {in, out, next, adapter}
+      if (lane_mode) {
+        const int src = __ffs(__ballot_sync(kFull, mine)) - 1;
+        nd.x = __shfl_sync(kFull, my_nd.x, src);
+        nd.y = __shfl_sync(kFull, my_nd.y, src);
+        nd.z = __shfl_sync(kFull, my_nd.z, src);
+        nd.w = __shfl_sync(kFull, my_nd.w, src);
+      } else {
+        nd = node[id];
+      }
+      const bool sf = mask_bit(slotful_w, a);
       const bool cl = mask_bit(claimed_w, a);
       if (sf && !cl && !can_claim(a)) {
         block_adapter(a);
@@ -500,45 +612,66 @@ struct WarpEngine {
           stop_id = id;
           break;
         }
-        __syncwarp();
-        if (lane == (a & 31)) fresh_best(&lk, &la, mass);
-        __syncwarp();
+        if (mine) {
+          if (lane_mode) {
+            lk = INT_MAX;
+          } else {
+            act_key[a] = INT_MAX;
+            local_best(&lk, &la);
+          }
+        }
         continue;
       }
-      const int in = P.r_in[rb + id];
-      const int64_t demand = static_cast<int64_t>(in) + 1;
+      const int64_t demand = static_cast<int64_t>(nd.x) + 1;
       if (used + demand > cap) {
         stop_id = id;  // strict FCFS on memory
         break;
       }
       used += demand;
       if (sf) claim(a);
-      const int outv = P.r_out[rb + id];
-      const int fin = iter + outv;
+      const int fin = iter + nd.y;
+      const int c = q_cnt[a] - 1;
+      run_append(make_int4(id, fin, a | kFreshBit, nd.x + nd.y));
       if (lane == 0) {
         run_cnt[a] += 1;
-        run[R] = make_int4(id, fin, a | kFreshBit, in + outv);
         P.r_phase[rb + id] = kRunning;
-        const int c = q_cnt[a] - 1;
         q_cnt[a] = c;
         if (c == 0) {
           q_head[a] = -1;
           q_tail[a] = -1;
         } else {
-          q_head[a] = nxt[id];
+          q_head[a] = nd.z;
         }
       }
-      ++R;
+      if (c == 0) mask_clear(nonempty_w, a, lane);
       --Wf;
       ++sum_m;
-      min_fin = min(min_fin, fin);
-      __syncwarp();
       const bool mass2 = P.priority && free_slots == 0 && !pool_any();
-      if (mass2 != mass) {
-        mass = mass2;
-        fresh_best(&lk, &la, mass);
-      } else if (lane == (a & 31)) {
-        fresh_best(&lk, &la, mass);
+      const int next_key = (c == 0) ? INT_MAX : nd.z;
+      if (lane_mode) {
+        if (mine) {
+          lk = next_key;
+          if (next_key != INT_MAX) my_nd = node[next_key];  // in flight until this lane wins again
+        }
+        if (mass2 != mass) {
+          mass = mass2;
+          // every unclaimed adapter that needs a slot is now blocked
+          const int la0 = la < 0 ? 0 : la;
+          const bool s_l = mask_bit(slotful_w, la0);  // all lanes shuffle (no short-circuit)
+          const bool c_l = mask_bit(claimed_w, la0);
+          if (la >= 0 && s_l && !c_l) lk = INT_MAX;
+        }
+      } else {
+        if (mine) act_key[a] = next_key;
+        if (mass2 != mass) {
+          mass = mass2;
+          __syncwarp();
+          build_act_keys(mass, true);
+          __syncwarp();
+          local_best(&lk, &la);
+        } else if (mine) {
+          local_best(&lk, &la);
+        }
       }
       __syncwarp();
     }
@@ -624,6 +757,20 @@ __device__ __forceinline__ double ordered_add(double acc, double v, bool f) {
 
 __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_warp) {
   const long long t_start = clock64();
+#ifdef LT_PHASE_PROF
+  long long ph[6] = {0, 0, 0, 0, 0, 0};
+  long long tp = clock64();
+#define LT_PH(k)                 \
+  do {                           \
+    const long long t_ = clock64(); \
+    ph[k] += t_ - tp;            \
+    tp = t_;                     \
+  } while (0)
+#else
+#define LT_PH(k) \
+  do {           \
+  } while (0)
+#endif
   WarpEngine E;
   E.lane = threadIdx.x & 31;
   const int lane = E.lane;
@@ -658,11 +805,11 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   E.q_head = E.run_cnt + NA;
   E.q_tail = E.q_head + NA;
   E.q_cnt = E.q_tail + NA;
-  E.blk_ep = E.q_cnt + NA;
-  E.aflag = E.blk_ep + NA;
+  E.act_key = E.q_cnt + NA;
   E.run = P.ws_run + static_cast<int64_t>(slot) * P.ws_stride;
+  E.cmin = P.ws_cmin + static_cast<int64_t>(slot) * (P.ws_stride / 32 + 2);
   E.pq = P.ws_pq + static_cast<int64_t>(slot) * P.ws_stride;
-  E.nxt = P.ws_nxt + static_cast<int64_t>(slot) * P.ws_stride;
+  E.node = P.ws_node + static_cast<int64_t>(slot) * P.ws_stride;
   E.ov = P.ws_ov + static_cast<int64_t>(slot) * P.ws_stride;
   for (int a = lane; a < E.N; a += 32) {
     E.last_used[a] = 0.0;
@@ -670,8 +817,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     E.q_head[a] = -1;
     E.q_tail[a] = -1;
     E.q_cnt[a] = 0;
-    E.blk_ep[a] = -1;
-    E.aflag[a] = P.adapters[E.ab + a].rank > 0 ? 1 : 0;
+    E.act_key[a] = INT_MAX;
   }
   __syncwarp();
   for (int b = 0; b < 32; ++b) {
@@ -690,7 +836,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     }
     // ingest arrivals <= clock (engine.cpp:88-92): append to the adapter's
     // FIFO chain, or to the oversized FIFO when in + 1 > capacity.
-    while (E.ingest < E.n_req) {
+    while (E.ingest < E.n_req && P.r_arr[E.rb + E.ingest] <= E.clock) {
       const int i = E.ingest + lane;
       const int ic = i < E.n_req ? i : E.n_req - 1;  // clamped: no divergent load before the vote
       const double ta = P.r_arr[E.rb + ic];
@@ -698,12 +844,15 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
       const unsigned b = __ballot_sync(kFull, ok);
       const int n = (b == kFull) ? 32 : __ffs(~b) - 1;
       const int a_l = P.r_adp[E.rb + ic];
-      const bool over_l = static_cast<int64_t>(P.r_in[E.rb + ic]) + 1 > E.cap;
+      const int in_l = P.r_in[E.rb + ic];
+      const bool over_l = static_cast<int64_t>(in_l) + 1 > E.cap;
       const unsigned live = (n >= 32) ? kFull : ((1u << n) - 1);
       const unsigned overm = __ballot_sync(kFull, over_l) & live;
       if ((overm >> lane) & 1u) E.ov[E.ov_tail + __popc(overm & lanemask_lt())] = i;
       E.ov_tail += __popc(overm);
       unsigned m = live & ~overm;
+      if ((m >> lane) & 1u) E.node[i] = make_int4(in_l, P.r_out[E.rb + i], -1, a_l);
+      __syncwarp();
       while (m) {
         const int src = __ffs(m) - 1;
         m &= m - 1;
@@ -714,10 +863,11 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
           if (t < 0)
             E.q_head[a] = id;
           else
-            E.nxt[t] = id;
+            reinterpret_cast<int*>(&E.node[t])[2] = id;
           E.q_tail[a] = id;
           E.q_cnt[a] += 1;
         }
+        mask_set(E.nonempty_w, a, lane);
       }
       E.Wf += n;
       E.ingest += n;
@@ -726,11 +876,24 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
       if (n < 32) break;
     }
     __syncwarp();
-    if (E.R > 0 && E.iter >= E.min_fin) E.retire(P);
+    LT_PH(0);
+    if (E.R > 0) E.retire(P);
+    LT_PH(1);
     if (!E.alloc(P)) break;
-    const int r_before = E.R;
-    E.admit(P);
+    LT_PH(2);
+    const int r_before = E.R_end;
+    // admit (kv_scheduler.cpp:170-181): preempted queue first, then fresh
+    E.free_slots = E.G - E.resident_count;
+    E.evicted_w = 0;
+    E.blocked_w = 0;
+    {
+      bool go = true;
+      E.Wp = E.scan(P, E.pq, E.Wp, true, &go);
+      LT_PH(3);
+      if (go) E.scan_fresh(P);
+    }
     __syncwarp();
+    LT_PH(4);
     if (E.R == 0) {
       if (E.Wp + E.Wf != 0) {
         E.fail(LT_ERR_INTERNAL, LT_K_ADMISSION_STUCK, 0, 0);
@@ -755,7 +918,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     const double lat = sched + loads + model * adapters;
     const double emit = E.clock + lat;
     // first tokens of this iteration's fresh admissions (engine.cpp:131)
-    for (int i = r_before + lane; i < E.R; i += 32) {
+    for (int i = r_before + lane; i < E.R_end; i += 32) {
       const int4 e = E.run[i];
       if (e.z & kFreshBit) P.r_first[E.rb + e.x] = emit;
     }
@@ -770,6 +933,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     }
     E.clock = emit;
     ++E.iter;
+    LT_PH(5);
     if (E.iter >= E.iter_cap) {
       if (capped_by_range) {
         E.fail(LT_ERR_UNSUPPORTED, LT_K_ITERATION_RANGE, E.iter, 0);
@@ -781,8 +945,9 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   }
   __syncwarp();
   // Requests still running keep their emitted tokens (truncation / error).
-  for (int i = lane; i < E.R; i += 32) {
+  for (int i = lane; i < E.R_end; i += 32) {
     const int4 e = E.run[i];
+    if (e.x < 0) continue;
     const int outv = P.r_out[E.rb + e.x];
     P.r_gen[E.rb + e.x] = outv - (e.y - E.iter);
     P.r_last[E.rb + e.x] = E.clock;
@@ -851,6 +1016,10 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
       o.starved = o.throughput_tok_s < 0.9 * eff;
     }
   }
+  LT_PH(5);
+#ifdef LT_PHASE_PROF
+  for (int k = 0; k < 6; ++k) o.phase_cycles[k] = ph[k];
+#endif
   o.device_cycles = clock64() - t_start;
   if (lane == 0) P.out[s] = o;
 }

@@ -6,7 +6,7 @@
 //   requests   arrival f64 / in / out / adapter i32   [sum n_req]   (inputs)
 //              phase u8 / gen i32 / first f64 / last f64 / preempt i32  (state + outputs)
 //   workspace  per persistent warp slot: running int4[cap], preempted int2[cap],
-//              next-in-adapter-chain i32[cap], oversized FIFO i32[cap]
+//              chain node int4[cap] {in, out, next, adapter}, oversized FIFO i32[cap]
 //              (cap = max n_req of the batch)
 //   smem       per warp: last_used f64[NA], run_count, chain head/tail/count,
 //              block epoch, flags i32[NA] (NA = max adapters)
@@ -95,7 +95,8 @@ struct EngineParams {
   int32_t* r_pre;
   int4* ws_run;
   int2* ws_pq;
-  int32_t* ws_nxt;
+  int4* ws_node;
+  int32_t* ws_cmin;  // (ws_stride / 32 + 2) per warp slot
   int32_t* ws_ov;
   int64_t ws_stride;  // entries per warp slot
   double k1, k2, k3, k4, k5, k6, k7;
