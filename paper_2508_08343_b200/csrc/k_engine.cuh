@@ -138,6 +138,11 @@ struct WarpEngine {
   int32_t* q_cnt = nullptr;
   int32_t* act_key = nullptr;  // scan-local: chain head if the adapter can act, else INT_MAX
   int32_t ov_head = 0, ov_tail = 0;
+  // fresh-scan stop cache (see scan_fresh)
+  int32_t last_stop = -1;
+  int64_t last_stop_demand = 0;
+  uint32_t act_epoch = 0, stop_epoch = 0;
+  bool stop_mass = false;
   int4* run = nullptr;
   int32_t* cmin = nullptr;  // per 32-entry chunk of run[]: lower bound of live retire iterations
   int2* pq = nullptr;
@@ -155,7 +160,10 @@ struct WarpEngine {
 
   // An adapter left the running batch: its slot is no longer claimed.
   __device__ __forceinline__ void release_adapter(int a, bool dec_to_zero) {
-    if (dec_to_zero) mask_clear(claimed_w, a, lane);
+    if (dec_to_zero) {
+      mask_clear(claimed_w, a, lane);
+      ++act_epoch;
+    }
   }
 
   __device__ __forceinline__ bool pool_any() const {
@@ -189,6 +197,7 @@ struct WarpEngine {
       }
     }
     mask_set(claimed_w, a, lane);
+    ++act_epoch;
   }
 
   // Running set = run[0, R_end) in admission order with tombstones (x = -1)
@@ -546,6 +555,18 @@ struct WarpEngine {
   // stop point, as the reference rejects them when the scan passes them.
   __device__ __forceinline__ void scan_fresh(const EngineParams& P) {
     bool mass = P.priority && free_slots == 0 && !pool_any();
+    // Steady-state shortcut: the previous fresh scan stopped on memory at
+    // entry last_stop and no adapter has been claimed or released since (the
+    // same adapters act, and every entry that arrived since sorts after it),
+    // so this scan's first acting entry is last_stop again. If it still does
+    // not fit, the scan stops right there, exactly as the full scan would.
+    if (P.priority && last_stop >= 0 && stop_epoch == act_epoch && mass == stop_mass &&
+        used + last_stop_demand > cap) {
+      ++sum_v;
+      reject_oversized(P, last_stop);
+      return;
+    }
+    last_stop = -1;
     // Acting adapters of this scan. When at most 32 can act (always for
     // N <= 32; and in the slot-starved steady state, where only the <= G
     // claimed adapters act), each lane holds one of them and an event is a
@@ -625,6 +646,10 @@ struct WarpEngine {
       const int64_t demand = static_cast<int64_t>(nd.x) + 1;
       if (used + demand > cap) {
         stop_id = id;  // strict FCFS on memory
+        last_stop = id;
+        last_stop_demand = demand;
+        stop_epoch = act_epoch;
+        stop_mass = mass;
         break;
       }
       used += demand;
@@ -675,7 +700,13 @@ struct WarpEngine {
       }
       __syncwarp();
     }
-    // oversized entries in front of the stop point are rejected in place
+    reject_oversized(P, stop_id);
+  }
+
+  // Oversized fresh entries in front of the stop point are rejected in place
+  // (kv_scheduler.cpp:119-124): the reference rejects them when its scan
+  // passes them.
+  __device__ __forceinline__ void reject_oversized(const EngineParams& P, int stop_id) {
     while (ov_head < ov_tail) {
       const int i = ov_head + lane;
       const int id = i < ov_tail ? ov[i] : INT_MAX;
@@ -826,32 +857,40 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   }
   __syncwarp();
   const bool capped_by_range = sc.iter_cap > 0x7ff00000LL;
+  double pf_t = INFINITY;
+  int pf_a = 0, pf_in = 0, pf_out = 0;
+  if (E.n_req > 0) {
+    const int jc = lane < E.n_req ? lane : E.n_req - 1;
+    pf_t = lane < E.n_req ? P.r_arr[E.rb + jc] : INFINITY;
+    pf_a = P.r_adp[E.rb + jc];
+    pf_in = P.r_in[E.rb + jc];
+    pf_out = P.r_out[E.rb + jc];
+  }
 
   while (true) {
     __syncwarp();
     if (E.R == 0 && E.Wp + E.Wf == 0) {
       if (E.ingest >= E.n_req) break;  // fully drained
-      const double t = P.r_arr[E.rb + E.ingest];
+      const double t = __shfl_sync(kFull, pf_t, 0);
       E.clock = E.clock < t ? t : E.clock;  // std::max(clock_, arrival)
     }
     // ingest arrivals <= clock (engine.cpp:88-92): append to the adapter's
-    // FIFO chain, or to the oversized FIFO when in + 1 > capacity.
-    while (E.ingest < E.n_req && P.r_arr[E.rb + E.ingest] <= E.clock) {
+    // FIFO chain, or to the oversized FIFO when in + 1 > capacity. The next
+    // 32 arrivals are kept prefetched in registers (pf_*), so an iteration
+    // with no arrival costs one comparison and one with arrivals no waiting.
+    while (E.ingest < E.n_req && __shfl_sync(kFull, pf_t, 0) <= E.clock) {
       const int i = E.ingest + lane;
-      const int ic = i < E.n_req ? i : E.n_req - 1;  // clamped: no divergent load before the vote
-      const double ta = P.r_arr[E.rb + ic];
-      const bool ok = (i < E.n_req) & (ta <= E.clock);
+      const bool ok = (i < E.n_req) & (pf_t <= E.clock);
       const unsigned b = __ballot_sync(kFull, ok);
       const int n = (b == kFull) ? 32 : __ffs(~b) - 1;
-      const int a_l = P.r_adp[E.rb + ic];
-      const int in_l = P.r_in[E.rb + ic];
+      const int a_l = pf_a, in_l = pf_in, out_l = pf_out;
       const bool over_l = static_cast<int64_t>(in_l) + 1 > E.cap;
       const unsigned live = (n >= 32) ? kFull : ((1u << n) - 1);
       const unsigned overm = __ballot_sync(kFull, over_l) & live;
       if ((overm >> lane) & 1u) E.ov[E.ov_tail + __popc(overm & lanemask_lt())] = i;
       E.ov_tail += __popc(overm);
       unsigned m = live & ~overm;
-      if ((m >> lane) & 1u) E.node[i] = make_int4(in_l, P.r_out[E.rb + i], -1, a_l);
+      if ((m >> lane) & 1u) E.node[i] = make_int4(in_l, out_l, -1, a_l);
       __syncwarp();
       while (m) {
         const int src = __ffs(m) - 1;
@@ -872,6 +911,26 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
       E.Wf += n;
       E.ingest += n;
       E.sum_a += n;
+      {  // slide the prefetch window by n
+        const int srcl = lane + n;
+        const double t2 = __shfl_sync(kFull, pf_t, srcl & 31);
+        const int a2 = __shfl_sync(kFull, pf_a, srcl & 31);
+        const int in2 = __shfl_sync(kFull, pf_in, srcl & 31);
+        const int out2 = __shfl_sync(kFull, pf_out, srcl & 31);
+        if (srcl < 32) {
+          pf_t = t2;
+          pf_a = a2;
+          pf_in = in2;
+          pf_out = out2;
+        } else {
+          const int j = E.ingest + lane;
+          const int jc = j < E.n_req ? j : E.n_req - 1;
+          pf_t = j < E.n_req ? P.r_arr[E.rb + jc] : INFINITY;
+          pf_a = P.r_adp[E.rb + jc];
+          pf_in = P.r_in[E.rb + jc];
+          pf_out = P.r_out[E.rb + jc];
+        }
+      }
       __syncwarp();
       if (n < 32) break;
     }
