@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -19,6 +20,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <set>
 #include <string>
@@ -185,6 +187,7 @@ struct Config {
   std::map<int, double> load;
   HostErr body_err;  // config.validate() failure other than slots
   bool body_ok = true;
+  std::vector<double> lat_cache;
   int variant = 1;
 };
 
@@ -213,6 +216,16 @@ double load_latency(const Config& c, int rank) {
   auto it = c.load.find(rank);
   if (it == c.load.end()) return NAN;
   return c.raw.load_source == LT_SOURCE_CPU ? it->second : it->second * c.raw.disk_multiplier;
+}
+
+double load_latency_cached(Config& c, int rank) {
+  if (rank >= 0 && rank < 1024) {
+    if (c.lat_cache.empty()) c.lat_cache.assign(1024, -2.0);
+    double& v = c.lat_cache[rank];
+    if (v == -2.0) v = load_latency(c, rank);
+    return v;
+  }
+  return load_latency(c, rank);
 }
 
 struct Stats {
@@ -264,23 +277,89 @@ DLen as_dlen(const lt_length_spec& l, const int32_t* full) {
 // ----------------------------------------------------------------------------
 // Device buffers
 
+// Grow-only caching allocator: device buffers are recycled across plans and
+// calls (cudaMalloc/cudaFree of GB-sized workspaces would otherwise dominate
+// small end-to-end calls). Blocks are keyed by device and size class.
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> free_blocks;
+  static BlockCache& get() {
+    static BlockCache* c = new BlockCache();  // never destroyed: outlives static DBufs
+    return *c;
+  }
+  static size_t size_class(size_t bytes) {
+    size_t c = 256;
+    while (c < bytes) c <<= 1;  // power-of-two classes bound waste at 2x
+    return c;
+  }
+  void* take(size_t bytes, size_t* got) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t cls = size_class(bytes);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = free_blocks.find({dev, cls});
+      if (it != free_blocks.end()) {
+        void* p = it->second;
+        free_blocks.erase(it);
+        *got = cls;
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, cls);
+    if (e != cudaSuccess) {
+      // release cached blocks of this device and retry once
+      trim(dev);
+      cudaGetLastError();
+      e = cudaMalloc(&p, cls);
+    }
+    if (e != cudaSuccess) throw CudaError{std::string("cudaMalloc: ") + cudaGetErrorString(e)};
+    *got = cls;
+    return p;
+  }
+  void give(void* p, size_t cls) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    free_blocks.emplace(std::make_pair(dev, cls), p);
+  }
+  void trim(int dev) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto it = free_blocks.begin(); it != free_blocks.end();) {
+      if (it->first.first == dev) {
+        cudaFree(it->second);
+        it = free_blocks.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+};
+
 template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  size_t cls = 0;
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) BlockCache::get().give(p, cls);
     p = nullptr;
     n = 0;
+    cls = 0;
   }
   void alloc(size_t count) {
+    if (p && count * sizeof(T) <= cls) {  // reuse the current block
+      n = count;
+      return;
+    }
     release();
     n = count;
-    if (count) LT_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (count) p = static_cast<T*>(BlockCache::get().take(count * sizeof(T), &cls));
   }
   void upload(const std::vector<T>& v, cudaStream_t s) {
     alloc(v.size());
@@ -333,10 +412,17 @@ struct lt_plan {
   DBuf<unsigned long long> scen_count, base_count, scen_off;
   DBuf<char> scan_tmp;
   size_t scan_tmp_bytes = 0;
+  // sort-based merge of adapter streams
+  DBuf<unsigned long long> pair_excl, sv_in, sv_out;
+  DBuf<double> st_in, st_out;
+  DBuf<int> seg_begin, seg_end;
+  DBuf<char> sort_tmp, pscan_tmp;
+  size_t sort_tmp_bytes = 0, pscan_tmp_bytes = 0;
   int64_t n_pairs = 0;
   int n_keys = 0;
   bool fresh = true;
   int64_t ws_stride = 0;
+  int ws_per_scenario = 0;
   int grid = 0;
   int block = 256;
   size_t smem = 0;
@@ -359,7 +445,12 @@ struct Prep {
   std::vector<int32_t> pair_scen, pair_adp;
   std::vector<int64_t> pair_begin;
   std::unordered_map<std::string, int> len_index;
-  std::map<std::pair<uint64_t, int64_t>, int> key_index;
+  struct KeyHash {
+    size_t operator()(const std::pair<uint64_t, int64_t>& k) const {
+      return std::hash<uint64_t>()(k.first * 0x9e3779b97f4a7c15ULL ^ static_cast<uint64_t>(k.second));
+    }
+  };
+  std::unordered_map<std::pair<uint64_t, int64_t>, int, KeyHash> key_index;
   std::vector<double> cost;
 };
 
@@ -409,18 +500,30 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
     if (s.n_adapters <= 0) return e.set(LT_ERR_VALIDATION, "workload.adapters: must be non-empty"), fail();
     if (s.duration_s <= 0.0)
       return e.set(LT_ERR_VALIDATION, "workload.duration_s: must be > 0, got " + std::to_string(s.duration_s)), fail();
-    std::set<int> seen;
-    for (int k = 0; k < s.n_adapters; ++k) {
-      const std::string path = "workload.adapters[" + std::to_string(k) + "]";
-      if (ad[k].rank < 0)
-        return e.set(LT_ERR_VALIDATION, path + ".rank: must be >= 0, got " + std::to_string(ad[k].rank)), fail();
-      if (ad[k].rate <= 0.0)
-        return e.set(LT_ERR_VALIDATION, path + ".rate: must be > 0, got " + std::to_string(ad[k].rate)), fail();
-      if (!seen.insert(ad[k].adapter_id).second)
-        return e.set(LT_ERR_VALIDATION, path + ".adapter_id: duplicate id " + std::to_string(ad[k].adapter_id)), fail();
-      if (ad[k].length_index >= 0 &&
-          !validate_lengths(b.lengths[ad[k].length_index], full, path + ".lengths", &e))
-        return fail();
+    // fast screen; the exact first error (in spec order) is rebuilt only on failure
+    bool suspect = false;
+    for (int k = 0; k < s.n_adapters && !suspect; ++k)
+      suspect = ad[k].rank < 0 || !(ad[k].rate > 0.0) || ad[k].length_index >= 0;
+    if (!suspect) {
+      std::vector<int> ids(s.n_adapters);
+      for (int k = 0; k < s.n_adapters; ++k) ids[k] = ad[k].adapter_id;
+      std::sort(ids.begin(), ids.end());
+      suspect = std::adjacent_find(ids.begin(), ids.end()) != ids.end();
+    }
+    if (suspect) {
+      std::set<int> seen;
+      for (int k = 0; k < s.n_adapters; ++k) {
+        const std::string path = "workload.adapters[" + std::to_string(k) + "]";
+        if (ad[k].rank < 0)
+          return e.set(LT_ERR_VALIDATION, path + ".rank: must be >= 0, got " + std::to_string(ad[k].rank)), fail();
+        if (ad[k].rate <= 0.0)
+          return e.set(LT_ERR_VALIDATION, path + ".rate: must be > 0, got " + std::to_string(ad[k].rate)), fail();
+        if (!seen.insert(ad[k].adapter_id).second)
+          return e.set(LT_ERR_VALIDATION, path + ".adapter_id: duplicate id " + std::to_string(ad[k].adapter_id)), fail();
+        if (ad[k].length_index >= 0 &&
+            !validate_lengths(b.lengths[ad[k].length_index], full, path + ".lengths", &e))
+          return fail();
+      }
     }
     if (!validate_lengths(b.lengths[s.length_index], full, "workload.lengths", &e)) return fail();
     // generate_arrivals mode handling (workload.cpp:185-192)
@@ -480,7 +583,7 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
     x.id = a.adapter_id;
     x.rank = a.rank;
     x.rate = a.rate;
-    x.load_lat = load_latency(P.cfg, a.rank);
+    x.load_lat = load_latency_cached(P.cfg, a.rank);
     x.length_param = a.length_index >= 0 ? intern_len(pr, as_dlen(b.lengths[a.length_index], full)) : -1;
     x.key = -1;
     if (!scripted) {
@@ -681,6 +784,23 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   P.r_first.alloc(nr);
   P.r_last.alloc(nr);
   P.r_pre.alloc(nr);
+  if (P.total_req >= (int64_t(1) << 31)) throw CudaError{"batch too large: more than 2^31 requests in one plan"};
+  if (n_pairs > 0) {
+    P.pair_excl.alloc(n_pairs);
+    P.st_in.alloc(nr);
+    P.st_out.alloc(nr);
+    P.sv_in.alloc(nr);
+    P.sv_out.alloc(nr);
+    P.seg_begin.alloc(P.n_scen);
+    P.seg_end.alloc(P.n_scen);
+    LT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, P.pscan_tmp_bytes, P.adp_count.p, P.pair_excl.p,
+                                          static_cast<int>(n_pairs), st));
+    P.pscan_tmp.alloc(std::max<size_t>(P.pscan_tmp_bytes, 1));
+    LT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, P.sort_tmp_bytes, P.st_in.p, P.st_out.p, P.sv_in.p,
+                                                      P.sv_out.p, static_cast<int>(nr), static_cast<int>(P.n_scen),
+                                                      P.seg_begin.p, P.seg_end.p, st));
+    P.sort_tmp.alloc(std::max<size_t>(P.sort_tmp_bytes, 1));
+  }
   // scripted requests
   {
     std::vector<double> arr;
@@ -714,8 +834,6 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     P.h2d_bytes += cursor * 20;
     LT_CUDA(cudaStreamSynchronize(st));
   }
-  LT_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(size_t(4) * P.max_adapters * 16)));
   // engine order: most expensive first
   P.h_order.resize(P.n_scen);
   for (int64_t i = 0; i < P.n_scen; ++i) P.h_order[i] = static_cast<int32_t>(i);
@@ -740,12 +858,21 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   const int64_t want = (P.n_scen + P.block / 32 - 1) / (P.block / 32);
   P.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(ctx->sm_count) * per_sm)));
   P.ws_stride = std::max<int64_t>(P.max_req, 1);
-  const int64_t slots = int64_t(P.grid) * (P.block / 32);
-  P.ws_run.alloc(slots * P.ws_stride);
-  P.ws_pq.alloc(slots * P.ws_stride);
-  P.ws_node.alloc(slots * P.ws_stride);
-  P.ws_cmin.alloc(slots * (P.ws_stride / 32 + 2));
-  P.ws_ov.alloc(slots * P.ws_stride);
+  {
+    // Workspace per persistent warp slot (slots x longest scenario) or per
+    // scenario (at its request offset), whichever is smaller.
+    const int64_t slots = int64_t(P.grid) * (P.block / 32);
+    const int64_t per_slot = slots * P.ws_stride;
+    const int64_t per_scen = std::max<int64_t>(P.total_req, 1);
+    P.ws_per_scenario = per_scen < per_slot;
+    const int64_t entries = P.ws_per_scenario ? per_scen : per_slot;
+    const int64_t centries = P.ws_per_scenario ? per_scen / 32 + 2 * P.n_scen + 2 : slots * (P.ws_stride / 32 + 2);
+    P.ws_run.alloc(entries);
+    P.ws_pq.alloc(entries);
+    P.ws_node.alloc(entries);
+    P.ws_cmin.alloc(centries);
+    P.ws_ov.alloc(entries);
+  }
   LT_CUDA(cudaStreamSynchronize(st));
   P.tables_ms = elapsed(ctx->ev[0], ctx->ev[1]);
   P.fresh = true;
@@ -789,13 +916,27 @@ void prepare_requests(lt_plan& P) {
   }
   cudaEventRecord(ctx->ev[2], st);
   if (P.n_pairs > 0) {
-    const int wpb = 4;
-    const size_t smem = static_cast<size_t>(wpb) * P.max_adapters * 16;
-    merge_kernel<<<static_cast<unsigned>((P.n_scen + wpb - 1) / wpb), wpb * 32, smem, st>>>(
-        P.scen.p, static_cast<int>(P.n_scen), P.adapters.p, P.keys.p, P.lens.p, P.E.p, P.Z.p,
-        P.pair_begin.p, P.adp_count.p, P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p, P.max_adapters);
-    after_launch("merge_kernel", st);
-    ++launches;
+    // sort-based merge: unsorted times per (scenario, adapter), stable
+    // segmented sort by time, gather into request arrays
+    size_t tb = P.pscan_tmp_bytes;
+    LT_CUDA(cub::DeviceScan::ExclusiveSum(P.pscan_tmp.p, tb, P.adp_count.p, P.pair_excl.p,
+                                          static_cast<int>(P.n_pairs), st));
+    expand_kernel<<<static_cast<unsigned>((P.n_pairs + 127) / 128), 128, 0, st>>>(
+        P.scen.p, P.pair_scen.p, P.pair_adp.p, P.n_pairs, P.pair_begin.p, P.adapters.p, P.keys.p, P.E.p,
+        P.adp_count.p, P.pair_excl.p, P.st_in.p, P.sv_in.p);
+    after_launch("expand_kernel", st);
+    segments_kernel<<<static_cast<unsigned>((P.n_scen + 255) / 256), 256, 0, st>>>(
+        P.scen.p, static_cast<int>(P.n_scen), P.seg_begin.p, P.seg_end.p);
+    after_launch("segments_kernel", st);
+    size_t sb = P.sort_tmp_bytes;
+    LT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(P.sort_tmp.p, sb, P.st_in.p, P.st_out.p, P.sv_in.p,
+                                                      P.sv_out.p, static_cast<int>(std::max<int64_t>(P.total_req, 1)),
+                                                      static_cast<int>(P.n_scen), P.seg_begin.p, P.seg_end.p, st));
+    gather_kernel<<<static_cast<unsigned>((P.n_scen + 7) / 8), 256, 0, st>>>(
+        P.scen.p, static_cast<int>(P.n_scen), P.adapters.p, P.keys.p, P.lens.p, P.Z.p, P.st_out.p, P.sv_out.p,
+        P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p);
+    after_launch("gather_kernel", st);
+    launches += 3;  // + CUB scan and segmented sort (library kernels)
   }
   cudaEventRecord(ctx->ev[3], st);
   P.fresh = false;
@@ -835,6 +976,7 @@ void run_plan(lt_plan& P) {
   E.ws_cmin = P.ws_cmin.p;
   E.ws_ov = P.ws_ov.p;
   E.ws_stride = P.ws_stride;
+  E.ws_per_scenario = P.ws_per_scenario;
   E.k1 = P.cfg.raw.k1;
   E.k2 = P.cfg.raw.k2;
   E.k3 = P.cfg.raw.k3;

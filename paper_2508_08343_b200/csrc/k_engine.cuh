@@ -837,11 +837,14 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   E.q_tail = E.q_head + NA;
   E.q_cnt = E.q_tail + NA;
   E.act_key = E.q_cnt + NA;
-  E.run = P.ws_run + static_cast<int64_t>(slot) * P.ws_stride;
-  E.cmin = P.ws_cmin + static_cast<int64_t>(slot) * (P.ws_stride / 32 + 2);
-  E.pq = P.ws_pq + static_cast<int64_t>(slot) * P.ws_stride;
-  E.node = P.ws_node + static_cast<int64_t>(slot) * P.ws_stride;
-  E.ov = P.ws_ov + static_cast<int64_t>(slot) * P.ws_stride;
+  const int64_t wsb = P.ws_per_scenario ? sc.req_begin : static_cast<int64_t>(slot) * P.ws_stride;
+  const int64_t wcb = P.ws_per_scenario ? (sc.req_begin >> 5) + 2 * static_cast<int64_t>(s)
+                                        : static_cast<int64_t>(slot) * (P.ws_stride / 32 + 2);
+  E.run = P.ws_run + wsb;
+  E.cmin = P.ws_cmin + wcb;
+  E.pq = P.ws_pq + wsb;
+  E.node = P.ws_node + wsb;
+  E.ov = P.ws_ov + wsb;
   for (int a = lane; a < E.N; a += 32) {
     E.last_used[a] = 0.0;
     E.run_cnt[a] = 0;

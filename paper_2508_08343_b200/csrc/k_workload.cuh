@@ -88,6 +88,70 @@ __global__ void set_offsets_kernel(DScen* scen, int n_scen, const unsigned long 
   if (scen[i].generated && scen[i].status == LT_OK) scen[i].n_req = static_cast<int32_t>(count[i]);
 }
 
+// Arrival times of one (scenario, adapter) pair written unsorted at the pair's
+// slot of the scenario segment; a stable segmented sort by time then realises
+// the reference's stable_sort by (time, adapter_id, sequence)
+// (workload.cpp:204-207): pairs are laid out in adapter-id order.
+__global__ void expand_kernel(const DScen* scen, const int32_t* pair_scen, const int32_t* pair_adp,
+                              int64_t n_pairs, const int64_t* pair_begin, const DAdapter* adapters,
+                              const DKey* keys, const double* E, const int32_t* adp_count,
+                              const unsigned long long* pair_excl, double* t_out,
+                              unsigned long long* v_out) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p >= n_pairs) return;
+  const int si = pair_scen[p];
+  const DScen& s = scen[si];
+  const int k = pair_adp[p];
+  const DAdapter ad = adapters[s.adapter_begin + k];
+  const double* Ek = E + keys[ad.key].e_off;
+  const int64_t off = s.req_begin + static_cast<int64_t>(pair_excl[p] - pair_excl[pair_begin[si]]);
+  const int n = adp_count[p];
+  double t = 0.0;
+  for (int j = 0; j < n; ++j) {
+    t = t + Ek[j] / ad.rate;
+    t_out[off + j] = t;
+    v_out[off + j] = (static_cast<unsigned long long>(k) << 32) | static_cast<unsigned>(j);
+  }
+}
+
+// Segment bounds of the generated scenarios (scripted / failed: empty).
+__global__ void segments_kernel(const DScen* scen, int n_scen, int* seg_begin, int* seg_end) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_scen) return;
+  const DScen& s = scen[i];
+  const int b = static_cast<int>(s.req_begin);
+  seg_begin[i] = b;
+  seg_end[i] = (s.generated && s.status == LT_OK) ? b + s.n_req : b;
+}
+
+// Sorted (time, adapter, sequence) -> request arrays; lengths from the Z
+// table of the adapter's (seed, id) key (sample_lengths, workload.cpp:162-166).
+__global__ void __launch_bounds__(256) gather_kernel(const DScen* scen, int n_scen, const DAdapter* adapters,
+                                                    const DKey* keys, const DLen* lens, const double2* Z,
+                                                    const double* t_sorted, const unsigned long long* v_sorted,
+                                                    double* r_arr, int32_t* r_in, int32_t* r_out,
+                                                    int32_t* r_adp) {
+  const int lane = threadIdx.x & 31;
+  const int si = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (si >= n_scen) return;
+  const DScen sc = scen[si];
+  if (!sc.generated || sc.status != LT_OK) return;
+  const DLen gl = lens[sc.length_param];
+  for (int r = lane; r < sc.n_req; r += 32) {
+    const int64_t g = sc.req_begin + r;
+    const unsigned long long v = v_sorted[g];
+    const int a = static_cast<int>(v >> 32);
+    const int j = static_cast<int>(v & 0xffffffffULL);
+    const DAdapter ad = adapters[sc.adapter_begin + a];
+    const double2 z = Z[keys[ad.key].z_off + j];
+    const DLen L = ad.length_param >= 0 ? lens[ad.length_param] : gl;
+    r_arr[g] = t_sorted[g];
+    r_adp[g] = a;
+    r_in[g] = round_clamp_token(affine(L.mean_in, L.std_in, z.x));
+    r_out[g] = round_clamp_token(affine(L.mean_out, L.std_out, z.y));
+  }
+}
+
 // N-way merge of one scenario's adapter streams into request_id order.
 // Per-lane cache of the lane's best head; one warp argmin per request.
 __global__ void __launch_bounds__(256) merge_kernel(const DScen* scen, int n_scen,

@@ -99,6 +99,7 @@ struct EngineParams {
   int32_t* ws_cmin;  // (ws_stride / 32 + 2) per warp slot
   int32_t* ws_ov;
   int64_t ws_stride;  // entries per warp slot
+  int32_t ws_per_scenario;  // 1: workspace indexed by the scenario's request offset
   double k1, k2, k3, k4, k5, k6, k7;
   int32_t priority;
   int32_t want_digest;
