@@ -331,6 +331,7 @@ int32_t ltref_sweep_batch(void*, const lt_condition_batch* batch, const lt_serve
   run_pool(n, [&](std::size_t i) {
     lt_placement& o = out[i];
     std::memset(&o, 0, sizeof(o));
+    o.status_point = -1;
     try {
       const lt_condition& c = batch->conditions[i];
       Condition cond;

@@ -272,3 +272,23 @@ def test_plan_rerun_is_deterministic(dev):
     fields = [f for f in a.dtype.names if f != "device_cycles"]
     for f in fields:
         np.testing.assert_array_equal(a[f], c[f], err_msg=f)
+
+
+def test_derived_lat_step_fixture(dev):
+    """derived_values.json: lat_step = 0.075455 for R=10, W=5, g=4, n=8, a=1 and one 0.05 s rank-8 load."""
+    from tests.test_oracle import derived_values_case
+
+    cfg, ads, reqs, want = derived_values_case()
+    b = WorkloadBatch.from_workloads([W.scripted_workload(ads, 10.0)], scripted=[reqs])
+    out, _ = dev.simulate_batch(b, cfg, options=lt.SimOptions(iteration_cap_override=1))
+    assert out[0]["truncated"] == 1 and out[0]["iterations"] == 1
+    assert math.isclose(out[0]["final_clock_s"], want, rel_tol=1e-12)
+
+
+def test_port_oracle_c2_sample(dev, port):
+    """Against the C restatement (always buildable on the box), ITL included to 1e-9."""
+    b = W.c2_batch(duration_s=600.0, stride=29)
+    cfg = lt.h100_like_config(1)
+    g, _ = dev.simulate_batch(b, cfg, want_digest=True)
+    p, _ = port.simulate(b, cfg, sim_options(None, True))
+    assert_summaries(g, p)
