@@ -100,13 +100,21 @@ def measured_peaks():
 
 
 def ncu_traffic():
-    """dram bytes per engine launch from the committed ncu --set full summary, if present."""
-    p = os.path.join(ROOT, "profiles", "engine_ncu_summary.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d
-    return None, None
+    """dram bytes per engine launch from the latest committed ncu --set full
+    summary (profiles/r<NN>_engine_ncu.json), if present."""
+    import glob
+
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_engine_ncu.json")))
+    if not paths:
+        return None, None
+    with open(paths[-1]) as f:
+        d = json.load(f)
+    m = d.get("metrics", {})
+    brief = {"file": os.path.relpath(paths[-1], ROOT), "workload": d.get("workload"),
+             "kernel_ms": m.get("gpu__time_duration.sum", [None])[0],
+             "issue_active_pct_of_peak": m.get("smsp__issue_active.avg.pct_of_peak_sustained_active", [None])[0],
+             "warp_latency_per_inst": m.get("smsp__average_warp_latency_per_inst_issued.ratio", [None])[0]}
+    return d.get("dram_bytes_per_launch"), brief
 
 
 def c2_batch_for_rank(rank: int, duration: float, stride: int = 1):

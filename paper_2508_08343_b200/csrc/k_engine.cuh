@@ -944,6 +944,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     if (!E.alloc(P)) break;
     LT_PH(2);
     const int r_before = E.R_end;
+    const int w_before = E.Wp + E.Wf, rcount_before = E.R;
     // admit (kv_scheduler.cpp:170-181): preempted queue first, then fresh
     E.free_slots = E.G - E.resident_count;
     E.evicted_w = 0;
@@ -1003,6 +1004,51 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         E.truncated = 1;
       }
       break;
+    }
+    // Quiet stretch. This iteration's admission scan admitted and rejected
+    // nothing, so until the next arrival (engine.cpp:88-92), the next
+    // retirement (kv_scheduler.cpp:245), the next preemption
+    // (kv_scheduler.cpp:190: used + R > cap) or the iteration cap, every
+    // iteration of the reference repeats the same decisions: the same
+    // SlotPlan (resident/claimed sets unchanged), a scan that stops at the
+    // same entry (memory only tightens) or keeps the same slot-blocked
+    // entries, no loads, and the same (R, W, A) -> the same lat_step. Such
+    // iterations only advance the clock by `lat` (one rounded add each, as
+    // the reference does), grow the ledger by R and count R tokens.
+    if (E.Wp + E.Wf == w_before && E.R == rcount_before && E.waived < 0) {
+      int min_fin = INT_MAX;
+      for (int c = lane; c < ((E.R_end + 31) >> 5); c += 32) min_fin = min(min_fin, E.cmin[c]);
+      min_fin = warp_min_i(min_fin);
+      const long long n_fin = static_cast<long long>(min_fin) - E.iter;
+      const long long n_mem = (E.cap - E.used) / E.R;
+      const long long n_cap = static_cast<long long>(E.iter_cap) - 1 - E.iter;
+      long long n_max = n_fin < n_mem ? n_fin : n_mem;
+      n_max = n_max < n_cap ? n_max : n_cap;
+      const double t_next = E.ingest < E.n_req ? __shfl_sync(kFull, pf_t, 0) : INFINITY;
+      if (n_max > 0 && t_next > E.clock) {
+        const double lat_q = sched + model * adapters;  // loads == 0
+        double clk = E.clock, start = E.clock;
+        int n = 0, win = 0;
+        while (n < n_max && t_next > clk) {
+          start = clk;
+          clk = clk + lat_q;
+          win += (clk <= E.duration);
+          ++n;
+          if (P.want_digest) {
+            E.digest = fold64(E.digest, static_cast<uint32_t>(E.R) | (static_cast<uint64_t>(static_cast<uint32_t>(W)) << 32));
+            E.digest = fold64(E.digest, static_cast<uint32_t>(A));
+            E.digest = fold64(E.digest, static_cast<uint64_t>(__double_as_longlong(lat_q)));
+          }
+        }
+        const long long rn = static_cast<long long>(E.R) * n;
+        E.clock = clk;
+        E.prev_now = start;  // ensure_loaded's last_used refresh of the last skipped iteration
+        E.used += rn;
+        E.iter += n;
+        E.tok_tot += rn;
+        E.tok_win += static_cast<long long>(E.R) * win;
+        E.sum_r += rn;
+      }
     }
   }
   __syncwarp();
