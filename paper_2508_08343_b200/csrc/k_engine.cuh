@@ -33,8 +33,8 @@ namespace lt {
 
 constexpr unsigned kFull = 0xffffffffu;
 // per-warp shared memory per adapter: last_used f64 + run_cnt, q_head, q_tail,
-// q_cnt, act_key (i32)
-constexpr int kSmemPerAdapter = 8 + 5 * 4;
+// act_key (i32)
+constexpr int kSmemPerAdapter = 8 + 4 * 4;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -61,11 +61,12 @@ __device__ __forceinline__ int mask_lowest(uint32_t w) {
   return src * 32 + __ffs(ws) - 1;
 }
 
-__device__ __forceinline__ int warp_min_i(int v) {
-  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
-  return v;
-}
+__device__ __forceinline__ int warp_min_i(int v) { return __reduce_min_sync(kFull, v); }
 __device__ __forceinline__ long long warp_sum_ll(long long v) {
+  // one redux.sync when every lane's value fits in 26 bits (the sum then
+  // fits in 32), else a shuffle tree
+  if (__all_sync(kFull, v >= 0 && v < (1LL << 26)))
+    return static_cast<long long>(__reduce_add_sync(kFull, static_cast<unsigned>(v)));
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
 }
@@ -135,8 +136,22 @@ struct WarpEngine {
   // fresh queue = per-adapter FIFO chains in request-id order (+ oversized FIFO)
   int32_t* q_head = nullptr;
   int32_t* q_tail = nullptr;
-  int32_t* q_cnt = nullptr;
   int32_t* act_key = nullptr;  // scan-local: chain head if the adapter can act, else INT_MAX
+  // Lane mode of the fresh scan (<= 32 acting adapters), persistent across
+  // scans: lane L owns adapter pl_a (-1: none) whose chain head is pl_k with
+  // node pl_nd {in, out, next, adapter}; pl_sf / pl_cl are its slot-needing /
+  // claimed flags. built_w is the lane's word of the owned-adapter set.
+  int32_t pl_a = -1, pl_k = INT_MAX;
+  int4 pl_nd = make_int4(0, 0, -1, 0);
+  bool pl_sf = false, pl_cl = false, pl_valid = false;
+  uint32_t built_w = 0;
+  // Fresh admissions of the current iteration (first-token times): lane j
+  // holds the j-th request id; n_fresh > 32 falls back to a running-set walk.
+  int32_t fresh_id = 0, n_fresh = 0;
+  // Chunk minima of retire iterations: chunk c < 32 lives in lane c's
+  // cmin_r, chunks >= 32 in global cmin[]. next_fin <= every live retire
+  // iteration (warp-uniform).
+  int32_t cmin_r = INT_MAX, next_fin = INT_MAX;
   int32_t ov_head = 0, ov_tail = 0;
   // fresh-scan stop cache (see scan_fresh)
   int32_t last_stop = -1;
@@ -205,14 +220,33 @@ struct WarpEngine {
   // below, so an iteration only touches the chunks that hold a retiree. The
   // last entry is always live (trim), so LIFO preemption pops run[R_end-1].
   __device__ __forceinline__ void run_append(int4 e) {
+    const int pos = R_end;
+    const int c = pos >> 5;
     if (lane == 0) {
-      const int pos = R_end;
       run[pos] = e;
-      const int c = pos >> 5;
-      cmin[c] = (pos & 31) ? min(cmin[c], e.y) : e.y;
+      if (c >= 32) cmin[c] = (pos & 31) ? min(cmin[c], e.y) : e.y;
     }
+    if (c < 32 && lane == c) cmin_r = (pos & 31) ? min(cmin_r, e.y) : e.y;
+    next_fin = min(next_fin, e.y);
     ++R_end;
     ++R;
+  }
+
+  // Chunk minimum c (warp-uniform c).
+  __device__ __forceinline__ void cmin_set(int c, int v) {
+    if (c < 32) {
+      if (lane == c) cmin_r = v;
+    } else if (lane == 0) {
+      cmin[c] = v;
+    }
+  }
+
+  // next_fin = min over the live chunks' minima.
+  __device__ __forceinline__ void refresh_next_fin() {
+    const int nch = (R_end + 31) >> 5;
+    int m = (lane < nch) ? cmin_r : INT_MAX;
+    for (int c = 32 + lane; c < nch; c += 32) m = min(m, cmin[c]);
+    next_fin = __reduce_min_sync(kFull, m);
   }
 
   __device__ __forceinline__ void trim() {
@@ -245,19 +279,21 @@ struct WarpEngine {
     for (int base = 0; base < R_end; base += 32) {
       const int i = base + lane;
       const int y = (i < R_end) ? run[i].y : INT_MAX;
-      const int m = warp_min_i(y);
-      if (lane == 0) cmin[base >> 5] = m;
+      cmin_set(base >> 5, warp_min_i(y));
     }
     __syncwarp();
+    refresh_next_fin();
   }
 
-  // complete_finished (kv_scheduler.cpp:238-259).
+  // complete_finished (kv_scheduler.cpp:238-259). Only called once
+  // iter >= next_fin, i.e. when some chunk may hold a retiree.
   __device__ __forceinline__ void retire(const EngineParams& P) {
-    long long released = 0, nfin = 0;
+    long long released = 0;
+    int nf = 0;
     const int nch = (R_end + 31) >> 5;
     for (int c0 = 0; c0 < nch; c0 += 32) {
       const int c = c0 + lane;
-      const int cm = (c < nch) ? cmin[c] : INT_MAX;
+      const int cm = (c >= nch) ? INT_MAX : (c0 == 0 ? cmin_r : cmin[c]);
       unsigned due = __ballot_sync(kFull, cm <= iter);
       while (due) {
         const int cc = c0 + __ffs(due) - 1;
@@ -276,9 +312,8 @@ struct WarpEngine {
           zero = atomicSub(&run_cnt[a], 1) == 1;
           run[i] = make_int4(-1, INT_MAX, 0, 0);
         }
-        nfin += fin;
-        const int live_min = warp_min_i((e.x >= 0 && !fin) ? e.y : INT_MAX);
-        if (lane == 0) cmin[cc] = live_min;
+        nf += __popc(__ballot_sync(kFull, fin));
+        cmin_set(cc, warp_min_i((e.x >= 0 && !fin) ? e.y : INT_MAX));
         unsigned zm = __ballot_sync(kFull, zero);
         while (zm) {
           const int src = __ffs(zm) - 1;
@@ -288,16 +323,21 @@ struct WarpEngine {
       }
     }
     __syncwarp();
+    if (nf == 0) {
+      refresh_next_fin();
+      return;
+    }
     const long long rel = warp_sum_ll(released);
-    const long long nf = warp_sum_ll(nfin);
-    if (nf == 0) return;
     used -= rel;
     finished += nf;
     sum_m += nf;
     waived = -1;
     R -= static_cast<int>(nf);
     trim();
-    if (R_end - R > max(R, 32)) compact();
+    if (R_end - R > max(R, 32))
+      compact();
+    else
+      refresh_next_fin();
   }
 
   // Insert a preempted request into waiting_preempted ordered by
@@ -569,77 +609,125 @@ struct WarpEngine {
     last_stop = -1;
     // Acting adapters of this scan. When at most 32 can act (always for
     // N <= 32; and in the slot-starved steady state, where only the <= G
-    // claimed adapters act), each lane holds one of them and an event is a
-    // single warp argmin; otherwise act_key[] holds the candidate heads.
+    // claimed adapters act), each lane owns one of them (lane mode) and an
+    // event is one redux.sync argmin. The lane set persists across scans and
+    // is reconciled with this scan's acting set (adapters whose chain filled
+    // or emptied, claims and releases); otherwise act_key[] holds the heads.
     const uint32_t act_w = nonempty_w & ~blocked_w & ~(mass ? (slotful_w & ~claimed_w) : 0u);
-    const int cnt_w = __popc(act_w);
-    int pre = cnt_w;  // inclusive prefix over lanes
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(kFull, pre, o);
-      if (lane >= o) pre += t;
-    }
-    const int n_act = __shfl_sync(kFull, pre, 31);
+    const int n_act = __reduce_add_sync(kFull, __popc(act_w));
     const bool lane_mode = n_act <= 32;
-    int lk = INT_MAX, la = -1;
-    int4 my_nd = make_int4(0, 0, -1, 0);  // lane mode: node of this lane's head, prefetched
+    int lk = INT_MAX, la = -1;  // non-lane mode: this lane's best (head, adapter)
     if (lane_mode) {
-      const int excl = pre - cnt_w;  // exclusive prefix of this lane's word
-      for (int m = 0; m * 32 < N; ++m) {
-        const uint32_t wm = __shfl_sync(kFull, act_w, m);
-        const int base = __shfl_sync(kFull, excl, m);
-        const int k = lane - base;
-        if (wm && k >= 0 && k < __popc(wm)) {
-          const int a = m * 32 + static_cast<int>(__fns(wm, 0, k + 1));
-          la = a;
-          lk = q_head[a];
+      bool rebuild = !pl_valid;
+      if (!rebuild) {
+        const uint32_t removed = built_w & ~act_w;
+        if (__any_sync(kFull, removed != 0)) {
+          const bool rm = mask_bit(removed, pl_a < 0 ? 0 : pl_a);
+          if (pl_a >= 0 && rm) {
+            pl_a = -1;
+            pl_k = INT_MAX;
+          }
+          built_w &= ~removed;
+        }
+        uint32_t add = act_w & ~built_w;
+        const int n_add = __reduce_add_sync(kFull, __popc(add));
+        if (n_add > 8) {
+          rebuild = true;
+        } else {
+          for (int k = 0; k < n_add; ++k) {
+            const int a = mask_lowest(add);
+            mask_clear(add, a, lane);
+            const bool sfa = mask_bit(slotful_w, a);
+            const int fl = __ffs(__ballot_sync(kFull, pl_a < 0)) - 1;  // exists: n_act <= 32
+            if (lane == fl) {
+              pl_a = a;
+              pl_k = q_head[a];
+              pl_nd = node[pl_k];
+              pl_sf = sfa;
+            }
+            mask_set(built_w, a, lane);
+          }
         }
       }
-      if (lk != INT_MAX) my_nd = node[lk];
+      if (rebuild) {
+        const int cnt_w = __popc(act_w);
+        int pre = cnt_w;  // inclusive prefix over lanes
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(kFull, pre, o);
+          if (lane >= o) pre += t;
+        }
+        const int excl = pre - cnt_w;  // exclusive prefix of this lane's word
+        pl_a = -1;
+        pl_k = INT_MAX;
+        for (int m = 0; m * 32 < N; ++m) {
+          const uint32_t wm = __shfl_sync(kFull, act_w, m);
+          const int base = __shfl_sync(kFull, excl, m);
+          const int k = lane - base;
+          if (wm && k >= 0 && k < __popc(wm)) {
+            pl_a = m * 32 + static_cast<int>(__fns(wm, 0, k + 1));
+            pl_k = q_head[pl_a];
+          }
+        }
+        if (pl_k != INT_MAX) pl_nd = node[pl_k];
+        pl_sf = mask_bit(slotful_w, pl_a < 0 ? 0 : pl_a);
+        built_w = act_w;
+        pl_valid = true;
+      }
+      pl_cl = mask_bit(claimed_w, pl_a < 0 ? 0 : pl_a);  // claims/releases since the last scan
     } else {
+      pl_valid = false;
+      pl_a = -1;
+      pl_k = INT_MAX;
       build_act_keys(mass, false);
       __syncwarp();
       local_best(&lk, &la);
     }
     int stop_id = INT_MAX;
     for (;;) {
-      int k = lk, a = la;
-      for (int o = 16; o > 0; o >>= 1) {
-        const int ok = __shfl_xor_sync(kFull, k, o);
-        const int oa = __shfl_xor_sync(kFull, a, o);
-        if (ok < k) {
-          k = ok;
-          a = oa;
-        }
-      }
-      if (k == INT_MAX) break;
-      const int id = k;
-      const bool mine = lane_mode ? (la == a) : (lane == (a & 31));  // the lane that owns a
-      ++sum_v;
+      int id, a;
+      bool sf, cl;
       int4 nd;  // {in, out, next, adapter}
       if (lane_mode) {
-        const int src = __ffs(__ballot_sync(kFull, mine)) - 1;
-        nd.x = __shfl_sync(kFull, my_nd.x, src);
-        nd.y = __shfl_sync(kFull, my_nd.y, src);
-        nd.z = __shfl_sync(kFull, my_nd.z, src);
-        nd.w = __shfl_sync(kFull, my_nd.w, src);
+        const unsigned kmin = __reduce_min_sync(kFull, static_cast<unsigned>(pl_k));
+        if (kmin == static_cast<unsigned>(INT_MAX)) break;
+        const int src = __ffs(__ballot_sync(kFull, static_cast<unsigned>(pl_k) == kmin)) - 1;
+        id = static_cast<int>(kmin);
+        const int packed = pl_a | (pl_sf ? (1 << 29) : 0) | (pl_cl ? (1 << 28) : 0);
+        const int pk = __shfl_sync(kFull, packed, src);
+        a = pk & kAdapterMask;
+        sf = (pk >> 29) & 1;
+        cl = (pk >> 28) & 1;
+        nd.x = __shfl_sync(kFull, pl_nd.x, src);
+        nd.y = __shfl_sync(kFull, pl_nd.y, src);
+        nd.z = __shfl_sync(kFull, pl_nd.z, src);
+        nd.w = a;
       } else {
+        const unsigned kmin = __reduce_min_sync(kFull, static_cast<unsigned>(lk));
+        if (kmin == static_cast<unsigned>(INT_MAX)) break;
+        const int src = __ffs(__ballot_sync(kFull, static_cast<unsigned>(lk) == kmin)) - 1;
+        id = static_cast<int>(kmin);
+        a = __shfl_sync(kFull, la, src);
         nd = node[id];
+        sf = mask_bit(slotful_w, a);
+        cl = mask_bit(claimed_w, a);
       }
-      const bool sf = mask_bit(slotful_w, a);
-      const bool cl = mask_bit(claimed_w, a);
+      const bool mine = lane_mode ? (pl_a == a) : (lane == (a & 31));  // the lane that owns a
+      ++sum_v;
       if (sf && !cl && !can_claim(a)) {
         block_adapter(a);
         if (!P.priority) {
           stop_id = id;
           break;
         }
-        if (mine) {
-          if (lane_mode) {
-            lk = INT_MAX;
-          } else {
-            act_key[a] = INT_MAX;
-            local_best(&lk, &la);
+        if (lane_mode) {
+          if (mine) {
+            pl_a = -1;
+            pl_k = INT_MAX;
           }
+          mask_clear(built_w, a, lane);
+        } else if (mine) {
+          act_key[a] = INT_MAX;
+          local_best(&lk, &la);
         }
         continue;
       }
@@ -653,51 +741,57 @@ struct WarpEngine {
         break;
       }
       used += demand;
-      if (sf) claim(a);
-      const int fin = iter + nd.y;
-      const int c = q_cnt[a] - 1;
-      run_append(make_int4(id, fin, a | kFreshBit, nd.x + nd.y));
+      const bool claiming = sf && !cl;
+      if (claiming) claim(a);
+      run_append(make_int4(id, iter + nd.y, a | kFreshBit, nd.x + nd.y));
+      if (lane == (n_fresh & 31)) fresh_id = id;
+      ++n_fresh;
+      const int next = nd.z;
       if (lane == 0) {
         run_cnt[a] += 1;
         P.r_phase[rb + id] = kRunning;
-        q_cnt[a] = c;
-        if (c == 0) {
-          q_head[a] = -1;
-          q_tail[a] = -1;
-        } else {
-          q_head[a] = nd.z;
-        }
+        q_head[a] = next;
+        if (next < 0) q_tail[a] = -1;
       }
-      if (c == 0) mask_clear(nonempty_w, a, lane);
+      if (next < 0) mask_clear(nonempty_w, a, lane);
       --Wf;
       ++sum_m;
-      const bool mass2 = P.priority && free_slots == 0 && !pool_any();
-      const int next_key = (c == 0) ? INT_MAX : nd.z;
       if (lane_mode) {
         if (mine) {
-          lk = next_key;
-          if (next_key != INT_MAX) my_nd = node[next_key];  // in flight until this lane wins again
+          pl_cl = pl_cl || claiming;
+          if (next < 0) {
+            pl_a = -1;
+            pl_k = INT_MAX;
+          } else {
+            pl_k = next;
+            pl_nd = node[next];  // in flight until this lane wins again
+          }
         }
+        if (next < 0) mask_clear(built_w, a, lane);
+      } else if (mine) {
+        act_key[a] = (next < 0) ? INT_MAX : next;
+      }
+      if (claiming) {
+        const bool mass2 = P.priority && free_slots == 0 && !pool_any();
         if (mass2 != mass) {
           mass = mass2;
           // every unclaimed adapter that needs a slot is now blocked
-          const int la0 = la < 0 ? 0 : la;
-          const bool s_l = mask_bit(slotful_w, la0);  // all lanes shuffle (no short-circuit)
-          const bool c_l = mask_bit(claimed_w, la0);
-          if (la >= 0 && s_l && !c_l) lk = INT_MAX;
-        }
-      } else {
-        if (mine) act_key[a] = next_key;
-        if (mass2 != mass) {
-          mass = mass2;
-          __syncwarp();
-          build_act_keys(mass, true);
-          __syncwarp();
-          local_best(&lk, &la);
-        } else if (mine) {
-          local_best(&lk, &la);
+          if (lane_mode) {
+            if (pl_a >= 0 && pl_sf && !pl_cl) {
+              pl_a = -1;
+              pl_k = INT_MAX;
+            }
+            built_w &= ~(slotful_w & ~claimed_w);
+          } else {
+            __syncwarp();
+            build_act_keys(mass, true);
+            __syncwarp();
+            local_best(&lk, &la);
+            continue;
+          }
         }
       }
+      if (!lane_mode && mine) local_best(&lk, &la);
       __syncwarp();
     }
     reject_oversized(P, stop_id);
@@ -835,8 +929,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   E.run_cnt = reinterpret_cast<int32_t*>(E.last_used + NA);
   E.q_head = E.run_cnt + NA;
   E.q_tail = E.q_head + NA;
-  E.q_cnt = E.q_tail + NA;
-  E.act_key = E.q_cnt + NA;
+  E.act_key = E.q_tail + NA;
   const int64_t wsb = P.ws_per_scenario ? sc.req_begin : static_cast<int64_t>(slot) * P.ws_stride;
   const int64_t wcb = P.ws_per_scenario ? (sc.req_begin >> 5) + 2 * static_cast<int64_t>(s)
                                         : static_cast<int64_t>(slot) * (P.ws_stride / 32 + 2);
@@ -850,7 +943,6 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     E.run_cnt[a] = 0;
     E.q_head[a] = -1;
     E.q_tail[a] = -1;
-    E.q_cnt[a] = 0;
     E.act_key[a] = INT_MAX;
   }
   __syncwarp();
@@ -869,19 +961,19 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     pf_in = P.r_in[E.rb + jc];
     pf_out = P.r_out[E.rb + jc];
   }
+  double next_arr = __shfl_sync(kFull, pf_t, 0);  // arrival time of request `ingest`
 
   while (true) {
     __syncwarp();
     if (E.R == 0 && E.Wp + E.Wf == 0) {
       if (E.ingest >= E.n_req) break;  // fully drained
-      const double t = __shfl_sync(kFull, pf_t, 0);
-      E.clock = E.clock < t ? t : E.clock;  // std::max(clock_, arrival)
+      E.clock = E.clock < next_arr ? next_arr : E.clock;  // std::max(clock_, arrival)
     }
     // ingest arrivals <= clock (engine.cpp:88-92): append to the adapter's
     // FIFO chain, or to the oversized FIFO when in + 1 > capacity. The next
     // 32 arrivals are kept prefetched in registers (pf_*), so an iteration
     // with no arrival costs one comparison and one with arrivals no waiting.
-    while (E.ingest < E.n_req && __shfl_sync(kFull, pf_t, 0) <= E.clock) {
+    while (E.ingest < E.n_req && next_arr <= E.clock) {
       const int i = E.ingest + lane;
       const bool ok = (i < E.n_req) & (pf_t <= E.clock);
       const unsigned b = __ballot_sync(kFull, ok);
@@ -899,17 +991,19 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         const int src = __ffs(m) - 1;
         m &= m - 1;
         const int a = __shfl_sync(kFull, a_l, src);
+        const int id = E.ingest + src;
+        const int t = E.q_tail[a];
         if (lane == 0) {
-          const int id = E.ingest + src;
-          const int t = E.q_tail[a];
           if (t < 0)
             E.q_head[a] = id;
           else
             reinterpret_cast<int*>(&E.node[t])[2] = id;
           E.q_tail[a] = id;
-          E.q_cnt[a] += 1;
         }
+        // the lane holding this chain's head node in registers sees its link
+        if (E.pl_a == a && E.pl_k == t) E.pl_nd.z = id;
         mask_set(E.nonempty_w, a, lane);
+        __syncwarp();
       }
       E.Wf += n;
       E.ingest += n;
@@ -920,6 +1014,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         const int a2 = __shfl_sync(kFull, pf_a, srcl & 31);
         const int in2 = __shfl_sync(kFull, pf_in, srcl & 31);
         const int out2 = __shfl_sync(kFull, pf_out, srcl & 31);
+        const double nxt = __shfl_sync(kFull, t2, 0);  // lane 0's new head when n < 32
         if (srcl < 32) {
           pf_t = t2;
           pf_a = a2;
@@ -933,13 +1028,15 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
           pf_in = P.r_in[E.rb + jc];
           pf_out = P.r_out[E.rb + jc];
         }
+        // (n == 32: lane 0 refilled from memory, wait for it)
+        next_arr = (n < 32) ? nxt : __shfl_sync(kFull, pf_t, 0);
       }
       __syncwarp();
       if (n < 32) break;
     }
     __syncwarp();
     LT_PH(0);
-    if (E.R > 0) E.retire(P);
+    if (E.R > 0 && E.iter >= E.next_fin) E.retire(P);
     LT_PH(1);
     if (!E.alloc(P)) break;
     LT_PH(2);
@@ -949,6 +1046,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     E.free_slots = E.G - E.resident_count;
     E.evicted_w = 0;
     E.blocked_w = 0;
+    E.n_fresh = 0;
     {
       bool go = true;
       E.Wp = E.scan(P, E.pq, E.Wp, true, &go);
@@ -981,9 +1079,13 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     const double lat = sched + loads + model * adapters;
     const double emit = E.clock + lat;
     // first tokens of this iteration's fresh admissions (engine.cpp:131)
-    for (int i = r_before + lane; i < E.R_end; i += 32) {
-      const int4 e = E.run[i];
-      if (e.z & kFreshBit) P.r_first[E.rb + e.x] = emit;
+    if (E.n_fresh <= 32) {
+      if (lane < E.n_fresh) P.r_first[E.rb + E.fresh_id] = emit;
+    } else {
+      for (int i = r_before + lane; i < E.R_end; i += 32) {
+        const int4 e = E.run[i];
+        if (e.z & kFreshBit) P.r_first[E.rb + e.x] = emit;
+      }
     }
     __syncwarp();
     E.tok_tot += E.R;
@@ -1016,15 +1118,12 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     // iterations only advance the clock by `lat` (one rounded add each, as
     // the reference does), grow the ledger by R and count R tokens.
     if (E.Wp + E.Wf == w_before && E.R == rcount_before && E.waived < 0) {
-      int min_fin = INT_MAX;
-      for (int c = lane; c < ((E.R_end + 31) >> 5); c += 32) min_fin = min(min_fin, E.cmin[c]);
-      min_fin = warp_min_i(min_fin);
-      const long long n_fin = static_cast<long long>(min_fin) - E.iter;
+      const long long n_fin = static_cast<long long>(E.next_fin) - E.iter;
       const long long n_mem = (E.cap - E.used) / E.R;
       const long long n_cap = static_cast<long long>(E.iter_cap) - 1 - E.iter;
       long long n_max = n_fin < n_mem ? n_fin : n_mem;
       n_max = n_max < n_cap ? n_max : n_cap;
-      const double t_next = E.ingest < E.n_req ? __shfl_sync(kFull, pf_t, 0) : INFINITY;
+      const double t_next = E.ingest < E.n_req ? next_arr : INFINITY;
       if (n_max > 0 && t_next > E.clock) {
         const double lat_q = sched + model * adapters;  // loads == 0
         double clk = E.clock, start = E.clock;
@@ -1134,7 +1233,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
 
 // Persistent kernel: each warp pulls scenarios (cost-descending order) from a
 // global counter until the batch is drained.
-__global__ void __launch_bounds__(256) engine_kernel(EngineParams P) {
+__global__ void __launch_bounds__(256, 1) engine_kernel(EngineParams P) {
   extern __shared__ __align__(16) char smem[];
   const int warp = threadIdx.x >> 5;
   const int slot = blockIdx.x * (blockDim.x >> 5) + warp;

@@ -28,8 +28,9 @@ def main():
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, capture_output=True)
     cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-    dis = subprocess.run(["nvdisasm", "-g", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+    dis = subprocess.run(["nvdisasm", "-g", "-gi", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
     line_of = {}
+    chain = []  # consecutive //## lines: the inline chain, innermost first
     cur = None
     infn = False
     for l in dis.splitlines():
@@ -37,7 +38,13 @@ def main():
             infn = fn in l
         m = re.search(r'//## File "([^"]+)", line (\d+)', l)
         if m:
-            cur = (os.path.basename(m.group(1)), int(m.group(2)))
+            chain.append((os.path.basename(m.group(1)), int(m.group(2))))
+            continue
+        if chain:
+            # charge warp intrinsics / helper headers to the innermost kernel-source line
+            ks = [c for c in chain if c[0].startswith("k_")]
+            cur = ks[0] if ks else chain[0]
+            chain = []
         m = re.search(r"/\*([0-9a-f]{4,})\*/", l)
         if m and infn:
             line_of[int(m.group(1), 16)] = cur
@@ -49,7 +56,7 @@ def main():
         agg[key] += s
         exe[key] += e
         tot += s
-    print("total samples", tot)
+    print("total samples", tot, "instructions", sum(exe.values()))
     for key, s in agg.most_common(top):
         print(f"{s / tot * 100:6.2f}%  {key[0]}:{key[1]}  inst={exe[key]}")
 
