@@ -41,21 +41,22 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build_gpu(force: bool = False, verbose: bool = False, prof: bool = False) -> str:
+def build_gpu(force: bool = False, verbose: bool = False, prof: bool = False, stats: bool = False) -> str:
     """libloratwin_gpu.so; prof=True builds libloratwin_gpu_prof.so with the
-    per-phase cycle counters (-DLT_PHASE_PROF) used by tools/diag_phase.py."""
-    lib = LIB.replace(".so", "_prof.so") if prof else LIB
+    per-phase cycle counters (-DLT_PHASE_PROF) used by tools/diag_phase.py,
+    stats=True libloratwin_gpu_stats.so with scan counters (-DLT_SCAN_STATS)."""
+    lib = LIB.replace(".so", "_prof.so") if prof else (LIB.replace(".so", "_stats.so") if stats else LIB)
     deps = glob.glob(os.path.join(CSRC, "*")) + [os.path.join(INCLUDE, "loratwin_gpu.h")]
     if not force and not _stale(lib, deps):
         return lib
     os.makedirs(os.path.dirname(lib), exist_ok=True)
-    cmd = [nvcc()] + NVCC_FLAGS + (["-DLT_PHASE_PROF"] if prof else []) + [
+    cmd = [nvcc()] + NVCC_FLAGS + (["-DLT_PHASE_PROF"] if prof else []) + (["-DLT_SCAN_STATS"] if stats else []) + [
         "-I" + INCLUDE, "-I" + CSRC, "-shared", "-o", lib, os.path.join(CSRC, "capi.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libloratwin_gpu.so")
-    with open(os.path.join(os.path.dirname(lib), "ptxas_prof.log" if prof else "ptxas.log"), "w") as f:
+    with open(os.path.join(os.path.dirname(lib), "ptxas" + ("_prof" if prof else "_stats" if stats else "") + ".log"), "w") as f:
         f.write(res.stderr)
     if verbose:
         sys.stderr.write(res.stderr)

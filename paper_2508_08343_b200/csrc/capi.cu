@@ -394,6 +394,7 @@ struct lt_plan {
   DBuf<DAdapter> adapters;
   DBuf<DLen> lens;
   DBuf<DKey> keys;
+  DBuf<uint64_t> seed_state;   // K0a -> K0b: seeded MT19937-64 states of one key chunk
   DBuf<double> E;
   DBuf<double2> Z;
   DBuf<int32_t> order;
@@ -426,6 +427,7 @@ struct lt_plan {
   int grid = 0;
   int block = 256;
   size_t smem = 0;
+  int32_t run_cap = 0, smem_per_warp = 0;
   int want_digest = 0;
   double tables_ms = 0, h2d_ms = 0;
   int64_t h2d_bytes = 0;
@@ -650,6 +652,31 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+// Keys seeded and drawn per chunk (the seeded states take 5 KB per key).
+constexpr int64_t kSeedChunk = 1 << 18;
+
+// K0: seed_kernel (seed_seq, one thread per stream) then tables_draw_kernel
+// (one warp per key), chunk by chunk. Returns the launches.
+int launch_tables(lt_plan& P, int nk, cudaStream_t st) {
+  LT_CUDA(cudaFuncSetAttribute(seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(kSeedSmem)));
+  int launches = 0;
+  for (int64_t k0 = 0; k0 < nk; k0 += kSeedChunk) {
+    const int n = static_cast<int>(std::min<int64_t>(kSeedChunk, nk - k0));
+    seed_kernel<<<(2 * n + kSeedThreads - 1) / kSeedThreads, kSeedThreads, kSeedSmem, st>>>(
+        P.keys.p, static_cast<int>(k0), n, P.seed_state.p);
+    after_launch("seed_kernel", st);
+    const unsigned g = static_cast<unsigned>((n + 3) / 4);
+    if (P.cfg.variant)
+      tables_draw_kernel<true><<<g, 128, 0, st>>>(P.keys.p, static_cast<int>(k0), n, P.seed_state.p, P.E.p, P.Z.p);
+    else
+      tables_draw_kernel<false><<<g, 128, 0, st>>>(P.keys.p, static_cast<int>(k0), n, P.seed_state.p, P.E.p, P.Z.p);
+    after_launch("tables_draw_kernel", st);
+    launches += 2;
+  }
+  return launches;
+}
+
 // Builds a plan: validation, RNG tables, counting, merge, request arrays,
 // workspace. Leaves everything resident; returns nullptr + status on error.
 lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_config* cfg,
@@ -688,20 +715,14 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     k.z_off = e_total;
     e_total += k.cap;
   }
+  if (!pr.keys.empty())
+    P.seed_state.alloc(std::min<int64_t>(static_cast<int64_t>(pr.keys.size()), kSeedChunk) * 2 * kMtN);
   for (int attempt = 0;; ++attempt) {
     P.keys.upload(pr.keys, st);
     P.E.alloc(std::max<int64_t>(e_total, 1));
     P.Z.alloc(std::max<int64_t>(e_total, 1));
     P.h2d_bytes += pr.keys.size() * sizeof(DKey);
-    if (!pr.keys.empty()) {
-      const int nk = static_cast<int>(pr.keys.size());
-      if (P.cfg.variant)
-        tables_kernel<true><<<(nk + 127) / 128, 128, 0, st>>>(P.keys.p, nk, P.E.p, P.Z.p);
-      else
-        tables_kernel<false><<<(nk + 127) / 128, 128, 0, st>>>(P.keys.p, nk, P.E.p, P.Z.p);
-      after_launch("tables_kernel", st);
-      ++P.launches_prep;
-    }
+    if (!pr.keys.empty()) P.launches_prep += launch_tables(P, static_cast<int>(pr.keys.size()), st);
     std::vector<DKey> back(pr.keys.size());
     if (!back.empty())
       LT_CUDA(cudaMemcpyAsync(back.data(), P.keys.p, back.size() * sizeof(DKey), cudaMemcpyDeviceToHost, st));
@@ -748,7 +769,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     P.adp_count.alloc(n_pairs);
     LT_CUDA(cudaMemsetAsync(P.scen_count.p, 0, P.n_scen * sizeof(unsigned long long), st));
     LT_CUDA(cudaMemsetAsync(P.overflow.p, 0, sizeof(int32_t), st));
-    count_kernel<<<static_cast<unsigned>((n_pairs + 255) / 256), 256, 0, st>>>(
+    count_kernel<<<static_cast<unsigned>((n_pairs + 7) / 8), 256, 0, st>>>(
         P.scen.p, P.pair_scen.p, P.pair_adp.p, n_pairs, P.adapters.p, P.keys.p, P.E.p, P.adp_count.p,
         P.scen_count.p, P.overflow.p);
     after_launch("count_kernel", st);
@@ -842,13 +863,20 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   P.order.upload(P.h_order, st);
   P.counter.alloc(1);
   P.out.alloc(std::max<int64_t>(P.n_scen, 1));
-  // occupancy-sized persistent grid
+  // occupancy-sized persistent grid: 8 warps per block, one block per SM
+  // (the engine kernel runs at ~200 registers). Per warp: the adapter tables
+  // plus as much of the running set as fits in shared memory.
   {
-    const size_t per_warp = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter;
-    int warps = 8;
-    while (warps > 1 && per_warp * warps > 200 * 1024) warps /= 2;
+    const int warps = 8;
+    const size_t budget = 216 * 1024;  // per block, below the 227 KB opt-in limit
+    const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter;
+    const size_t per_warp_max = budget / warps;
+    int64_t cap = per_warp_max > adapters ? static_cast<int64_t>((per_warp_max - adapters) / sizeof(int4)) : 0;
+    cap = std::min<int64_t>(cap, 1024) / 32 * 32;
+    P.run_cap = static_cast<int32_t>(cap);
+    P.smem_per_warp = static_cast<int32_t>(adapters + static_cast<size_t>(cap) * sizeof(int4));
     P.block = warps * 32;
-    P.smem = per_warp * warps;
+    P.smem = static_cast<size_t>(P.smem_per_warp) * warps;
   }
   LT_CUDA(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(P.smem)));
@@ -887,20 +915,14 @@ void prepare_requests(lt_plan& P) {
   // K0: RNG tables, arrival counts and request offsets are recomputed on
   // device every run (the first run after lt_plan_simulate reuses the ones
   // computed while sizing the buffers).
-  if (!P.fresh && P.n_keys > 0) {
-    if (P.cfg.variant)
-      tables_kernel<true><<<(P.n_keys + 127) / 128, 128, 0, st>>>(P.keys.p, P.n_keys, P.E.p, P.Z.p);
-    else
-      tables_kernel<false><<<(P.n_keys + 127) / 128, 128, 0, st>>>(P.keys.p, P.n_keys, P.E.p, P.Z.p);
-    after_launch("tables_kernel", st);
-  }
+  int64_t launches = 0;
+  if (!P.fresh && P.n_keys > 0) launches += launch_tables(P, P.n_keys, st);
   cudaEventRecord(ctx->ev[1], st);
-  int64_t launches = (!P.fresh && P.n_keys > 0) ? 1 : 0;
   if (!P.fresh && P.n_scen > 0) {
     LT_CUDA(cudaMemcpyAsync(P.scen_count.p, P.base_count.p, P.n_scen * sizeof(unsigned long long),
                             cudaMemcpyDeviceToDevice, st));
     if (P.n_pairs > 0) {
-      count_kernel<<<static_cast<unsigned>((P.n_pairs + 255) / 256), 256, 0, st>>>(
+      count_kernel<<<static_cast<unsigned>((P.n_pairs + 7) / 8), 256, 0, st>>>(
           P.scen.p, P.pair_scen.p, P.pair_adp.p, P.n_pairs, P.adapters.p, P.keys.p, P.E.p, P.adp_count.p,
           P.scen_count.p, P.overflow.p);
       after_launch("count_kernel", st);
@@ -921,7 +943,7 @@ void prepare_requests(lt_plan& P) {
     size_t tb = P.pscan_tmp_bytes;
     LT_CUDA(cub::DeviceScan::ExclusiveSum(P.pscan_tmp.p, tb, P.adp_count.p, P.pair_excl.p,
                                           static_cast<int>(P.n_pairs), st));
-    expand_kernel<<<static_cast<unsigned>((P.n_pairs + 127) / 128), 128, 0, st>>>(
+    expand_kernel<<<static_cast<unsigned>((P.n_pairs + 7) / 8), 256, 0, st>>>(
         P.scen.p, P.pair_scen.p, P.pair_adp.p, P.n_pairs, P.pair_begin.p, P.adapters.p, P.keys.p, P.E.p,
         P.adp_count.p, P.pair_excl.p, P.st_in.p, P.sv_in.p);
     after_launch("expand_kernel", st);
@@ -932,9 +954,9 @@ void prepare_requests(lt_plan& P) {
     LT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(P.sort_tmp.p, sb, P.st_in.p, P.st_out.p, P.sv_in.p,
                                                       P.sv_out.p, static_cast<int>(std::max<int64_t>(P.total_req, 1)),
                                                       static_cast<int>(P.n_scen), P.seg_begin.p, P.seg_end.p, st));
-    gather_kernel<<<static_cast<unsigned>((P.n_scen + 7) / 8), 256, 0, st>>>(
-        P.scen.p, static_cast<int>(P.n_scen), P.adapters.p, P.keys.p, P.lens.p, P.Z.p, P.st_out.p, P.sv_out.p,
-        P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p);
+    gather_kernel<<<static_cast<unsigned>((std::max<int64_t>(P.total_req, 1) + 255) / 256), 256, 0, st>>>(
+        P.scen.p, static_cast<int>(P.n_scen), P.total_req, P.adapters.p, P.keys.p, P.lens.p, P.Z.p, P.st_out.p,
+        P.sv_out.p, P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p);
     after_launch("gather_kernel", st);
     launches += 3;  // + CUB scan and segmented sort (library kernels)
   }
@@ -959,6 +981,8 @@ void run_plan(lt_plan& P) {
   E.order = P.order.p;
   E.n_scen = static_cast<int32_t>(P.n_scen);
   E.max_adapters = P.max_adapters;
+  E.run_cap = P.run_cap;
+  E.smem_per_warp = P.smem_per_warp;
   E.counter = P.counter.p;
   E.adapters = P.adapters.p;
   E.r_arr = P.r_arr.p;

@@ -107,7 +107,18 @@ __device__ __forceinline__ uint64_t fold64(uint64_t h, uint64_t w) {
   return h;
 }
 
+#ifdef LT_SCAN_STATS
+#define LT_STAT(k) (++st[k])
+#else
+#define LT_STAT(k) ((void)0)
+#endif
+
 struct WarpEngine {
+#ifdef LT_SCAN_STATS
+  // diagnostics build: fresh scans, stop-cache hits, lane-mode scans,
+  // lane-set rebuilds, non-lane scans, retire calls
+  long long st[6] = {0, 0, 0, 0, 0, 0};
+#endif
   // --- warp-uniform scalars
   double clock = 0.0, prev_now = 0.0, duration = 0.0;
   int64_t used = 0, cap = 0;
@@ -158,7 +169,9 @@ struct WarpEngine {
   int64_t last_stop_demand = 0;
   uint32_t act_epoch = 0, stop_epoch = 0;
   bool stop_mass = false;
-  int4* run = nullptr;
+  int4* run = nullptr;   // global tier of the running set (positions >= run_cap)
+  int4* runs = nullptr;  // shared-memory tier (positions < run_cap)
+  int32_t run_cap = 0;
   int32_t* cmin = nullptr;  // per 32-entry chunk of run[]: lower bound of live retire iterations
   int2* pq = nullptr;
   int4* node = nullptr;  // per waiting fresh request: {in, out, next-in-chain, adapter}
@@ -219,11 +232,14 @@ struct WarpEngine {
   // for retired entries; cmin[c] bounds the retire iteration of chunk c from
   // below, so an iteration only touches the chunks that hold a retiree. The
   // last entry is always live (trim), so LIFO preemption pops run[R_end-1].
+  // Running-set slot `pos`: the first run_cap slots live in shared memory.
+  __device__ __forceinline__ int4* rp(int pos) const { return pos < run_cap ? runs + pos : run + pos; }
+
   __device__ __forceinline__ void run_append(int4 e) {
     const int pos = R_end;
     const int c = pos >> 5;
     if (lane == 0) {
-      run[pos] = e;
+      *rp(pos) = e;
       if (c >= 32) cmin[c] = (pos & 31) ? min(cmin[c], e.y) : e.y;
     }
     if (c < 32 && lane == c) cmin_r = (pos & 31) ? min(cmin_r, e.y) : e.y;
@@ -253,7 +269,7 @@ struct WarpEngine {
     while (R_end > 0) {
       const int lo = max(0, R_end - 32);
       const int i = lo + lane;
-      const bool live = i < R_end && run[i].x >= 0;
+      const bool live = i < R_end && rp(i)->x >= 0;
       const unsigned lm = __ballot_sync(kFull, live);
       if (lm) {
         R_end = lo + 32 - __clz(lm);
@@ -269,16 +285,16 @@ struct WarpEngine {
     int w = 0;
     for (int base = 0; base < R_end; base += 32) {
       const int i = base + lane;
-      const int4 e = (i < R_end) ? run[i] : make_int4(-1, INT_MAX, 0, 0);
+      const int4 e = (i < R_end) ? *rp(i) : make_int4(-1, INT_MAX, 0, 0);
       const unsigned lm = __ballot_sync(kFull, e.x >= 0);
-      if (e.x >= 0) run[w + __popc(lm & lanemask_lt())] = e;
+      if (e.x >= 0) *rp(w + __popc(lm & lanemask_lt())) = e;
       w += __popc(lm);
     }
     __syncwarp();
     R_end = w;
     for (int base = 0; base < R_end; base += 32) {
       const int i = base + lane;
-      const int y = (i < R_end) ? run[i].y : INT_MAX;
+      const int y = (i < R_end) ? rp(i)->y : INT_MAX;
       cmin_set(base >> 5, warp_min_i(y));
     }
     __syncwarp();
@@ -288,6 +304,7 @@ struct WarpEngine {
   // complete_finished (kv_scheduler.cpp:238-259). Only called once
   // iter >= next_fin, i.e. when some chunk may hold a retiree.
   __device__ __forceinline__ void retire(const EngineParams& P) {
+    LT_STAT(5);
     long long released = 0;
     int nf = 0;
     const int nch = (R_end + 31) >> 5;
@@ -299,7 +316,7 @@ struct WarpEngine {
         const int cc = c0 + __ffs(due) - 1;
         due &= due - 1;
         const int i = cc * 32 + lane;
-        const int4 e = (i < R_end) ? run[i] : make_int4(-1, INT_MAX, 0, 0);
+        const int4 e = (i < R_end) ? *rp(i) : make_int4(-1, INT_MAX, 0, 0);
         const bool fin = e.x >= 0 && e.y <= iter;
         int a = 0;
         bool zero = false;
@@ -310,7 +327,7 @@ struct WarpEngine {
           P.r_last[rb + idx] = clock;  // completion == the final emit (engine.cpp:134)
           a = e.z & kAdapterMask;
           zero = atomicSub(&run_cnt[a], 1) == 1;
-          run[i] = make_int4(-1, INT_MAX, 0, 0);
+          *rp(i) = make_int4(-1, INT_MAX, 0, 0);
         }
         nf += __popc(__ballot_sync(kFull, fin));
         cmin_set(cc, warp_min_i((e.x >= 0 && !fin) ? e.y : INT_MAX));
@@ -381,7 +398,7 @@ struct WarpEngine {
     if (R == 0) return true;
     int64_t demand = R;
     while (used + demand > cap && R > 1) {
-      const int4 e = run[R_end - 1];
+      const int4 e = *rp(R_end - 1);
       --R;
       --R_end;
       trim();
@@ -409,7 +426,7 @@ struct WarpEngine {
       --demand;
     }
     if (used + demand > cap) {
-      const int4 e = run[R_end - 1];  // the sole survivor
+      const int4 e = *rp(R_end - 1);  // the sole survivor
       const int rem = e.y - iter;
       if (rem > 1 || used + demand - 1 > cap) {
         fail(LT_ERR_SIMULATION, LT_K_SOLE_SURVIVOR, e.x, 0);
@@ -594,6 +611,7 @@ struct WarpEngine {
   // entries (can never fit) sit in their own FIFO and are rejected up to the
   // stop point, as the reference rejects them when the scan passes them.
   __device__ __forceinline__ void scan_fresh(const EngineParams& P) {
+    LT_STAT(0);
     bool mass = P.priority && free_slots == 0 && !pool_any();
     // Steady-state shortcut: the previous fresh scan stopped on memory at
     // entry last_stop and no adapter has been claimed or released since (the
@@ -602,6 +620,7 @@ struct WarpEngine {
     // not fit, the scan stops right there, exactly as the full scan would.
     if (P.priority && last_stop >= 0 && stop_epoch == act_epoch && mass == stop_mass &&
         used + last_stop_demand > cap) {
+      LT_STAT(1);
       ++sum_v;
       reject_oversized(P, last_stop);
       return;
@@ -618,6 +637,7 @@ struct WarpEngine {
     const bool lane_mode = n_act <= 32;
     int lk = INT_MAX, la = -1;  // non-lane mode: this lane's best (head, adapter)
     if (lane_mode) {
+      LT_STAT(2);
       bool rebuild = !pl_valid;
       if (!rebuild) {
         const uint32_t removed = built_w & ~act_w;
@@ -650,6 +670,7 @@ struct WarpEngine {
         }
       }
       if (rebuild) {
+        LT_STAT(3);
         const int cnt_w = __popc(act_w);
         int pre = cnt_w;  // inclusive prefix over lanes
         for (int o = 1; o < 32; o <<= 1) {
@@ -675,6 +696,7 @@ struct WarpEngine {
       }
       pl_cl = mask_bit(claimed_w, pl_a < 0 ? 0 : pl_a);  // claims/releases since the last scan
     } else {
+      LT_STAT(4);
       pl_valid = false;
       pl_a = -1;
       pl_k = INT_MAX;
@@ -869,14 +891,14 @@ struct WarpEngine {
   }
 };
 
-// Ordered (sequential) FP sum of up to 32 per-lane values with flags.
+// Ordered (sequential) FP sum of the 32 lanes' values, lane 0 first: the
+// reference's std::accumulate order (metrics.cpp:29-32, :86-105). Unflagged
+// lanes add +0.0, which leaves a non-negative accumulator unchanged, so the
+// 32 shuffles are independent and only the adds form a chain.
 __device__ __forceinline__ double ordered_add(double acc, double v, bool f) {
-  unsigned m = __ballot_sync(kFull, f);
-  while (m) {
-    const int src = __ffs(m) - 1;
-    m &= m - 1;
-    acc = acc + __shfl_sync(kFull, v, src);
-  }
+  const double x = f ? v : 0.0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) acc = acc + __shfl_sync(kFull, x, k);
   return acc;
 }
 
@@ -930,6 +952,8 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   E.q_head = E.run_cnt + NA;
   E.q_tail = E.q_head + NA;
   E.act_key = E.q_tail + NA;
+  E.runs = reinterpret_cast<int4*>(E.act_key + NA);  // NA is a multiple of 32: 16-byte aligned
+  E.run_cap = P.run_cap;
   const int64_t wsb = P.ws_per_scenario ? sc.req_begin : static_cast<int64_t>(slot) * P.ws_stride;
   const int64_t wcb = P.ws_per_scenario ? (sc.req_begin >> 5) + 2 * static_cast<int64_t>(s)
                                         : static_cast<int64_t>(slot) * (P.ws_stride / 32 + 2);
@@ -1083,7 +1107,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
       if (lane < E.n_fresh) P.r_first[E.rb + E.fresh_id] = emit;
     } else {
       for (int i = r_before + lane; i < E.R_end; i += 32) {
-        const int4 e = E.run[i];
+        const int4 e = *E.rp(i);
         if (e.z & kFreshBit) P.r_first[E.rb + e.x] = emit;
       }
     }
@@ -1153,7 +1177,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   __syncwarp();
   // Requests still running keep their emitted tokens (truncation / error).
   for (int i = lane; i < E.R_end; i += 32) {
-    const int4 e = E.run[i];
+    const int4 e = *E.rp(i);
     if (e.x < 0) continue;
     const int outv = P.r_out[E.rb + e.x];
     P.r_gen[E.rb + e.x] = outv - (e.y - E.iter);
@@ -1208,7 +1232,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         nrej += __popc(__ballot_sync(kFull, is_rej));
         nfin += __popc(__ballot_sync(kFull, v && ph == kFinished));
         nttft += __popc(__ballot_sync(kFull, has_first));
-        rej_demand = ordered_add(rej_demand, static_cast<double>(outv) / window, is_rej);
+        if (__any_sync(kFull, is_rej)) rej_demand = ordered_add(rej_demand, static_cast<double>(outv) / window, is_rej);
         ttft_sum = ordered_add(ttft_sum, first - arr, has_first);
         itl_sum = ordered_add(itl_sum, last - first, has_itl);
         nitl += warp_sum_ll(has_itl ? gen - 1 : 0);
@@ -1227,6 +1251,9 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
 #ifdef LT_PHASE_PROF
   for (int k = 0; k < 6; ++k) o.phase_cycles[k] = ph[k];
 #endif
+#ifdef LT_SCAN_STATS
+  for (int k = 0; k < 6; ++k) o.phase_cycles[k] = E.st[k];
+#endif
   o.device_cycles = clock64() - t_start;
   if (lane == 0) P.out[s] = o;
 }
@@ -1237,7 +1264,7 @@ __global__ void __launch_bounds__(256, 1) engine_kernel(EngineParams P) {
   extern __shared__ __align__(16) char smem[];
   const int warp = threadIdx.x >> 5;
   const int slot = blockIdx.x * (blockDim.x >> 5) + warp;
-  char* mine = smem + static_cast<size_t>(warp) * P.max_adapters * kSmemPerAdapter;
+  char* mine = smem + static_cast<size_t>(warp) * P.smem_per_warp;
   for (;;) {
     int k = 0;
     if ((threadIdx.x & 31) == 0) k = atomicAdd(P.counter, 1);

@@ -8,75 +8,291 @@
 // tables shared by every scenario with that key:
 //   E_j = -log1p(-u_j)            arrivals: t_j = t_{j-1} + E_j / rate  (bit-identical)
 //   (zc_j, zs_j) Box-Muller pair  lengths:  in = round_clamp(mean_in + std_in*zc_j), out likewise with zs_j
-//   tables_kernel  one thread per key (MT19937-64 state in local memory)
-//   count_kernel   one thread per (scenario, adapter): arrivals in [0, duration)
-//   merge_kernel   one warp per scenario: N-way merge by (time, adapter_id)
+//   seed_kernel         one thread per stream: seed_seq -> MT19937-64 state (shared memory)
+//   tables_draw_kernel  one warp per key: block twists + E / Box-Muller transforms in parallel
+//   count_kernel        one thread per (scenario, adapter): arrivals in [0, duration)
+//   expand_kernel + CUB stable segmented sort + gather_kernel: the merge by (time, adapter_id)
 #pragma once
 #include "lt_device.cuh"
 #include "lt_rng.h"
 
 namespace lt {
 
-// Longest a key's tables may need to be: arrivals counted at the key's
-// largest rate and duration bound every use (t_j is monotone in the rate:
-// division and addition are monotone under round-to-nearest).
+constexpr int kMtN = 312;  // MT19937-64 state words
+
+// ---- K0a: seeding. RngStream(seed, {a, id}) = std::seed_seq over
+// [seed_lo, seed_hi, a_lo, a_hi, id_lo, id_hi] -> mt19937_64::seed
+// (rng.hpp:35-46; [rand.util.seedseq]). The generate() recurrence is strictly
+// sequential, so it runs one thread per stream (two streams per key) with the
+// 624-word array in shared memory (row stride 625: conflict-free both when
+// every thread touches its own row and when a row is copied out), then the
+// block writes each stream's state contiguously to `state`.
+constexpr int kSeedThreads = 64;
+constexpr int kSeedStride = 625;
+constexpr size_t kSeedSmem = sizeof(uint32_t) * kSeedThreads * kSeedStride;
+
+__device__ __forceinline__ void seed_seq_row(uint32_t* b, const uint32_t* v) {
+  constexpr int n = 624, p = 306, q = 317, s = 6;
+  for (int k = 0; k < n; ++k) b[k] = 0x8b8b8b8bu;
+  uint32_t prev = b[n - 1];
+  uint32_t x0 = b[0], x1 = b[p];  // operands of the next step, loaded one step ahead
+  for (int k = 0; k < n; ++k) {    // m = max(s + 1, n) = n
+    const int kp = (k + p < n) ? k + p : k + p - n;
+    const int kq = (k + q < n) ? k + q : k + q - n;
+    const uint32_t r1 = 1664525u * seedseq_T(x0 ^ x1 ^ prev);
+    const int k1 = k + 1 < n ? k + 1 : 0;  // step k+1 reads b[k+1], b[k+1+p]: not written by step k
+    x0 = b[k1];
+    x1 = b[(k1 + p < n) ? k1 + p : k1 + p - n];
+    const uint32_t add = (k == 0) ? static_cast<uint32_t>(s) : (k <= s ? static_cast<uint32_t>(k) + v[k - 1]
+                                                                          : static_cast<uint32_t>(k));
+    const uint32_t r2 = r1 + add;
+    b[kp] += r1;
+    b[kq] += r2;
+    b[k] = r2;
+    prev = r2;
+  }
+  x0 = b[0];
+  x1 = b[p];
+  for (int k = 0; k < n; ++k) {  // k + m, m = n: indices repeat modulo n
+    const int kp = (k + p < n) ? k + p : k + p - n;
+    const int kq = (k + q < n) ? k + q : k + q - n;
+    const uint32_t r3 = 1566083941u * seedseq_T(x0 + x1 + prev);
+    const int k1 = k + 1 < n ? k + 1 : 0;
+    x0 = b[k1];
+    x1 = b[(k1 + p < n) ? k1 + p : k1 + p - n];
+    const uint32_t r4 = r3 - static_cast<uint32_t>(k);
+    b[kp] ^= r3;
+    b[kq] ^= r4;
+    b[k] = r4;
+    prev = r4;
+  }
+  // [rand.eng.mers] seed(q): an all-zero state (top w-r bits of x[0]) -> 2^(w-1)
+  if ((b[1] == 0u) && ((b[0] & 0x80000000u) == 0u)) {
+    bool zero = true;
+    for (int k = 2; zero && k < n; ++k) zero = b[k] == 0u;
+    if (zero) {
+      b[0] = 0u;
+      b[1] = 0x80000000u;
+    }
+  }
+}
+
+// keys[k0 .. k0 + nk): stream 2(k-k0) = {1, id}, 2(k-k0)+1 = {2, id}; stream t's
+// 312-word state at state[312 t].
+__global__ void __launch_bounds__(kSeedThreads) seed_kernel(const DKey* keys, int k0, int nk, uint64_t* state) {
+  extern __shared__ uint32_t sb[];
+  const int tid = threadIdx.x;
+  const int base = blockIdx.x * kSeedThreads;
+  const int t = base + tid;
+  const int n_streams = 2 * nk;
+  if (t < n_streams) {
+    const DKey key = keys[k0 + (t >> 1)];
+    const uint64_t a = (t & 1) ? 2 : 1;
+    const uint64_t id = static_cast<uint64_t>(key.id);
+    const uint32_t v[6] = {static_cast<uint32_t>(key.seed), static_cast<uint32_t>(key.seed >> 32),
+                           static_cast<uint32_t>(a), static_cast<uint32_t>(a >> 32),
+                           static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32)};
+    seed_seq_row(sb + tid * kSeedStride, v);
+  }
+  __syncthreads();
+  const int ns = min(kSeedThreads, n_streams - base);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(state) + static_cast<size_t>(base) * 2 * kMtN;
+  for (int idx = tid; idx < ns * 2 * kMtN; idx += kSeedThreads) {
+    const int sidx = idx / (2 * kMtN);
+    dst[idx] = sb[sidx * kSeedStride + (idx - sidx * 2 * kMtN)];
+  }
+}
+
+// One warp replaces st[0..311] by the next MT19937-64 state block: the
+// standard's whole-array twist ([rand.eng.mers]) done in two parallel halves
+// (i < 156 reads only old words; i >= 156 reads old words and the new
+// st[i - 156]), every read before any write of a half.
+__device__ __forceinline__ void mt64_twist_block(uint64_t* st, int lane) {
+  constexpr uint64_t UM = 0xffffffff80000000ULL, LM = 0x7fffffffULL, MA = 0xb5026f5aa96619e9ULL;
+  uint64_t nv[5];
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const int i = lane + 32 * r;
+    if (i < 156) {
+      const uint64_t y = (st[i] & UM) | (st[i + 1] & LM);
+      nv[r] = st[i + 156] ^ (y >> 1) ^ ((y & 1ULL) ? MA : 0ULL);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const int i = lane + 32 * r;
+    if (i < 156) st[i] = nv[r];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const int i = 156 + lane + 32 * r;
+    if (i < kMtN) {
+      const uint64_t nx = (i + 1 < kMtN) ? st[i + 1] : st[0];
+      const uint64_t y = (st[i] & UM) | (nx & LM);
+      nv[r] = st[i - 156] ^ (y >> 1) ^ ((y & 1ULL) ? MA : 0ULL);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const int i = 156 + lane + 32 * r;
+    if (i < kMtN) st[i] = nv[r];
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ double mt64_unit(uint64_t w) {
+  return static_cast<double>(mt64_temper(w) >> 11) * 0x1.0p-53;  // uniform01 (rng.hpp:51)
+}
+
+// ---- K0b: drawing, one warp per key: 312 outputs per block, transformed by all lanes.
+// E: -log1p(-u) in parallel; only the stop rule t += E/rate_max >= dur_max
+// (workload.cpp:179-183) is a sequential add chain (lane 0). Z: pair q of a
+// block is (u[2q], u[2q+1]) exactly as normal() draws them (rng.hpp:57-71)
+// unless some u1 == 0 forces a resample; then lane 0 redraws the stream
+// sequentially with the reference's loop.
 template <bool Fma>
-__global__ void tables_kernel(DKey* keys, int n_keys, double* E, double2* Z) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n_keys) return;
+__global__ void __launch_bounds__(128) tables_draw_kernel(DKey* keys, int k0, int nk, const uint64_t* state,
+                                                          double* E, double2* Z) {
+  __shared__ uint64_t st_all[4][kMtN];
+  __shared__ double buf_all[4][kMtN];
+  __shared__ double q_all[4][kMtN];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int li = blockIdx.x * 4 + warp;
+  if (li >= nk) return;
+  uint64_t* st = st_all[warp];
+  double* buf = buf_all[warp];
+  double* qv = q_all[warp];
+  const int k = k0 + li;
   DKey key = keys[k];
-  Mt64 e;
-  rng_stream_init(e, key.seed, 1, static_cast<uint64_t>(key.id));
-  double t = 0.0;
-  int j = 0;
+  key.overflow = 0;
+  const uint64_t* src = state + static_cast<size_t>(li) * (2 * kMtN);
+  for (int w = lane; w < kMtN; w += 32) st[w] = src[w];
+  __syncwarp();
+  // ---- E table (arrivals stream {1, id})
   double* Ek = E + key.e_off;
-  for (;;) {
-    if (j >= key.cap) {
-      key.overflow = 1;
+  double t = 0.0;
+  int j = 0, overflow = 0;
+  for (bool done = false; !done;) {
+    mt64_twist_block(st, lane);
+    for (int w = lane; w < kMtN; w += 32) {
+      const double x = -glibc_log1p<Fma>(-mt64_unit(st[w]));
+      buf[w] = x;
+      qv[w] = x / key.rate_max;
+    }
+    __syncwarp();
+    int take = kMtN, stop = 0;
+    if (lane == 0) {
+      for (int w = 0; w < kMtN; ++w) {
+        if (j + w >= key.cap) {
+          overflow = 1;
+          take = w;
+          stop = 1;
+          break;
+        }
+        t = t + qv[w];
+        if (t >= key.dur_max) {
+          take = w + 1;
+          stop = 1;
+          break;
+        }
+      }
+    }
+    take = __shfl_sync(0xffffffffu, take, 0);
+    done = __shfl_sync(0xffffffffu, stop, 0) != 0;
+    for (int w = lane; w < take; w += 32) Ek[j + w] = buf[w];
+    j += take;
+    __syncwarp();
+  }
+  overflow = __shfl_sync(0xffffffffu, overflow, 0);
+  const int n = overflow ? j : j - 1;  // arrivals strictly inside the window
+  // ---- Z table (lengths stream {2, id})
+  for (int w = lane; w < kMtN; w += 32) st[w] = src[kMtN + w];
+  __syncwarp();
+  double2* Zk = Z + key.z_off;
+  bool slow = false;
+  for (int p = 0; p < n; p += kMtN / 2) {
+    mt64_twist_block(st, lane);
+    bool zero = false;
+    for (int q = lane; q < kMtN / 2 && p + q < n; q += 32) zero |= !(mt64_unit(st[2 * q]) > 0.0);
+    if (__any_sync(0xffffffffu, zero)) {
+      slow = true;
       break;
     }
-    const double x = exp_unit<Fma>(e);
-    Ek[j++] = x;
-    t = t + x / key.rate_max;
-    if (t >= key.dur_max) break;
+    for (int q = lane; q < kMtN / 2 && p + q < n; q += 32) {
+      const double u1 = mt64_unit(st[2 * q]);
+      const double u2 = mt64_unit(st[2 * q + 1]);
+      const double radius = sqrt(-2.0 * glibc_log<Fma>(u1));
+      const double angle = 6.283185307179586 * u2;
+      Zk[p + q] = make_double2(radius * glibc_cos<Fma>(angle), radius * glibc_sin<Fma>(angle));
+    }
+    __syncwarp();
   }
-  key.e_len = j;
-  const int n = key.overflow ? j : j - 1;  // arrivals strictly inside the window
-  rng_stream_init(e, key.seed, 2, static_cast<uint64_t>(key.id));
-  double2* Zk = Z + key.z_off;
-  for (int i = 0; i < n; ++i) {
-    double sp;
-    const double c = box_muller<Fma>(e, &sp);
-    Zk[i] = make_double2(c, sp);
+  if (slow && lane == 0) {
+    Mt64 e;
+    for (int w = 0; w < kMtN; ++w) e.x[w] = src[kMtN + w];
+    e.i = 0;
+    for (int i = 0; i < n; ++i) {
+      double sp;
+      const double c = box_muller<Fma>(e, &sp);
+      Zk[i] = make_double2(c, sp);
+    }
   }
-  key.z_len = n;
-  keys[k] = key;
+  if (lane == 0) {
+    key.e_len = j;
+    key.z_len = n;
+    key.overflow = overflow;
+    keys[k] = key;
+  }
 }
 
 // Arrivals of one (scenario, adapter): count t < duration (workload.cpp:179-183).
-__global__ void count_kernel(const DScen* scen, const int32_t* pair_scen, const int32_t* pair_adp,
-                             int64_t n_pairs, const DAdapter* adapters, const DKey* keys,
-                             const double* E, int32_t* adp_count, unsigned long long* scen_count,
-                             int32_t* overflow) {
-  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+// One warp per pair: the table loads and divisions E_j / rate of 32 draws run
+// in parallel; the running sum t is the reference's sequential chain, one add
+// per draw in draw order, broadcast by shuffles.
+__global__ void __launch_bounds__(256) count_kernel(const DScen* scen, const int32_t* pair_scen,
+                                                    const int32_t* pair_adp, int64_t n_pairs,
+                                                    const DAdapter* adapters, const DKey* keys, const double* E,
+                                                    int32_t* adp_count, unsigned long long* scen_count,
+                                                    int32_t* overflow) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   if (p >= n_pairs) return;
-  const DScen& s = scen[pair_scen[p]];
-  const DAdapter ad = adapters[s.adapter_begin + pair_adp[p]];
+  const int si = pair_scen[p];
+  const double duration = scen[si].duration;
+  const DAdapter ad = adapters[scen[si].adapter_begin + pair_adp[p]];
   const DKey& key = keys[ad.key];
   const double* Ek = E + key.e_off;
+  const int len = key.e_len;
   double t = 0.0;
-  int j = 0;
-  for (;;) {
-    if (j >= key.e_len) {
-      atomicExch(overflow, 1);
+  int count = -1;
+  for (int j0 = 0; count < 0; j0 += 32) {
+    if (j0 >= len) {  // table exhausted before the window closed
+      if (lane == 0) atomicExch(overflow, 1);
+      count = len;
       break;
     }
-    t = t + Ek[j] / ad.rate;
-    if (t >= s.duration) break;
-    ++j;
+    const int j = j0 + lane;
+    const double q = (j < len) ? Ek[j] / ad.rate : 0.0;
+    int hit = 32;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      t = t + __shfl_sync(0xffffffffu, q, k);
+      if (hit == 32 && t >= duration) hit = k;
+    }
+    if (hit < 32) {
+      count = j0 + hit;
+    } else if (j0 + 32 > len) {
+      if (lane == 0) atomicExch(overflow, 1);
+      count = len;
+    }
   }
-  adp_count[p] = j;
-  atomicAdd(&scen_count[pair_scen[p]], static_cast<unsigned long long>(j));
+  if (lane == 0) {
+    adp_count[p] = count;
+    atomicAdd(&scen_count[si], static_cast<unsigned long long>(count));
+  }
 }
 
 // Request offsets of every scenario from the device exclusive scan.
@@ -91,13 +307,16 @@ __global__ void set_offsets_kernel(DScen* scen, int n_scen, const unsigned long 
 // Arrival times of one (scenario, adapter) pair written unsorted at the pair's
 // slot of the scenario segment; a stable segmented sort by time then realises
 // the reference's stable_sort by (time, adapter_id, sequence)
-// (workload.cpp:204-207): pairs are laid out in adapter-id order.
-__global__ void expand_kernel(const DScen* scen, const int32_t* pair_scen, const int32_t* pair_adp,
-                              int64_t n_pairs, const int64_t* pair_begin, const DAdapter* adapters,
-                              const DKey* keys, const double* E, const int32_t* adp_count,
-                              const unsigned long long* pair_excl, double* t_out,
-                              unsigned long long* v_out) {
-  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+// (workload.cpp:204-207): pairs are laid out in adapter-id order. One warp
+// per pair, the same sequential sum as count_kernel.
+__global__ void __launch_bounds__(256) expand_kernel(const DScen* scen, const int32_t* pair_scen,
+                                                     const int32_t* pair_adp, int64_t n_pairs,
+                                                     const int64_t* pair_begin, const DAdapter* adapters,
+                                                     const DKey* keys, const double* E, const int32_t* adp_count,
+                                                     const unsigned long long* pair_excl, double* t_out,
+                                                     unsigned long long* v_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   if (p >= n_pairs) return;
   const int si = pair_scen[p];
   const DScen& s = scen[si];
@@ -107,10 +326,19 @@ __global__ void expand_kernel(const DScen* scen, const int32_t* pair_scen, const
   const int64_t off = s.req_begin + static_cast<int64_t>(pair_excl[p] - pair_excl[pair_begin[si]]);
   const int n = adp_count[p];
   double t = 0.0;
-  for (int j = 0; j < n; ++j) {
-    t = t + Ek[j] / ad.rate;
-    t_out[off + j] = t;
-    v_out[off + j] = (static_cast<unsigned long long>(k) << 32) | static_cast<unsigned>(j);
+  for (int j0 = 0; j0 < n; j0 += 32) {
+    const int j = j0 + lane;
+    const double q = (j < n) ? Ek[j] / ad.rate : 0.0;
+    double mine = 0.0;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      t = t + __shfl_sync(0xffffffffu, q, u);
+      if (u == lane) mine = t;
+    }
+    if (j < n) {
+      t_out[off + j] = mine;
+      v_out[off + j] = (static_cast<unsigned long long>(k) << 32) | static_cast<unsigned>(j);
+    }
   }
 }
 
@@ -126,30 +354,35 @@ __global__ void segments_kernel(const DScen* scen, int n_scen, int* seg_begin, i
 
 // Sorted (time, adapter, sequence) -> request arrays; lengths from the Z
 // table of the adapter's (seed, id) key (sample_lengths, workload.cpp:162-166).
-__global__ void __launch_bounds__(256) gather_kernel(const DScen* scen, int n_scen, const DAdapter* adapters,
-                                                    const DKey* keys, const DLen* lens, const double2* Z,
-                                                    const double* t_sorted, const unsigned long long* v_sorted,
-                                                    double* r_arr, int32_t* r_in, int32_t* r_out,
-                                                    int32_t* r_adp) {
-  const int lane = threadIdx.x & 31;
-  const int si = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (si >= n_scen) return;
-  const DScen sc = scen[si];
-  if (!sc.generated || sc.status != LT_OK) return;
-  const DLen gl = lens[sc.length_param];
-  for (int r = lane; r < sc.n_req; r += 32) {
-    const int64_t g = sc.req_begin + r;
-    const unsigned long long v = v_sorted[g];
-    const int a = static_cast<int>(v >> 32);
-    const int j = static_cast<int>(v & 0xffffffffULL);
-    const DAdapter ad = adapters[sc.adapter_begin + a];
-    const double2 z = Z[keys[ad.key].z_off + j];
-    const DLen L = ad.length_param >= 0 ? lens[ad.length_param] : gl;
-    r_arr[g] = t_sorted[g];
-    r_adp[g] = a;
-    r_in[g] = round_clamp_token(affine(L.mean_in, L.std_in, z.x));
-    r_out[g] = round_clamp_token(affine(L.mean_out, L.std_out, z.y));
+// One thread per request of the whole batch; its scenario is found by binary
+// search over the (ascending) request offsets.
+__global__ void __launch_bounds__(256) gather_kernel(const DScen* scen, int n_scen, int64_t total_req,
+                                                    const DAdapter* adapters, const DKey* keys, const DLen* lens,
+                                                    const double2* Z, const double* t_sorted,
+                                                    const unsigned long long* v_sorted, double* r_arr,
+                                                    int32_t* r_in, int32_t* r_out, int32_t* r_adp) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= total_req) return;
+  int lo = 0, hi = n_scen - 1;  // last scenario with req_begin <= g
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (scen[mid].req_begin <= g)
+      lo = mid;
+    else
+      hi = mid - 1;
   }
+  const DScen& sc = scen[lo];
+  if (!sc.generated || sc.status != LT_OK || g >= sc.req_begin + sc.n_req) return;
+  const unsigned long long v = v_sorted[g];
+  const int a = static_cast<int>(v >> 32);
+  const int j = static_cast<int>(v & 0xffffffffULL);
+  const DAdapter ad = adapters[sc.adapter_begin + a];
+  const double2 z = Z[keys[ad.key].z_off + j];
+  const DLen L = lens[ad.length_param >= 0 ? ad.length_param : sc.length_param];
+  r_arr[g] = t_sorted[g];
+  r_adp[g] = a;
+  r_in[g] = round_clamp_token(affine(L.mean_in, L.std_in, z.x));
+  r_out[g] = round_clamp_token(affine(L.mean_out, L.std_out, z.y));
 }
 
 // N-way merge of one scenario's adapter streams into request_id order.

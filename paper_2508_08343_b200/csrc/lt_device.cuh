@@ -81,7 +81,9 @@ struct EngineParams {
   const DScen* scen;
   const int32_t* order;
   int32_t n_scen;
-  int32_t max_adapters;  // smem stride per warp
+  int32_t max_adapters;  // adapters per warp in shared memory
+  int32_t run_cap;       // running-set slots per warp in shared memory
+  int32_t smem_per_warp; // bytes
   int32_t* counter;
   const DAdapter* adapters;
   const double* r_arr;

@@ -80,6 +80,15 @@ LT_HD uint64_t mt64_next(Mt64& e) {
   return z;
 }
 
+// MT19937-64 tempering of one state word.
+LT_HD uint64_t mt64_temper(uint64_t z) {
+  z ^= (z >> 29) & 0x5555555555555555ULL;
+  z ^= (z << 17) & 0x71d67fffeda60000ULL;
+  z ^= (z << 37) & 0xfff7eee000000000ULL;
+  z ^= z >> 43;
+  return z;
+}
+
 // RngStream(seed, {a, b}) (rng.hpp:35-46).
 LT_HD void rng_stream_init(Mt64& e, uint64_t seed, uint64_t a, uint64_t b) {
   uint32_t w[6] = {static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32),
