@@ -304,7 +304,7 @@ def impl_gpu(args):
     e2e = None
     if not args.no_e2e:
         pb, keep = pinned_copy(batch)
-        walls = []
+        walls, plan_ms, wait_ms = [], [], []
         h2d = d2h = 0
         for i in range(max(1, args.e2e_steps) + 1):
             torch.cuda.synchronize()
@@ -313,6 +313,8 @@ def impl_gpu(args):
             walls.append(time.perf_counter() - t0)
             tm = dev.timing()
             h2d, d2h = int(tm["h2d_bytes"]), int(tm["d2h_bytes"])
+            plan_ms.append(tm["plan_ms"])
+            wait_ms.append(tm["run_wait_ms"])
         walls = walls[1:]
         e2e_val = int(out["iterations"].sum()) / statistics.mean(walls)
         if dist:
@@ -320,7 +322,8 @@ def impl_gpu(args):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_val = iters_all / float(tt.item())
         e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": 1000 * statistics.mean(walls), "call": "lt_simulate_batch (host pinned buffers)"}
+               "ms_per_step": 1000 * statistics.mean(walls), "call": "lt_simulate_batch (host pinned buffers)",
+               "plan_ms": statistics.mean(plan_ms[1:]), "run_wait_ms": statistics.mean(wait_ms[1:])}
 
     log(f"[{time.strftime('%X')}] e2e: {e2e}")
     secondary = None

@@ -302,6 +302,8 @@ typedef struct lt_timing {
   int64_t h2d_bytes, d2h_bytes;
   int64_t engine_launches; /* kernels this library launched in the call */
   int64_t algorithmic_bytes; /* B_iter summed over the engine launches */
+  double plan_ms;    /* host wall time of building the plan (validation, packing, sizing passes) */
+  double run_wait_ms; /* host wall time from lt_plan_run to results copied back */
 } lt_timing;
 
 int32_t lt_abi_version(void);

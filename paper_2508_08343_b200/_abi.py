@@ -139,7 +139,8 @@ class lt_timing(C.Structure):
     _fields_ = [("h2d_ms", C.c_double), ("tables_ms", C.c_double), ("merge_ms", C.c_double),
                 ("engine_ms", C.c_double), ("reduce_ms", C.c_double), ("d2h_ms", C.c_double),
                 ("total_ms", C.c_double), ("run_ms", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-                ("engine_launches", C.c_int64), ("algorithmic_bytes", C.c_int64)]
+                ("engine_launches", C.c_int64), ("algorithmic_bytes", C.c_int64), ("plan_ms", C.c_double),
+                ("run_wait_ms", C.c_double)]
 
 
 # numpy views with the exact C layouts (numpy honours ctypes field offsets)

@@ -395,6 +395,7 @@ struct lt_plan {
   DBuf<DLen> lens;
   DBuf<DKey> keys;
   DBuf<uint64_t> seed_state;   // K0a -> K0b: seeded MT19937-64 states of one key chunk
+  DBuf<int32_t> tab_overflow;  // set when some key's table was too short
   DBuf<double> E;
   DBuf<double2> Z;
   DBuf<int32_t> order;
@@ -447,13 +448,38 @@ struct Prep {
   std::vector<int32_t> pair_scen, pair_adp;
   std::vector<int64_t> pair_begin;
   std::unordered_map<std::string, int> len_index;
-  struct KeyHash {
-    size_t operator()(const std::pair<uint64_t, int64_t>& k) const {
-      return std::hash<uint64_t>()(k.first * 0x9e3779b97f4a7c15ULL ^ static_cast<uint64_t>(k.second));
-    }
+  // (seed, adapter_id) -> key index. Keys are looked up per seed: a batch has
+  // few distinct seeds with many adapters each (sweeps share one seed across
+  // every grid point), and ids are small (instantiate_condition: 1..N), so
+  // each seed keeps a dense id table (hash map for ids outside [0, 65536)).
+  struct SeedKeys {
+    std::vector<int32_t> dense;
+    std::unordered_map<int64_t, int32_t> sparse;
   };
-  std::unordered_map<std::pair<uint64_t, int64_t>, int, KeyHash> key_index;
+  std::unordered_map<uint64_t, int32_t> seed_index;
+  std::vector<SeedKeys> seeds;
   std::vector<double> cost;
+
+  SeedKeys& seed_keys(uint64_t seed) {
+    auto it = seed_index.find(seed);
+    if (it != seed_index.end()) return seeds[it->second];
+    seed_index.emplace(seed, static_cast<int32_t>(seeds.size()));
+    seeds.emplace_back();
+    return seeds.back();
+  }
+  // Returns the key index of (seed, id) in `sk`, inserting `fresh` when absent.
+  static int32_t find_or_insert(SeedKeys& sk, int64_t id, int32_t fresh, bool* inserted) {
+    int32_t* slot;
+    if (id >= 0 && id < 65536) {
+      if (static_cast<int64_t>(sk.dense.size()) <= id) sk.dense.resize(static_cast<size_t>(id) + 1, -1);
+      slot = &sk.dense[static_cast<size_t>(id)];
+    } else {
+      slot = &sk.sparse.emplace(id, -1).first->second;
+    }
+    *inserted = *slot < 0;
+    if (*inserted) *slot = fresh;
+    return *slot;
+  }
 };
 
 int intern_len(Prep& p, const DLen& d) {
@@ -507,10 +533,15 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
     for (int k = 0; k < s.n_adapters && !suspect; ++k)
       suspect = ad[k].rank < 0 || !(ad[k].rate > 0.0) || ad[k].length_index >= 0;
     if (!suspect) {
-      std::vector<int> ids(s.n_adapters);
-      for (int k = 0; k < s.n_adapters; ++k) ids[k] = ad[k].adapter_id;
-      std::sort(ids.begin(), ids.end());
-      suspect = std::adjacent_find(ids.begin(), ids.end()) != ids.end();
+      // ids are usually ascending already (instantiate_condition: 1..N)
+      bool asc = true;
+      for (int k = 1; k < s.n_adapters && asc; ++k) asc = ad[k - 1].adapter_id < ad[k].adapter_id;
+      if (!asc) {
+        std::vector<int> ids(s.n_adapters);
+        for (int k = 0; k < s.n_adapters; ++k) ids[k] = ad[k].adapter_id;
+        std::sort(ids.begin(), ids.end());
+        suspect = std::adjacent_find(ids.begin(), ids.end()) != ids.end();
+      }
     }
     if (suspect) {
       std::set<int> seen;
@@ -554,16 +585,17 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
     perm[k] = k;
     max_rank = std::max(max_rank, ad[k].rank);
   }
-  std::sort(perm.begin(), perm.end(), [&](int x, int y) { return ad[x].adapter_id < ad[y].adapter_id; });
+  bool ascending = true;
+  for (int k = 1; k < s.n_adapters && ascending; ++k) ascending = ad[k - 1].adapter_id < ad[k].adapter_id;
+  if (!ascending)
+    std::sort(perm.begin(), perm.end(), [&](int x, int y) { return ad[x].adapter_id < ad[y].adapter_id; });
   for (int k = 1; k < s.n_adapters; ++k)
     if (ad[perm[k]].adapter_id == ad[perm[k - 1]].adapter_id)
       return e.set(LT_ERR_VALIDATION, "workload.adapters: duplicate adapter_id"), fail();
-  int64_t capacity = P.cfg.raw.total_kv_budget;
-  for (int g = 0; g < G; ++g) {
-    int64_t c;
-    if (!slot_cost(P.cfg, max_rank, &c, &e)) return fail();
-    capacity -= c;
-  }
+  // mem_max (estimators.cpp:100-108): budget - G * slot_cost(max_rank), floored at 0
+  int64_t c_slot;
+  if (!slot_cost(P.cfg, max_rank, &c_slot, &e)) return fail();
+  int64_t capacity = P.cfg.raw.total_kv_budget - static_cast<int64_t>(G) * c_slot;
   capacity = std::max<int64_t>(capacity, 0);
   if (capacity <= 0)
     return e.set(LT_ERR_CONFIG, render(LT_ERR_CONFIG, LT_K_INFEASIBLE_SLOTS, G, 0), LT_K_INFEASIBLE_SLOTS, G), fail();
@@ -579,6 +611,7 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
   d.ideal = ideal;
   d.length_param = intern_len(pr, as_dlen(b.lengths[s.length_index], full));
   double cost = 0.0;
+  Prep::SeedKeys* sk = scripted ? nullptr : &pr.seed_keys(s.seed);
   for (int k = 0; k < s.n_adapters; ++k) {
     const lt_adapter& a = ad[perm[k]];
     DAdapter x{};
@@ -589,20 +622,16 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
     x.length_param = a.length_index >= 0 ? intern_len(pr, as_dlen(b.lengths[a.length_index], full)) : -1;
     x.key = -1;
     if (!scripted) {
-      auto key = std::make_pair(s.seed, static_cast<int64_t>(a.adapter_id));
-      auto it = pr.key_index.find(key);
-      int kidx;
-      if (it == pr.key_index.end()) {
-        kidx = static_cast<int>(pr.keys.size());
+      bool inserted = false;
+      const int kidx = Prep::find_or_insert(*sk, a.adapter_id, static_cast<int32_t>(pr.keys.size()), &inserted);
+      if (inserted) {
         DKey k{};
         k.seed = s.seed;
         k.id = a.adapter_id;
         k.rate_max = a.rate;
         k.dur_max = s.duration_s;
         pr.keys.push_back(k);
-        pr.key_index.emplace(key, kidx);
       } else {
-        kidx = it->second;
         DKey& k = pr.keys[kidx];
         k.rate_max = std::max(k.rate_max, a.rate);
         k.dur_max = std::max(k.dur_max, s.duration_s);
@@ -668,9 +697,11 @@ int launch_tables(lt_plan& P, int nk, cudaStream_t st) {
     after_launch("seed_kernel", st);
     const unsigned g = static_cast<unsigned>((n + 3) / 4);
     if (P.cfg.variant)
-      tables_draw_kernel<true><<<g, 128, 0, st>>>(P.keys.p, static_cast<int>(k0), n, P.seed_state.p, P.E.p, P.Z.p);
+      tables_draw_kernel<true><<<g, 128, 0, st>>>(P.keys.p, static_cast<int>(k0), n, P.seed_state.p, P.E.p, P.Z.p,
+                                                  P.tab_overflow.p);
     else
-      tables_draw_kernel<false><<<g, 128, 0, st>>>(P.keys.p, static_cast<int>(k0), n, P.seed_state.p, P.E.p, P.Z.p);
+      tables_draw_kernel<false><<<g, 128, 0, st>>>(P.keys.p, static_cast<int>(k0), n, P.seed_state.p, P.E.p, P.Z.p,
+                                                   P.tab_overflow.p);
     after_launch("tables_draw_kernel", st);
     launches += 2;
   }
@@ -690,8 +721,16 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   P.n_scen = b->n_scenarios;
   P.h_scen.resize(P.n_scen);
   P.errs.resize(P.n_scen);
+  using hclk = std::chrono::steady_clock;
+  const auto h0 = hclk::now();
+  auto hms = [&](hclk::time_point t) { return std::chrono::duration<double, std::milli>(t - h0).count(); };
   Prep pr;
   pr.cost.assign(P.n_scen, 0.0);
+  pr.keys.reserve(b->n_adapters);
+  P.adapter_ids.reserve(b->n_adapters);
+  pr.adapters.reserve(b->n_adapters);
+  pr.pair_scen.reserve(b->n_adapters);
+  pr.pair_adp.reserve(b->n_adapters);
   pr.pair_begin.resize(P.n_scen);
   for (int64_t i = 0; i < P.n_scen; ++i) {
     pr.pair_begin[i] = static_cast<int64_t>(pr.pair_scen.size());
@@ -704,6 +743,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   }
   P.max_adapters = (P.max_adapters + 31) / 32 * 32;
   if (pr.lens.empty()) pr.lens.push_back(DLen{1, 0, 1, 0});
+  const auto h_prep = hclk::now();
   cudaEventRecord(ctx->ev[0], st);
   // keys: reserve rate_max * dur_max + 8 sigma + slack draws
   int64_t e_total = 0;
@@ -717,24 +757,21 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   }
   if (!pr.keys.empty())
     P.seed_state.alloc(std::min<int64_t>(static_cast<int64_t>(pr.keys.size()), kSeedChunk) * 2 * kMtN);
+  P.tab_overflow.alloc(1);
   for (int attempt = 0;; ++attempt) {
     P.keys.upload(pr.keys, st);
+    LT_CUDA(cudaMemsetAsync(P.tab_overflow.p, 0, sizeof(int32_t), st));
     P.E.alloc(std::max<int64_t>(e_total, 1));
     P.Z.alloc(std::max<int64_t>(e_total, 1));
     P.h2d_bytes += pr.keys.size() * sizeof(DKey);
     if (!pr.keys.empty()) P.launches_prep += launch_tables(P, static_cast<int>(pr.keys.size()), st);
-    std::vector<DKey> back(pr.keys.size());
-    if (!back.empty())
-      LT_CUDA(cudaMemcpyAsync(back.data(), P.keys.p, back.size() * sizeof(DKey), cudaMemcpyDeviceToHost, st));
+    int32_t any = 0;
+    LT_CUDA(cudaMemcpyAsync(&any, P.tab_overflow.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     LT_CUDA(cudaStreamSynchronize(st));
-    bool overflow = false;
-    for (size_t k = 0; k < back.size(); ++k) {
-      if (back[k].overflow) overflow = true;
-    }
-    if (!overflow) {
-      pr.keys = back;
-      break;
-    }
+    if (!any) break;
+    std::vector<DKey> back(pr.keys.size());
+    LT_CUDA(cudaMemcpyAsync(back.data(), P.keys.p, back.size() * sizeof(DKey), cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaStreamSynchronize(st));
     if (attempt > 4) throw CudaError{"RNG table sizing failed"};
     e_total = 0;
     for (size_t k = 0; k < pr.keys.size(); ++k) {
@@ -745,6 +782,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     }
   }
   cudaEventRecord(ctx->ev[1], st);
+  const auto h_tables = hclk::now();
   // count arrivals per (scenario, adapter): sizes the request arrays
   const int64_t n_pairs = static_cast<int64_t>(pr.pair_scen.size());
   P.n_pairs = n_pairs;
@@ -904,6 +942,9 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   LT_CUDA(cudaStreamSynchronize(st));
   P.tables_ms = elapsed(ctx->ev[0], ctx->ev[1]);
   P.fresh = true;
+  if (std::getenv("LT_HOST_TIMING"))
+    std::fprintf(stderr, "[lt] build_plan host: prep %.2f ms, +tables sync %.2f ms, total %.2f ms (%lld scenarios)\n",
+                 hms(h_prep), hms(h_tables), hms(hclk::now()), static_cast<long long>(P.n_scen));
   return plan.release();
 }
 
@@ -1129,6 +1170,26 @@ extern "C" {
 
 int32_t lt_abi_version(void) { return LT_ABI_VERSION; }
 
+// Diagnostics (not in the public header): host wall time of the plan's
+// validation + packing pass alone, no device calls.
+double lt__host_prep_ms(const lt_workload_batch* b, const lt_server_config* cfg) {
+  const auto t0 = std::chrono::steady_clock::now();
+  lt_plan P;
+  load_config(P.cfg, cfg, nullptr);
+  P.n_scen = b->n_scenarios;
+  P.h_scen.resize(P.n_scen);
+  P.errs.resize(P.n_scen);
+  Prep pr;
+  pr.cost.assign(P.n_scen, 0.0);
+  pr.keys.reserve(b->n_adapters);
+  P.adapter_ids.reserve(b->n_adapters);
+  pr.adapters.reserve(b->n_adapters);
+  pr.pair_scen.reserve(b->n_adapters);
+  pr.pair_adp.reserve(b->n_adapters);
+  for (int64_t i = 0; i < P.n_scen; ++i) prepare_scenario(P, pr, *b, i);
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
 int32_t lt_host_libm_variant(void) {
   static int cached = -1;
   if (cached >= 0) return cached;
@@ -1301,14 +1362,18 @@ void lt_plan_destroy(lt_plan* plan) {
 int32_t lt_simulate_batch(lt_ctx* ctx, const lt_workload_batch* batch, const lt_server_config* config,
                           const lt_sim_options* options, lt_sim_summary* out, lt_request_states* states,
                           lt_status* status) {
-  const auto t0 = std::chrono::steady_clock::now();
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   lt_plan* plan = lt_plan_simulate(ctx, batch, config, options, status);
   if (!plan) return status ? status->code : LT_ERR_DEVICE;
+  const auto t1 = clk::now();
   int32_t rc = lt_plan_run(plan, status);
   if (rc == LT_OK) rc = lt_plan_results(plan, out, states, status);
+  const auto t2 = clk::now();
   lt_plan_destroy(plan);
-  ctx->timing.total_ms =
-      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  ctx->timing.total_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+  ctx->timing.plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  ctx->timing.run_wait_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
   return rc;
 }
 

@@ -155,7 +155,7 @@ __device__ __forceinline__ double mt64_unit(uint64_t w) {
 // sequentially with the reference's loop.
 template <bool Fma>
 __global__ void __launch_bounds__(128) tables_draw_kernel(DKey* keys, int k0, int nk, const uint64_t* state,
-                                                          double* E, double2* Z) {
+                                                          double* E, double2* Z, int32_t* any_overflow) {
   __shared__ uint64_t st_all[4][kMtN];
   __shared__ double buf_all[4][kMtN];
   __shared__ double q_all[4][kMtN];
@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(128) tables_draw_kernel(DKey* keys, int k0, in
     key.z_len = n;
     key.overflow = overflow;
     keys[k] = key;
+    if (overflow) atomicOr(any_overflow, 1);
   }
 }
 
