@@ -166,7 +166,8 @@ typedef struct lt_sim_options {
   int32_t want_digest;           /* fold each iteration's decisions into summary.digest */
   int64_t iteration_cap_override; /* <= 0: none */
   int32_t libm_variant;          /* -1: match the host glibc; 0: generic build; 1: FMA build */
-  int32_t _pad;
+  int32_t want_percentiles;      /* fill the TTFT/ITL p50/p99 of compute_metrics (a second, recording
+                                    engine pass + segmented sorts); sweeps never need them */
 } lt_sim_options;
 
 /* SimulationResult (engine.hpp:47-64) scalars + MetricsSummary
@@ -194,6 +195,8 @@ typedef struct lt_sim_summary {
   double ideal_throughput_tok_s;
   double ttft_mean_s;
   double itl_mean_s;
+  double ttft_p50_s, ttft_p99_s; /* nearest rank (metrics.cpp:47-54); 0 unless want_percentiles */
+  double itl_p50_s, itl_p99_s;
   int32_t degenerate;
   int32_t _pad;
   uint64_t digest; /* FNV-1a over per-iteration (R, W, A, loads, lat bits) */

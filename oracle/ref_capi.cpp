@@ -257,6 +257,10 @@ int32_t ltref_simulate_batch(void*, const lt_workload_batch* batch, const lt_ser
       o.ideal_throughput_tok_s = m.ideal_throughput_tok_s;
       o.ttft_mean_s = m.ttft_mean_s;
       o.itl_mean_s = m.itl_mean_s;
+      o.ttft_p50_s = m.ttft_p50_s;
+      o.ttft_p99_s = m.ttft_p99_s;
+      o.itl_p50_s = m.itl_p50_s;
+      o.itl_p99_s = m.itl_p99_s;
       o.degenerate = m.degenerate;
       int64_t pre = 0, tot = 0, win = 0;
       for (const RequestState& q : r.requests) {

@@ -522,6 +522,19 @@ static void run_push(St* r, int it) {
 
 /* Engine::run + metrics (engine.cpp:73-161, kv_scheduler.cpp:49-259,
  * adapter_cache.cpp:40-78, estimators.cpp:110-139, metrics.cpp:70-113). */
+/* percentile_nearest_rank (metrics.cpp:47-54): sort, 1-based rank ceil(p/100 n) clamped to [1, n] */
+static int cmp_double(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+static double nearest_rank_sorted(const double* v, int64_t n, double pct) {
+  if (n == 0) return 0.0;
+  int64_t rank = (int64_t)ceil(pct / 100.0 * (double)n);
+  if (rank < 1) rank = 1;
+  if (rank > n) rank = n;
+  return v[rank - 1];
+}
+
 static void simulate(const lt_server_config* c, int G, const Adp* ads, int n_ad, double duration, const Req* req,
                      int64_t n, double ideal, lt_sim_summary* o, Err* e, int want_digest, int64_t cap_override,
                      lt_request_states* states, int64_t st_off) {
@@ -851,6 +864,9 @@ static void simulate(const lt_server_config* c, int G, const Adp* ads, int n_ad,
       const double window = duration;
       double rej = 0.0, ttft = 0.0, itl = 0.0;
       int64_t nttft = 0, nitl = 0, win = 0, tot = 0, pre = 0;
+      double* ttft_v = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+      size_t itl_cap = 1024, itl_n = 0;
+      double* itl_v = (double*)malloc(sizeof(double) * itl_cap);
       for (int64_t i = 0; i < n; ++i) {
         St* r = &S.st[i];
         if (r->phase == P_REJECTED) {
@@ -860,6 +876,7 @@ static void simulate(const lt_server_config* c, int G, const Adp* ads, int n_ad,
         if (r->phase == P_FINISHED) o->finished_count++;
         if (r->has_first) {
           ttft += r->first - req[i].t;
+          ttft_v[nttft] = r->first - req[i].t;
           nttft++;
         }
         double prev = 0.0;
@@ -871,6 +888,11 @@ static void simulate(const lt_server_config* c, int G, const Adp* ads, int n_ad,
             if (have) {
               itl += t - prev;
               nitl++;
+              if (itl_n == itl_cap) {
+                itl_cap *= 2;
+                itl_v = (double*)realloc(itl_v, sizeof(double) * itl_cap);
+              }
+              itl_v[itl_n++] = t - prev;
             }
             prev = t;
             have = 1;
@@ -884,6 +906,14 @@ static void simulate(const lt_server_config* c, int G, const Adp* ads, int n_ad,
       o->throughput_tok_s = (double)win / window;
       o->ttft_mean_s = nttft ? ttft / (double)nttft : 0.0;
       o->itl_mean_s = nitl ? itl / (double)nitl : 0.0;
+      qsort(ttft_v, (size_t)nttft, sizeof(double), cmp_double);
+      qsort(itl_v, itl_n, sizeof(double), cmp_double);
+      o->ttft_p50_s = nearest_rank_sorted(ttft_v, nttft, 50.0);
+      o->ttft_p99_s = nearest_rank_sorted(ttft_v, nttft, 99.0);
+      o->itl_p50_s = nearest_rank_sorted(itl_v, (int64_t)itl_n, 50.0);
+      o->itl_p99_s = nearest_rank_sorted(itl_v, (int64_t)itl_n, 99.0);
+      free(ttft_v);
+      free(itl_v);
       const double eff_raw = ideal - rej;
       const double eff = eff_raw < 0.0 ? 0.0 : eff_raw;
       o->starved = o->throughput_tok_s < 0.9 * eff;

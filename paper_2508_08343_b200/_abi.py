@@ -71,7 +71,8 @@ class lt_workload_batch(C.Structure):
 
 class lt_sim_options(C.Structure):
     _fields_ = [("check_invariants", C.c_int32), ("want_digest", C.c_int32),
-                ("iteration_cap_override", C.c_int64), ("libm_variant", C.c_int32), ("_pad", C.c_int32)]
+                ("iteration_cap_override", C.c_int64), ("libm_variant", C.c_int32),
+                ("want_percentiles", C.c_int32)]
 
 
 class lt_sim_summary(C.Structure):
@@ -83,7 +84,9 @@ class lt_sim_summary(C.Structure):
                 ("rejected_count", C.c_int64), ("preemptions", C.c_int64), ("load_events", C.c_int64),
                 ("tokens_in_window", C.c_int64), ("tokens_total", C.c_int64),
                 ("throughput_tok_s", C.c_double), ("ideal_throughput_tok_s", C.c_double),
-                ("ttft_mean_s", C.c_double), ("itl_mean_s", C.c_double), ("degenerate", C.c_int32),
+                ("ttft_mean_s", C.c_double), ("itl_mean_s", C.c_double), ("ttft_p50_s", C.c_double),
+                ("ttft_p99_s", C.c_double), ("itl_p50_s", C.c_double), ("itl_p99_s", C.c_double),
+                ("degenerate", C.c_int32),
                 ("_pad", C.c_int32), ("digest", C.c_uint64), ("sum_running", C.c_int64),
                 ("sum_visited", C.c_int64), ("sum_arrivals", C.c_int64), ("sum_moves", C.c_int64),
                 ("device_cycles", C.c_int64), ("phase_cycles", C.c_int64 * 6)]

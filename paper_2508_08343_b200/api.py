@@ -73,8 +73,13 @@ class Device:
 
     # --- batched entry points (the product) -----------------------------------
     def simulate_batch(self, batch: WorkloadBatch, config: ServerConfig, options: Optional[SimOptions] = None,
-                       want_states: bool = False, want_digest: bool = False, libm_variant: int = -1):
-        return self.runner.simulate(batch, config, sim_options(options, want_digest, libm_variant), want_states)
+                       want_states: bool = False, want_digest: bool = False, libm_variant: int = -1,
+                       want_percentiles: bool = False):
+        """run_simulation / run_scripted + compute_metrics for every scenario. The
+        TTFT/ITL percentiles cost a second recording engine pass; they are filled
+        only with want_percentiles (sweeps never read them)."""
+        return self.runner.simulate(batch, config, sim_options(options, want_digest, libm_variant, want_percentiles),
+                                    want_states)
 
     def generate_arrivals_batch(self, batch: WorkloadBatch, libm_variant: int = -1):
         return self.runner.generate_arrivals(batch, sim_options(None, False, libm_variant))
@@ -151,7 +156,9 @@ def raise_for(row, message: str):
 
 def metrics_of(row) -> MetricsSummary:
     return MetricsSummary(throughput_tok_s=float(row["throughput_tok_s"]), itl_mean_s=float(row["itl_mean_s"]),
-                          ttft_mean_s=float(row["ttft_mean_s"]),
+                          itl_p50_s=float(row["itl_p50_s"]), itl_p99_s=float(row["itl_p99_s"]),
+                          ttft_mean_s=float(row["ttft_mean_s"]), ttft_p50_s=float(row["ttft_p50_s"]),
+                          ttft_p99_s=float(row["ttft_p99_s"]),
                           ideal_throughput_tok_s=float(row["ideal_throughput_tok_s"]),
                           starved=bool(row["starved"]), finished_count=int(row["finished_count"]),
                           rejected_count=int(row["rejected_count"]), degenerate=bool(row["degenerate"]))
@@ -197,7 +204,7 @@ def run_simulation(workload: WorkloadSpec, config: ServerConfig, mode: LengthMod
     """engine.hpp:70-71 — one engine on the B200 (result + device-computed metrics)."""
     dev = dev or device()
     batch = WorkloadBatch.from_workloads([workload], mode=mode)
-    out, states = dev.simulate_batch(batch, config, options, want_states=True)
+    out, states = dev.simulate_batch(batch, config, options, want_states=True, want_percentiles=True)
     raise_for(out[0], dev.message(0))
     return result_of(out[0], states, 0)
 
@@ -210,7 +217,7 @@ def run_scripted(requests: Sequence[Request], adapters: Sequence[AdapterSpec], d
     w = WorkloadSpec(adapters=list(adapters), duration_s=duration_s)
     w.lengths.mean_input = w.lengths.mean_output = 1.0  # unused by scripted runs
     batch = WorkloadBatch.from_workloads([w], scripted=[list(requests)])
-    out, states = dev.simulate_batch(batch, config, options, want_states=True)
+    out, states = dev.simulate_batch(batch, config, options, want_states=True, want_percentiles=True)
     raise_for(out[0], dev.message(0))
     return result_of(out[0], states, 0)
 

@@ -172,13 +172,14 @@ class ConditionBatch:
 
 
 def sim_options(opts: Optional[SimOptions] = None, want_digest: bool = False,
-                libm_variant: int = -1) -> A.lt_sim_options:
+                libm_variant: int = -1, want_percentiles: bool = False) -> A.lt_sim_options:
     o = A.lt_sim_options()
     opts = opts or SimOptions()
     o.check_invariants = int(opts.check_invariants)
     o.want_digest = int(want_digest)
     o.iteration_cap_override = int(opts.iteration_cap_override or 0)
     o.libm_variant = libm_variant
+    o.want_percentiles = int(want_percentiles)
     return o
 
 

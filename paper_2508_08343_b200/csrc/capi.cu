@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "k_engine.cuh"
+#include "k_metrics.cuh"
 #include "k_sweep.cuh"
 #include "k_workload.cuh"
 #include "loratwin_gpu.h"
@@ -408,6 +409,12 @@ struct lt_plan {
   DBuf<int4> ws_node;
   DBuf<int32_t> ws_ov, ws_cmin;
   DBuf<lt_sim_summary> out;
+  // percentiles (want_percentiles): recording pass + segmented sorts
+  int want_pct = 0;
+  DBuf<int64_t> rec_off, rec_len;
+  DBuf<double> rec_d, rec_d_sorted, ttft_keys, ttft_sorted;
+  DBuf<int32_t> rec_c, rec_c_sorted, pct_seg_b, pct_seg_e, pct_rseg_b, pct_rseg_e;
+  DBuf<char> pct_tmp;
   // re-run state (lt_plan_run recomputes K0 tables, counts, offsets, merge)
   DBuf<int32_t> pair_scen, pair_adp, adp_count, overflow;
   DBuf<int64_t> pair_begin;
@@ -718,6 +725,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   cudaStream_t st = ctx->stream;
   load_config(P.cfg, cfg, opts);
   P.want_digest = opts ? opts->want_digest : 0;
+  P.want_pct = opts ? opts->want_percentiles : 0;
   P.n_scen = b->n_scenarios;
   P.h_scen.resize(P.n_scen);
   P.errs.resize(P.n_scen);
@@ -1006,17 +1014,25 @@ void prepare_requests(lt_plan& P) {
   P.launches_run = launches + 1;
 }
 
-void run_plan(lt_plan& P) {
-  lt_ctx* ctx = P.ctx;
-  cudaStream_t st = ctx->stream;
+// Per-request engine state before an engine pass.
+void reset_state(lt_plan& P) {
+  cudaStream_t st = P.ctx->stream;
   const int64_t nr = std::max<int64_t>(P.total_req, 1);
-  prepare_requests(P);
   LT_CUDA(cudaMemsetAsync(P.r_phase.p, 0, nr, st));
   LT_CUDA(cudaMemsetAsync(P.r_gen.p, 0, nr * sizeof(int32_t), st));
   LT_CUDA(cudaMemsetAsync(P.r_pre.p, 0, nr * sizeof(int32_t), st));
   LT_CUDA(cudaMemsetAsync(P.r_first.p, 0xff, nr * sizeof(double), st));  // NaN: no first token
   LT_CUDA(cudaMemsetAsync(P.r_last.p, 0, nr * sizeof(double), st));
   LT_CUDA(cudaMemsetAsync(P.counter.p, 0, sizeof(int32_t), st));
+}
+
+void run_percentiles(lt_plan& P, EngineParams E);
+
+void run_plan(lt_plan& P) {
+  lt_ctx* ctx = P.ctx;
+  cudaStream_t st = ctx->stream;
+  prepare_requests(P);
+  reset_state(P);
   EngineParams E{};
   E.scen = P.scen.p;
   E.order = P.order.p;
@@ -1058,6 +1074,74 @@ void run_plan(lt_plan& P) {
     after_launch("engine_kernel", st);
   }
   cudaEventRecord(ctx->ev[5], st);
+  if (P.want_pct && P.n_scen > 0) run_percentiles(P, E);
+}
+
+// TTFT/ITL p50/p99 (metrics.cpp:47-54): a second, recording engine pass sized
+// by the first pass's iteration and preemption counts, then segmented sorts
+// and a weighted rank select (k_metrics.cuh).
+void run_percentiles(lt_plan& P, EngineParams E) {
+  cudaStream_t st = P.ctx->stream;
+  const int64_t n = P.n_scen;
+  std::vector<lt_sim_summary> h(n);
+  LT_CUDA(cudaMemcpyAsync(h.data(), P.out.p, n * sizeof(lt_sim_summary), cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> off(n), len(n);
+  std::vector<int32_t> rb(n), re(n), tb(n), te(n);
+  int64_t tot = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    len[i] = (h[i].status == LT_OK) ? h[i].iterations + h[i].preemptions : 0;
+    off[i] = tot;
+    tot += len[i];
+    tb[i] = static_cast<int32_t>(P.h_scen[i].req_begin);
+    te[i] = static_cast<int32_t>(P.h_scen[i].req_begin + P.h_scen[i].n_req);
+  }
+  if (tot >= (int64_t(1) << 31)) throw CudaError{"percentiles: more than 2^31 ITL records in one plan"};
+  for (int64_t i = 0; i < n; ++i) {
+    rb[i] = static_cast<int32_t>(off[i]);
+    re[i] = static_cast<int32_t>(off[i] + len[i]);
+  }
+  const int64_t nt = std::max<int64_t>(tot, 1), nr = std::max<int64_t>(P.total_req, 1);
+  P.rec_off.upload(off, st);
+  P.rec_len.upload(len, st);
+  P.pct_rseg_b.upload(rb, st);
+  P.pct_rseg_e.upload(re, st);
+  P.pct_seg_b.upload(tb, st);
+  P.pct_seg_e.upload(te, st);
+  P.rec_d.alloc(nt);
+  P.rec_c.alloc(nt);
+  P.rec_d_sorted.alloc(nt);
+  P.rec_c_sorted.alloc(nt);
+  P.ttft_keys.alloc(nr);
+  P.ttft_sorted.alloc(nr);
+  LT_CUDA(cudaMemsetAsync(P.rec_c.p, 0, nt * sizeof(int32_t), st));
+  reset_state(P);
+  E.record = 1;
+  E.rec_off = P.rec_off.p;
+  E.rec_d = P.rec_d.p;
+  E.rec_c = P.rec_c.p;
+  engine_kernel<<<P.grid, P.block, P.smem, st>>>(E);
+  after_launch("engine_kernel(record)", st);
+  ttft_keys_kernel<<<static_cast<unsigned>((nr + 255) / 256), 256, 0, st>>>(P.r_arr.p, P.r_first.p, nr,
+                                                                            P.ttft_keys.p);
+  after_launch("ttft_keys_kernel", st);
+  size_t b1 = 0, b2 = 0;
+  LT_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, b1, P.ttft_keys.p, P.ttft_sorted.p, static_cast<int>(nr),
+                                             static_cast<int>(n), P.pct_seg_b.p, P.pct_seg_e.p, st));
+  LT_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, b2, P.rec_d.p, P.rec_d_sorted.p, P.rec_c.p,
+                                              P.rec_c_sorted.p, static_cast<int>(nt), static_cast<int>(n),
+                                              P.pct_rseg_b.p, P.pct_rseg_e.p, st));
+  P.pct_tmp.alloc(static_cast<int64_t>(std::max<size_t>(std::max(b1, b2), 1)));
+  LT_CUDA(cub::DeviceSegmentedSort::SortKeys(P.pct_tmp.p, b1, P.ttft_keys.p, P.ttft_sorted.p, static_cast<int>(nr),
+                                             static_cast<int>(n), P.pct_seg_b.p, P.pct_seg_e.p, st));
+  LT_CUDA(cub::DeviceSegmentedSort::SortPairs(P.pct_tmp.p, b2, P.rec_d.p, P.rec_d_sorted.p, P.rec_c.p,
+                                              P.rec_c_sorted.p, static_cast<int>(nt), static_cast<int>(n),
+                                              P.pct_rseg_b.p, P.pct_rseg_e.p, st));
+  percentile_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, st>>>(
+      P.scen.p, static_cast<int>(n), P.ttft_sorted.p, P.rec_off.p, P.rec_len.p, P.rec_d_sorted.p,
+      P.rec_c_sorted.p, P.out.p);
+  after_launch("percentile_kernel", st);
+  P.launches_run += 4;
 }
 
 void fetch_results(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {

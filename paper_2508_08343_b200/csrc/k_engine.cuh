@@ -159,6 +159,8 @@ struct WarpEngine {
   // Fresh admissions of the current iteration (first-token times): lane j
   // holds the j-th request id; n_fresh > 32 falls back to a running-set walk.
   int32_t fresh_id = 0, n_fresh = 0;
+  // Re-admissions from the preempted queue this iteration (recording pass).
+  int32_t readmit_id = 0, n_readmit = 0;
   // Chunk minima of retire iterations: chunk c < 32 lives in lane c's
   // cmin_r, chunks >= 32 in global cmin[]. next_fin <= every live retire
   // iteration (warp-uniform).
@@ -520,6 +522,10 @@ struct WarpEngine {
           const int f = __shfl_sync(kFull, fin_l, src);
           const int sv = __shfl_sync(kFull, s_l, src);
           run_append(make_int4(idx, f, ad | (is_pq ? 0 : kFreshBit), sv));
+          if (is_pq) {
+            if (lane == (n_readmit & 31)) readmit_id = idx;
+            ++n_readmit;
+          }
         }
       }
       if ((rejected >> lane) & 1u) P.r_phase[rb + e.x] = kRejected;
@@ -986,6 +992,8 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     pf_out = P.r_out[E.rb + jc];
   }
   double next_arr = __shfl_sync(kFull, pf_t, 0);  // arrival time of request `ingest`
+  const int64_t rec_base = P.record ? P.rec_off[s] : 0;
+  int64_t rec_n = 0;
 
   while (true) {
     __syncwarp();
@@ -1071,6 +1079,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     E.evicted_w = 0;
     E.blocked_w = 0;
     E.n_fresh = 0;
+    E.n_readmit = 0;
     {
       bool go = true;
       E.Wp = E.scan(P, E.pq, E.Wp, true, &go);
@@ -1102,6 +1111,40 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     const double adapters = (A == 0) ? 1.0 : P.k6 * static_cast<double>(A) + P.k7;
     const double lat = sched + loads + model * adapters;
     const double emit = E.clock + lat;
+    if (P.record) {  // ITL multiset of compute_metrics (metrics.cpp:92-105)
+      const int64_t r0 = rec_base + rec_n;
+      if (lane == 0) {
+        P.rec_d[r0] = emit - E.clock;
+        P.rec_c[r0] = E.R - E.n_fresh - E.n_readmit;
+      }
+      int wrote = 1;
+      if (E.n_readmit <= 32) {
+        if (lane < E.n_readmit) {
+          P.rec_d[r0 + 1 + lane] = emit - P.r_last[E.rb + E.readmit_id];
+          P.rec_c[r0 + 1 + lane] = 1;
+        }
+        wrote += E.n_readmit;
+      } else {  // this iteration's admissions without the fresh bit
+        for (int base = r_before; base < E.R_end; base += 32) {
+          const int i = base + lane;
+          bool re = false;
+          int idx = 0;
+          if (i < E.R_end) {
+            const int4 e = *E.rp(i);
+            re = e.x >= 0 && !(e.z & kFreshBit);
+            idx = e.x;
+          }
+          const unsigned m = __ballot_sync(kFull, re);
+          if (re) {
+            const int64_t o = r0 + wrote + __popc(m & lanemask_lt());
+            P.rec_d[o] = emit - P.r_last[E.rb + idx];
+            P.rec_c[o] = 1;
+          }
+          wrote += __popc(m);
+        }
+      }
+      rec_n += wrote;
+    }
     // first tokens of this iteration's fresh admissions (engine.cpp:131)
     if (E.n_fresh <= 32) {
       if (lane < E.n_fresh) P.r_first[E.rb + E.fresh_id] = emit;
@@ -1155,6 +1198,10 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         while (n < n_max && t_next > clk) {
           start = clk;
           clk = clk + lat_q;
+          if (P.record && lane == 0) {
+            P.rec_d[rec_base + rec_n + n] = clk - start;
+            P.rec_c[rec_base + rec_n + n] = E.R;
+          }
           win += (clk <= E.duration);
           ++n;
           if (P.want_digest) {
@@ -1164,6 +1211,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
           }
         }
         const long long rn = static_cast<long long>(E.R) * n;
+        rec_n += n;
         E.clock = clk;
         E.prev_now = start;  // ensure_loaded's last_used refresh of the last skipped iteration
         E.used += rn;

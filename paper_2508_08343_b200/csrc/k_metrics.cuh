@@ -1,0 +1,101 @@
+// K2b: the nearest-rank percentiles of compute_metrics (metrics.cpp:47-54,
+// :101-105), filled only when a run asks for them (sweep_optimal reads only
+// throughput and the starved verdict, placement.cpp:216).
+//
+//   TTFT: one value per request with a first token (first - arrival), sorted
+//         per scenario (CUB segmented sort); requests without one carry +inf
+//         and sort last.
+//   ITL:  the reference's list holds every gap between consecutive emits of
+//         every request. All running requests emit at the same time, so the
+//         list is the multiset {(emit_k - emit_{k-1}) x c_k} over iterations
+//         (c_k = requests emitting in both k-1 and k) plus one gap per
+//         re-admitted preempted request (first emit after - last emit
+//         before). The recording engine pass writes those (value, weight)
+//         records; a segmented sort by value and a weighted rank select give
+//         the identical order statistic.
+#pragma once
+#include "lt_device.cuh"
+
+namespace lt {
+
+__global__ void ttft_keys_kernel(const double* r_arr, const double* r_first, int64_t n, double* keys) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double f = r_first[i];
+  keys[i] = (f == f) ? f - r_arr[i] : INFINITY;
+}
+
+// 1-based nearest rank ceil(pct/100 * n) clamped to [1, n] (n >= 1).
+__device__ __forceinline__ int64_t nearest_rank(double pct, int64_t n) {
+  int64_t r = static_cast<int64_t>(ceil(pct / 100.0 * static_cast<double>(n)));
+  return r < 1 ? 1 : (r > n ? n : r);
+}
+
+// One warp per scenario.
+__global__ void __launch_bounds__(256) percentile_kernel(const DScen* scen, int n_scen, const double* ttft_sorted,
+                                                        const int64_t* rec_off, const int64_t* rec_len,
+                                                        const double* rec_d, const int32_t* rec_c,
+                                                        lt_sim_summary* out) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= n_scen) return;
+  lt_sim_summary& o = out[s];
+  if (o.status != LT_OK || o.degenerate) return;
+  // --- TTFT: count of finite keys by binary search for the first +inf
+  const double* t = ttft_sorted + scen[s].req_begin;
+  const int64_t nr = scen[s].n_req;
+  int64_t lo = 0, hi = nr;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (t[mid] == INFINITY)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  const int64_t nt = lo;
+  if (lane == 0) {
+    o.ttft_p50_s = nt ? t[nearest_rank(50.0, nt) - 1] : 0.0;
+    o.ttft_p99_s = nt ? t[nearest_rank(99.0, nt) - 1] : 0.0;
+  }
+  // --- ITL: weighted rank select over (value, weight) records sorted by value
+  const int64_t b = rec_off[s], len = rec_len[s];
+  long long total = 0;
+  for (int64_t i = lane; i < len; i += 32) total += rec_c[b + i];
+  for (int off = 16; off > 0; off >>= 1) total += __shfl_xor_sync(full, total, off);
+  double p50 = 0.0, p99 = 0.0;
+  if (total > 0) {
+    const long long r50 = nearest_rank(50.0, total), r99 = nearest_rank(99.0, total);
+    long long base = 0;  // weight of the records before this chunk
+    bool got50 = false, got99 = false;
+    for (int64_t c0 = 0; c0 < len && !got99; c0 += 32) {
+      const int64_t i = c0 + lane;
+      const long long w = (i < len) ? rec_c[b + i] : 0;
+      long long incl = w;  // inclusive prefix within the chunk
+      for (int off = 1; off < 32; off <<= 1) {
+        const long long y = __shfl_up_sync(full, incl, off);
+        if (lane >= off) incl += y;
+      }
+      const long long cum = base + incl;
+      const unsigned h50 = __ballot_sync(full, !got50 && w > 0 && cum >= r50);
+      const unsigned h99 = __ballot_sync(full, w > 0 && cum >= r99);
+      if (h50) {
+        const int src = __ffs(h50) - 1;
+        p50 = __shfl_sync(full, (i < len) ? rec_d[b + (c0 + lane)] : 0.0, src);
+        got50 = true;
+      }
+      if (h99) {
+        const int src = __ffs(h99) - 1;
+        p99 = __shfl_sync(full, (i < len) ? rec_d[b + (c0 + lane)] : 0.0, src);
+        got99 = true;
+      }
+      base += __shfl_sync(full, incl, 31);
+    }
+  }
+  if (lane == 0) {
+    o.itl_p50_s = p50;
+    o.itl_p99_s = p99;
+  }
+}
+
+}  // namespace lt

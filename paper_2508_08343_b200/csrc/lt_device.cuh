@@ -106,6 +106,13 @@ struct EngineParams {
   int32_t priority;
   int32_t want_digest;
   lt_sim_summary* out;
+  // recording pass (want_percentiles): per iteration one ITL record
+  // (emit_k - emit_{k-1}, requests emitting in both iterations) and one
+  // (gap, 1) record per re-admitted preempted request, at rec_off[s]
+  int32_t record;
+  const int64_t* rec_off;
+  double* rec_d;
+  int32_t* rec_c;
 };
 
 }  // namespace lt

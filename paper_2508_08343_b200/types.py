@@ -179,10 +179,14 @@ class RequestState:  # kv_scheduler.hpp:30-41 (token emit vectors are not materi
 
 
 @dataclass
-class MetricsSummary:  # metrics.hpp:27-40 (percentiles are not computed on device yet)
+class MetricsSummary:  # metrics.hpp:27-40
     throughput_tok_s: float = 0.0
     itl_mean_s: float = 0.0
+    itl_p50_s: float = 0.0
+    itl_p99_s: float = 0.0
     ttft_mean_s: float = 0.0
+    ttft_p50_s: float = 0.0
+    ttft_p99_s: float = 0.0
     ideal_throughput_tok_s: float = 0.0
     starved: bool = False
     finished_count: int = 0

@@ -292,3 +292,58 @@ def test_port_oracle_c2_sample(dev, port):
     g, _ = dev.simulate_batch(b, cfg, want_digest=True)
     p, _ = port.simulate(b, cfg, sim_options(None, True))
     assert_summaries(g, p)
+
+
+# --- compute_metrics percentiles (metrics.cpp:47-54, :101-105) -------------------------------------
+
+PCT_FIELDS = ["ttft_p50_s", "ttft_p99_s", "itl_p50_s", "itl_p99_s"]
+
+
+def assert_percentiles(g, r, where=""):
+    ok = g["status"] == 0
+    for f in PCT_FIELDS:
+        bad = np.nonzero(ok & (g[f] != r[f]))[0]
+        assert bad.size == 0, f"{where}{f} differs at {bad[:10]}: gpu={g[f][bad[:3]]} ref={r[f][bad[:3]]}"
+
+
+def test_percentiles_summary_cases(dev, ref):
+    """Nearest-rank TTFT/ITL p50/p99 bit-exact (recording pass + segmented sorts)."""
+    b, cfg = W.summary_cases()
+    g, _ = dev.simulate_batch(b, cfg, want_digest=True, want_percentiles=True)
+    r, _ = ref.simulate(b, cfg, sim_options(None, True))
+    assert_summaries(g, r)
+    assert_percentiles(g, r)
+    assert (g["itl_p99_s"] > 0).sum() > 10
+
+
+def test_percentiles_c2_subset_and_truncation(dev, ref):
+    b = W.c2_batch(duration_s=600.0, stride=16)
+    cfg = lt.h100_like_config(1)
+    g, _ = dev.simulate_batch(b, cfg, want_percentiles=True)
+    r, _ = ref.simulate(b, cfg, sim_options())
+    assert_summaries(g, r, digest=False)
+    assert_percentiles(g, r)
+    b2, cfg2 = W.summary_cases()
+    opts = lt.SimOptions(iteration_cap_override=700)
+    g, _ = dev.simulate_batch(b2, cfg2, options=opts, want_percentiles=True)
+    r, _ = ref.simulate(b2, cfg2, sim_options(opts))
+    assert_percentiles(g, r, "truncated: ")
+
+
+def test_percentiles_scripted_fuzz_with_preemption(dev, ref):
+    wls, scripts, cfgs = [], [], []
+    for seed in range(24):
+        ads, reqs, cfg = W.scripted_fuzz(5000 + seed)
+        b = WorkloadBatch.from_workloads([W.scripted_workload(ads, 6.0)], scripted=[reqs])
+        g, _ = dev.simulate_batch(b, cfg, want_percentiles=True)
+        r, _ = ref.simulate(b, cfg, sim_options())
+        assert_percentiles(g, r, f"seed {seed}: ")
+
+
+def test_percentiles_through_run_simulation(dev, ref):
+    wl = lt.WorkloadSpec(adapters=[lt.AdapterSpec(i, 16, 0.4) for i in range(1, 9)],
+                         lengths=lt.LengthSpec.mean(250, 50, 231, 50), duration_s=300.0, seed=1)
+    cfg = lt.h100_like_config(4)
+    m = lt.compute_metrics(lt.run_simulation(wl, cfg, dev=dev), wl)
+    r, _ = ref.simulate(WorkloadBatch.from_workloads([wl]), cfg, sim_options())
+    assert (m.ttft_p50_s, m.ttft_p99_s, m.itl_p50_s, m.itl_p99_s) == tuple(float(r[0][f]) for f in PCT_FIELDS)
