@@ -396,6 +396,12 @@ struct lt_plan {
   DBuf<DLen> lens;
   DBuf<DKey> keys;
   DBuf<uint64_t> seed_state;   // K0a -> K0b: seeded MT19937-64 states of one key chunk
+  // Full-mode length decks
+  std::vector<DDeck> h_decks;
+  DBuf<DDeck> decks;
+  DBuf<int32_t> deck_tab, big_deck, full;
+  DBuf<int64_t> big_off;
+  size_t deck_smem = 0;
   DBuf<int32_t> tab_overflow;  // set when some key's table was too short
   DBuf<double> E;
   DBuf<double2> Z;
@@ -465,6 +471,8 @@ struct Prep {
   };
   std::unordered_map<uint64_t, int32_t> seed_index;
   std::vector<SeedKeys> seeds;
+  std::vector<DDeck> decks;                        // Full-mode decks, table_off set after sizing
+  std::map<std::pair<int32_t, int32_t>, int32_t> deck_index;  // (key, D) -> deck
   std::vector<double> cost;
 
   SeedKeys& seed_keys(uint64_t seed) {
@@ -571,10 +579,6 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
       const lt_length_spec& l = lengths_of(ad[k]);
       if (s.mode != l.mode && s.mode == LT_MODE_FULL)
         return e.set(LT_ERR_VALIDATION, "workload.lengths: cannot force Full mode without a length list"), fail();
-      if (s.mode == LT_MODE_FULL && l.mode == LT_MODE_FULL)
-        return e.set(LT_ERR_UNSUPPORTED, "Full-mode length sampling is not implemented on the device path",
-                     LT_K_MESSAGE),
-               fail();
     }
   }
   // Engine::Engine (engine.cpp:32-71)
@@ -628,6 +632,7 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
     x.load_lat = load_latency_cached(P.cfg, a.rank);
     x.length_param = a.length_index >= 0 ? intern_len(pr, as_dlen(b.lengths[a.length_index], full)) : -1;
     x.key = -1;
+    x.deck = -1;
     if (!scripted) {
       bool inserted = false;
       const int kidx = Prep::find_or_insert(*sk, a.adapter_id, static_cast<int32_t>(pr.keys.size()), &inserted);
@@ -644,6 +649,17 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
         k.dur_max = std::max(k.dur_max, s.duration_s);
       }
       x.key = kidx;
+      const lt_length_spec& la = lengths_of(a);
+      if (s.mode == LT_MODE_FULL && la.mode == LT_MODE_FULL) {  // deck sampling (workload.cpp:149-161)
+        const auto dkey = std::make_pair(static_cast<int32_t>(kidx), static_cast<int32_t>(la.full_count));
+        auto it = pr.deck_index.find(dkey);
+        if (it == pr.deck_index.end()) {
+          it = pr.deck_index.emplace(dkey, static_cast<int32_t>(pr.decks.size())).first;
+          pr.decks.push_back(DDeck{0, dkey.first, dkey.second});
+        }
+        x.deck = it->second;
+        x.list_off = la.full_offset;
+      }
       pr.pair_scen.push_back(static_cast<int32_t>(i));
       pr.pair_adp.push_back(k);
       const lt_length_spec& l = lengths_of(a);
@@ -712,7 +728,39 @@ int launch_tables(lt_plan& P, int nk, cudaStream_t st) {
     after_launch("tables_draw_kernel", st);
     launches += 2;
   }
+  if (!P.h_decks.empty()) {
+    LT_CUDA(cudaFuncSetAttribute(deck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(P.deck_smem)));
+    deck_kernel<<<static_cast<unsigned>(P.h_decks.size()), 32, P.deck_smem, st>>>(
+        P.keys.p, P.decks.p, P.deck_tab.p, P.big_deck.p, P.big_off.p);
+    after_launch("deck_kernel", st);
+    ++launches;
+  }
   return launches;
+}
+
+// Full-mode deck tables: one slot per possible arrival of the deck's key.
+void size_decks(lt_plan& P, const std::vector<DKey>& keys, cudaStream_t st) {
+  if (P.h_decks.empty()) return;
+  int64_t off = 0, big = 0;
+  int max_small = 0;
+  std::vector<int64_t> boff(P.h_decks.size(), 0);
+  for (size_t d = 0; d < P.h_decks.size(); ++d) {
+    DDeck& dk = P.h_decks[d];
+    dk.table_off = off;
+    off += keys[dk.key].cap;
+    if (dk.D > kDeckSmemMax) {
+      boff[d] = big;
+      big += dk.D;
+    } else {
+      max_small = std::max(max_small, dk.D);
+    }
+  }
+  P.decks.upload(P.h_decks, st);
+  P.deck_tab.alloc(std::max<int64_t>(off, 1));
+  P.big_off.upload(boff, st);
+  P.big_deck.alloc(std::max<int64_t>(big, 1));
+  P.deck_smem = 624 * sizeof(uint32_t) + kMtN * sizeof(uint64_t) + static_cast<size_t>(max_small) * sizeof(int32_t);
 }
 
 // Builds a plan: validation, RNG tables, counting, merge, request arrays,
@@ -766,7 +814,13 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   if (!pr.keys.empty())
     P.seed_state.alloc(std::min<int64_t>(static_cast<int64_t>(pr.keys.size()), kSeedChunk) * 2 * kMtN);
   P.tab_overflow.alloc(1);
+  P.h_decks = pr.decks;
+  if (!P.h_decks.empty() && b->n_full_pairs > 0) {
+    std::vector<int32_t> fl(b->full_lengths, b->full_lengths + 2 * b->n_full_pairs);
+    P.full.upload(fl, st);
+  }
   for (int attempt = 0;; ++attempt) {
+    size_decks(P, pr.keys, st);
     P.keys.upload(pr.keys, st);
     LT_CUDA(cudaMemsetAsync(P.tab_overflow.p, 0, sizeof(int32_t), st));
     P.E.alloc(std::max<int64_t>(e_total, 1));
@@ -1005,7 +1059,7 @@ void prepare_requests(lt_plan& P) {
                                                       static_cast<int>(P.n_scen), P.seg_begin.p, P.seg_end.p, st));
     gather_kernel<<<static_cast<unsigned>((std::max<int64_t>(P.total_req, 1) + 255) / 256), 256, 0, st>>>(
         P.scen.p, static_cast<int>(P.n_scen), P.total_req, P.adapters.p, P.keys.p, P.lens.p, P.Z.p, P.st_out.p,
-        P.sv_out.p, P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p);
+        P.sv_out.p, P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p, P.decks.p, P.deck_tab.p, P.full.p);
     after_launch("gather_kernel", st);
     launches += 3;  // + CUB scan and segmented sort (library kernels)
   }

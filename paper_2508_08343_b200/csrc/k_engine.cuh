@@ -930,13 +930,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   const DScen sc = P.scen[s];
   lt_sim_summary o;
   memset(&o, 0, sizeof(o));
-  o.n_requests = sc.n_req;
-  o.duration_s = sc.duration;
-  o.slots = sc.G;
-  o.served_adapters = sc.n_adapters;
-  o.kv_capacity_tokens = sc.capacity;
-  o.ideal_throughput_tok_s = sc.ideal;
-  if (sc.status != LT_OK) {
+  if (sc.status != LT_OK) {  // failed before the loop (validation / Engine ctor): status only
     o.status = sc.status;
     o.status_kind = sc.status_kind;
     o.status_a = sc.status_a;
@@ -944,6 +938,12 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     if (lane == 0) P.out[s] = o;
     return;
   }
+  o.n_requests = sc.n_req;
+  o.duration_s = sc.duration;
+  o.slots = sc.G;
+  o.served_adapters = sc.n_adapters;
+  o.kv_capacity_tokens = sc.capacity;
+  o.ideal_throughput_tok_s = sc.ideal;
   E.rb = sc.req_begin;
   E.ab = sc.adapter_begin;
   E.n_req = sc.n_req;

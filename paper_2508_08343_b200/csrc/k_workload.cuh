@@ -249,6 +249,72 @@ __global__ void __launch_bounds__(128) tables_draw_kernel(DKey* keys, int k0, in
   }
 }
 
+// ---- K0c: Full-mode decks, one warp per (key, D). Lane 0 runs seed_seq for
+// the lengths stream {2, id} (rng.hpp:35-46) and every Fisher-Yates step
+// (rng.hpp:86-91) with uniform_below's rejection (rng.hpp:76-82); the warp
+// refills 312 tempered outputs at a time. After each shuffle the deck order
+// is written as the list indices of the next D arrivals.
+constexpr int kDeckSmemMax = 8192;
+
+__global__ void __launch_bounds__(32) deck_kernel(const DKey* keys, const DDeck* decks, int32_t* tab,
+                                                  int32_t* big_deck, const int64_t* big_off) {
+  extern __shared__ __align__(16) char dsm[];
+  uint32_t* sb = reinterpret_cast<uint32_t*>(dsm);                        // 624 words: seed_seq / state
+  uint64_t* obuf = reinterpret_cast<uint64_t*>(dsm + 624 * sizeof(uint32_t));  // 312 tempered outputs
+  int32_t* sdeck = reinterpret_cast<int32_t*>(obuf + kMtN);
+  const int lane = threadIdx.x;
+  const DDeck dk = decks[blockIdx.x];
+  const DKey key = keys[dk.key];
+  const int D = dk.D;
+  const int64_t n = key.z_len;  // arrivals at the key's largest rate and window
+  if (n <= 0) return;
+  int32_t* deck = (D <= kDeckSmemMax) ? sdeck : big_deck + big_off[blockIdx.x];
+  if (lane == 0) {
+    const uint64_t id = static_cast<uint64_t>(key.id);
+    const uint32_t v[6] = {static_cast<uint32_t>(key.seed), static_cast<uint32_t>(key.seed >> 32), 2u, 0u,
+                           static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32)};
+    seed_seq_row(sb, v);
+  }
+  for (int c = lane; c < D; c += 32) deck[c] = c;
+  __syncwarp();
+  uint64_t* st = reinterpret_cast<uint64_t*>(sb);
+  int32_t* out = tab + dk.table_off;
+  const int64_t nshuf = 1 + (n - 1) / D;
+  int i = D;       // lane 0: Fisher-Yates position of the current shuffle
+  int64_t k = 0;   // lane 0: shuffles completed
+  for (;;) {
+    mt64_twist_block(st, lane);
+    for (int w = lane; w < kMtN; w += 32) obuf[w] = mt64_temper(st[w]);
+    __syncwarp();
+    int stop = 0;
+    if (lane == 0) {
+      int p = 0;
+      while (k < nshuf) {
+        if (i > 1) {
+          if (p == kMtN) break;  // block exhausted: refill
+          const uint64_t bound = static_cast<uint64_t>(i);
+          const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+          const uint64_t draw = obuf[p++];
+          if (draw >= limit) continue;  // rejected: redraw for the same bound
+          const int j = static_cast<int>(draw % bound);
+          const int32_t tmp = deck[i - 1];
+          deck[i - 1] = deck[j];
+          deck[j] = tmp;
+          --i;
+          continue;
+        }
+        const int64_t base = k * D;
+        const int64_t cnt = (n - base < D) ? n - base : D;
+        for (int64_t c = 0; c < cnt; ++c) out[base + c] = deck[c];
+        ++k;
+        i = D;
+      }
+      stop = k >= nshuf;
+    }
+    if (__shfl_sync(0xffffffffu, stop, 0)) break;
+  }
+}
+
 // Arrivals of one (scenario, adapter): count t < duration (workload.cpp:179-183).
 // One warp per pair: the table loads and divisions E_j / rate of 32 draws run
 // in parallel; the running sum t is the reference's sequential chain, one add
@@ -361,7 +427,9 @@ __global__ void __launch_bounds__(256) gather_kernel(const DScen* scen, int n_sc
                                                     const DAdapter* adapters, const DKey* keys, const DLen* lens,
                                                     const double2* Z, const double* t_sorted,
                                                     const unsigned long long* v_sorted, double* r_arr,
-                                                    int32_t* r_in, int32_t* r_out, int32_t* r_adp) {
+                                                    int32_t* r_in, int32_t* r_out, int32_t* r_adp,
+                                                    const DDeck* decks, const int32_t* deck_tab,
+                                                    const int32_t* full) {
   const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (g >= total_req) return;
   int lo = 0, hi = n_scen - 1;  // last scenario with req_begin <= g
@@ -378,10 +446,16 @@ __global__ void __launch_bounds__(256) gather_kernel(const DScen* scen, int n_sc
   const int a = static_cast<int>(v >> 32);
   const int j = static_cast<int>(v & 0xffffffffULL);
   const DAdapter ad = adapters[sc.adapter_begin + a];
-  const double2 z = Z[keys[ad.key].z_off + j];
-  const DLen L = lens[ad.length_param >= 0 ? ad.length_param : sc.length_param];
   r_arr[g] = t_sorted[g];
   r_adp[g] = a;
+  if (ad.deck >= 0) {  // Full mode: the shuffled deck's list entry
+    const int64_t q = ad.list_off + deck_tab[decks[ad.deck].table_off + j];
+    r_in[g] = full[2 * q];
+    r_out[g] = full[2 * q + 1];
+    return;
+  }
+  const double2 z = Z[keys[ad.key].z_off + j];
+  const DLen L = lens[ad.length_param >= 0 ? ad.length_param : sc.length_param];
   r_in[g] = round_clamp_token(affine(L.mean_in, L.std_in, z.x));
   r_out[g] = round_clamp_token(affine(L.mean_out, L.std_out, z.y));
 }

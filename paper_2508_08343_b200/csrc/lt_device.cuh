@@ -56,6 +56,18 @@ struct DAdapter {
   double load_lat;  // NaN: rank missing from cpu_load_seconds (lazy ConfigError)
   int32_t key;      // RNG table key (generated scenarios)
   int32_t length_param;
+  int32_t deck;     // >= 0: Full-mode lengths from DDeck[deck] (sample_lengths, workload.cpp:149-161)
+  int32_t _pad;
+  int64_t list_off; // Full mode: first (in, out) pair of the adapter's length list
+};
+
+// Full-mode length deck of one (RNG key, list size D): the lengths stream
+// {2, id} shuffles the deck once, then again every D requests
+// (workload.cpp:149-161). tab[table_off + j] is the list index of arrival j.
+struct DDeck {
+  int64_t table_off;
+  int32_t key;
+  int32_t D;
 };
 
 struct DLen {

@@ -347,3 +347,18 @@ def test_percentiles_through_run_simulation(dev, ref):
     m = lt.compute_metrics(lt.run_simulation(wl, cfg, dev=dev), wl)
     r, _ = ref.simulate(WorkloadBatch.from_workloads([wl]), cfg, sim_options())
     assert (m.ttft_p50_s, m.ttft_p99_s, m.itl_p50_s, m.itl_p99_s) == tuple(float(r[0][f]) for f in PCT_FIELDS)
+
+
+# --- Full-mode length decks (workload.cpp:149-161, rng.hpp:76-91) -----------------------------------
+
+def test_full_mode_arrivals_and_summaries(dev, ref):
+    b, cfg = W.full_mode_cases()
+    g, gc = dev.generate_arrivals_batch(b)
+    r, rc = ref.generate_arrivals(b, sim_options())
+    np.testing.assert_array_equal(gc, rc)
+    for f in ("request_id", "adapter_id", "input_tokens", "output_tokens", "arrival_time_s"):
+        np.testing.assert_array_equal(g[f], r[f], err_msg=f)
+    g, _ = dev.simulate_batch(b, cfg, want_digest=True, want_percentiles=True)
+    r, _ = ref.simulate(b, cfg, sim_options(None, True))
+    assert_summaries(g, r)
+    assert_percentiles(g, r)

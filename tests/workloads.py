@@ -176,3 +176,25 @@ def scripted_fuzz(seed: int, n_requests: int = 60, n_adapters: int = 5, tight: b
         load=lt.LoadLatencyTable(cpu_load_seconds={8: 0.05, 16: 0.09}),
         loaded_adapter_priority=bool(seed % 2 == 0))
     return ads, reqs, cfg
+
+
+def full_mode_cases():
+    """Full-mode length decks (sample_lengths, workload.cpp:149-161): deck sizes
+    from 1 to beyond the device's shared-memory deck (8192), per-adapter lists,
+    reshuffles on wrap, shared seeds."""
+    rng = np.random.default_rng(77)
+    wls = []
+    for i in range(18):
+        D = [1, 2, 7, 50, 300, 9000][i % 6]
+        pairs = [(int(rng.integers(1, 400)), int(rng.integers(1, 300))) for _ in range(D)]
+        n = [1, 5, 12, 40][i % 4]
+        ads = [lt.AdapterSpec(k + 1, (8, 16, 32)[k % 3], float(rng.choice([0.05, 0.3, 2.0]))) for k in range(n)]
+        if i % 3 == 1:
+            own = [(int(rng.integers(1, 900)), int(rng.integers(1, 90))) for _ in range(int(rng.integers(1, 40)))]
+            for a in ads[::2]:
+                a.lengths = lt.LengthSpec.full(own)
+        if i % 5 == 2:
+            ads[0].lengths = lt.LengthSpec.mean(100.0, 20.0, 60.0, 10.0)
+        wls.append(lt.WorkloadSpec(adapters=ads, lengths=lt.LengthSpec.full(pairs), duration_s=150.0,
+                                   seed=100 + i // 2))
+    return WorkloadBatch.from_workloads(wls, mode=lt.LengthMode.Full), lt.h100_like_config(8)
