@@ -347,6 +347,53 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch,
                        const lt_sim_options* sim_options, lt_placement* out,
                        lt_frontier_point* frontier, int32_t max_frontier, lt_status* status);
 
+/* ---- Dataset generation (placement.hpp:104-158) -------------------------- */
+
+/* DatasetSpec (placement.hpp:126-137). lengths.full_offset / full_count index
+ * full_lengths (in, out pairs). */
+typedef struct lt_dataset_spec {
+  const double* rates;
+  int32_t n_rates;
+  int32_t triple_size;
+  const int32_t* ranks;
+  int32_t n_ranks;
+  int32_t condition_stride;
+  lt_length_spec lengths;
+  const int32_t* full_lengths;
+  int64_t n_full_pairs;
+  double duration_s;
+  uint64_t seed;
+  lt_sweep_grid grid;
+  lt_sweep_options sweep; /* jobs is accepted and ignored: conditions run as one device batch */
+} lt_dataset_spec;
+
+/* DatasetProgress (placement.hpp:143-147). */
+typedef struct lt_dataset_progress {
+  int64_t total_conditions;
+  int64_t completed; /* includes rows found on resume */
+  int64_t failed;
+} lt_dataset_progress;
+
+/* on_error of generate_dataset: called in canonical condition order. */
+typedef void (*lt_error_fn)(const char* message, void* user);
+
+/* generate_dataset (placement.cpp:415-527): enumerates the conditions, resumes
+ * from the hashes already in out_csv (truncating a torn tail), sweeps every
+ * pending condition on the device in one batched lt_sweep_batch per chunk and
+ * appends the rows in canonical order. Same file bytes as the reference. */
+int32_t lt_generate_dataset(lt_ctx* ctx, const lt_dataset_spec* spec, const lt_server_config* config,
+                            const char* out_csv, lt_error_fn on_error, void* user,
+                            lt_dataset_progress* progress, lt_status* status);
+
+/* condition_hash (placement.cpp:266-296): FNV-1a over the canonical text. */
+uint64_t lt_condition_hash(const lt_template* mix, int32_t n_mix, const lt_length_spec* lengths,
+                           const int32_t* full_lengths, double duration_s, uint64_t seed,
+                           const lt_sweep_grid* grid);
+
+/* encode_workload (placement.cpp:117-137): the 16 features. */
+int32_t lt_encode_workload(const lt_template* mix, int32_t n_mix, const lt_length_spec* lengths,
+                           const int32_t* full_lengths, double* features16, lt_status* status);
+
 /* Resident-input form for timing the device path alone: upload once, run
  * many times with inputs already in HBM, read results back once. */
 typedef struct lt_plan lt_plan;

@@ -38,11 +38,12 @@ def build(target: str = "all") -> None:
 class _Oracle(Runner):
     prefix = ""
     path = ""
+    extra_symbols: list = []
 
     def __init__(self, threads: int = 1):
         if not os.path.exists(self.path):
             build("ref" if self.prefix == "ltref_" else "restate")
-        lib = A.Lib(self.path, self.prefix, A.ORACLE_SYMBOLS)
+        lib = A.Lib(self.path, self.prefix, A.ORACLE_SYMBOLS + self.extra_symbols)
         self._set_threads = getattr(lib.dll, self.prefix + "set_threads")
         self._set_threads.argtypes = [C.c_int32]
         self._msg = getattr(lib.dll, self.prefix + "message")
@@ -64,6 +65,7 @@ class _Oracle(Runner):
 class RefOracle(_Oracle):
     prefix = "ltref_"
     path = REF_LIB
+    extra_symbols = A.DATASET_SYMBOLS
 
 
 class PortOracle(_Oracle):

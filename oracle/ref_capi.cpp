@@ -380,3 +380,89 @@ int32_t ltref_sweep_batch(void*, const lt_condition_batch* batch, const lt_serve
 }
 
 }  // extern "C"
+
+// generate_dataset / condition_hash / encode_workload (placement.hpp:104-158)
+// of the unmodified reference, for the dataset parity tests.
+namespace {
+DatasetSpec to_dataset(const lt_dataset_spec& d) {
+  DatasetSpec s;
+  s.rates.assign(d.rates, d.rates + d.n_rates);
+  s.ranks.assign(d.ranks, d.ranks + d.n_ranks);
+  s.triple_size = d.triple_size;
+  s.condition_stride = d.condition_stride;
+  s.lengths = to_lengths(d.lengths, d.full_lengths);
+  s.duration_s = d.duration_s;
+  s.seed = d.seed;
+  s.grid.n_values.assign(d.grid.n_values, d.grid.n_values + d.grid.n_count);
+  s.grid.g_mode = d.grid.g_mode == LT_G_EXPLICIT ? SweepGrid::GMode::Explicit : SweepGrid::GMode::Geometric;
+  if (d.grid.g_values) s.grid.g_values.assign(d.grid.g_values, d.grid.g_values + d.grid.g_count);
+  s.sweep.early_exit = d.sweep.early_exit != 0;
+  s.sweep.early_exit_k = d.sweep.early_exit_k;
+  s.sweep.jobs = d.sweep.jobs < 1 ? 1 : d.sweep.jobs;
+  s.sweep.mode = d.sweep.mode == LT_MODE_FULL ? LengthMode::Full : LengthMode::Mean;
+  return s;
+}
+Condition to_condition(const lt_template* mix, int32_t n_mix, const lt_length_spec* l, const int32_t* full) {
+  Condition c;
+  for (int32_t i = 0; i < n_mix; ++i) {
+    AdapterTemplate t;
+    t.rank = mix[i].rank;
+    t.rate = mix[i].rate;
+    c.mix.push_back(t);
+  }
+  c.lengths = to_lengths(*l, full);
+  return c;
+}
+}  // namespace
+
+extern "C" {
+
+int32_t ltref_generate_dataset(void*, const lt_dataset_spec* spec, const lt_server_config* config,
+                               const char* out_csv, lt_error_fn on_error, void* user,
+                               lt_dataset_progress* progress, lt_status* status) {
+  if (status) status->code = LT_OK;
+  try {
+    const DatasetSpec ds = to_dataset(*spec);
+    const DatasetProgress p = generate_dataset(ds, to_config(*config), out_csv, [&](const std::string& m) {
+      if (on_error) on_error(m.c_str(), user);
+    });
+    if (progress) {
+      progress->total_conditions = static_cast<int64_t>(p.total_conditions);
+      progress->completed = static_cast<int64_t>(p.completed);
+      progress->failed = static_cast<int64_t>(p.failed);
+    }
+    return LT_OK;
+  } catch (...) {
+    std::string msg;
+    const int32_t code = classify(std::current_exception(), &msg);
+    set_status(status, code, -1, msg);
+    return code;
+  }
+}
+
+uint64_t ltref_condition_hash(const lt_template* mix, int32_t n_mix, const lt_length_spec* lengths,
+                              const int32_t* full_lengths, double duration_s, uint64_t seed,
+                              const lt_sweep_grid* grid) {
+  SweepGrid g;
+  g.n_values.assign(grid->n_values, grid->n_values + grid->n_count);
+  g.g_mode = grid->g_mode == LT_G_EXPLICIT ? SweepGrid::GMode::Explicit : SweepGrid::GMode::Geometric;
+  if (grid->g_values) g.g_values.assign(grid->g_values, grid->g_values + grid->g_count);
+  return condition_hash(to_condition(mix, n_mix, lengths, full_lengths), duration_s, seed, g);
+}
+
+int32_t ltref_encode_workload(const lt_template* mix, int32_t n_mix, const lt_length_spec* lengths,
+                              const int32_t* full_lengths, double* features16, lt_status* status) {
+  if (status) status->code = LT_OK;
+  try {
+    const WorkloadFeatures f = encode_workload(to_condition(mix, n_mix, lengths, full_lengths));
+    for (int i = 0; i < 16; ++i) features16[i] = f.values[static_cast<size_t>(i)];
+    return LT_OK;
+  } catch (...) {
+    std::string msg;
+    const int32_t code = classify(std::current_exception(), &msg);
+    set_status(status, code, -1, msg);
+    return code;
+  }
+}
+
+}  // extern "C"

@@ -125,6 +125,21 @@ class lt_sweep_options(C.Structure):
                 ("mode", C.c_int32)]
 
 
+class lt_dataset_spec(C.Structure):
+    _fields_ = [("rates", C.POINTER(C.c_double)), ("n_rates", C.c_int32), ("triple_size", C.c_int32),
+                ("ranks", C.POINTER(C.c_int32)), ("n_ranks", C.c_int32), ("condition_stride", C.c_int32),
+                ("lengths", lt_length_spec), ("full_lengths", C.POINTER(C.c_int32)), ("n_full_pairs", C.c_int64),
+                ("duration_s", C.c_double), ("seed", C.c_uint64), ("grid", lt_sweep_grid),
+                ("sweep", lt_sweep_options)]
+
+
+class lt_dataset_progress(C.Structure):
+    _fields_ = [("total_conditions", C.c_int64), ("completed", C.c_int64), ("failed", C.c_int64)]
+
+
+ERROR_FN = C.CFUNCTYPE(None, C.c_char_p, C.c_void_p)
+
+
 class lt_frontier_point(C.Structure):
     _fields_ = [("n", C.c_int32), ("g", C.c_int32), ("throughput_tok_s", C.c_double),
                 ("starved", C.c_int32), ("skipped", C.c_int32)]
@@ -189,6 +204,13 @@ SIGNATURES = {
                                 C.POINTER(lt_sweep_grid), C.c_double, C.c_uint64,
                                 C.POINTER(lt_sweep_options), C.POINTER(lt_sim_options), C.c_void_p,
                                 C.c_void_p, C.c_int32, C.POINTER(lt_status)]),
+    "generate_dataset": (C.c_int32, [C.c_void_p, C.POINTER(lt_dataset_spec), C.POINTER(lt_server_config),
+                                     C.c_char_p, ERROR_FN, C.c_void_p, C.POINTER(lt_dataset_progress),
+                                     C.POINTER(lt_status)]),
+    "condition_hash": (C.c_uint64, [C.POINTER(lt_template), C.c_int32, C.POINTER(lt_length_spec),
+                                    C.POINTER(C.c_int32), C.c_double, C.c_uint64, C.POINTER(lt_sweep_grid)]),
+    "encode_workload": (C.c_int32, [C.POINTER(lt_template), C.c_int32, C.POINTER(lt_length_spec),
+                                    C.POINTER(C.c_int32), C.POINTER(C.c_double), C.POINTER(lt_status)]),
     "plan_simulate": (C.c_void_p, [C.c_void_p, C.POINTER(lt_workload_batch), C.POINTER(lt_server_config),
                                    C.POINTER(lt_sim_options), C.POINTER(lt_status)]),
     "plan_run": (C.c_int32, [C.c_void_p, C.POINTER(lt_status)]),
@@ -199,6 +221,8 @@ SIGNATURES = {
 
 # Symbols the oracle libraries must export (same meaning, other prefix).
 ORACLE_SYMBOLS = ["generate_arrivals_batch", "simulate_batch", "sweep_batch"]
+# ... and the dataset entry points (the compiled reference only)
+DATASET_SYMBOLS = ["generate_dataset", "condition_hash", "encode_workload"]
 
 
 class Lib:

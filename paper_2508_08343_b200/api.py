@@ -17,8 +17,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import _abi as A
-from .batch import (ConditionBatch, PackedConfig, Runner, WorkloadBatch, sim_options)
-from .types import (AdapterSpec, Condition, DeviceError, ERROR_CLASSES, FrontierPoint, LengthMode,
+from .batch import (ConditionBatch, PackedConfig, PackedGrid, Runner, WorkloadBatch, sim_options)
+from .types import (AdapterSpec, Condition, DatasetProgress, DatasetSpec, DeviceError, ERROR_CLASSES, FrontierPoint, LengthMode,
                     LoratwinError, MetricsSummary, Phase, PlacementResult, Request, RequestState,
                     ServerConfig, SimOptions, SimulationResult, SweepGrid, SweepOptions, WorkloadSpec)
 
@@ -266,3 +266,101 @@ def sweep_conditions(conditions: Sequence[Condition], config: ServerConfig, grid
         else:
             res.append(placement_of(out[i], fr[i]))
     return res
+
+
+# --- dataset generation (placement.hpp:104-158) -------------------------------------------------
+
+class _PackedDataset:
+    """lt_dataset_spec plus the arrays its pointers reference."""
+
+    def __init__(self, spec: DatasetSpec):
+        from .batch import _LengthTable
+        lt = _LengthTable()
+        lt.add(spec.lengths)
+        self.lens, self.full = lt.arrays()
+        self.rates = np.array(spec.rates if spec.rates else [0.0], dtype=np.float64)
+        self.ranks = np.array(spec.ranks if spec.ranks else [0], dtype=np.int32)
+        self.grid = PackedGrid(spec.grid)
+        c = A.lt_dataset_spec()
+        c.rates = self.rates.ctypes.data_as(C.POINTER(C.c_double))
+        c.n_rates = len(spec.rates)
+        c.triple_size = spec.triple_size
+        c.ranks = self.ranks.ctypes.data_as(C.POINTER(C.c_int32))
+        c.n_ranks = len(spec.ranks)
+        c.condition_stride = spec.condition_stride
+        c.lengths = A.lt_length_spec.from_buffer_copy(self.lens[0].tobytes())
+        c.full_lengths = self.full.ctypes.data_as(C.POINTER(C.c_int32))
+        c.n_full_pairs = len(self.full) // 2
+        c.duration_s = spec.duration_s
+        c.seed = spec.seed
+        c.grid = self.grid.c
+        o = A.lt_sweep_options()
+        o.early_exit, o.early_exit_k = int(spec.sweep.early_exit), spec.sweep.early_exit_k
+        o.jobs, o.mode = spec.sweep.jobs, int(spec.sweep.mode)
+        c.sweep = o
+        self.c = c
+
+
+def run_generate_dataset(lib: A.Lib, ctx, spec: DatasetSpec, config: ServerConfig, out_csv: str,
+                         on_error=None) -> DatasetProgress:
+    """Calls lib.generate_dataset (the GPU library or an oracle with the same ABI)."""
+    pd = _PackedDataset(spec)
+    pc = PackedConfig(config)
+    msgs: List[str] = []
+
+    def cb(msg, _user):
+        msgs.append(msg.decode())
+
+    fn = A.ERROR_FN(cb)
+    prog = A.lt_dataset_progress()
+    st = A.lt_status()
+    rc = lib.generate_dataset(ctx, C.byref(pd.c), C.byref(pc.c), os.fsencode(out_csv), fn, None, C.byref(prog),
+                              C.byref(st))
+    if rc != A.LT_OK:
+        raise ERROR_CLASSES.get(rc, LoratwinError)(st.message.decode())
+    if on_error:
+        for m in msgs:
+            on_error(m)
+    return DatasetProgress(prog.total_conditions, prog.completed, prog.failed)
+
+
+def generate_dataset(spec: DatasetSpec, config: ServerConfig, out_csv: str, on_error=None,
+                     dev: Optional[Device] = None) -> DatasetProgress:
+    """placement.hpp:151-153 — every pending condition of the spec swept on the
+    B200 in batched lt_sweep_batch calls; rows appended in canonical order,
+    resumable by condition hash. Same CSV bytes as the reference."""
+    dev = dev or device()
+    return run_generate_dataset(dev.lib, dev.ctx, spec, config, out_csv, on_error)
+
+
+def _condition_args(condition: Condition):
+    from .batch import _LengthTable
+    lt = _LengthTable()
+    lt.add(condition.lengths)
+    lens, full = lt.arrays()
+    mix = (A.lt_template * max(len(condition.mix), 1))()
+    for i, leg in enumerate(condition.mix):
+        mix[i].rank, mix[i].rate = leg.rank, leg.rate
+    return mix, A.lt_length_spec.from_buffer_copy(lens[0].tobytes()), full
+
+
+def condition_hash(condition: Condition, duration_s: float, seed: int, grid: SweepGrid, lib=None) -> int:
+    """placement.cpp:266-296 (host code of the library; no device needed)."""
+    lib = lib or load_library()
+    mix, ls, full = _condition_args(condition)
+    pg = PackedGrid(grid)
+    return int(lib.condition_hash(mix, len(condition.mix), C.byref(ls), full.ctypes.data_as(C.POINTER(C.c_int32)),
+                                  duration_s, seed, C.byref(pg.c)))
+
+
+def encode_workload(condition: Condition, lib=None) -> List[float]:
+    """placement.cpp:117-137: the 16 WorkloadFeatures values (FEATURE_NAMES order)."""
+    lib = lib or load_library()
+    mix, ls, full = _condition_args(condition)
+    out = (C.c_double * 16)()
+    st = A.lt_status()
+    rc = lib.encode_workload(mix, len(condition.mix), C.byref(ls), full.ctypes.data_as(C.POINTER(C.c_int32)), out,
+                             C.byref(st))
+    if rc != A.LT_OK:
+        raise ERROR_CLASSES.get(rc, LoratwinError)(st.message.decode())
+    return list(out)

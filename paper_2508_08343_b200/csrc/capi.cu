@@ -1828,3 +1828,4 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
 }
 
 }  // extern "C"
+#include "host_dataset.h"

@@ -280,6 +280,31 @@ def instantiate_condition(condition: Condition, served_adapters: int, duration_s
     return WorkloadSpec(adapters=adapters, lengths=condition.lengths, duration_s=duration_s, seed=seed)
 
 
+@dataclass
+class DatasetSpec:  # placement.hpp:126-137
+    rates: List[float] = field(default_factory=list)
+    ranks: List[int] = field(default_factory=list)
+    triple_size: int = 3
+    condition_stride: int = 1
+    lengths: LengthSpec = field(default_factory=LengthSpec)
+    duration_s: float = 600.0
+    seed: int = 0
+    grid: SweepGrid = field(default_factory=SweepGrid)
+    sweep: SweepOptions = field(default_factory=SweepOptions)
+
+
+@dataclass
+class DatasetProgress:  # placement.hpp:143-147
+    total_conditions: int = 0
+    completed: int = 0
+    failed: int = 0
+
+
+FEATURE_NAMES = ["rate_max", "rate_min", "rate_mean", "rate_std", "rank_max", "rank_min", "rank_mean", "rank_std",
+                 "input_len_max", "input_len_min", "input_len_mean", "input_len_std", "output_len_max",
+                 "output_len_min", "output_len_mean", "output_len_std"]  # placement.cpp:100-107
+
+
 def enumerate_conditions(rates, ranks, lengths: LengthSpec, triple_size: int = 3,
                          condition_stride: int = 1) -> List[Condition]:
     """placement.cpp:298-340: non-decreasing index tuples of rates x ranks, lexicographic."""
