@@ -157,8 +157,9 @@ def cpu_reference_run(sample_stride: int, duration: float, threads: int):
     wall = time.perf_counter() - t0
     iters = int(out["iterations"].sum())
     return {"value": iters / wall, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"every {sample_stride}th C2 scenario ({len(out)} of 1024), run_simulation + compute_metrics, "
-                      f"{iters} engine-iterations in {wall:.2f} s"}, out, b
+            "sample": (("the whole C2 grid" if sample_stride == 1 else f"every {sample_stride}th C2 scenario")
+                       + f" ({len(out)} of 1024 scenarios), run_simulation + compute_metrics (the reference's own "
+                       f"TUs, {threads} host threads), {iters} engine-iterations in {wall:.2f} s")}, out, b
 
 
 def impl_reference(args):
@@ -324,6 +325,16 @@ def impl_gpu(args):
         e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": 1000 * statistics.mean(walls), "call": "lt_simulate_batch (host pinned buffers)",
                "plan_ms": statistics.mean(plan_ms[1:]), "run_wait_ms": statistics.mean(wait_ms[1:])}
+        # The reference's compute_metrics always sorts TTFT/ITL for percentiles
+        # (metrics.cpp:101-105); sweeps never read them, so the timed device
+        # path skips them. Same call with the percentiles (recording pass +
+        # segmented sorts), reported beside it:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dev.simulate_batch(pb, cfg, want_percentiles=True)
+        e2e["with_percentiles"] = {"value": iters_all / (time.perf_counter() - t0), "unit": UNIT,
+                                   "note": "lt_simulate_batch(want_percentiles=1): full compute_metrics incl. "
+                                           "TTFT/ITL p50/p99, as the CPU reference computes"}
 
     log(f"[{time.strftime('%X')}] e2e: {e2e}")
     secondary = None
@@ -374,8 +385,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["gpu", "reference"], default="gpu")
     ap.add_argument("--duration", type=float, default=600.0)
-    ap.add_argument("--cpu-stride", type=int, default=5)
-    ap.add_argument("--ref-stride", type=int, default=9)
+    ap.add_argument("--cpu-stride", type=int, default=1, help="cpu_baseline sample: every k-th C2 scenario")
+    ap.add_argument("--ref-stride", type=int, default=3, help="--impl reference sample per step")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--sweep-conditions", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
