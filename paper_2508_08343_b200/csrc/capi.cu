@@ -1497,21 +1497,127 @@ void lt_plan_destroy(lt_plan* plan) {
   delete plan;
 }
 
+// One plan over the whole batch (the caller bounds its size).
+static int32_t simulate_one(lt_ctx* ctx, const lt_workload_batch* batch, const lt_server_config* config,
+                            const lt_sim_options* options, lt_sim_summary* out, lt_request_states* states,
+                            lt_status* status, double* plan_ms) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  lt_plan* plan = lt_plan_simulate(ctx, batch, config, options, status);
+  if (!plan) return status ? status->code : LT_ERR_DEVICE;
+  *plan_ms += std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+  int32_t rc = lt_plan_run(plan, status);
+  if (rc == LT_OK) rc = lt_plan_results(plan, out, states, status);
+  lt_plan_destroy(plan);
+  return rc;
+}
+
+// Requests a scenario can generate: the Poisson mean of every adapter plus
+// 8 sigma and slack (the same bound that sizes the RNG tables), or the
+// scripted list.
+static double est_requests(const lt_workload_batch* b, int64_t i) {
+  const lt_scenario& s = b->scenarios[i];
+  if (s.n_requests >= 0) return static_cast<double>(s.n_requests);
+  double e = 0.0;
+  for (int32_t k = 0; k < s.n_adapters; ++k) {
+    const double lam = std::max(b->adapters[s.adapter_offset + k].rate, 0.0) * std::max(s.duration_s, 0.0);
+    e += lam + 8.0 * std::sqrt(lam) + 32.0;
+  }
+  return e;
+}
+
 int32_t lt_simulate_batch(lt_ctx* ctx, const lt_workload_batch* batch, const lt_server_config* config,
                           const lt_sim_options* options, lt_sim_summary* out, lt_request_states* states,
                           lt_status* status) {
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
-  lt_plan* plan = lt_plan_simulate(ctx, batch, config, options, status);
-  if (!plan) return status ? status->code : LT_ERR_DEVICE;
-  const auto t1 = clk::now();
-  int32_t rc = lt_plan_run(plan, status);
-  if (rc == LT_OK) rc = lt_plan_results(plan, out, states, status);
-  const auto t2 = clk::now();
-  lt_plan_destroy(plan);
+  ok_status(status);
+  // Device memory is bounded by splitting the batch into consecutive chunks of
+  // at most kChunkRequests estimated requests (~100 B of device state each).
+  double kChunkRequests = 2.0e8;
+  if (const char* env = std::getenv("LT_CHUNK_REQUESTS")) kChunkRequests = std::max(1.0, std::atof(env));
+  const int64_t n = batch->n_scenarios;
+  std::vector<int64_t> cuts{0};
+  double acc = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double e = est_requests(batch, i);
+    if (acc > 0.0 && acc + e > kChunkRequests) {
+      cuts.push_back(i);
+      acc = 0.0;
+    }
+    acc += e;
+  }
+  cuts.push_back(n);
+  double plan_ms = 0.0;
+  int32_t rc = LT_OK;
+  if (cuts.size() <= 2) {
+    rc = simulate_one(ctx, batch, config, options, out, states, status, &plan_ms);
+  } else {
+    std::vector<std::string> msgs(n);
+    lt_timing tsum{};
+    int64_t req_off = 0;
+    lt_status first{};
+    first.code = LT_OK;
+    for (size_t c = 0; c + 1 < cuts.size(); ++c) {
+      const int64_t c0 = cuts[c], nc = cuts[c + 1] - c0;
+      lt_workload_batch sub = *batch;
+      sub.scenarios = batch->scenarios + c0;
+      sub.n_scenarios = nc;
+      lt_request_states sst;
+      lt_request_states* sp = nullptr;
+      if (states) {
+        sst = *states;
+        sst.capacity = std::max<int64_t>(states->capacity - req_off, 0);
+        sst.req_offset = states->req_offset ? states->req_offset + c0 : nullptr;
+        auto shift = [&](auto*& p) {
+          if (p) p += req_off;
+        };
+        shift(sst.phase);
+        shift(sst.tokens_generated);
+        shift(sst.first_token_time_s);
+        shift(sst.completion_time_s);
+        shift(sst.preemption_count);
+        shift(sst.adapter_id);
+        shift(sst.input_tokens);
+        shift(sst.output_tokens);
+        shift(sst.arrival_time_s);
+        sp = &sst;
+      }
+      lt_status st{};
+      const int32_t r = simulate_one(ctx, &sub, config, options, out + c0, sp, &st, &plan_ms);
+      if (r == LT_ERR_DEVICE && st.index < 0) {  // the chunk itself failed
+        if (status) *status = st;
+        return r;
+      }
+      const int64_t base = req_off;
+      for (int64_t i = 0; i < nc; ++i) {
+        msgs[c0 + i] = ctx->messages[i];
+        if (states && states->req_offset) states->req_offset[c0 + i] += base;
+        req_off += out[c0 + i].n_requests;
+      }
+      if (r != LT_OK && first.code == LT_OK) {
+        first = st;
+        first.index += c0;
+        rc = r;
+      }
+      const lt_timing& t = ctx->timing;
+      tsum.tables_ms += t.tables_ms;
+      tsum.merge_ms += t.merge_ms;
+      tsum.engine_ms += t.engine_ms;
+      tsum.d2h_ms += t.d2h_ms;
+      tsum.run_ms += t.run_ms;
+      tsum.h2d_bytes += t.h2d_bytes;
+      tsum.d2h_bytes += t.d2h_bytes;
+      tsum.engine_launches += t.engine_launches;
+      tsum.algorithmic_bytes += t.algorithmic_bytes;
+    }
+    ctx->messages = std::move(msgs);
+    ctx->timing = tsum;
+    if (status && rc != LT_OK) *status = first;
+  }
   ctx->timing.total_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
-  ctx->timing.plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
-  ctx->timing.run_wait_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+  ctx->timing.plan_ms = plan_ms;
+  ctx->timing.run_wait_ms = ctx->timing.total_ms - plan_ms;
   return rc;
 }
 

@@ -113,6 +113,32 @@ def h100_like_config(slots: int) -> ServerConfig:
                               disk_multiplier=1.7, default_source=LoadSource.Cpu))
 
 
+def config_from_json(d: dict, slots: int = None) -> ServerConfig:
+    """ServerConfig from the reference's JSON schema (json_io.cpp:188-235)."""
+    lat, mem, load = d["latency"], d["memory"], d["load"]
+    return ServerConfig(
+        slots=d.get("slots", 1) if slots is None else slots,
+        loaded_adapter_priority=d.get("loaded_adapter_priority", True),
+        iteration_cap=d.get("iteration_cap", 100_000_000), ideal_includes_input=d.get("ideal_includes_input", False),
+        latency=LatencyCoefficients(*(lat[k] for k in ("k1", "k2", "k3", "k4", "k5", "k6", "k7"))),
+        memory=MemoryModel(total_kv_budget=mem["total_kv_budget"], kv_bytes_per_token=mem.get("kv_bytes_per_token", 0.0),
+                           slot_cost_table={int(k): v for k, v in mem.get("slot_cost_tokens", {}).items()},
+                           slot_cost_base_rank8=mem.get("slot_cost_base_rank8")),
+        load=LoadLatencyTable(cpu_load_seconds={int(k): v for k, v in load["cpu_load_seconds"].items()},
+                              disk_multiplier=load.get("disk_multiplier", 1.7),
+                              default_source=LoadSource.Disk if load.get("default_source") == "disk" else LoadSource.Cpu))
+
+
+def profile_config(name: str, slots: int) -> ServerConfig:
+    """A packaged profile: h100_like (the reference preset), llama31_8b or
+    qwen25_7b (synthetic, configs/README.md)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "configs", name + ".json")
+    with open(path) as f:
+        return config_from_json(json.load(f), slots)
+
+
 @dataclass
 class LengthSpec:  # workload.hpp:31-65
     mode: LengthMode = LengthMode.Mean

@@ -362,3 +362,21 @@ def test_full_mode_arrivals_and_summaries(dev, ref):
     r, _ = ref.simulate(b, cfg, sim_options(None, True))
     assert_summaries(g, r)
     assert_percentiles(g, r)
+
+
+def test_chunked_batch_matches_single(dev, ref, monkeypatch):
+    """lt_simulate_batch splits large batches into consecutive chunks; forcing
+    many tiny chunks must not change any summary, state or message."""
+    b, cfg = W.summary_cases()
+    g1, s1 = dev.simulate_batch(b, cfg, want_states=True, want_digest=True)
+    monkeypatch.setenv("LT_CHUNK_REQUESTS", "3000")
+    g2, s2 = dev.simulate_batch(b, cfg, want_states=True, want_digest=True)
+    m2 = [dev.message(i) for i in range(len(g2))]
+    monkeypatch.delenv("LT_CHUNK_REQUESTS")
+    for f in g1.dtype.names:
+        if f not in ("device_cycles", "phase_cycles"):
+            np.testing.assert_array_equal(g1[f], g2[f], err_msg=f)
+    for k in s1:
+        np.testing.assert_array_equal(s1[k], s2[k], err_msg=k)
+    r, _ = ref.simulate(b, cfg, sim_options(None, True))
+    assert m2 == [ref.message(i) for i in range(len(r))]

@@ -198,3 +198,59 @@ def full_mode_cases():
         wls.append(lt.WorkloadSpec(adapters=ads, lengths=lt.LengthSpec.full(pairs), duration_s=150.0,
                                    seed=100 + i // 2))
     return WorkloadBatch.from_workloads(wls, mode=lt.LengthMode.Full), lt.h100_like_config(8)
+
+
+def _flat_batch(ns, ranks_per_adapter, rates_per_adapter, seeds, slots, lens_row, duration_s):
+    """WorkloadBatch of generated scenarios with adapter ids 1..N each."""
+    ns = np.asarray(ns, dtype=np.int64)
+    scen = np.zeros(len(ns), dtype=A.SCENARIO_DT)
+    scen["adapter_offset"] = np.concatenate([[0], np.cumsum(ns)[:-1]])
+    scen["n_adapters"] = ns
+    scen["length_index"] = 0
+    scen["duration_s"] = duration_s
+    scen["seed"] = np.asarray(seeds, dtype=np.uint64)
+    scen["slots"] = slots
+    scen["mode"] = A.MODE_MEAN
+    scen["n_requests"] = -1
+    ads = np.zeros(int(ns.sum()), dtype=A.ADAPTER_DT)
+    ads["adapter_id"] = np.concatenate([np.arange(1, n + 1) for n in ns])
+    ads["rank"] = ranks_per_adapter
+    ads["rate"] = rates_per_adapter
+    ads["length_index"] = -1
+    lens = np.zeros(1, dtype=A.LENGTH_DT)
+    lens[0] = lens_row
+    return WorkloadBatch(scen, ads, lens, np.zeros(2, dtype=np.int32), np.zeros(0, dtype=A.REQUEST_DT))
+
+
+def c3_batch(n_conditions: int = 2048, duration_s: float = 600.0) -> WorkloadBatch:
+    """C3: the first 2,048 conditions of enumerate_conditions over the
+    paper's rates x ranks {8,16,32}, triple size 3, each instantiated
+    (placement.cpp:139-157) at N in {3, 6, ..., 96} with G = min(N, 16):
+    65,536 scenarios, Mean(250,80,231,80), 600 s, one shared seed 7."""
+    conds = lt.enumerate_conditions(PAPER_RATES, [8, 16, 32], lt.LengthSpec.mean(250, 80, 231, 80))[:n_conditions]
+    n_list = np.arange(3, 97, 3)
+    ns, rk, rt = [], [], []
+    for c in conds:
+        mr = np.array([leg.rank for leg in c.mix])
+        mt = np.array([leg.rate for leg in c.mix])
+        for n in n_list:
+            ids = np.arange(n) % len(c.mix)
+            ns.append(n)
+            rk.append(mr[ids])
+            rt.append(mt[ids])
+    ns = np.array(ns)
+    return _flat_batch(ns, np.concatenate(rk), np.concatenate(rt), np.full(len(ns), 7, dtype=np.uint64),
+                       np.minimum(ns, 16), (A.MODE_MEAN, 0, 250.0, 80.0, 231.0, 80.0, 0, 0), duration_s)
+
+
+def c5_batch(start: int = 0, count: int = 524_288, duration_s: float = 600.0) -> WorkloadBatch:
+    """C5, scenarios [start, start + count) of 524,288: N = 8(1 + i mod 32),
+    rank {8,16,32}[(i/32) mod 3], aggregate rate {0.5,1,2,4}[(i/96) mod 4] req/s
+    split over the N adapters, Mean(2048,512,1024,256), 600 s, G = min(N, 32),
+    seed 2^32 + i (per-scenario keys). Run under the llama31_8b / qwen25_7b profiles."""
+    i = np.arange(start, start + count, dtype=np.int64)
+    ns = 8 * (1 + i % 32)
+    rank = np.array([8, 16, 32])[(i // 32) % 3]
+    lam = np.array([0.5, 1.0, 2.0, 4.0])[(i // 96) % 4]
+    return _flat_batch(ns, np.repeat(rank, ns), np.repeat(lam / ns, ns), (2 ** 32 + i).astype(np.uint64),
+                       np.minimum(ns, 32), (A.MODE_MEAN, 0, 2048.0, 512.0, 1024.0, 256.0, 0, 0), duration_s)
