@@ -115,8 +115,8 @@ __device__ __forceinline__ uint64_t fold64(uint64_t h, uint64_t w) {
 
 struct WarpEngine {
 #ifdef LT_SCAN_STATS
-  // diagnostics build: fresh scans, stop-cache hits, lane-mode scans,
-  // lane-set rebuilds, non-lane scans, retire calls
+  // diagnostics build: fresh scans, stop-cache hits, lane-set reconciles,
+  // lane-set rebuilds, scan events, fresh admissions
   long long st[6] = {0, 0, 0, 0, 0, 0};
 #endif
   // --- warp-uniform scalars
@@ -235,13 +235,27 @@ struct WarpEngine {
   // below, so an iteration only touches the chunks that hold a retiree. The
   // last entry is always live (trim), so LIFO preemption pops run[R_end-1].
   // Running-set slot `pos`: the first run_cap slots live in shared memory.
-  __device__ __forceinline__ int4* rp(int pos) const { return pos < run_cap ? runs + pos : run + pos; }
+  // (separate accesses per tier keep the shared one an LDS/STS, not a generic access)
+  __device__ __forceinline__ int4 run_get(int pos) const {
+    int4 v;
+    if (pos < run_cap)
+      v = runs[pos];
+    else
+      v = run[pos];
+    return v;
+  }
+  __device__ __forceinline__ void run_put(int pos, int4 e) const {
+    if (pos < run_cap)
+      runs[pos] = e;
+    else
+      run[pos] = e;
+  }
 
   __device__ __forceinline__ void run_append(int4 e) {
     const int pos = R_end;
     const int c = pos >> 5;
     if (lane == 0) {
-      *rp(pos) = e;
+      run_put(pos, e);
       if (c >= 32) cmin[c] = (pos & 31) ? min(cmin[c], e.y) : e.y;
     }
     if (c < 32 && lane == c) cmin_r = (pos & 31) ? min(cmin_r, e.y) : e.y;
@@ -271,7 +285,7 @@ struct WarpEngine {
     while (R_end > 0) {
       const int lo = max(0, R_end - 32);
       const int i = lo + lane;
-      const bool live = i < R_end && rp(i)->x >= 0;
+      const bool live = i < R_end && run_get(i).x >= 0;
       const unsigned lm = __ballot_sync(kFull, live);
       if (lm) {
         R_end = lo + 32 - __clz(lm);
@@ -287,16 +301,16 @@ struct WarpEngine {
     int w = 0;
     for (int base = 0; base < R_end; base += 32) {
       const int i = base + lane;
-      const int4 e = (i < R_end) ? *rp(i) : make_int4(-1, INT_MAX, 0, 0);
+      const int4 e = (i < R_end) ? run_get(i) : make_int4(-1, INT_MAX, 0, 0);
       const unsigned lm = __ballot_sync(kFull, e.x >= 0);
-      if (e.x >= 0) *rp(w + __popc(lm & lanemask_lt())) = e;
+      if (e.x >= 0) run_put(w + __popc(lm & lanemask_lt()), e);
       w += __popc(lm);
     }
     __syncwarp();
     R_end = w;
     for (int base = 0; base < R_end; base += 32) {
       const int i = base + lane;
-      const int y = (i < R_end) ? rp(i)->y : INT_MAX;
+      const int y = (i < R_end) ? run_get(i).y : INT_MAX;
       cmin_set(base >> 5, warp_min_i(y));
     }
     __syncwarp();
@@ -306,7 +320,6 @@ struct WarpEngine {
   // complete_finished (kv_scheduler.cpp:238-259). Only called once
   // iter >= next_fin, i.e. when some chunk may hold a retiree.
   __device__ __forceinline__ void retire(const EngineParams& P) {
-    LT_STAT(5);
     long long released = 0;
     int nf = 0;
     const int nch = (R_end + 31) >> 5;
@@ -318,7 +331,7 @@ struct WarpEngine {
         const int cc = c0 + __ffs(due) - 1;
         due &= due - 1;
         const int i = cc * 32 + lane;
-        const int4 e = (i < R_end) ? *rp(i) : make_int4(-1, INT_MAX, 0, 0);
+        const int4 e = (i < R_end) ? run_get(i) : make_int4(-1, INT_MAX, 0, 0);
         const bool fin = e.x >= 0 && e.y <= iter;
         int a = 0;
         bool zero = false;
@@ -329,7 +342,7 @@ struct WarpEngine {
           P.r_last[rb + idx] = clock;  // completion == the final emit (engine.cpp:134)
           a = e.z & kAdapterMask;
           zero = atomicSub(&run_cnt[a], 1) == 1;
-          *rp(i) = make_int4(-1, INT_MAX, 0, 0);
+          run_put(i, make_int4(-1, INT_MAX, 0, 0));
         }
         nf += __popc(__ballot_sync(kFull, fin));
         cmin_set(cc, warp_min_i((e.x >= 0 && !fin) ? e.y : INT_MAX));
@@ -352,7 +365,7 @@ struct WarpEngine {
     sum_m += nf;
     waived = -1;
     R -= static_cast<int>(nf);
-    trim();
+    if (R_end > 0 && run_get(R_end - 1).x < 0) trim();
     if (R_end - R > max(R, 32))
       compact();
     else
@@ -400,7 +413,7 @@ struct WarpEngine {
     if (R == 0) return true;
     int64_t demand = R;
     while (used + demand > cap && R > 1) {
-      const int4 e = *rp(R_end - 1);
+      const int4 e = run_get(R_end - 1);
       --R;
       --R_end;
       trim();
@@ -428,7 +441,7 @@ struct WarpEngine {
       --demand;
     }
     if (used + demand > cap) {
-      const int4 e = *rp(R_end - 1);  // the sole survivor
+      const int4 e = run_get(R_end - 1);  // the sole survivor
       const int rem = e.y - iter;
       if (rem > 1 || used + demand - 1 > cap) {
         fail(LT_ERR_SIMULATION, LT_K_SOLE_SURVIVOR, e.x, 0);
@@ -643,9 +656,9 @@ struct WarpEngine {
     const bool lane_mode = n_act <= 32;
     int lk = INT_MAX, la = -1;  // non-lane mode: this lane's best (head, adapter)
     if (lane_mode) {
-      LT_STAT(2);
       bool rebuild = !pl_valid;
-      if (!rebuild) {
+      if (!rebuild && __any_sync(kFull, act_w != built_w)) {
+        LT_STAT(2);
         const uint32_t removed = built_w & ~act_w;
         if (__any_sync(kFull, removed != 0)) {
           const bool rm = mask_bit(removed, pl_a < 0 ? 0 : pl_a);
@@ -702,7 +715,6 @@ struct WarpEngine {
       }
       pl_cl = mask_bit(claimed_w, pl_a < 0 ? 0 : pl_a);  // claims/releases since the last scan
     } else {
-      LT_STAT(4);
       pl_valid = false;
       pl_a = -1;
       pl_k = INT_MAX;
@@ -741,6 +753,7 @@ struct WarpEngine {
       }
       const bool mine = lane_mode ? (pl_a == a) : (lane == (a & 31));  // the lane that owns a
       ++sum_v;
+      LT_STAT(4);
       if (sf && !cl && !can_claim(a)) {
         block_adapter(a);
         if (!P.priority) {
@@ -769,6 +782,7 @@ struct WarpEngine {
         break;
       }
       used += demand;
+      LT_STAT(5);
       const bool claiming = sf && !cl;
       if (claiming) claim(a);
       run_append(make_int4(id, iter + nd.y, a | kFreshBit, nd.x + nd.y));
@@ -903,7 +917,7 @@ struct WarpEngine {
 // 32 shuffles are independent and only the adds form a chain.
 __device__ __forceinline__ double ordered_add(double acc, double v, bool f) {
   const double x = f ? v : 0.0;
-#pragma unroll
+#pragma unroll 8
   for (int k = 0; k < 32; ++k) acc = acc + __shfl_sync(kFull, x, k);
   return acc;
 }
@@ -1130,7 +1144,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
           bool re = false;
           int idx = 0;
           if (i < E.R_end) {
-            const int4 e = *E.rp(i);
+            const int4 e = E.run_get(i);
             re = e.x >= 0 && !(e.z & kFreshBit);
             idx = e.x;
           }
@@ -1150,7 +1164,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
       if (lane < E.n_fresh) P.r_first[E.rb + E.fresh_id] = emit;
     } else {
       for (int i = r_before + lane; i < E.R_end; i += 32) {
-        const int4 e = *E.rp(i);
+        const int4 e = E.run_get(i);
         if (e.z & kFreshBit) P.r_first[E.rb + e.x] = emit;
       }
     }
@@ -1184,7 +1198,8 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     // entries, no loads, and the same (R, W, A) -> the same lat_step. Such
     // iterations only advance the clock by `lat` (one rounded add each, as
     // the reference does), grow the ledger by R and count R tokens.
-    if (E.Wp + E.Wf == w_before && E.R == rcount_before && E.waived < 0) {
+    if (E.Wp + E.Wf == w_before && E.R == rcount_before && E.waived < 0 && E.next_fin > E.iter &&
+        (E.ingest >= E.n_req || next_arr > E.clock) && E.used + E.R <= E.cap) {
       const long long n_fin = static_cast<long long>(E.next_fin) - E.iter;
       const long long n_mem = (E.cap - E.used) / E.R;
       const long long n_cap = static_cast<long long>(E.iter_cap) - 1 - E.iter;
@@ -1225,7 +1240,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   __syncwarp();
   // Requests still running keep their emitted tokens (truncation / error).
   for (int i = lane; i < E.R_end; i += 32) {
-    const int4 e = *E.rp(i);
+    const int4 e = E.run_get(i);
     if (e.x < 0) continue;
     const int outv = P.r_out[E.rb + e.x];
     P.r_gen[E.rb + e.x] = outv - (e.y - E.iter);

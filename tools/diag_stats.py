@@ -10,7 +10,7 @@ full = W.c2_batch(600.0)
 pick = [i for i in range(len(full.scenarios)) if i % 8 == 0 and full.scenarios[i]["n_adapters"] >= 160]
 b = WorkloadBatch(full.scenarios[pick].copy(), full.adapters, full.lengths, full.full_lengths, full.requests)
 out, _ = lt.device().simulate_batch(b, lt.h100_like_config(1))
-names = ["fresh_scans", "stop_cache_hits", "lane_scans", "rebuilds", "nonlane_scans", "retires"]
+names = ["fresh_scans", "stop_cache_hits", "reconciles", "rebuilds", "events", "admissions"]
 st = out["phase_cycles"]
 for k in range(4):
     it = int(out["iterations"][k])
