@@ -983,7 +983,10 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   int per_sm = 0;
   LT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, engine_kernel, P.block, P.smem));
   per_sm = std::max(per_sm, 1);
-  const int64_t want = (P.n_scen + P.block / 32 - 1) / (P.block / 32);
+  // at least one block per SM while there are scenarios for them (the first
+  // round spreads the heaviest engines one per SM)
+  const int64_t want = std::max<int64_t>((P.n_scen + P.block / 32 - 1) / (P.block / 32),
+                                         std::min<int64_t>(P.n_scen, ctx->sm_count));
   P.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(ctx->sm_count) * per_sm)));
   P.ws_stride = std::max<int64_t>(P.max_req, 1);
   {

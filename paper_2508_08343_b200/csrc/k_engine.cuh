@@ -1328,9 +1328,15 @@ __global__ void __launch_bounds__(256, 1) engine_kernel(EngineParams P) {
   const int warp = threadIdx.x >> 5;
   const int slot = blockIdx.x * (blockDim.x >> 5) + warp;
   char* mine = smem + static_cast<size_t>(warp) * P.smem_per_warp;
+  // First round: scenario warp * gridDim + block, so the most expensive
+  // scenarios (the head of the cost order) land on different SMs instead of
+  // sharing one SM's schedulers; then a global counter hands out the rest.
+  const int warps = blockDim.x >> 5;
+  const int first = warp * gridDim.x + blockIdx.x;
+  if (first < P.n_scen) engine_run(P, P.order[first], slot, mine);
   for (;;) {
     int k = 0;
-    if ((threadIdx.x & 31) == 0) k = atomicAdd(P.counter, 1);
+    if ((threadIdx.x & 31) == 0) k = atomicAdd(P.counter, 1) + gridDim.x * warps;
     k = __shfl_sync(kFull, k, 0);
     if (k >= P.n_scen) break;
     engine_run(P, P.order[k], slot, mine);
