@@ -374,6 +374,7 @@ struct lt_ctx {
   std::vector<std::string> messages;  // per scenario / condition of the last call
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // second part of a staged plan
   int sm_count = 0;
   lt_timing timing{};
   cudaEvent_t ev[8]{};
@@ -382,6 +383,22 @@ struct lt_ctx {
 // A prepared batch: everything the kernels need, resident in HBM.
 struct lt_plan {
   lt_ctx* ctx = nullptr;
+  cudaStream_t st = nullptr;  // the stream this plan's work runs on
+  cudaEvent_t ev[8]{};        // this plan's timing events
+  // staged plan: parts[0] = the most expensive scenarios (engine started
+  // first, one warp per block so the other part's K0/merge kernels share the
+  // SMs), parts[1] = the rest, prepared concurrently on a second stream
+  std::unique_ptr<lt_plan> parts[2];
+  std::vector<int64_t> part_idx[2];
+  DBuf<int64_t> part_map[2];
+  cudaEvent_t ev_start = nullptr, ev_join = nullptr;
+  int warps_per_block = 8;
+  ~lt_plan() {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (ev_join) cudaEventDestroy(ev_join);
+  }
   Config cfg;
   int64_t n_scen = 0;
   int max_adapters = 32;
@@ -712,6 +729,8 @@ constexpr int64_t kSeedChunk = 1 << 18;
 int launch_tables(lt_plan& P, int nk, cudaStream_t st) {
   LT_CUDA(cudaFuncSetAttribute(seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(kSeedSmem)));
+  LT_CUDA(cudaFuncSetAttribute(seed_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared));
   int launches = 0;
   for (int64_t k0 = 0; k0 < nk; k0 += kSeedChunk) {
     const int n = static_cast<int>(std::min<int64_t>(kSeedChunk, nk - k0));
@@ -766,11 +785,14 @@ void size_decks(lt_plan& P, const std::vector<DKey>& keys, cudaStream_t st) {
 // Builds a plan: validation, RNG tables, counting, merge, request arrays,
 // workspace. Leaves everything resident; returns nullptr + status on error.
 lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_config* cfg,
-                    const lt_sim_options* opts) {
+                    const lt_sim_options* opts, int warps_per_block = 8, int max_run_cap = 1024) {
   auto plan = std::make_unique<lt_plan>();
   lt_plan& P = *plan;
   P.ctx = ctx;
-  cudaStream_t st = ctx->stream;
+  P.st = ctx->stream;
+  for (cudaEvent_t& e : P.ev) LT_CUDA(cudaEventCreate(&e));
+  P.warps_per_block = warps_per_block;
+  cudaStream_t st = P.st;
   load_config(P.cfg, cfg, opts);
   P.want_digest = opts ? opts->want_digest : 0;
   P.want_pct = opts ? opts->want_percentiles : 0;
@@ -800,7 +822,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   P.max_adapters = (P.max_adapters + 31) / 32 * 32;
   if (pr.lens.empty()) pr.lens.push_back(DLen{1, 0, 1, 0});
   const auto h_prep = hclk::now();
-  cudaEventRecord(ctx->ev[0], st);
+  cudaEventRecord(P.ev[0], st);
   // keys: reserve rate_max * dur_max + 8 sigma + slack draws
   int64_t e_total = 0;
   for (DKey& k : pr.keys) {
@@ -843,7 +865,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
       e_total += key.cap;
     }
   }
-  cudaEventRecord(ctx->ev[1], st);
+  cudaEventRecord(P.ev[1], st);
   const auto h_tables = hclk::now();
   // count arrivals per (scenario, adapter): sizes the request arrays
   const int64_t n_pairs = static_cast<int64_t>(pr.pair_scen.size());
@@ -967,19 +989,24 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   // (the engine kernel runs at ~200 registers). Per warp: the adapter tables
   // plus as much of the running set as fits in shared memory.
   {
-    const int warps = 8;
-    const size_t budget = 216 * 1024;  // per block, below the 227 KB opt-in limit
+    const int warps = P.warps_per_block;
+    const size_t budget = 216 * 1024;  // per 8-warp block, below the 227 KB opt-in limit
     const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter;
-    const size_t per_warp_max = budget / warps;
+    const size_t per_warp_max = budget / 8;
     int64_t cap = per_warp_max > adapters ? static_cast<int64_t>((per_warp_max - adapters) / sizeof(int4)) : 0;
-    cap = std::min<int64_t>(cap, 1024) / 32 * 32;
+    cap = std::min<int64_t>(cap, max_run_cap) / 32 * 32;
     P.run_cap = static_cast<int32_t>(cap);
     P.smem_per_warp = static_cast<int32_t>(adapters + static_cast<size_t>(cap) * sizeof(int4));
     P.block = warps * 32;
     P.smem = static_cast<size_t>(P.smem_per_warp) * warps;
   }
+  // The largest engine block any plan of this context may launch, and the
+  // max-shared carveout, so blocks of a staged plan's two parts (and the K0
+  // seed kernel) can share an SM.
   LT_CUDA(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(P.smem)));
+                               static_cast<int>(std::max<size_t>(P.smem, P.smem_per_warp * 8))));
+  LT_CUDA(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared));
   int per_sm = 0;
   LT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, engine_kernel, P.block, P.smem));
   per_sm = std::max(per_sm, 1);
@@ -1005,7 +1032,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     P.ws_ov.alloc(entries);
   }
   LT_CUDA(cudaStreamSynchronize(st));
-  P.tables_ms = elapsed(ctx->ev[0], ctx->ev[1]);
+  P.tables_ms = elapsed(P.ev[0], P.ev[1]);
   P.fresh = true;
   if (std::getenv("LT_HOST_TIMING"))
     std::fprintf(stderr, "[lt] build_plan host: prep %.2f ms, +tables sync %.2f ms, total %.2f ms (%lld scenarios)\n",
@@ -1016,14 +1043,14 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
 // K0 + merge: (re)generates every request of every generated scenario.
 void prepare_requests(lt_plan& P) {
   lt_ctx* ctx = P.ctx;
-  cudaStream_t st = ctx->stream;
-  cudaEventRecord(ctx->ev[0], st);
+  cudaStream_t st = P.st;
+  cudaEventRecord(P.ev[0], st);
   // K0: RNG tables, arrival counts and request offsets are recomputed on
   // device every run (the first run after lt_plan_simulate reuses the ones
   // computed while sizing the buffers).
   int64_t launches = 0;
   if (!P.fresh && P.n_keys > 0) launches += launch_tables(P, P.n_keys, st);
-  cudaEventRecord(ctx->ev[1], st);
+  cudaEventRecord(P.ev[1], st);
   if (!P.fresh && P.n_scen > 0) {
     LT_CUDA(cudaMemcpyAsync(P.scen_count.p, P.base_count.p, P.n_scen * sizeof(unsigned long long),
                             cudaMemcpyDeviceToDevice, st));
@@ -1042,7 +1069,7 @@ void prepare_requests(lt_plan& P) {
     after_launch("set_offsets_kernel", st);
     launches += 2;
   }
-  cudaEventRecord(ctx->ev[2], st);
+  cudaEventRecord(P.ev[2], st);
   if (P.n_pairs > 0) {
     // sort-based merge: unsorted times per (scenario, adapter), stable
     // segmented sort by time, gather into request arrays
@@ -1066,14 +1093,14 @@ void prepare_requests(lt_plan& P) {
     after_launch("gather_kernel", st);
     launches += 3;  // + CUB scan and segmented sort (library kernels)
   }
-  cudaEventRecord(ctx->ev[3], st);
+  cudaEventRecord(P.ev[3], st);
   P.fresh = false;
   P.launches_run = launches + 1;
 }
 
 // Per-request engine state before an engine pass.
 void reset_state(lt_plan& P) {
-  cudaStream_t st = P.ctx->stream;
+  cudaStream_t st = P.st;
   const int64_t nr = std::max<int64_t>(P.total_req, 1);
   LT_CUDA(cudaMemsetAsync(P.r_phase.p, 0, nr, st));
   LT_CUDA(cudaMemsetAsync(P.r_gen.p, 0, nr * sizeof(int32_t), st));
@@ -1087,7 +1114,7 @@ void run_percentiles(lt_plan& P, EngineParams E);
 
 void run_plan(lt_plan& P) {
   lt_ctx* ctx = P.ctx;
-  cudaStream_t st = ctx->stream;
+  cudaStream_t st = P.st;
   prepare_requests(P);
   reset_state(P);
   EngineParams E{};
@@ -1125,12 +1152,12 @@ void run_plan(lt_plan& P) {
   E.priority = P.cfg.raw.loaded_adapter_priority;
   E.want_digest = P.want_digest;
   E.out = P.out.p;
-  cudaEventRecord(ctx->ev[4], st);
+  cudaEventRecord(P.ev[4], st);
   if (P.n_scen > 0) {
     engine_kernel<<<P.grid, P.block, P.smem, st>>>(E);
     after_launch("engine_kernel", st);
   }
-  cudaEventRecord(ctx->ev[5], st);
+  cudaEventRecord(P.ev[5], st);
   if (P.want_pct && P.n_scen > 0) run_percentiles(P, E);
 }
 
@@ -1138,7 +1165,7 @@ void run_plan(lt_plan& P) {
 // by the first pass's iteration and preemption counts, then segmented sorts
 // and a weighted rank select (k_metrics.cuh).
 void run_percentiles(lt_plan& P, EngineParams E) {
-  cudaStream_t st = P.ctx->stream;
+  cudaStream_t st = P.st;
   const int64_t n = P.n_scen;
   std::vector<lt_sim_summary> h(n);
   LT_CUDA(cudaMemcpyAsync(h.data(), P.out.p, n * sizeof(lt_sim_summary), cudaMemcpyDeviceToHost, st));
@@ -1203,7 +1230,7 @@ void run_percentiles(lt_plan& P, EngineParams E) {
 
 void fetch_results(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {
   lt_ctx* ctx = P.ctx;
-  cudaStream_t st = ctx->stream;
+  cudaStream_t st = P.st;
   if (P.n_scen > 0)
     LT_CUDA(cudaMemcpyAsync(out, P.out.p, P.n_scen * sizeof(lt_sim_summary), cudaMemcpyDeviceToHost, st));
   int64_t d2h = P.n_scen * sizeof(lt_sim_summary);
@@ -1234,7 +1261,7 @@ void fetch_results(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {
     }
     d2h += n * 45;
   }
-  cudaEventRecord(ctx->ev[6], st);
+  cudaEventRecord(P.ev[6], st);
   LT_CUDA(cudaStreamSynchronize(st));
   ctx->messages.assign(P.n_scen, std::string());
   for (int64_t i = 0; i < P.n_scen; ++i) {
@@ -1275,11 +1302,11 @@ void fetch_results(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {
     }
   }
   lt_timing& t = ctx->timing;
-  t.tables_ms = elapsed(ctx->ev[0], ctx->ev[1]);
-  t.merge_ms = elapsed(ctx->ev[1], ctx->ev[3]);
-  t.engine_ms = elapsed(ctx->ev[4], ctx->ev[5]);
-  t.d2h_ms = elapsed(ctx->ev[5], ctx->ev[6]);
-  t.run_ms = elapsed(ctx->ev[0], ctx->ev[5]);
+  t.tables_ms = elapsed(P.ev[0], P.ev[1]);
+  t.merge_ms = elapsed(P.ev[1], P.ev[3]);
+  t.engine_ms = elapsed(P.ev[4], P.ev[5]);
+  t.d2h_ms = elapsed(P.ev[5], P.ev[6]);
+  t.run_ms = elapsed(P.ev[0], P.ev[5]);
   t.d2h_bytes = d2h;
   t.h2d_bytes = P.h2d_bytes;
   t.engine_launches = P.launches_run;
@@ -1300,6 +1327,192 @@ int32_t first_error(lt_ctx* ctx, const lt_sim_summary* out, int64_t n, lt_status
     }
   }
   return LT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Staged plans: the few most expensive engines set the step time (one warp
+// each, ~10^4 dependent iterations), while everything else -- the K0 tables
+// and the arrival merge of the other scenarios, and their shorter engines --
+// can run beside them. A staged plan builds two plans: part 0 holds the
+// most expensive scenarios and launches its engine with one warp per block
+// (small blocks leave shared memory for the other part's kernels), part 1
+// the rest on a second stream. Outputs are scattered back to batch order.
+
+__global__ void scatter_summaries(const lt_sim_summary* src, const int64_t* map, int64_t n, lt_sim_summary* dst) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) dst[map[i]] = src[i];
+}
+
+bool want_staged(lt_ctx* ctx, const lt_workload_batch* b, const lt_sim_options* opts) {
+  if (opts && opts->want_percentiles) return false;  // the recording pass synchronises the host
+  // Opt-in (LT_STAGED=1). Measured on C2 (1,024 engines): the expensive part's
+  // own K0 is not small (3.4 ms) and the two parts' engines slow each other on
+  // shared SMs, so the step got slower (47.7 vs 37.8 ms); kept for batches
+  // whose preparation dwarfs their few long engines.
+  (void)ctx;
+  if (const char* env = std::getenv("LT_STAGED")) return std::atoi(env) != 0 && b->n_scenarios >= 2;
+  return false;
+}
+
+lt_plan* build_staged(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_config* cfg,
+                      const lt_sim_options* opts) {
+  const int64_t n = b->n_scenarios;
+  std::vector<double> cost(n, 0.0);
+  for (int64_t i = 0; i < n; ++i) {
+    const lt_scenario& s = b->scenarios[i];
+    if (s.n_requests >= 0) {
+      cost[i] = static_cast<double>(s.n_requests);
+      continue;
+    }
+    for (int32_t k = 0; k < s.n_adapters; ++k) cost[i] += b->adapters[s.adapter_offset + k].rate * s.duration_s;
+  }
+  std::vector<int64_t> order(n);
+  for (int64_t i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return cost[x] > cost[y]; });
+  const int64_t na = std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count, n / 4));
+  std::vector<char> in_a(n, 0);
+  for (int64_t k = 0; k < na; ++k) in_a[order[k]] = 1;
+  auto plan = std::make_unique<lt_plan>();
+  lt_plan& P = *plan;
+  P.ctx = ctx;
+  P.st = ctx->stream;
+  P.n_scen = n;
+  for (int64_t i = 0; i < n; ++i) P.part_idx[in_a[i] ? 0 : 1].push_back(i);
+  for (int g = 0; g < 2; ++g) {
+    std::vector<lt_scenario> sc;
+    for (int64_t i : P.part_idx[g]) sc.push_back(b->scenarios[i]);
+    lt_workload_batch sub = *b;
+    sub.scenarios = sc.data();
+    sub.n_scenarios = static_cast<int64_t>(sc.size());
+    int rc_b = 1024;
+    if (const char* env = std::getenv("LT_STAGED_B_RUNCAP")) rc_b = std::atoi(env);
+    P.parts[g].reset(build_plan(ctx, &sub, cfg, opts, g == 0 ? 1 : 8, g == 0 ? 1024 : rc_b));
+    P.part_map[g].upload(P.part_idx[g], ctx->stream);
+  }
+  P.parts[1]->st = ctx->stream2;
+  P.out.alloc(n);
+  LT_CUDA(cudaEventCreate(&P.ev_start));
+  LT_CUDA(cudaEventCreate(&P.ev_join));
+  LT_CUDA(cudaStreamSynchronize(ctx->stream));
+  return plan.release();
+}
+
+void run_staged(lt_plan& P) {
+  cudaStream_t s1 = P.ctx->stream, s2 = P.parts[1]->st;
+  LT_CUDA(cudaEventRecord(P.ev_start, s1));
+  LT_CUDA(cudaStreamWaitEvent(s2, P.ev_start, 0));
+  run_plan(*P.parts[0]);  // expensive engines first ...
+  run_plan(*P.parts[1]);  // ... the rest prepared and simulated beside them
+  LT_CUDA(cudaEventRecord(P.parts[1]->ev[7], s2));
+  LT_CUDA(cudaStreamWaitEvent(s1, P.parts[1]->ev[7], 0));
+  for (int g = 0; g < 2; ++g) {
+    const int64_t m = P.parts[g]->n_scen;
+    if (m == 0) continue;
+    scatter_summaries<<<static_cast<unsigned>((m + 255) / 256), 256, 0, s1>>>(P.parts[g]->out.p, P.part_map[g].p, m,
+                                                                           P.out.p);
+    after_launch("scatter_summaries", s1);
+  }
+  LT_CUDA(cudaEventRecord(P.ev_join, s1));
+}
+
+void fetch_staged(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {
+  lt_ctx* ctx = P.ctx;
+  const int64_t n = P.n_scen;
+  std::vector<std::string> msgs(n);
+  // per part: summaries, messages and (optionally) request states in part order
+  struct PartStates {
+    std::vector<int64_t> off;
+    std::vector<int8_t> phase;
+    std::vector<int32_t> gen, pre, aid, in, outv;
+    std::vector<double> first, comp, arr;
+  } ps[2];
+  std::vector<lt_sim_summary> po[2];
+  lt_timing tsum{};
+  for (int g = 0; g < 2; ++g) {
+    lt_plan& Q = *P.parts[g];
+    po[g].resize(std::max<int64_t>(Q.n_scen, 1));
+    lt_request_states qs{};
+    if (states) {
+      PartStates& q = ps[g];
+      const int64_t r = std::max<int64_t>(Q.total_req, 1);
+      q.off.resize(std::max<int64_t>(Q.n_scen, 1));
+      q.phase.resize(r);
+      q.gen.resize(r);
+      q.pre.resize(r);
+      q.aid.resize(r);
+      q.in.resize(r);
+      q.outv.resize(r);
+      q.first.resize(r);
+      q.comp.resize(r);
+      q.arr.resize(r);
+      qs.capacity = Q.total_req;
+      qs.req_offset = q.off.data();
+      qs.phase = q.phase.data();
+      qs.tokens_generated = q.gen.data();
+      qs.first_token_time_s = q.first.data();
+      qs.completion_time_s = q.comp.data();
+      qs.preemption_count = q.pre.data();
+      qs.adapter_id = q.aid.data();
+      qs.input_tokens = q.in.data();
+      qs.output_tokens = q.outv.data();
+      qs.arrival_time_s = q.arr.data();
+    }
+    fetch_results(Q, po[g].data(), states ? &qs : nullptr);
+    for (int64_t i = 0; i < Q.n_scen; ++i) {
+      out[P.part_idx[g][i]] = po[g][i];
+      msgs[P.part_idx[g][i]] = ctx->messages[i];
+    }
+    const lt_timing& t = ctx->timing;
+    tsum.tables_ms = std::max(tsum.tables_ms, t.tables_ms);
+    tsum.merge_ms = std::max(tsum.merge_ms, t.merge_ms);
+    tsum.h2d_bytes += t.h2d_bytes;
+    tsum.d2h_bytes += t.d2h_bytes;
+    tsum.engine_launches += t.engine_launches;
+  }
+  if (states) {  // request states back in batch order
+    std::vector<std::pair<int, int64_t>> where(n);
+    for (int g = 0; g < 2; ++g)
+      for (int64_t i = 0; i < static_cast<int64_t>(P.part_idx[g].size()); ++i) where[P.part_idx[g][i]] = {g, i};
+    int64_t off = 0;
+    for (int64_t k = 0; k < n; ++k) {
+      const auto [g, i] = where[k];
+      const PartStates& q = ps[g];
+      if (states->req_offset) states->req_offset[k] = off;
+      const int64_t b0 = q.off[i];
+      for (int64_t r = 0; r < out[k].n_requests; ++r, ++off) {
+        if (off >= states->capacity) continue;
+        const int64_t j = b0 + r;
+        if (states->phase) states->phase[off] = q.phase[j];
+        if (states->tokens_generated) states->tokens_generated[off] = q.gen[j];
+        if (states->first_token_time_s) states->first_token_time_s[off] = q.first[j];
+        if (states->completion_time_s) states->completion_time_s[off] = q.comp[j];
+        if (states->preemption_count) states->preemption_count[off] = q.pre[j];
+        if (states->adapter_id) states->adapter_id[off] = q.aid[j];
+        if (states->input_tokens) states->input_tokens[off] = q.in[j];
+        if (states->output_tokens) states->output_tokens[off] = q.outv[j];
+        if (states->arrival_time_s) states->arrival_time_s[off] = q.arr[j];
+      }
+    }
+  }
+  ctx->messages = std::move(msgs);
+  if (std::getenv("LT_HOST_TIMING")) {
+    lt_plan &A = *P.parts[0], &B = *P.parts[1];
+    std::fprintf(stderr,
+                 "[lt] staged: A prep %.2f engine %.2f..%.2f ms | B prep %.2f..%.2f engine %.2f..%.2f ms | join %.2f\n",
+                 elapsed(P.ev_start, A.ev[4]), elapsed(P.ev_start, A.ev[4]), elapsed(P.ev_start, A.ev[5]),
+                 elapsed(P.ev_start, B.ev[0]), elapsed(P.ev_start, B.ev[3]), elapsed(P.ev_start, B.ev[4]),
+                 elapsed(P.ev_start, B.ev[5]), elapsed(P.ev_start, P.ev_join));
+  }
+  tsum.run_ms = elapsed(P.ev_start, P.ev_join);
+  tsum.engine_ms = elapsed(P.parts[0]->ev[4], P.ev_join);  // first engine launch .. both parts done
+  tsum.engine_launches += 2;
+  int64_t bytes = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const lt_sim_summary& o = out[i];
+    bytes += 20 * o.sum_running + 16 * o.sum_visited + 24 * o.sum_arrivals + 16 * o.sum_moves + 64 * o.iterations;
+  }
+  tsum.algorithmic_bytes = bytes;
+  ctx->timing = tsum;
 }
 
 }  // namespace
@@ -1416,6 +1629,7 @@ lt_ctx* lt_create(int32_t device, lt_status* status) {
     }
     ctx->sm_count = prop.multiProcessorCount;
     LT_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    LT_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
     for (auto& e : ctx->ev) LT_CUDA(cudaEventCreate(&e));
     return ctx.release();
   } catch (const CudaError& e) {
@@ -1430,6 +1644,7 @@ void lt_destroy(lt_ctx* ctx) {
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
   delete ctx;
 }
 
@@ -1456,6 +1671,7 @@ lt_plan* lt_plan_simulate(lt_ctx* ctx, const lt_workload_batch* batch, const lt_
   ok_status(status);
   try {
     cudaSetDevice(ctx->device);
+    if (want_staged(ctx, batch, options)) return build_staged(ctx, batch, config, options);
     return build_plan(ctx, batch, config, options);
   } catch (const CudaError& e) {
     set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
@@ -1467,7 +1683,10 @@ int32_t lt_plan_run(lt_plan* plan, lt_status* status) {
   ok_status(status);
   try {
     cudaSetDevice(plan->ctx->device);
-    run_plan(*plan);
+    if (plan->parts[0])
+      run_staged(*plan);
+    else
+      run_plan(*plan);
     return LT_OK;
   } catch (const CudaError& e) {
     set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
@@ -1479,7 +1698,10 @@ int32_t lt_plan_results(lt_plan* plan, lt_sim_summary* out, lt_request_states* s
   ok_status(status);
   try {
     cudaSetDevice(plan->ctx->device);
-    fetch_results(*plan, out, states);
+    if (plan->parts[0])
+      fetch_staged(*plan, out, states);
+    else
+      fetch_results(*plan, out, states);
     return first_error(plan->ctx, out, plan->n_scen, status);
   } catch (const CudaError& e) {
     set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);

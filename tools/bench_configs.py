@@ -101,11 +101,11 @@ def main():
     c4_n = int(args[args.index("--c4-conditions") + 1]) if "--c4-conditions" in args else 512
     ref = ref_oracle()
     if "c3" in which:
-        run_sim("C3 65,536 scenarios (shared seed 7, G=min(N,16))", W.c3_batch(), lt.h100_like_config(1), 64, ref)
+        run_sim("C3 65,536 scenarios (shared seed 7, G=min(N,16))", W.c3_batch(), lt.h100_like_config(1), 61, ref)
     if "c5" in which:
         for prof in ("llama31_8b", "qwen25_7b"):
             run_sim(f"C5 {prof} scenarios [0, {c5_count}) of 524,288", W.c5_batch(0, c5_count),
-                    profile_config(prof, 1), 256, ref)
+                    profile_config(prof, 1), 257, ref)
     if "c4" in which:
         run_c4(c4_n, ref)
 
