@@ -459,6 +459,7 @@ struct lt_plan {
   int block = 256;
   size_t smem = 0;
   int32_t run_cap = 0, smem_per_warp = 0;
+  int engine_variant = 1;  // engine_kernel<1> (latency) or <2> (occupancy)
   int want_digest = 0;
   double tables_ms = 0, h2d_ms = 0;
   int64_t h2d_bytes = 0;
@@ -989,8 +990,14 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   // (the engine kernel runs at ~200 registers). Per warp: the adapter tables
   // plus as much of the running set as fits in shared memory.
   {
+    // engine_kernel<1> (~200 registers, 8 warps per SM) is the default: the
+    // longest engines set every batch's time, even C3's 65,536 (3.25 s vs
+    // 3.93 s with engine_kernel<2>: <=128 registers with spills, 16 warps per
+    // SM, half the shared memory per warp). LT_ENGINE_VARIANT=2 selects it.
+    P.engine_variant = 1;
+    if (const char* env = std::getenv("LT_ENGINE_VARIANT")) P.engine_variant = std::atoi(env) == 2 ? 2 : 1;
     const int warps = P.warps_per_block;
-    const size_t budget = 216 * 1024;  // per 8-warp block, below the 227 KB opt-in limit
+    const size_t budget = 216 * 1024 / P.engine_variant;  // per 8-warp block, below the 227 KB opt-in limit
     const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter;
     const size_t per_warp_max = budget / 8;
     int64_t cap = per_warp_max > adapters ? static_cast<int64_t>((per_warp_max - adapters) / sizeof(int4)) : 0;
@@ -1003,12 +1010,13 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   // The largest engine block any plan of this context may launch, and the
   // max-shared carveout, so blocks of a staged plan's two parts (and the K0
   // seed kernel) can share an SM.
-  LT_CUDA(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const void* ek = P.engine_variant == 2 ? reinterpret_cast<const void*>(engine_kernel<2>)
+                                          : reinterpret_cast<const void*>(engine_kernel<1>);
+  LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(std::max<size_t>(P.smem, P.smem_per_warp * 8))));
-  LT_CUDA(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared));
+  LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
   int per_sm = 0;
-  LT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, engine_kernel, P.block, P.smem));
+  LT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ek, P.block, P.smem));
   per_sm = std::max(per_sm, 1);
   // at least one block per SM while there are scenarios for them (the first
   // round spreads the heaviest engines one per SM)
@@ -1098,6 +1106,13 @@ void prepare_requests(lt_plan& P) {
   P.launches_run = launches + 1;
 }
 
+void launch_engine(lt_plan& P, const EngineParams& E, cudaStream_t st) {
+  if (P.engine_variant == 2)
+    engine_kernel<2><<<P.grid, P.block, P.smem, st>>>(E);
+  else
+    engine_kernel<1><<<P.grid, P.block, P.smem, st>>>(E);
+}
+
 // Per-request engine state before an engine pass.
 void reset_state(lt_plan& P) {
   cudaStream_t st = P.st;
@@ -1154,7 +1169,7 @@ void run_plan(lt_plan& P) {
   E.out = P.out.p;
   cudaEventRecord(P.ev[4], st);
   if (P.n_scen > 0) {
-    engine_kernel<<<P.grid, P.block, P.smem, st>>>(E);
+    launch_engine(P, E, st);
     after_launch("engine_kernel", st);
   }
   cudaEventRecord(P.ev[5], st);
@@ -1204,7 +1219,7 @@ void run_percentiles(lt_plan& P, EngineParams E) {
   E.rec_off = P.rec_off.p;
   E.rec_d = P.rec_d.p;
   E.rec_c = P.rec_c.p;
-  engine_kernel<<<P.grid, P.block, P.smem, st>>>(E);
+  launch_engine(P, E, st);
   after_launch("engine_kernel(record)", st);
   ttft_keys_kernel<<<static_cast<unsigned>((nr + 255) / 256), 256, 0, st>>>(P.r_arr.p, P.r_first.p, nr,
                                                                             P.ttft_keys.p);
