@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -375,6 +376,7 @@ struct lt_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;  // second part of a staged plan
+  int smem_optin = 0;              // max dynamic shared memory per block (opt-in)
   int sm_count = 0;
   lt_timing timing{};
   cudaEvent_t ev[8]{};
@@ -749,8 +751,7 @@ int launch_tables(lt_plan& P, int nk, cudaStream_t st) {
     launches += 2;
   }
   if (!P.h_decks.empty()) {
-    LT_CUDA(cudaFuncSetAttribute(deck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(P.deck_smem)));
+    LT_CUDA(cudaFuncSetAttribute(deck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P.ctx->smem_optin));
     deck_kernel<<<static_cast<unsigned>(P.h_decks.size()), 32, P.deck_smem, st>>>(
         P.keys.p, P.decks.p, P.deck_tab.p, P.big_deck.p, P.big_off.p);
     after_launch("deck_kernel", st);
@@ -1007,13 +1008,13 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     P.block = warps * 32;
     P.smem = static_cast<size_t>(P.smem_per_warp) * warps;
   }
-  // The largest engine block any plan of this context may launch, and the
-  // max-shared carveout, so blocks of a staged plan's two parts (and the K0
-  // seed kernel) can share an SM.
+  // The device's opt-in maximum (a constant, so plans built concurrently on
+  // other host threads never lower it under each other) and the max-shared
+  // carveout, so blocks of a staged plan's two parts (and the K0 seed kernel)
+  // can share an SM.
   const void* ek = P.engine_variant == 2 ? reinterpret_cast<const void*>(engine_kernel<2>)
                                           : reinterpret_cast<const void*>(engine_kernel<1>);
-  LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(std::max<size_t>(P.smem, P.smem_per_warp * 8))));
+  LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_optin));
   LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
   int per_sm = 0;
   LT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ek, P.block, P.smem));
@@ -1643,6 +1644,7 @@ lt_ctx* lt_create(int32_t device, lt_status* status) {
       return nullptr;
     }
     ctx->sm_count = prop.multiProcessorCount;
+    ctx->smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
     LT_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     LT_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
     for (auto& e : ctx->ev) LT_CUDA(cudaEventCreate(&e));

@@ -80,7 +80,7 @@ def run_c4(n_cond, ref):
             "conditions_per_s": len(conds) / wall, "points_simulated": int(pl["points_simulated"].sum()),
             "engine_iterations": int(pl["iterations"].sum())}
     if ref is not None:
-        k = max(1, len(conds) // 64)
+        k = max(1, len(conds) // 16)
         idx = np.arange(0, len(conds), k)
         cbs = ConditionBatch.from_conditions([conds[i] for i in idx])
         t0 = time.perf_counter()
