@@ -432,7 +432,7 @@ struct lt_plan {
   DBuf<int4> ws_run;
   DBuf<int2> ws_pq;
   DBuf<int4> ws_node;
-  DBuf<int32_t> ws_ov, ws_cmin;
+  DBuf<int32_t> ws_ov, ws_next;
   DBuf<lt_sim_summary> out;
   // percentiles (want_percentiles): recording pass + segmented sorts
   int want_pct = 0;
@@ -999,12 +999,15 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     if (const char* env = std::getenv("LT_ENGINE_VARIANT")) P.engine_variant = std::atoi(env) == 2 ? 2 : 1;
     const int warps = P.warps_per_block;
     const size_t budget = 216 * 1024 / P.engine_variant;  // per 8-warp block, below the 227 KB opt-in limit
-    const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter;
+    // per warp: adapter tables, retire calendar, then the running-set slots
+    // (int4 entry + int32 calendar link each) that fit
+    const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter + kCalBuckets * sizeof(int32_t);
+    const size_t per_slot = sizeof(int4) + sizeof(int32_t);
     const size_t per_warp_max = budget / 8;
-    int64_t cap = per_warp_max > adapters ? static_cast<int64_t>((per_warp_max - adapters) / sizeof(int4)) : 0;
+    int64_t cap = per_warp_max > adapters ? static_cast<int64_t>((per_warp_max - adapters) / per_slot) : 0;
     cap = std::min<int64_t>(cap, max_run_cap) / 32 * 32;
     P.run_cap = static_cast<int32_t>(cap);
-    P.smem_per_warp = static_cast<int32_t>(adapters + static_cast<size_t>(cap) * sizeof(int4));
+    P.smem_per_warp = static_cast<int32_t>(adapters + static_cast<size_t>(cap) * per_slot);
     P.block = warps * 32;
     P.smem = static_cast<size_t>(P.smem_per_warp) * warps;
   }
@@ -1033,11 +1036,10 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     const int64_t per_scen = std::max<int64_t>(P.total_req, 1);
     P.ws_per_scenario = per_scen < per_slot;
     const int64_t entries = P.ws_per_scenario ? per_scen : per_slot;
-    const int64_t centries = P.ws_per_scenario ? per_scen / 32 + 2 * P.n_scen + 2 : slots * (P.ws_stride / 32 + 2);
     P.ws_run.alloc(entries);
     P.ws_pq.alloc(entries);
     P.ws_node.alloc(entries);
-    P.ws_cmin.alloc(centries);
+    P.ws_next.alloc(entries);
     P.ws_ov.alloc(entries);
   }
   LT_CUDA(cudaStreamSynchronize(st));
@@ -1154,7 +1156,7 @@ void run_plan(lt_plan& P) {
   E.ws_run = P.ws_run.p;
   E.ws_pq = P.ws_pq.p;
   E.ws_node = P.ws_node.p;
-  E.ws_cmin = P.ws_cmin.p;
+  E.ws_next = P.ws_next.p;
   E.ws_ov = P.ws_ov.p;
   E.ws_stride = P.ws_stride;
   E.ws_per_scenario = P.ws_per_scenario;

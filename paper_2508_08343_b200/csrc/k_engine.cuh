@@ -35,6 +35,9 @@ constexpr unsigned kFull = 0xffffffffu;
 // per-warp shared memory per adapter: last_used f64 + run_cnt, q_head, q_tail,
 // act_key (i32)
 constexpr int kSmemPerAdapter = 8 + 4 * 4;
+// Retire calendar: running entries are linked into bucket (retire iteration
+// mod kCalBuckets); the bucket of the current iteration holds every retiree.
+constexpr int kCalBuckets = 512;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -161,10 +164,12 @@ struct WarpEngine {
   int32_t fresh_id = 0, n_fresh = 0;
   // Re-admissions from the preempted queue this iteration (recording pass).
   int32_t readmit_id = 0, n_readmit = 0;
-  // Chunk minima of retire iterations: chunk c < 32 lives in lane c's
-  // cmin_r, chunks >= 32 in global cmin[]. next_fin <= every live retire
-  // iteration (warp-uniform).
-  int32_t cmin_r = INT_MAX, next_fin = INT_MAX;
+  // Retire calendar: cal[b] heads a singly linked list (links next-by-slot,
+  // nexts[] for shared slots, nextg[] for global ones) of the running slots
+  // whose retire iteration is = b mod kCalBuckets.
+  int32_t* cal = nullptr;
+  int32_t* nexts = nullptr;
+  int32_t* nextg = nullptr;
   int32_t ov_head = 0, ov_tail = 0;
   // fresh-scan stop cache (see scan_fresh)
   int32_t last_stop = -1;
@@ -174,7 +179,6 @@ struct WarpEngine {
   int4* run = nullptr;   // global tier of the running set (positions >= run_cap)
   int4* runs = nullptr;  // shared-memory tier (positions < run_cap)
   int32_t run_cap = 0;
-  int32_t* cmin = nullptr;  // per 32-entry chunk of run[]: lower bound of live retire iterations
   int2* pq = nullptr;
   int4* node = nullptr;  // per waiting fresh request: {in, out, next-in-chain, adapter}
   int32_t* ov = nullptr;
@@ -251,34 +255,56 @@ struct WarpEngine {
       run[pos] = e;
   }
 
+  __device__ __forceinline__ int nx_get(int pos) const { return pos < run_cap ? nexts[pos] : nextg[pos]; }
+  __device__ __forceinline__ void nx_put(int pos, int v) const {
+    if (pos < run_cap)
+      nexts[pos] = v;
+    else
+      nextg[pos] = v;
+  }
+
+  // Link slot `pos` into the bucket of its retire iteration (one lane).
+  __device__ __forceinline__ void cal_push(int pos, int fin) const {
+    nx_put(pos, atomicExch(&cal[fin & (kCalBuckets - 1)], pos));
+  }
+
   __device__ __forceinline__ void run_append(int4 e) {
     const int pos = R_end;
-    const int c = pos >> 5;
     if (lane == 0) {
       run_put(pos, e);
-      if (c >= 32) cmin[c] = (pos & 31) ? min(cmin[c], e.y) : e.y;
+      cal_push(pos, e.y);
     }
-    if (c < 32 && lane == c) cmin_r = (pos & 31) ? min(cmin_r, e.y) : e.y;
-    next_fin = min(next_fin, e.y);
     ++R_end;
     ++R;
   }
 
-  // Chunk minimum c (warp-uniform c).
-  __device__ __forceinline__ void cmin_set(int c, int v) {
-    if (c < 32) {
-      if (lane == c) cmin_r = v;
-    } else if (lane == 0) {
-      cmin[c] = v;
+  // Unlink slot `pos` (retire iteration fin) from its bucket: a popped
+  // (preempted) entry must not stay listed, its slot is reused.
+  __device__ __forceinline__ void cal_unlink(int pos, int fin) {
+    const int b = fin & (kCalBuckets - 1);
+    int prev = -1, p = cal[b];
+    while (p != pos) {
+      prev = p;
+      p = nx_get(p);
     }
+    const int nx = nx_get(pos);
+    if (lane == 0) {
+      if (prev < 0)
+        cal[b] = nx;
+      else
+        nx_put(prev, nx);
+    }
+    __syncwarp();
   }
 
-  // next_fin = min over the live chunks' minima.
-  __device__ __forceinline__ void refresh_next_fin() {
-    const int nch = (R_end + 31) >> 5;
-    int m = (lane < nch) ? cmin_r : INT_MAX;
-    for (int c = 32 + lane; c < nch; c += 32) m = min(m, cmin[c]);
-    next_fin = __reduce_min_sync(kFull, m);
+  // A lower bound on every live retire iteration >= iter: the first
+  // non-empty bucket from iter on (a bucket may hold only later laps).
+  __device__ __forceinline__ int next_retire_bound() const {
+    for (int j0 = 0; j0 < kCalBuckets; j0 += 32) {
+      const unsigned m = __ballot_sync(kFull, cal[(iter + j0 + lane) & (kCalBuckets - 1)] >= 0);
+      if (m) return iter + j0 + __ffs(m) - 1;
+    }
+    return INT_MAX;
   }
 
   __device__ __forceinline__ void trim() {
@@ -296,7 +322,7 @@ struct WarpEngine {
   }
 
   // Stable compaction of the live entries (amortised: only when tombstones
-  // outnumber live entries), then chunk bounds are rebuilt.
+  // outnumber live entries), then the calendar is rebuilt for the new slots.
   __device__ __forceinline__ void compact() {
     int w = 0;
     for (int base = 0; base < R_end; base += 32) {
@@ -308,68 +334,62 @@ struct WarpEngine {
     }
     __syncwarp();
     R_end = w;
-    for (int base = 0; base < R_end; base += 32) {
-      const int i = base + lane;
-      const int y = (i < R_end) ? run_get(i).y : INT_MAX;
-      cmin_set(base >> 5, warp_min_i(y));
-    }
+    for (int b = lane; b < kCalBuckets; b += 32) cal[b] = -1;
     __syncwarp();
-    refresh_next_fin();
+    for (int i = lane; i < R_end; i += 32) cal_push(i, run_get(i).y);
+    __syncwarp();
   }
 
-  // complete_finished (kv_scheduler.cpp:238-259). Only called once
-  // iter >= next_fin, i.e. when some chunk may hold a retiree.
+  // complete_finished (kv_scheduler.cpp:238-259): the retirees of this
+  // iteration are exactly the current bucket's entries with y == iter (the
+  // others are later laps and stay listed).
   __device__ __forceinline__ void retire(const EngineParams& P) {
+    const int b = iter & (kCalBuckets - 1);
+    int p = cal[b];
+    if (p < 0) return;
     long long released = 0;
-    int nf = 0;
-    const int nch = (R_end + 31) >> 5;
-    for (int c0 = 0; c0 < nch; c0 += 32) {
-      const int c = c0 + lane;
-      const int cm = (c >= nch) ? INT_MAX : (c0 == 0 ? cmin_r : cmin[c]);
-      unsigned due = __ballot_sync(kFull, cm <= iter);
-      while (due) {
-        const int cc = c0 + __ffs(due) - 1;
-        due &= due - 1;
-        const int i = cc * 32 + lane;
-        const int4 e = (i < R_end) ? run_get(i) : make_int4(-1, INT_MAX, 0, 0);
-        const bool fin = e.x >= 0 && e.y <= iter;
-        int a = 0;
-        bool zero = false;
-        if (fin) {
-          const int idx = e.x;
-          released += static_cast<long long>(e.w) - (idx == waived ? 1 : 0);
+    int nf = 0, kept_head = -1, kept_tail = -1;
+    while (p >= 0) {
+      const int4 e = run_get(p);
+      const int nxt = nx_get(p);
+      if (e.y == iter) {
+        const int idx = e.x;
+        const int a = e.z & kAdapterMask;
+        released += static_cast<long long>(e.w) - (idx == waived ? 1 : 0);
+        const int left = run_cnt[a] - 1;
+        if (lane == 0) {
           P.r_phase[rb + idx] = kFinished;
           P.r_last[rb + idx] = clock;  // completion == the final emit (engine.cpp:134)
-          a = e.z & kAdapterMask;
-          zero = atomicSub(&run_cnt[a], 1) == 1;
-          run_put(i, make_int4(-1, INT_MAX, 0, 0));
+          run_cnt[a] = left;
+          run_put(p, make_int4(-1, INT_MAX, 0, 0));
         }
-        nf += __popc(__ballot_sync(kFull, fin));
-        cmin_set(cc, warp_min_i((e.x >= 0 && !fin) ? e.y : INT_MAX));
-        unsigned zm = __ballot_sync(kFull, zero);
-        while (zm) {
-          const int src = __ffs(zm) - 1;
-          zm &= zm - 1;
-          release_adapter(__shfl_sync(kFull, a, src), true);
+        if (left == 0) release_adapter(a, true);
+        ++nf;
+      } else {
+        if (lane == 0) {
+          if (kept_tail < 0)
+            kept_head = p;
+          else
+            nx_put(kept_tail, p);
         }
+        kept_tail = p;
       }
+      __syncwarp();
+      p = nxt;
+    }
+    if (lane == 0) {
+      if (kept_tail >= 0) nx_put(kept_tail, -1);
+      cal[b] = kept_head;
     }
     __syncwarp();
-    if (nf == 0) {
-      refresh_next_fin();
-      return;
-    }
-    const long long rel = warp_sum_ll(released);
-    used -= rel;
+    if (nf == 0) return;
+    used -= released;
     finished += nf;
     sum_m += nf;
     waived = -1;
-    R -= static_cast<int>(nf);
+    R -= nf;
     if (R_end > 0 && run_get(R_end - 1).x < 0) trim();
-    if (R_end - R > max(R, 32))
-      compact();
-    else
-      refresh_next_fin();
+    if (R_end - R > max(R, 32)) compact();
   }
 
   // Insert a preempted request into waiting_preempted ordered by
@@ -414,6 +434,7 @@ struct WarpEngine {
     int64_t demand = R;
     while (used + demand > cap && R > 1) {
       const int4 e = run_get(R_end - 1);
+      cal_unlink(R_end - 1, e.y);
       --R;
       --R_end;
       trim();
@@ -974,11 +995,11 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   E.act_key = E.q_tail + NA;
   E.runs = reinterpret_cast<int4*>(E.act_key + NA);  // NA is a multiple of 32: 16-byte aligned
   E.run_cap = P.run_cap;
+  E.cal = reinterpret_cast<int32_t*>(E.runs + E.run_cap);
+  E.nexts = E.cal + kCalBuckets;
   const int64_t wsb = P.ws_per_scenario ? sc.req_begin : static_cast<int64_t>(slot) * P.ws_stride;
-  const int64_t wcb = P.ws_per_scenario ? (sc.req_begin >> 5) + 2 * static_cast<int64_t>(s)
-                                        : static_cast<int64_t>(slot) * (P.ws_stride / 32 + 2);
   E.run = P.ws_run + wsb;
-  E.cmin = P.ws_cmin + wcb;
+  E.nextg = P.ws_next + wsb;
   E.pq = P.ws_pq + wsb;
   E.node = P.ws_node + wsb;
   E.ov = P.ws_ov + wsb;
@@ -989,6 +1010,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     E.q_tail[a] = -1;
     E.act_key[a] = INT_MAX;
   }
+  for (int b = lane; b < kCalBuckets; b += 32) E.cal[b] = -1;
   __syncwarp();
   for (int b = 0; b < 32; ++b) {
     const int a = lane * 32 + b;
@@ -1082,7 +1104,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     }
     __syncwarp();
     LT_PH(0);
-    if (E.R > 0 && E.iter >= E.next_fin) E.retire(P);
+    if (E.R > 0) E.retire(P);
     LT_PH(1);
     if (!E.alloc(P)) break;
     LT_PH(2);
@@ -1198,9 +1220,10 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     // entries, no loads, and the same (R, W, A) -> the same lat_step. Such
     // iterations only advance the clock by `lat` (one rounded add each, as
     // the reference does), grow the ledger by R and count R tokens.
-    if (E.Wp + E.Wf == w_before && E.R == rcount_before && E.waived < 0 && E.next_fin > E.iter &&
-        (E.ingest >= E.n_req || next_arr > E.clock) && E.used + E.R <= E.cap) {
-      const long long n_fin = static_cast<long long>(E.next_fin) - E.iter;
+    if (E.Wp + E.Wf == w_before && E.R == rcount_before && E.waived < 0 &&
+        (E.ingest >= E.n_req || next_arr > E.clock) && E.used + E.R <= E.cap &&
+        E.cal[E.iter & (kCalBuckets - 1)] < 0) {
+      const long long n_fin = static_cast<long long>(E.next_retire_bound()) - E.iter;
       const long long n_mem = (E.cap - E.used) / E.R;
       const long long n_cap = static_cast<long long>(E.iter_cap) - 1 - E.iter;
       long long n_max = n_fin < n_mem ? n_fin : n_mem;

@@ -110,7 +110,7 @@ struct EngineParams {
   int4* ws_run;
   int2* ws_pq;
   int4* ws_node;
-  int32_t* ws_cmin;  // (ws_stride / 32 + 2) per warp slot
+  int32_t* ws_next;  // retire-calendar links of the global running-set tier
   int32_t* ws_ov;
   int64_t ws_stride;  // entries per warp slot
   int32_t ws_per_scenario;  // 1: workspace indexed by the scenario's request offset
