@@ -430,7 +430,7 @@ struct lt_plan {
   DBuf<int32_t> r_in, r_out, r_adp, r_gen, r_pre;
   DBuf<int8_t> r_phase;
   DBuf<int4> ws_run;
-  DBuf<int2> ws_pq;
+  DBuf<int4> ws_pq;
   DBuf<int4> ws_node;
   DBuf<int32_t> ws_ov, ws_next;
   DBuf<lt_sim_summary> out;
@@ -1001,7 +1001,8 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     const size_t budget = 216 * 1024 / P.engine_variant;  // per 8-warp block, below the 227 KB opt-in limit
     // per warp: adapter tables, retire calendar, then the running-set slots
     // (int4 entry + int32 calendar link each) that fit
-    const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter + kCalBuckets * sizeof(int32_t);
+    const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter + kCalBuckets * sizeof(int32_t) +
+                            kPqSmem * sizeof(int4);
     const size_t per_slot = sizeof(int4) + sizeof(int32_t);
     const size_t per_warp_max = budget / 8;
     int64_t cap = per_warp_max > adapters ? static_cast<int64_t>((per_warp_max - adapters) / per_slot) : 0;

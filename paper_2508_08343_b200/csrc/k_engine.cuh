@@ -38,6 +38,8 @@ constexpr int kSmemPerAdapter = 8 + 4 * 4;
 // Retire calendar: running entries are linked into bucket (retire iteration
 // mod kCalBuckets); the bucket of the current iteration holds every retiree.
 constexpr int kCalBuckets = 512;
+// Preempted-queue slots kept in shared memory (the rest in HBM).
+constexpr int kPqSmem = 64;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -179,7 +181,8 @@ struct WarpEngine {
   int4* run = nullptr;   // global tier of the running set (positions >= run_cap)
   int4* runs = nullptr;  // shared-memory tier (positions < run_cap)
   int32_t run_cap = 0;
-  int2* pq = nullptr;
+  int4* pq = nullptr;   // preempted queue, global tier: {request, adapter|over, demand, remaining tokens}
+  int4* pqs = nullptr;  // its first kPqSmem slots in shared memory
   int4* node = nullptr;  // per waiting fresh request: {in, out, next-in-chain, adapter}
   int32_t* ov = nullptr;
 
@@ -253,6 +256,21 @@ struct WarpEngine {
       runs[pos] = e;
     else
       run[pos] = e;
+  }
+
+  __device__ __forceinline__ int4 pq_get(int i) const {
+    int4 v;
+    if (i < kPqSmem)
+      v = pqs[i];
+    else
+      v = pq[i];
+    return v;
+  }
+  __device__ __forceinline__ void pq_put(int i, int4 e) const {
+    if (i < kPqSmem)
+      pqs[i] = e;
+    else
+      pq[i] = e;
   }
 
   __device__ __forceinline__ int nx_get(int pos) const { return pos < run_cap ? nexts[pos] : nextg[pos]; }
@@ -394,7 +412,8 @@ struct WarpEngine {
 
   // Insert a preempted request into waiting_preempted ordered by
   // (arrival, request_id) (kv_scheduler.cpp:206-215).
-  __device__ __forceinline__ void pq_insert(const EngineParams& P, int idx, int adapter_word) {
+  __device__ __forceinline__ void pq_insert(const EngineParams& P, int idx, int adapter_word, int demand,
+                                            int rem) {
     const double arr = P.r_arr[rb + idx];
     // Victims are the latest admissions, so their slot is near the back:
     // scan backwards for the first entry that is not greater.
@@ -403,7 +422,7 @@ struct WarpEngine {
       const int i = hi - 32 + lane;
       bool greater = false;  // entry i sorts after the victim
       if (i >= 0) {
-        const int j = pq[i].x;
+        const int j = pq_get(i).x;
         const double aj = P.r_arr[rb + j];
         greater = (arr < aj) || (arr == aj && idx < j);
       }
@@ -417,13 +436,13 @@ struct WarpEngine {
     for (int hi = Wp; hi > pos; hi -= 32) {
       const int lo = max(pos, hi - 32);
       const int i = lo + lane;
-      int2 e;
-      if (i < hi) e = pq[i];
+      int4 e;
+      if (i < hi) e = pq_get(i);
       __syncwarp();
-      if (i < hi) pq[i + 1] = e;
+      if (i < hi) pq_put(i + 1, e);
       __syncwarp();
     }
-    if (lane == 0) pq[pos] = make_int2(idx, adapter_word);
+    if (lane == 0) pq_put(pos, make_int4(idx, adapter_word, demand, rem));
     __syncwarp();
     ++Wp;
   }
@@ -456,7 +475,7 @@ struct WarpEngine {
       zero = __shfl_sync(kFull, zero, 0);
       release_adapter(a, zero);
       const bool over = static_cast<int64_t>(in) + gen + 1 > cap;
-      pq_insert(P, idx, a | (over ? kOverBit : 0));
+      pq_insert(P, idx, a | (over ? kOverBit : 0), in + gen + 1, rem);
       ++preempts;
       ++sum_m;
       --demand;
@@ -477,16 +496,17 @@ struct WarpEngine {
 
   // scan_queue (kv_scheduler.cpp:109-166) over one waiting queue, in place.
   // Returns false if the scan stopped.
-  __device__ __forceinline__ int scan(const EngineParams& P, int2* q, const int W, bool is_pq,
-                                      bool* keep_scanning) {
+  // Entries carry their demand (in + gen + 1) and remaining tokens, so the
+  // scan reads no per-request arrays.
+  __device__ __forceinline__ int scan(const EngineParams& P, const int W, bool* keep_scanning) {
     int read = 0, write = 0;
     bool stopped = false;
     const unsigned lt_mask = lanemask_lt();
     while (read < W) {
       const int i = read + lane;
       const bool v = i < W;
-      int2 e = make_int2(0, 0);
-      if (v) e = q[i];
+      int4 e = make_int4(0, 0, 0, 0);
+      if (v) e = pq_get(i);
       const int a = e.y & kAdapterMask;
       const bool over = v && (e.y & kOverBit);
       // every lane must execute the shuffles (no short-circuit around warp intrinsics)
@@ -501,13 +521,7 @@ struct WarpEngine {
       int stop = 32;
       if (!P.priority && kbm) stop = __ffs(kbm) - 1;
       cand &= (stop >= 32) ? kFull : ((1u << stop) - 1);
-      int64_t demand = 0;
-      int gen = 0;
-      if ((cand >> lane) & 1u) {
-        gen = is_pq ? P.r_gen[rb + e.x] : 0;
-        demand = static_cast<int64_t>(P.r_in[rb + e.x]) + gen + 1;
-      }
-      __syncwarp();
+      const int64_t demand = ((cand >> lane) & 1u) ? static_cast<int64_t>(e.z) : 0;
       const unsigned sfm = __ballot_sync(kFull, sf);
       unsigned admitted = 0;
       while (cand) {
@@ -542,9 +556,8 @@ struct WarpEngine {
       {
         int fin_l = 0, s_l = 0;
         if ((admitted >> lane) & 1u) {
-          const int outv = P.r_out[rb + e.x];
-          fin_l = iter + (outv - gen);
-          s_l = P.r_in[rb + e.x] + outv;
+          fin_l = iter + e.w;    // + remaining tokens
+          s_l = e.z - 1 + e.w;   // in + out
           P.r_phase[rb + e.x] = kRunning;
         }
         unsigned am = admitted;
@@ -555,11 +568,9 @@ struct WarpEngine {
           const int ad = __shfl_sync(kFull, a, src);
           const int f = __shfl_sync(kFull, fin_l, src);
           const int sv = __shfl_sync(kFull, s_l, src);
-          run_append(make_int4(idx, f, ad | (is_pq ? 0 : kFreshBit), sv));
-          if (is_pq) {
-            if (lane == (n_readmit & 31)) readmit_id = idx;
-            ++n_readmit;
-          }
+          run_append(make_int4(idx, f, ad, sv));
+          if (lane == (n_readmit & 31)) readmit_id = idx;
+          ++n_readmit;
         }
       }
       if ((rejected >> lane) & 1u) P.r_phase[rb + e.x] = kRejected;
@@ -567,7 +578,7 @@ struct WarpEngine {
       sum_m += __popc(admitted);
       const unsigned keep = vm & ~removed;
       __syncwarp();
-      if ((keep >> lane) & 1u) q[write + __popc(keep & lt_mask)] = e;
+      if ((keep >> lane) & 1u) pq_put(write + __popc(keep & lt_mask), e);
       write += __popc(keep);
       sum_v += (stop < 32) ? stop + 1 : __popc(vm);
       read += 32;
@@ -581,10 +592,10 @@ struct WarpEngine {
       if (write < read) {
         for (int base = read; base < W; base += 32) {
           const int i = base + lane;
-          int2 e;
-          if (i < W) e = q[i];
+          int4 e;
+          if (i < W) e = pq_get(i);
           __syncwarp();
-          if (i < W) q[write + (i - read)] = e;
+          if (i < W) pq_put(write + (i - read), e);
           __syncwarp();
         }
       }
@@ -600,7 +611,7 @@ struct WarpEngine {
     evicted_w = 0;
     blocked_w = 0;
     bool go = true;
-    Wp = scan(P, pq, Wp, true, &go);
+    Wp = scan(P, Wp, &go);
     if (go) scan_fresh(P);
   }
 
@@ -997,6 +1008,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   E.run_cap = P.run_cap;
   E.cal = reinterpret_cast<int32_t*>(E.runs + E.run_cap);
   E.nexts = E.cal + kCalBuckets;
+  E.pqs = reinterpret_cast<int4*>(E.nexts + E.run_cap);  // run_cap is a multiple of 32: 16-byte aligned
   const int64_t wsb = P.ws_per_scenario ? sc.req_begin : static_cast<int64_t>(slot) * P.ws_stride;
   E.run = P.ws_run + wsb;
   E.nextg = P.ws_next + wsb;
@@ -1118,7 +1130,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     E.n_readmit = 0;
     {
       bool go = true;
-      E.Wp = E.scan(P, E.pq, E.Wp, true, &go);
+      E.Wp = E.scan(P, E.Wp, &go);
       LT_PH(3);
       if (go) E.scan_fresh(P);
     }

@@ -108,7 +108,7 @@ struct EngineParams {
   double* r_last;
   int32_t* r_pre;
   int4* ws_run;
-  int2* ws_pq;
+  int4* ws_pq;
   int4* ws_node;
   int32_t* ws_next;  // retire-calendar links of the global running-set tier
   int32_t* ws_ov;
