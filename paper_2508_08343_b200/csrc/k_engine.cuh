@@ -605,6 +605,18 @@ struct WarpEngine {
     return write;
   }
 
+  // The preempted queue's head needs no slot decision and does not fit: the
+  // scan (kv_scheduler.cpp:115-152) stops right there, admitting and
+  // rejecting nothing (known-blocked adapters are reset per admit).
+  __device__ __forceinline__ bool pq_stops_at_head() {
+    const int4 e = pq_get(0);
+    const int a = e.y & kAdapterMask;
+    const bool sf = mask_bit(slotful_w, a), cl = mask_bit(claimed_w, a);
+    if ((e.y & kOverBit) || (sf && !cl) || used + static_cast<int64_t>(e.z) <= cap) return false;
+    ++sum_v;
+    return true;
+  }
+
   // admit (kv_scheduler.cpp:170-181).
   __device__ __forceinline__ void admit(const EngineParams& P) {
     free_slots = G - resident_count;
@@ -1130,7 +1142,11 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     E.n_readmit = 0;
     {
       bool go = true;
-      E.Wp = E.scan(P, E.Wp, &go);
+      if (E.Wp > 0 && E.pq_stops_at_head()) {
+        go = false;  // the scan would stop at its first entry (memory)
+      } else {
+        E.Wp = E.scan(P, E.Wp, &go);
+      }
       LT_PH(3);
       if (go) E.scan_fresh(P);
     }
