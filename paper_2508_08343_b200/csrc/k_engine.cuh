@@ -32,6 +32,11 @@
 namespace lt {
 
 constexpr unsigned kFull = 0xffffffffu;
+
+// Branch-layout hints: the engine loop is large enough that instruction fetch
+// stalls show up (ncu no_instruction); rare paths are kept out of line.
+#define LT_UNLIKELY(x) __builtin_expect(!!(x), 0)
+#define LT_LIKELY(x) __builtin_expect(!!(x), 1)
 // per-warp shared memory per adapter: last_used f64 + run_cnt, q_head, q_tail,
 // act_key (i32)
 constexpr int kSmemPerAdapter = 8 + 4 * 4;
@@ -407,7 +412,7 @@ struct WarpEngine {
     waived = -1;
     R -= nf;
     if (R_end > 0 && run_get(R_end - 1).x < 0) trim();
-    if (R_end - R > max(R, 32)) compact();
+    if (LT_UNLIKELY(R_end - R > max(R, 32))) compact();
   }
 
   // Insert a preempted request into waiting_preempted ordered by
@@ -451,7 +456,7 @@ struct WarpEngine {
   __device__ __forceinline__ bool alloc(const EngineParams& P) {
     if (R == 0) return true;
     int64_t demand = R;
-    while (used + demand > cap && R > 1) {
+    while (LT_UNLIKELY(used + demand > cap && R > 1)) {
       const int4 e = run_get(R_end - 1);
       cal_unlink(R_end - 1, e.y);
       --R;
@@ -699,7 +704,7 @@ struct WarpEngine {
     const int n_act = __reduce_add_sync(kFull, __popc(act_w));
     const bool lane_mode = n_act <= 32;
     int lk = INT_MAX, la = -1;  // non-lane mode: this lane's best (head, adapter)
-    if (lane_mode) {
+    if (LT_LIKELY(lane_mode)) {
       bool rebuild = !pl_valid;
       if (!rebuild && __any_sync(kFull, act_w != built_w)) {
         LT_STAT(2);
@@ -714,7 +719,7 @@ struct WarpEngine {
         }
         uint32_t add = act_w & ~built_w;
         const int n_add = __reduce_add_sync(kFull, __popc(add));
-        if (n_add > 8) {
+        if (LT_UNLIKELY(n_add > 8)) {
           rebuild = true;
         } else {
           for (int k = 0; k < n_add; ++k) {
@@ -732,7 +737,7 @@ struct WarpEngine {
           }
         }
       }
-      if (rebuild) {
+      if (LT_UNLIKELY(rebuild)) {
         LT_STAT(3);
         const int cnt_w = __popc(act_w);
         int pre = cnt_w;  // inclusive prefix over lanes
@@ -771,7 +776,7 @@ struct WarpEngine {
       int id, a;
       bool sf, cl;
       int4 nd;  // {in, out, next, adapter}
-      if (lane_mode) {
+      if (LT_LIKELY(lane_mode)) {
         const unsigned kmin = __reduce_min_sync(kFull, static_cast<unsigned>(pl_k));
         if (kmin == static_cast<unsigned>(INT_MAX)) break;
         const int src = __ffs(__ballot_sync(kFull, static_cast<unsigned>(pl_k) == kmin)) - 1;
@@ -798,7 +803,7 @@ struct WarpEngine {
       const bool mine = lane_mode ? (pl_a == a) : (lane == (a & 31));  // the lane that owns a
       ++sum_v;
       LT_STAT(4);
-      if (sf && !cl && !can_claim(a)) {
+      if (LT_UNLIKELY(sf && !cl) && !can_claim(a)) {
         block_adapter(a);
         if (!P.priority) {
           stop_id = id;
@@ -828,7 +833,7 @@ struct WarpEngine {
       used += demand;
       LT_STAT(5);
       const bool claiming = sf && !cl;
-      if (claiming) claim(a);
+      if (LT_UNLIKELY(claiming)) claim(a);
       run_append(make_int4(id, iter + nd.y, a | kFreshBit, nd.x + nd.y));
       if (lane == (n_fresh & 31)) fresh_id = id;
       ++n_fresh;
@@ -857,7 +862,7 @@ struct WarpEngine {
       } else if (mine) {
         act_key[a] = (next < 0) ? INT_MAX : next;
       }
-      if (claiming) {
+      if (LT_UNLIKELY(claiming)) {
         const bool mass2 = P.priority && free_slots == 0 && !pool_any();
         if (mass2 != mass) {
           mass = mass2;
@@ -1175,7 +1180,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     const double adapters = (A == 0) ? 1.0 : P.k6 * static_cast<double>(A) + P.k7;
     const double lat = sched + loads + model * adapters;
     const double emit = E.clock + lat;
-    if (P.record) {  // ITL multiset of compute_metrics (metrics.cpp:92-105)
+    if (LT_UNLIKELY(P.record)) {  // ITL multiset of compute_metrics (metrics.cpp:92-105)
       const int64_t r0 = rec_base + rec_n;
       if (lane == 0) {
         P.rec_d[r0] = emit - E.clock;
@@ -1210,7 +1215,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
       rec_n += wrote;
     }
     // first tokens of this iteration's fresh admissions (engine.cpp:131)
-    if (E.n_fresh <= 32) {
+    if (LT_LIKELY(E.n_fresh <= 32)) {
       if (lane < E.n_fresh) P.r_first[E.rb + E.fresh_id] = emit;
     } else {
       for (int i = r_before + lane; i < E.R_end; i += 32) {
@@ -1222,7 +1227,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     E.tok_tot += E.R;
     if (emit <= E.duration) E.tok_win += E.R;
     E.sum_r += E.R;
-    if (P.want_digest) {
+    if (LT_UNLIKELY(P.want_digest)) {
       E.digest = fold64(E.digest, static_cast<uint32_t>(E.R) | (static_cast<uint64_t>(static_cast<uint32_t>(W)) << 32));
       E.digest = fold64(E.digest, static_cast<uint32_t>(A) | (static_cast<uint64_t>(static_cast<uint32_t>(nl)) << 32));
       E.digest = fold64(E.digest, static_cast<uint64_t>(__double_as_longlong(lat)));
@@ -1230,7 +1235,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     E.clock = emit;
     ++E.iter;
     LT_PH(5);
-    if (E.iter >= E.iter_cap) {
+    if (LT_UNLIKELY(E.iter >= E.iter_cap)) {
       if (capped_by_range) {
         E.fail(LT_ERR_UNSUPPORTED, LT_K_ITERATION_RANGE, E.iter, 0);
       } else {
@@ -1270,7 +1275,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
           }
           win += (clk <= E.duration);
           ++n;
-          if (P.want_digest) {
+          if (LT_UNLIKELY(P.want_digest)) {
             E.digest = fold64(E.digest, static_cast<uint32_t>(E.R) | (static_cast<uint64_t>(static_cast<uint32_t>(W)) << 32));
             E.digest = fold64(E.digest, static_cast<uint32_t>(A));
             E.digest = fold64(E.digest, static_cast<uint64_t>(__double_as_longlong(lat_q)));
