@@ -27,7 +27,7 @@ constexpr int kMtN = 312;  // MT19937-64 state words
 // 624-word array in shared memory (row stride 625: conflict-free both when
 // every thread touches its own row and when a row is copied out), then the
 // block writes each stream's state contiguously to `state`.
-constexpr int kSeedThreads = 64;
+constexpr int kSeedThreads = 90;  // 90 rows x 625 words = 225 KB: three warps' worth of streams per SM
 constexpr int kSeedStride = 625;
 constexpr size_t kSeedSmem = sizeof(uint32_t) * kSeedThreads * kSeedStride;
 
