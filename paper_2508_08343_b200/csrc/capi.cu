@@ -1779,7 +1779,7 @@ int32_t lt_simulate_batch(lt_ctx* ctx, const lt_workload_batch* batch, const lt_
   ok_status(status);
   // Device memory is bounded by splitting the batch into consecutive chunks of
   // at most kChunkRequests estimated requests (~100 B of device state each).
-  double kChunkRequests = 2.0e8;
+  double kChunkRequests = 5.0e8;
   if (const char* env = std::getenv("LT_CHUNK_REQUESTS")) kChunkRequests = std::max(1.0, std::atof(env));
   const int64_t n = batch->n_scenarios;
   std::vector<int64_t> cuts{0};
@@ -2035,7 +2035,9 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
     so.want_digest = 0;
     double engine_ms = 0, tables_ms = 0, merge_ms = 0, run_ms = 0;
     int64_t launches = 0, algo = 0;
-    const double budget = 6.0e7;  // estimated requests per device batch
+    // estimated requests per device batch: a whole row in one batch lets its
+    // longest engines run side by side (lt_simulate_batch bounds memory itself)
+    const double budget = 5.0e8;
     for (size_t ni = 0; ni < rows.size(); ++ni) {
       const SweepRow& r = rows[ni];
       std::vector<int64_t> conds;
@@ -2082,6 +2084,17 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
         for (size_t k = 0; k < scen.size(); ++k) {
           pts[pidx[k]] = part[k];
           pt_msg[pidx[k]] = ctx->messages[k];
+        }
+        if (std::getenv("LT_HOST_TIMING")) {
+          int64_t it = 0, itmax = 0, cyc = 0;
+          for (const lt_sim_summary& q : part) {
+            it += q.iterations;
+            itmax = std::max<int64_t>(itmax, q.iterations);
+            cyc = std::max<int64_t>(cyc, q.device_cycles);
+          }
+          std::fprintf(stderr, "[lt] sweep row N=%d: %zu points, engine %.1f ms, iterations %lld (max %lld), "
+                       "longest engine %.1f Mcycles\n", r.n, scen.size(), ctx->timing.engine_ms,
+                       static_cast<long long>(it), static_cast<long long>(itmax), cyc / 1e6);
         }
         engine_ms += ctx->timing.engine_ms;
         tables_ms += ctx->timing.tables_ms;
