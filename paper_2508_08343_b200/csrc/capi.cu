@@ -432,7 +432,8 @@ struct lt_plan {
   DBuf<int4> ws_run;
   DBuf<int4> ws_pq;
   DBuf<int4> ws_node;
-  DBuf<int32_t> ws_ov, ws_next;
+  DBuf<int32_t> ws_ov;
+  DBuf<int2> ws_link;
   DBuf<lt_sim_summary> out;
   // percentiles (want_percentiles): recording pass + segmented sorts
   int want_pct = 0;
@@ -544,6 +545,7 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
   d.n_adapters = s.n_adapters;
   d.adapter_begin = static_cast<int64_t>(pr.adapters.size());
   d.generated = s.n_requests < 0;
+  d.ids_sorted = 1;  // generated: request ids are the (arrival, adapter) order
   d.iter_cap = P.cfg.raw.iteration_cap;
   const bool scripted = s.n_requests >= 0;
   const lt_adapter* ad = b.adapters + s.adapter_offset;
@@ -702,6 +704,7 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
                                             " references unknown adapter " + std::to_string(rq[r].adapter_id)),
                fail();
       cost += rq[r].output_tokens + 1.0;
+      if (r > 0 && rq[r].arrival_time_s < rq[r - 1].arrival_time_s) d.ids_sorted = 0;
     }
     d.n_req = static_cast<int32_t>(s.n_requests);
   }
@@ -1003,7 +1006,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     // (int4 entry + int32 calendar link each) that fit
     const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter + kCalBuckets * sizeof(int32_t) +
                             kPqSmem * sizeof(int4);
-    const size_t per_slot = sizeof(int4) + sizeof(int32_t);
+    const size_t per_slot = sizeof(int4) + sizeof(int2);
     const size_t per_warp_max = budget / 8;
     int64_t cap = per_warp_max > adapters ? static_cast<int64_t>((per_warp_max - adapters) / per_slot) : 0;
     cap = std::min<int64_t>(cap, max_run_cap) / 32 * 32;
@@ -1040,7 +1043,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     P.ws_run.alloc(entries);
     P.ws_pq.alloc(entries);
     P.ws_node.alloc(entries);
-    P.ws_next.alloc(entries);
+    P.ws_link.alloc(entries);
     P.ws_ov.alloc(entries);
   }
   LT_CUDA(cudaStreamSynchronize(st));
@@ -1157,7 +1160,7 @@ void run_plan(lt_plan& P) {
   E.ws_run = P.ws_run.p;
   E.ws_pq = P.ws_pq.p;
   E.ws_node = P.ws_node.p;
-  E.ws_next = P.ws_next.p;
+  E.ws_link = P.ws_link.p;
   E.ws_ov = P.ws_ov.p;
   E.ws_stride = P.ws_stride;
   E.ws_per_scenario = P.ws_per_scenario;

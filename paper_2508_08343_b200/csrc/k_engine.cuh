@@ -125,7 +125,7 @@ __device__ __forceinline__ uint64_t fold64(uint64_t h, uint64_t w) {
 
 struct WarpEngine {
 #ifdef LT_SCAN_STATS
-  // diagnostics build: fresh scans, stop-cache hits, lane-set reconciles,
+  // diagnostics build: fresh scans, stop-cache hits, non-lane scans,
   // lane-set rebuilds, scan events, fresh admissions
   long long st[6] = {0, 0, 0, 0, 0, 0};
 #endif
@@ -171,12 +171,12 @@ struct WarpEngine {
   int32_t fresh_id = 0, n_fresh = 0;
   // Re-admissions from the preempted queue this iteration (recording pass).
   int32_t readmit_id = 0, n_readmit = 0;
-  // Retire calendar: cal[b] heads a singly linked list (links next-by-slot,
-  // nexts[] for shared slots, nextg[] for global ones) of the running slots
-  // whose retire iteration is = b mod kCalBuckets.
+  // Retire calendar: cal[b] heads a doubly linked list ({next, prev} per
+  // slot: links[] for shared slots, linkg[] for global ones; prev -1 at the
+  // head) of the running slots whose retire iteration is = b mod kCalBuckets.
   int32_t* cal = nullptr;
-  int32_t* nexts = nullptr;
-  int32_t* nextg = nullptr;
+  int2* links = nullptr;
+  int2* linkg = nullptr;
   int32_t ov_head = 0, ov_tail = 0;
   // fresh-scan stop cache (see scan_fresh)
   int32_t last_stop = -1;
@@ -186,8 +186,13 @@ struct WarpEngine {
   int4* run = nullptr;   // global tier of the running set (positions >= run_cap)
   int4* runs = nullptr;  // shared-memory tier (positions < run_cap)
   int32_t run_cap = 0;
-  int4* pq = nullptr;   // preempted queue, global tier: {request, adapter|over, demand, remaining tokens}
-  int4* pqs = nullptr;  // its first kPqSmem slots in shared memory
+  // Preempted queue: a ring of pq_cap slots holding {request, adapter|over,
+  // demand, remaining tokens}; logical entry i is ring slot pq_h + i (mod
+  // pq_cap). Ring slots < kPqSmem live in shared memory (pqs), the rest in HBM.
+  int4* pq = nullptr;
+  int4* pqs = nullptr;
+  int32_t pq_h = 0, pq_cap = 1;
+  bool ids_sorted = true;  // request ids follow arrival order: (arrival, id) order == id order
   int4* node = nullptr;  // per waiting fresh request: {in, out, next-in-chain, adapter}
   int32_t* ov = nullptr;
 
@@ -263,32 +268,54 @@ struct WarpEngine {
       run[pos] = e;
   }
 
+  __device__ __forceinline__ int pq_slot(int i) const {
+    const int j = pq_h + i;
+    return j >= pq_cap ? j - pq_cap : j;
+  }
   __device__ __forceinline__ int4 pq_get(int i) const {
+    const int j = pq_slot(i);
     int4 v;
-    if (i < kPqSmem)
-      v = pqs[i];
+    if (j < kPqSmem)
+      v = pqs[j];
     else
-      v = pq[i];
+      v = pq[j];
     return v;
   }
   __device__ __forceinline__ void pq_put(int i, int4 e) const {
-    if (i < kPqSmem)
-      pqs[i] = e;
+    const int j = pq_slot(i);
+    if (j < kPqSmem)
+      pqs[j] = e;
     else
-      pq[i] = e;
+      pq[j] = e;
   }
 
-  __device__ __forceinline__ int nx_get(int pos) const { return pos < run_cap ? nexts[pos] : nextg[pos]; }
-  __device__ __forceinline__ void nx_put(int pos, int v) const {
+  __device__ __forceinline__ int2 lk_get(int pos) const { return pos < run_cap ? links[pos] : linkg[pos]; }
+  __device__ __forceinline__ void lk_put(int pos, int2 v) const {
     if (pos < run_cap)
-      nexts[pos] = v;
+      links[pos] = v;
     else
-      nextg[pos] = v;
+      linkg[pos] = v;
+  }
+  __device__ __forceinline__ void lk_next(int pos, int v) const {
+    if (pos < run_cap)
+      links[pos].x = v;
+    else
+      linkg[pos].x = v;
+  }
+  __device__ __forceinline__ void lk_prev(int pos, int v) const {
+    if (pos < run_cap)
+      links[pos].y = v;
+    else
+      linkg[pos].y = v;
   }
 
-  // Link slot `pos` into the bucket of its retire iteration (one lane).
+  // Link slot `pos` at the head of the bucket of its retire iteration (one lane).
   __device__ __forceinline__ void cal_push(int pos, int fin) const {
-    nx_put(pos, atomicExch(&cal[fin & (kCalBuckets - 1)], pos));
+    int* h = &cal[fin & (kCalBuckets - 1)];
+    const int old = *h;
+    lk_put(pos, make_int2(old, -1));
+    if (old >= 0) lk_prev(old, pos);
+    *h = pos;
   }
 
   __device__ __forceinline__ void run_append(int4 e) {
@@ -301,21 +328,16 @@ struct WarpEngine {
     ++R;
   }
 
-  // Unlink slot `pos` (retire iteration fin) from its bucket: a popped
-  // (preempted) entry must not stay listed, its slot is reused.
+  // Unlink slot `pos` (retire iteration fin) from its bucket in O(1): a
+  // popped (preempted) entry must not stay listed, its slot is reused.
   __device__ __forceinline__ void cal_unlink(int pos, int fin) {
-    const int b = fin & (kCalBuckets - 1);
-    int prev = -1, p = cal[b];
-    while (p != pos) {
-      prev = p;
-      p = nx_get(p);
-    }
-    const int nx = nx_get(pos);
     if (lane == 0) {
-      if (prev < 0)
-        cal[b] = nx;
+      const int2 l = lk_get(pos);
+      if (l.y < 0)
+        cal[fin & (kCalBuckets - 1)] = l.x;
       else
-        nx_put(prev, nx);
+        lk_next(l.y, l.x);
+      if (l.x >= 0) lk_prev(l.x, l.y);
     }
     __syncwarp();
   }
@@ -359,7 +381,14 @@ struct WarpEngine {
     R_end = w;
     for (int b = lane; b < kCalBuckets; b += 32) cal[b] = -1;
     __syncwarp();
-    for (int i = lane; i < R_end; i += 32) cal_push(i, run_get(i).y);
+    // next links by atomic head exchange, then each node's successor learns
+    // its predecessor (one writer per node)
+    for (int i = lane; i < R_end; i += 32) lk_put(i, make_int2(atomicExch(&cal[run_get(i).y & (kCalBuckets - 1)], i), -1));
+    __syncwarp();
+    for (int i = lane; i < R_end; i += 32) {
+      const int nx = lk_get(i).x;
+      if (nx >= 0) lk_prev(nx, i);
+    }
     __syncwarp();
   }
 
@@ -374,7 +403,7 @@ struct WarpEngine {
     int nf = 0, kept_head = -1, kept_tail = -1;
     while (p >= 0) {
       const int4 e = run_get(p);
-      const int nxt = nx_get(p);
+      const int nxt = lk_get(p).x;
       if (e.y == iter) {
         const int idx = e.x;
         const int a = e.z & kAdapterMask;
@@ -393,7 +422,8 @@ struct WarpEngine {
           if (kept_tail < 0)
             kept_head = p;
           else
-            nx_put(kept_tail, p);
+            lk_next(kept_tail, p);
+          lk_prev(p, kept_tail);
         }
         kept_tail = p;
       }
@@ -401,7 +431,7 @@ struct WarpEngine {
       p = nxt;
     }
     if (lane == 0) {
-      if (kept_tail >= 0) nx_put(kept_tail, -1);
+      if (kept_tail >= 0) lk_next(kept_tail, -1);
       cal[b] = kept_head;
     }
     __syncwarp();
@@ -417,19 +447,39 @@ struct WarpEngine {
 
   // Insert a preempted request into waiting_preempted ordered by
   // (arrival, request_id) (kv_scheduler.cpp:206-215).
+  // Victims are the latest admissions: fresh ones sort at the back, and
+  // re-admitted preempted ones (the queue's oldest, admitted first) sort at
+  // the front again -- both O(1) on the ring; other positions shift the tail.
   __device__ __forceinline__ void pq_insert(const EngineParams& P, int idx, int adapter_word, int demand,
                                             int rem) {
+    const int4 ent = make_int4(idx, adapter_word, demand, rem);
+    if (ids_sorted) {
+      if (Wp == 0 || idx > pq_get(Wp - 1).x) {  // append
+        if (lane == 0) pq_put(Wp, ent);
+        __syncwarp();
+        ++Wp;
+        return;
+      }
+      if (idx < pq_get(0).x) {  // prepend
+        pq_h = (pq_h == 0 ? pq_cap : pq_h) - 1;
+        if (lane == 0) pq_put(0, ent);
+        __syncwarp();
+        ++Wp;
+        return;
+      }
+    }
     const double arr = P.r_arr[rb + idx];
-    // Victims are the latest admissions, so their slot is near the back:
-    // scan backwards for the first entry that is not greater.
+    // scan backwards for the first entry that is not greater
     int pos = 0;
     for (int hi = Wp; hi > 0; hi -= 32) {
       const int i = hi - 32 + lane;
       bool greater = false;  // entry i sorts after the victim
       if (i >= 0) {
         const int j = pq_get(i).x;
-        const double aj = P.r_arr[rb + j];
-        greater = (arr < aj) || (arr == aj && idx < j);
+        greater = ids_sorted ? idx < j : [&] {
+          const double aj = P.r_arr[rb + j];
+          return (arr < aj) || (arr == aj && idx < j);
+        }();
       }
       const unsigned notg = __ballot_sync(kFull, i >= 0 && !greater);
       if (notg) {
@@ -447,7 +497,7 @@ struct WarpEngine {
       if (i < hi) pq_put(i + 1, e);
       __syncwarp();
     }
-    if (lane == 0) pq_put(pos, make_int4(idx, adapter_word, demand, rem));
+    if (lane == 0) pq_put(pos, ent);
     __syncwarp();
     ++Wp;
   }
@@ -707,7 +757,6 @@ struct WarpEngine {
     if (LT_LIKELY(lane_mode)) {
       bool rebuild = !pl_valid;
       if (!rebuild && __any_sync(kFull, act_w != built_w)) {
-        LT_STAT(2);
         const uint32_t removed = built_w & ~act_w;
         if (__any_sync(kFull, removed != 0)) {
           const bool rm = mask_bit(removed, pl_a < 0 ? 0 : pl_a);
@@ -764,6 +813,7 @@ struct WarpEngine {
       }
       pl_cl = mask_bit(claimed_w, pl_a < 0 ? 0 : pl_a);  // claims/releases since the last scan
     } else {
+      LT_STAT(2);
       pl_valid = false;
       pl_a = -1;
       pl_k = INT_MAX;
@@ -1024,12 +1074,14 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   E.runs = reinterpret_cast<int4*>(E.act_key + NA);  // NA is a multiple of 32: 16-byte aligned
   E.run_cap = P.run_cap;
   E.cal = reinterpret_cast<int32_t*>(E.runs + E.run_cap);
-  E.nexts = E.cal + kCalBuckets;
-  E.pqs = reinterpret_cast<int4*>(E.nexts + E.run_cap);  // run_cap is a multiple of 32: 16-byte aligned
+  E.links = reinterpret_cast<int2*>(E.cal + kCalBuckets);
+  E.pqs = reinterpret_cast<int4*>(E.links + E.run_cap);  // run_cap is a multiple of 32: 16-byte aligned
   const int64_t wsb = P.ws_per_scenario ? sc.req_begin : static_cast<int64_t>(slot) * P.ws_stride;
   E.run = P.ws_run + wsb;
-  E.nextg = P.ws_next + wsb;
+  E.linkg = P.ws_link + wsb;
   E.pq = P.ws_pq + wsb;
+  E.pq_cap = static_cast<int32_t>(P.ws_per_scenario ? (sc.n_req > 0 ? sc.n_req : 1) : P.ws_stride);
+  E.ids_sorted = sc.ids_sorted != 0;
   E.node = P.ws_node + wsb;
   E.ov = P.ws_ov + wsb;
   for (int a = lane; a < E.N; a += 32) {

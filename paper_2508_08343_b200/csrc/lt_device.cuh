@@ -46,7 +46,7 @@ struct DScen {
   int64_t status_a;
   int64_t status_b;
   int32_t length_param;  // scenario-level Mean parameters (index into DLen)
-  int32_t _pad;
+  int32_t ids_sorted;    // arrivals non-decreasing in request id (generated: always)
 };
 
 struct DAdapter {
@@ -110,7 +110,7 @@ struct EngineParams {
   int4* ws_run;
   int4* ws_pq;
   int4* ws_node;
-  int32_t* ws_next;  // retire-calendar links of the global running-set tier
+  int2* ws_link;  // retire-calendar {next, prev} links of the global running-set tier
   int32_t* ws_ov;
   int64_t ws_stride;  // entries per warp slot
   int32_t ws_per_scenario;  // 1: workspace indexed by the scenario's request offset
