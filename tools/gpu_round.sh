@@ -19,4 +19,5 @@ timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --
 timeout 1500 $NCU --set full --clock-control none --import-source on -k regex:engine_kernel -s 1 -c 1 \
   -o "$OUT/engine_full" -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-sweeps \
   > "$OUT/ncu_full.log" 2>&1
+timeout 1200 python tools/bench_configs.py > "$OUT/configs.jsonl" 2> "$OUT/configs.err"
 echo done > "$OUT/DONE"
