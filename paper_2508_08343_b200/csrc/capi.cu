@@ -1004,7 +1004,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     const size_t budget = 216 * 1024 / P.engine_variant;  // per 8-warp block, below the 227 KB opt-in limit
     // per warp: adapter tables, retire calendar, then the running-set slots
     // (int4 entry + int32 calendar link each) that fit
-    const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter + kCalBuckets * sizeof(int32_t) +
+    const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter + 2 * kCalBuckets * sizeof(int32_t) +
                             kPqSmem * sizeof(int4);
     const size_t per_slot = sizeof(int4) + sizeof(int2);
     const size_t per_warp_max = budget / 8;

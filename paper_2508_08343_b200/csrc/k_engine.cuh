@@ -84,7 +84,7 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
 // LRU victim: argmin over set bits of `cand` of (last_used, adapter_id);
 // dense index order == adapter_id order. Adapters needed by the previous
 // ensure_loaded call still carry last_used == prev_now (lazy refresh).
-__device__ __forceinline__ int lru_victim(uint32_t cand, uint32_t prev_needed, double prev_now,
+__device__ __noinline__ int lru_victim(uint32_t cand, uint32_t prev_needed, double prev_now,
                                           const double* last_used, int lane) {
   double best = DBL_MAX;
   int best_a = INT_MAX;
@@ -122,6 +122,46 @@ __device__ __forceinline__ uint64_t fold64(uint64_t h, uint64_t w) {
 #else
 #define LT_STAT(k) ((void)0)
 #endif
+
+// Non-lane-mode helpers of the fresh scan (rare: more than 32 adapters can
+// act), kept out of line so the hot loop stays compact in the instruction cache.
+// Lane-local minimum of act_key over this lane's adapters a = lane + 32 m.
+__device__ __noinline__ int2 lane_best(const int32_t* act_key, int N, int lane) {
+  int best = INT_MAX, bi = -1;
+#pragma unroll 1
+  for (int a = lane; a < N; a += 32) {
+    const int k = act_key[a];
+    if (k < best) {
+      best = k;
+      bi = a;
+    }
+  }
+  return make_int2(best, bi);
+}
+
+// act_key for every adapter (round-robin layout: lane owns a = lane + 32 m,
+// whose mask bit is bit `lane` of word m).
+__device__ __noinline__ void act_keys(int32_t* act_key, const int32_t* q_head, int N, int lane, uint32_t blocked_w,
+                                      uint32_t slotful_w, uint32_t claimed_w, uint32_t nonempty_w, bool mass,
+                                      bool only_mass_exclusion) {
+#pragma unroll 1
+  for (int m = 0; m * 32 < N; ++m) {
+    const uint32_t wb = __shfl_sync(kFull, blocked_w, m);
+    const uint32_t ws = __shfl_sync(kFull, slotful_w, m);
+    const uint32_t wc = __shfl_sync(kFull, claimed_w, m);
+    const uint32_t wn = __shfl_sync(kFull, nonempty_w, m);
+    const int a = lane + 32 * m;
+    if (a < N) {
+      const bool excl = mass && ((ws >> lane) & 1u) && !((wc >> lane) & 1u);
+      if (only_mass_exclusion) {
+        if (excl) act_key[a] = INT_MAX;
+      } else {
+        const bool acting = ((wn >> lane) & 1u) && !((wb >> lane) & 1u) && !excl;
+        act_key[a] = acting ? q_head[a] : INT_MAX;
+      }
+    }
+  }
+}
 
 struct WarpEngine {
 #ifdef LT_SCAN_STATS
@@ -174,7 +214,11 @@ struct WarpEngine {
   // Retire calendar: cal[b] heads a doubly linked list ({next, prev} per
   // slot: links[] for shared slots, linkg[] for global ones; prev -1 at the
   // head) of the running slots whose retire iteration is = b mod kCalBuckets.
+  // cmin[b] is a lower bound on the bucket's retire iterations (INT_MAX when
+  // empty; exact after each walk), so buckets holding only later laps are
+  // neither walked nor mistaken for the next retirement.
   int32_t* cal = nullptr;
+  int32_t* cmin = nullptr;
   int2* links = nullptr;
   int2* linkg = nullptr;
   int32_t ov_head = 0, ov_tail = 0;
@@ -311,11 +355,12 @@ struct WarpEngine {
 
   // Link slot `pos` at the head of the bucket of its retire iteration (one lane).
   __device__ __forceinline__ void cal_push(int pos, int fin) const {
-    int* h = &cal[fin & (kCalBuckets - 1)];
-    const int old = *h;
+    const int b = fin & (kCalBuckets - 1);
+    const int old = cal[b];
     lk_put(pos, make_int2(old, -1));
     if (old >= 0) lk_prev(old, pos);
-    *h = pos;
+    cal[b] = pos;
+    cmin[b] = min(cmin[b], fin);
   }
 
   __device__ __forceinline__ void run_append(int4 e) {
@@ -333,23 +378,31 @@ struct WarpEngine {
   __device__ __forceinline__ void cal_unlink(int pos, int fin) {
     if (lane == 0) {
       const int2 l = lk_get(pos);
-      if (l.y < 0)
-        cal[fin & (kCalBuckets - 1)] = l.x;
-      else
+      if (l.y < 0) {
+        const int b = fin & (kCalBuckets - 1);
+        cal[b] = l.x;
+        if (l.x < 0) cmin[b] = INT_MAX;
+      } else
         lk_next(l.y, l.x);
       if (l.x >= 0) lk_prev(l.x, l.y);
     }
     __syncwarp();
   }
 
-  // A lower bound on every live retire iteration >= iter: the first
-  // non-empty bucket from iter on (a bucket may hold only later laps).
+  // A lower bound on every live retire iteration: the first iteration
+  // iter + j (j < kCalBuckets) whose bucket may retire something then, else
+  // the least bucket minimum (every retirement is a lap or more away).
   __device__ __forceinline__ int next_retire_bound() const {
+#pragma unroll 1
     for (int j0 = 0; j0 < kCalBuckets; j0 += 32) {
-      const unsigned m = __ballot_sync(kFull, cal[(iter + j0 + lane) & (kCalBuckets - 1)] >= 0);
+      const int it = iter + j0 + lane;
+      const unsigned m = __ballot_sync(kFull, cmin[it & (kCalBuckets - 1)] <= it);
       if (m) return iter + j0 + __ffs(m) - 1;
     }
-    return INT_MAX;
+    int m = INT_MAX;
+#pragma unroll 4
+    for (int j = 0; j < kCalBuckets / 32; ++j) m = min(m, cmin[j * 32 + lane]);
+    return __reduce_min_sync(kFull, m);
   }
 
   __device__ __forceinline__ void trim() {
@@ -379,11 +432,18 @@ struct WarpEngine {
     }
     __syncwarp();
     R_end = w;
-    for (int b = lane; b < kCalBuckets; b += 32) cal[b] = -1;
+    for (int b = lane; b < kCalBuckets; b += 32) {
+      cal[b] = -1;
+      cmin[b] = INT_MAX;
+    }
     __syncwarp();
     // next links by atomic head exchange, then each node's successor learns
     // its predecessor (one writer per node)
-    for (int i = lane; i < R_end; i += 32) lk_put(i, make_int2(atomicExch(&cal[run_get(i).y & (kCalBuckets - 1)], i), -1));
+    for (int i = lane; i < R_end; i += 32) {
+      const int fin = run_get(i).y;
+      lk_put(i, make_int2(atomicExch(&cal[fin & (kCalBuckets - 1)], i), -1));
+      atomicMin(&cmin[fin & (kCalBuckets - 1)], fin);
+    }
     __syncwarp();
     for (int i = lane; i < R_end; i += 32) {
       const int nx = lk_get(i).x;
@@ -397,10 +457,11 @@ struct WarpEngine {
   // others are later laps and stay listed).
   __device__ __forceinline__ void retire(const EngineParams& P) {
     const int b = iter & (kCalBuckets - 1);
+    const int m0 = cmin[b];
     int p = cal[b];
-    if (p < 0) return;
+    if (m0 > iter) return;  // empty, or later laps only
     long long released = 0;
-    int nf = 0, kept_head = -1, kept_tail = -1;
+    int nf = 0, kept_head = -1, kept_tail = -1, kept_min = INT_MAX;
     while (p >= 0) {
       const int4 e = run_get(p);
       const int nxt = lk_get(p).x;
@@ -426,6 +487,7 @@ struct WarpEngine {
           lk_prev(p, kept_tail);
         }
         kept_tail = p;
+        kept_min = min(kept_min, e.y);
       }
       __syncwarp();
       p = nxt;
@@ -433,6 +495,7 @@ struct WarpEngine {
     if (lane == 0) {
       if (kept_tail >= 0) lk_next(kept_tail, -1);
       cal[b] = kept_head;
+      cmin[b] = kept_min;
     }
     __syncwarp();
     if (nf == 0) return;
@@ -682,39 +745,14 @@ struct WarpEngine {
     if (go) scan_fresh(P);
   }
 
-  // Lane-local minimum of act_key over this lane's adapters a = lane + 32 m.
   __device__ __forceinline__ void local_best(int* bkey, int* ba) const {
-    int best = INT_MAX, bi = -1;
-    for (int a = lane; a < N; a += 32) {
-      const int k = act_key[a];
-      if (k < best) {
-        best = k;
-        bi = a;
-      }
-    }
-    *bkey = best;
-    *ba = bi;
+    const int2 r = lane_best(act_key, N, lane);
+    *bkey = r.x;
+    *ba = r.y;
   }
 
-  // act_key for every adapter (round-robin layout: lane owns a = lane + 32 m,
-  // whose mask bit is bit `lane` of word m).
   __device__ __forceinline__ void build_act_keys(bool mass, bool only_mass_exclusion) {
-    for (int m = 0; m * 32 < N; ++m) {
-      const uint32_t wb = __shfl_sync(kFull, blocked_w, m);
-      const uint32_t ws = __shfl_sync(kFull, slotful_w, m);
-      const uint32_t wc = __shfl_sync(kFull, claimed_w, m);
-      const uint32_t wn = __shfl_sync(kFull, nonempty_w, m);
-      const int a = lane + 32 * m;
-      if (a < N) {
-        const bool excl = mass && ((ws >> lane) & 1u) && !((wc >> lane) & 1u);
-        if (only_mass_exclusion) {
-          if (excl) act_key[a] = INT_MAX;
-        } else {
-          const bool acting = ((wn >> lane) & 1u) && !((wb >> lane) & 1u) && !excl;
-          act_key[a] = acting ? q_head[a] : INT_MAX;
-        }
-      }
-    }
+    act_keys(act_key, q_head, N, lane, blocked_w, slotful_w, claimed_w, nonempty_w, mass, only_mass_exclusion);
   }
 
   // scan_queue over waiting_fresh (kv_scheduler.cpp:109-166), event-driven.
@@ -797,6 +835,7 @@ struct WarpEngine {
         const int excl = pre - cnt_w;  // exclusive prefix of this lane's word
         pl_a = -1;
         pl_k = INT_MAX;
+#pragma unroll 1
         for (int m = 0; m * 32 < N; ++m) {
           const uint32_t wm = __shfl_sync(kFull, act_w, m);
           const int base = __shfl_sync(kFull, excl, m);
@@ -1074,7 +1113,8 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   E.runs = reinterpret_cast<int4*>(E.act_key + NA);  // NA is a multiple of 32: 16-byte aligned
   E.run_cap = P.run_cap;
   E.cal = reinterpret_cast<int32_t*>(E.runs + E.run_cap);
-  E.links = reinterpret_cast<int2*>(E.cal + kCalBuckets);
+  E.cmin = E.cal + kCalBuckets;
+  E.links = reinterpret_cast<int2*>(E.cmin + kCalBuckets);
   E.pqs = reinterpret_cast<int4*>(E.links + E.run_cap);  // run_cap is a multiple of 32: 16-byte aligned
   const int64_t wsb = P.ws_per_scenario ? sc.req_begin : static_cast<int64_t>(slot) * P.ws_stride;
   E.run = P.ws_run + wsb;
@@ -1091,8 +1131,12 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     E.q_tail[a] = -1;
     E.act_key[a] = INT_MAX;
   }
-  for (int b = lane; b < kCalBuckets; b += 32) E.cal[b] = -1;
+  for (int b = lane; b < kCalBuckets; b += 32) {
+    E.cal[b] = -1;
+    E.cmin[b] = INT_MAX;
+  }
   __syncwarp();
+#pragma unroll 1
   for (int b = 0; b < 32; ++b) {
     const int a = lane * 32 + b;
     if (a < E.N && P.adapters[E.ab + a].rank > 0) E.slotful_w |= 1u << b;
@@ -1307,7 +1351,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     // the reference does), grow the ledger by R and count R tokens.
     if (E.Wp + E.Wf == w_before && E.R == rcount_before && E.waived < 0 &&
         (E.ingest >= E.n_req || next_arr > E.clock) && E.used + E.R <= E.cap &&
-        E.cal[E.iter & (kCalBuckets - 1)] < 0) {
+        E.cmin[E.iter & (kCalBuckets - 1)] > E.iter) {
       const long long n_fin = static_cast<long long>(E.next_retire_bound()) - E.iter;
       const long long n_mem = (E.cap - E.used) / E.R;
       const long long n_cap = static_cast<long long>(E.iter_cap) - 1 - E.iter;
@@ -1445,13 +1489,12 @@ __global__ void __launch_bounds__(256, kMinBlocks) engine_kernel(EngineParams P)
   // sharing one SM's schedulers; then a global counter hands out the rest.
   const int warps = blockDim.x >> 5;
   const int first = warp * gridDim.x + blockIdx.x;
-  if (first < P.n_scen) engine_run(P, P.order[first], slot, mine);
-  for (;;) {
-    int k = 0;
-    if ((threadIdx.x & 31) == 0) k = atomicAdd(P.counter, 1) + gridDim.x * warps;
-    k = __shfl_sync(kFull, k, 0);
-    if (k >= P.n_scen) break;
+  // (one call site: engine_run is inlined once)
+  for (int k = first; k < P.n_scen;) {
     engine_run(P, P.order[k], slot, mine);
+    int nk = 0;
+    if ((threadIdx.x & 31) == 0) nk = atomicAdd(P.counter, 1) + gridDim.x * warps;
+    k = __shfl_sync(kFull, nk, 0);
   }
 }
 

@@ -1,7 +1,7 @@
 """Throughput on the other BASELINE configs on one B200,
 with a CPU-reference parity spot check on a sample of each.
 
-    python tools/bench_configs.py [c3] [c4] [c5] [--c5-count N] [--c4-conditions N]
+    python tools/bench_configs.py [c3] [c4] [c5] [--c5-count N] [--c4-conditions N] [--no-ref]
 
 C3: 65,536 scenarios (heterogeneous ranks, mixed rates, shared seed 7).
 C5: a contiguous chunk of the 524,288-scenario sweep per profile
@@ -99,7 +99,7 @@ def main():
     which = [a for a in args if not a.startswith("--") and not a.isdigit()] or ["c3", "c4", "c5"]
     c5_count = int(args[args.index("--c5-count") + 1]) if "--c5-count" in args else 32768
     c4_n = int(args[args.index("--c4-conditions") + 1]) if "--c4-conditions" in args else 512
-    ref = ref_oracle()
+    ref = None if "--no-ref" in args else ref_oracle()
     if "c3" in which:
         run_sim("C3 65,536 scenarios (shared seed 7, G=min(N,16))", W.c3_batch(), lt.h100_like_config(1), 61, ref)
     if "c5" in which:
