@@ -998,16 +998,35 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     // longest engines set every batch's time, even C3's 65,536 (3.25 s vs
     // 3.93 s with engine_kernel<2>: <=128 registers with spills, 16 warps per
     // SM, half the shared memory per warp). LT_ENGINE_VARIANT=2 selects it.
+    // Variant 3: 12 warps per block (<= 170 registers), one block per SM.
+    // Batches whose mean work per warp slot exceeds their longest engine are
+    // throughput-bound (C3 / C5 chunks: 12% / 17% faster with 12 warps);
+    // one-round batches are set by their longest engines, which run ~7%
+    // faster at the latency variant's register budget (C2).
+    // LT_ENGINE_VARIANT overrides.
     P.engine_variant = 1;
-    if (const char* env = std::getenv("LT_ENGINE_VARIANT")) P.engine_variant = std::atoi(env) == 2 ? 2 : 1;
+    if (warps_per_block == 8 && P.n_scen > 0) {
+      double total = 0.0, longest = 0.0;
+      for (int64_t i = 0; i < P.n_scen; ++i) {
+        total += pr.cost[i];
+        longest = std::max(longest, pr.cost[i]);
+      }
+      if (total / (static_cast<double>(ctx->sm_count) * 8.0) > longest) P.engine_variant = 3;
+    }
+    if (const char* env = std::getenv("LT_ENGINE_VARIANT")) {
+      const int v = std::atoi(env);
+      P.engine_variant = (v == 2 || v == 3) ? v : 1;
+    }
+    if (P.engine_variant == 3 && P.warps_per_block == 8) P.warps_per_block = 12;
     const int warps = P.warps_per_block;
-    const size_t budget = 216 * 1024 / P.engine_variant;  // per 8-warp block, below the 227 KB opt-in limit
+    // per SM, below the 227 KB opt-in limit (variant 2: two blocks per SM)
+    const size_t budget = 216 * 1024 / (P.engine_variant == 2 ? 2 : 1);
     // per warp: adapter tables, retire calendar, then the running-set slots
     // (int4 entry + int32 calendar link each) that fit
     const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter + 2 * kCalBuckets * sizeof(int32_t) +
                             kPqSmem * sizeof(int4);
     const size_t per_slot = sizeof(int4) + sizeof(int2);
-    const size_t per_warp_max = budget / 8;
+    const size_t per_warp_max = budget / warps;
     int64_t cap = per_warp_max > adapters ? static_cast<int64_t>((per_warp_max - adapters) / per_slot) : 0;
     cap = std::min<int64_t>(cap, max_run_cap) / 32 * 32;
     P.run_cap = static_cast<int32_t>(cap);
@@ -1019,8 +1038,9 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   // other host threads never lower it under each other) and the max-shared
   // carveout, so blocks of a staged plan's two parts (and the K0 seed kernel)
   // can share an SM.
-  const void* ek = P.engine_variant == 2 ? reinterpret_cast<const void*>(engine_kernel<2>)
-                                          : reinterpret_cast<const void*>(engine_kernel<1>);
+  const void* ek = P.engine_variant == 2   ? reinterpret_cast<const void*>(engine_kernel<256, 2>)
+                   : P.engine_variant == 3 ? reinterpret_cast<const void*>(engine_kernel<384, 1>)
+                                           : reinterpret_cast<const void*>(engine_kernel<256, 1>);
   LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_optin));
   LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
   int per_sm = 0;
@@ -1115,9 +1135,11 @@ void prepare_requests(lt_plan& P) {
 
 void launch_engine(lt_plan& P, const EngineParams& E, cudaStream_t st) {
   if (P.engine_variant == 2)
-    engine_kernel<2><<<P.grid, P.block, P.smem, st>>>(E);
+    engine_kernel<256, 2><<<P.grid, P.block, P.smem, st>>>(E);
+  else if (P.engine_variant == 3)
+    engine_kernel<384, 1><<<P.grid, P.block, P.smem, st>>>(E);
   else
-    engine_kernel<1><<<P.grid, P.block, P.smem, st>>>(E);
+    engine_kernel<256, 1><<<P.grid, P.block, P.smem, st>>>(E);
 }
 
 // Per-request engine state before an engine pass.

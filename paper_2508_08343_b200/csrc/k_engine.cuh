@@ -1478,8 +1478,8 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
 // one 8-warp block per SM, the shortest per-engine latency (the batch's
 // longest engines set its time). kMinBlocks = 2: <= 128 registers, 16 warps
 // per SM, for batches with many rounds of engines per warp (throughput).
-template <int kMinBlocks>
-__global__ void __launch_bounds__(256, kMinBlocks) engine_kernel(EngineParams P) {
+template <int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(EngineParams P) {
   extern __shared__ __align__(16) char smem[];
   const int warp = threadIdx.x >> 5;
   const int slot = blockIdx.x * (blockDim.x >> 5) + warp;
