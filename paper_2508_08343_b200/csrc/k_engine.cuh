@@ -139,6 +139,21 @@ __device__ __noinline__ int2 lane_best(const int32_t* act_key, int N, int lane) 
   return make_int2(best, bi);
 }
 
+// Lane-local minimum chain head over this lane's adapters a = lane + 32 m
+// (q_head -1, an empty chain, compares above every id).
+__device__ __noinline__ int2 lane_best_head(const int32_t* q_head, int N, int lane) {
+  int best = INT_MAX, bi = -1;
+#pragma unroll 1
+  for (int a = lane; a < N; a += 32) {
+    const int k = q_head[a];
+    if (static_cast<unsigned>(k) < static_cast<unsigned>(best)) {
+      best = k;
+      bi = a;
+    }
+  }
+  return make_int2(best, bi);
+}
+
 // act_key for every adapter (round-robin layout: lane owns a = lane + 32 m,
 // whose mask bit is bit `lane` of word m).
 __device__ __noinline__ void act_keys(int32_t* act_key, const int32_t* q_head, int N, int lane, uint32_t blocked_w,
@@ -755,6 +770,76 @@ struct WarpEngine {
     act_keys(act_key, q_head, N, lane, blocked_w, slotful_w, claimed_w, nonempty_w, mass, only_mass_exclusion);
   }
 
+  // Lane mode (at most 32 acting adapters, act_w): reconcile the persistent
+  // lane set with this acting set -- adapters whose chain filled or emptied,
+  // claims and releases -- or rebuild it when many changed.
+  __device__ __forceinline__ void enter_lane_mode(uint32_t act_w) {
+    bool rebuild = !pl_valid;
+    if (!rebuild && __any_sync(kFull, act_w != built_w)) {
+      const uint32_t removed = built_w & ~act_w;
+      if (__any_sync(kFull, removed != 0)) {
+        const bool rm = mask_bit(removed, pl_a < 0 ? 0 : pl_a);
+        if (pl_a >= 0 && rm) {
+          pl_a = -1;
+          pl_k = INT_MAX;
+        }
+        built_w &= ~removed;
+      }
+      uint32_t add = act_w & ~built_w;
+      const int n_add = __reduce_add_sync(kFull, __popc(add));
+      if (LT_UNLIKELY(n_add > 8)) {
+        rebuild = true;
+      } else {
+        for (int k = 0; k < n_add; ++k) {
+          const int a = mask_lowest(add);
+          mask_clear(add, a, lane);
+          const bool sfa = mask_bit(slotful_w, a);
+          const int fl = __ffs(__ballot_sync(kFull, pl_a < 0)) - 1;  // exists: n_act <= 32
+          if (lane == fl) {
+            pl_a = a;
+            pl_k = q_head[a];
+            pl_nd = node[pl_k];
+            pl_sf = sfa;
+          }
+          mask_set(built_w, a, lane);
+        }
+      }
+    }
+    if (LT_UNLIKELY(rebuild)) {
+      LT_STAT(3);
+      const int cnt_w = __popc(act_w);
+      int pre = cnt_w;  // inclusive prefix over lanes
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(kFull, pre, o);
+        if (lane >= o) pre += t;
+      }
+      const int excl = pre - cnt_w;  // exclusive prefix of this lane's word
+      pl_a = -1;
+      pl_k = INT_MAX;
+#pragma unroll 1
+      for (int m = 0; m * 32 < N; ++m) {
+        const uint32_t wm = __shfl_sync(kFull, act_w, m);
+        const int base = __shfl_sync(kFull, excl, m);
+        const int k = lane - base;
+        if (wm && k >= 0 && k < __popc(wm)) {
+          pl_a = m * 32 + static_cast<int>(__fns(wm, 0, k + 1));
+          pl_k = q_head[pl_a];
+        }
+      }
+      if (pl_k != INT_MAX) pl_nd = node[pl_k];
+      pl_sf = mask_bit(slotful_w, pl_a < 0 ? 0 : pl_a);
+      built_w = act_w;
+      pl_valid = true;
+    }
+    pl_cl = mask_bit(claimed_w, pl_a < 0 ? 0 : pl_a);  // claims/releases since the last scan
+  }
+
+  __device__ __forceinline__ void nonlane_best(bool direct, int* bkey, int* ba) const {
+    const int2 r = direct ? lane_best_head(q_head, N, lane) : lane_best(act_key, N, lane);
+    *bkey = r.x;
+    *ba = r.y;
+  }
+
   // scan_queue over waiting_fresh (kv_scheduler.cpp:109-166), event-driven.
   // The reference visits every waiting entry in order; here the fresh queue
   // is kept as per-adapter FIFO chains (request-id order), and the scan jumps
@@ -790,75 +875,24 @@ struct WarpEngine {
     // or emptied, claims and releases); otherwise act_key[] holds the heads.
     const uint32_t act_w = nonempty_w & ~blocked_w & ~(mass ? (slotful_w & ~claimed_w) : 0u);
     const int n_act = __reduce_add_sync(kFull, __popc(act_w));
-    const bool lane_mode = n_act <= 32;
-    int lk = INT_MAX, la = -1;  // non-lane mode: this lane's best (head, adapter)
+    bool lane_mode = n_act <= 32;
+    // Non-lane mode: lane L's best (head, adapter) over adapters a = L + 32 m,
+    // from act_key[], or straight from the chain heads when every non-empty
+    // chain acts ("direct": loaded-adapter priority with a free slot or an
+    // idle resident left, so nothing is blocked or excluded -- the slot
+    // turnover scan of a slot-starved engine).
+    int lk = INT_MAX, la = -1;
+    bool direct = false;
     if (LT_LIKELY(lane_mode)) {
-      bool rebuild = !pl_valid;
-      if (!rebuild && __any_sync(kFull, act_w != built_w)) {
-        const uint32_t removed = built_w & ~act_w;
-        if (__any_sync(kFull, removed != 0)) {
-          const bool rm = mask_bit(removed, pl_a < 0 ? 0 : pl_a);
-          if (pl_a >= 0 && rm) {
-            pl_a = -1;
-            pl_k = INT_MAX;
-          }
-          built_w &= ~removed;
-        }
-        uint32_t add = act_w & ~built_w;
-        const int n_add = __reduce_add_sync(kFull, __popc(add));
-        if (LT_UNLIKELY(n_add > 8)) {
-          rebuild = true;
-        } else {
-          for (int k = 0; k < n_add; ++k) {
-            const int a = mask_lowest(add);
-            mask_clear(add, a, lane);
-            const bool sfa = mask_bit(slotful_w, a);
-            const int fl = __ffs(__ballot_sync(kFull, pl_a < 0)) - 1;  // exists: n_act <= 32
-            if (lane == fl) {
-              pl_a = a;
-              pl_k = q_head[a];
-              pl_nd = node[pl_k];
-              pl_sf = sfa;
-            }
-            mask_set(built_w, a, lane);
-          }
-        }
-      }
-      if (LT_UNLIKELY(rebuild)) {
-        LT_STAT(3);
-        const int cnt_w = __popc(act_w);
-        int pre = cnt_w;  // inclusive prefix over lanes
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(kFull, pre, o);
-          if (lane >= o) pre += t;
-        }
-        const int excl = pre - cnt_w;  // exclusive prefix of this lane's word
-        pl_a = -1;
-        pl_k = INT_MAX;
-#pragma unroll 1
-        for (int m = 0; m * 32 < N; ++m) {
-          const uint32_t wm = __shfl_sync(kFull, act_w, m);
-          const int base = __shfl_sync(kFull, excl, m);
-          const int k = lane - base;
-          if (wm && k >= 0 && k < __popc(wm)) {
-            pl_a = m * 32 + static_cast<int>(__fns(wm, 0, k + 1));
-            pl_k = q_head[pl_a];
-          }
-        }
-        if (pl_k != INT_MAX) pl_nd = node[pl_k];
-        pl_sf = mask_bit(slotful_w, pl_a < 0 ? 0 : pl_a);
-        built_w = act_w;
-        pl_valid = true;
-      }
-      pl_cl = mask_bit(claimed_w, pl_a < 0 ? 0 : pl_a);  // claims/releases since the last scan
+      enter_lane_mode(act_w);
     } else {
       LT_STAT(2);
-      pl_valid = false;
-      pl_a = -1;
-      pl_k = INT_MAX;
-      build_act_keys(mass, false);
-      __syncwarp();
-      local_best(&lk, &la);
+      direct = P.priority && !mass && !__any_sync(kFull, blocked_w != 0);
+      if (!direct) {
+        build_act_keys(mass, false);
+        __syncwarp();
+      }
+      nonlane_best(direct, &lk, &la);
     }
     int stop_id = INT_MAX;
     for (;;) {
@@ -904,6 +938,12 @@ struct WarpEngine {
             pl_k = INT_MAX;
           }
           mask_clear(built_w, a, lane);
+        } else if (direct) {  // (not reached: nothing blocks while a slot is free)
+          __syncwarp();
+          build_act_keys(mass, false);
+          direct = false;
+          __syncwarp();
+          local_best(&lk, &la);
         } else if (mine) {
           act_key[a] = INT_MAX;
           local_best(&lk, &la);
@@ -936,21 +976,19 @@ struct WarpEngine {
       if (next < 0) mask_clear(nonempty_w, a, lane);
       --Wf;
       ++sum_m;
-      if (lane_mode) {
-        if (mine) {
-          pl_cl = pl_cl || claiming;
-          if (next < 0) {
-            pl_a = -1;
-            pl_k = INT_MAX;
-          } else {
-            pl_k = next;
-            pl_nd = node[next];  // in flight until this lane wins again
-          }
+      // the lane set follows every chain it holds, in both modes
+      if (pl_a == a) {
+        if (lane_mode) pl_cl = pl_cl || claiming;
+        if (next < 0) {
+          pl_a = -1;
+          pl_k = INT_MAX;
+        } else {
+          pl_k = next;
+          pl_nd = node[next];  // in flight until this lane wins again
         }
-        if (next < 0) mask_clear(built_w, a, lane);
-      } else if (mine) {
-        act_key[a] = (next < 0) ? INT_MAX : next;
       }
+      if (next < 0) mask_clear(built_w, a, lane);
+      if (!lane_mode && !direct && mine) act_key[a] = (next < 0) ? INT_MAX : next;
       if (LT_UNLIKELY(claiming)) {
         const bool mass2 = P.priority && free_slots == 0 && !pool_any();
         if (mass2 != mass) {
@@ -964,14 +1002,33 @@ struct WarpEngine {
             built_w &= ~(slotful_w & ~claimed_w);
           } else {
             __syncwarp();
-            build_act_keys(mass, true);
+            const uint32_t aw = nonempty_w & ~blocked_w & ~(slotful_w & ~claimed_w);
+            if (__reduce_add_sync(kFull, __popc(aw)) <= 32) {  // only claimed chains act now
+              enter_lane_mode(aw);
+              lane_mode = true;
+              __syncwarp();
+              continue;
+            }
+            if (direct) {
+              build_act_keys(mass, false);
+              direct = false;
+            } else {
+              build_act_keys(mass, true);
+            }
             __syncwarp();
             local_best(&lk, &la);
             continue;
           }
         }
       }
-      if (!lane_mode && mine) local_best(&lk, &la);
+      if (!lane_mode) {
+        if (direct) {
+          __syncwarp();  // lane 0's q_head store
+          if (mine) nonlane_best(true, &lk, &la);
+        } else if (mine) {
+          local_best(&lk, &la);
+        }
+      }
       __syncwarp();
     }
     reject_oversized(P, stop_id);
