@@ -1544,8 +1544,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(EnginePara
   // First round: scenario warp * gridDim + block, so the most expensive
   // scenarios (the head of the cost order) land on different SMs instead of
   // sharing one SM's schedulers; then a global counter hands out the rest.
+  // Warps w and w + 4 share a scheduler (SMSP w % 4): the other SMSP-0
+  // warps (4, 8) are filled last, so when a batch leaves spare slots the
+  // heaviest engines (warp 0 of each block) keep their scheduler to themselves.
   const int warps = blockDim.x >> 5;
-  const int first = warp * gridDim.x + blockIdx.x;
+  const int rank = (warp & 3) ? warp - (warp >> 2) : (warp == 0 ? 0 : warps - (warps >> 2) + (warp >> 2));
+  const int first = rank * gridDim.x + blockIdx.x;
   // (one call site: engine_run is inlined once)
   for (int k = first; k < P.n_scen;) {
     engine_run(P, P.order[k], slot, mine);
