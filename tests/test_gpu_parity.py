@@ -408,3 +408,36 @@ def test_staged_plan_matches_single(dev, ref, monkeypatch):
     for f in ("status", "iterations", "digest", "final_clock_s"):
         np.testing.assert_array_equal(a[f], g1[f], err_msg=f)
         np.testing.assert_array_equal(c[f], g1[f], err_msg=f)
+
+
+def many_adapter_batch(priority):
+    """Scripted engines with 33-200 adapters on 1-8 slots: more than 32 chains
+    act whenever a slot is free, so the fresh scan runs its non-lane forms
+    (argmin over the chain heads on slot turnover, act_key scans without the
+    loaded-adapter priority) and switches to lane mode mid-scan."""
+    rng = np.random.default_rng(11 if priority else 12)
+    wls, scripted = [], []
+    for s in range(60):
+        ads, reqs, _ = W.scripted_fuzz(5000 + s, n_requests=int(rng.integers(100, 500)),
+                                       n_adapters=int(rng.integers(33, 200)))
+        wls.append(W.scripted_workload(ads, 8.0))
+        scripted.append(reqs)
+    cfg = W.scripted_fuzz(8)[2]
+    cfg.loaded_adapter_priority = priority
+    cfg.memory.total_kv_budget = 1500
+    return WorkloadBatch.from_workloads(wls, slots=[1 + i % 8 for i in range(len(wls))], scripted=scripted), cfg
+
+
+@pytest.mark.parametrize("variant", ["1", "2", "3"])
+def test_engine_variants_match_reference(dev, ref, monkeypatch, variant):
+    """Every compiled engine variant (8 warps / 16 warps / 12 warps per SM,
+    LT_ENGINE_VARIANT) against the reference, on slot-turnover-heavy batches."""
+    monkeypatch.setenv("LT_ENGINE_VARIANT", variant)
+    cases = [many_adapter_batch(True), many_adapter_batch(False),
+             (W.c2_batch(duration_s=600.0, stride=16), lt.h100_like_config(1))]
+    for b, cfg in cases:
+        g, gs = dev.simulate_batch(b, cfg, want_states=True, want_digest=True)
+        r, rs = ref.simulate(b, cfg, sim_options(None, True), want_states=True)
+        assert_summaries(g, r)
+        for k in gs:
+            np.testing.assert_array_equal(gs[k], rs[k], err_msg=k)
