@@ -495,6 +495,8 @@ struct Prep {
   std::vector<DDeck> decks;                        // Full-mode decks, table_off set after sizing
   std::map<std::pair<int32_t, int32_t>, int32_t> deck_index;  // (key, D) -> deck
   std::vector<double> cost;
+  // a key appeared (or grew) after the early K0 launch (collect_keys)
+  bool late_keys = false;
 
   SeedKeys& seed_keys(uint64_t seed) {
     auto it = seed_index.find(seed);
@@ -665,8 +667,10 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
         k.rate_max = a.rate;
         k.dur_max = s.duration_s;
         pr.keys.push_back(k);
+        pr.late_keys = true;
       } else {
         DKey& k = pr.keys[kidx];
+        if (a.rate > k.rate_max || s.duration_s > k.dur_max) pr.late_keys = true;
         k.rate_max = std::max(k.rate_max, a.rate);
         k.dur_max = std::max(k.dur_max, s.duration_s);
       }
@@ -730,8 +734,10 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 // Keys seeded and drawn per chunk (the seeded states take 5 KB per key).
 constexpr int64_t kSeedChunk = 1 << 18;
 
+int launch_decks(lt_plan& P, cudaStream_t st);
+
 // K0: seed_kernel (seed_seq, one thread per stream) then tables_draw_kernel
-// (one warp per key), chunk by chunk. Returns the launches.
+// (one warp per key), chunk by chunk, then the decks. Returns the launches.
 int launch_tables(lt_plan& P, int nk, cudaStream_t st) {
   LT_CUDA(cudaFuncSetAttribute(seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(kSeedSmem)));
@@ -753,14 +759,17 @@ int launch_tables(lt_plan& P, int nk, cudaStream_t st) {
     after_launch("tables_draw_kernel", st);
     launches += 2;
   }
-  if (!P.h_decks.empty()) {
-    LT_CUDA(cudaFuncSetAttribute(deck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P.ctx->smem_optin));
-    deck_kernel<<<static_cast<unsigned>(P.h_decks.size()), 32, P.deck_smem, st>>>(
-        P.keys.p, P.decks.p, P.deck_tab.p, P.big_deck.p, P.big_off.p);
-    after_launch("deck_kernel", st);
-    ++launches;
-  }
-  return launches;
+  return launches + launch_decks(P, st);
+}
+
+// Full-mode decks (deck_kernel) of the plan's keys, once their tables are sized.
+int launch_decks(lt_plan& P, cudaStream_t st) {
+  if (P.h_decks.empty()) return 0;
+  LT_CUDA(cudaFuncSetAttribute(deck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P.ctx->smem_optin));
+  deck_kernel<<<static_cast<unsigned>(P.h_decks.size()), 32, P.deck_smem, st>>>(P.keys.p, P.decks.p, P.deck_tab.p,
+                                                                                P.big_deck.p, P.big_off.p);
+  after_launch("deck_kernel", st);
+  return 1;
 }
 
 // Full-mode deck tables: one slot per possible arrival of the deck's key.
@@ -785,6 +794,52 @@ void size_decks(lt_plan& P, const std::vector<DKey>& keys, cudaStream_t st) {
   P.big_off.upload(boff, st);
   P.big_deck.alloc(std::max<int64_t>(big, 1));
   P.deck_smem = 624 * sizeof(uint32_t) + kMtN * sizeof(uint64_t) + static_cast<size_t>(max_small) * sizeof(int32_t);
+}
+
+// First pass of build_plan: the RNG keys (seed, adapter id) with their
+// largest rate and duration over every generated scenario that can pass the
+// workload screen, so K0 runs on the device while the second pass validates
+// and packs the scenarios. Keys of scenarios that fail later only lengthen
+// tables (each table is a prefix-stable draw sequence), never change them.
+void collect_keys(Prep& pr, const lt_workload_batch& b) {
+  for (int64_t i = 0; i < b.n_scenarios; ++i) {
+    const lt_scenario& s = b.scenarios[i];
+    if (s.n_requests >= 0 || s.n_adapters <= 0 || s.n_adapters > kMaxAdapters || s.duration_s <= 0.0) continue;
+    const lt_adapter* ad = b.adapters + s.adapter_offset;
+    Prep::SeedKeys& sk = pr.seed_keys(s.seed);
+    for (int k = 0; k < s.n_adapters; ++k) {
+      const lt_adapter& a = ad[k];
+      if (!(a.rate > 0.0)) continue;
+      bool inserted = false;
+      const int kidx = Prep::find_or_insert(sk, a.adapter_id, static_cast<int32_t>(pr.keys.size()), &inserted);
+      if (inserted) {
+        DKey key{};
+        key.seed = s.seed;
+        key.id = a.adapter_id;
+        key.rate_max = a.rate;
+        key.dur_max = s.duration_s;
+        pr.keys.push_back(key);
+      } else {
+        DKey& key = pr.keys[kidx];
+        key.rate_max = std::max(key.rate_max, a.rate);
+        key.dur_max = std::max(key.dur_max, s.duration_s);
+      }
+    }
+  }
+}
+
+// Table capacity per key: rate_max * dur_max + 8 sigma + slack draws.
+int64_t size_keys(std::vector<DKey>& keys) {
+  int64_t e_total = 0;
+  for (DKey& k : keys) {
+    const double lam = k.rate_max * k.dur_max;
+    const double capd = lam + 8.0 * std::sqrt(lam) + 32.0;
+    k.cap = static_cast<int32_t>(std::min(capd, 2.0e9));
+    k.e_off = e_total;
+    k.z_off = e_total;
+    e_total += k.cap;
+  }
+  return e_total;
 }
 
 // Builds a plan: validation, RNG tables, counting, merge, request arrays,
@@ -815,6 +870,23 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   pr.pair_scen.reserve(b->n_adapters);
   pr.pair_adp.reserve(b->n_adapters);
   pr.pair_begin.resize(P.n_scen);
+  // pass 1 + early K0 (seed_seq and table draws; Full-mode decks follow pass 2)
+  collect_keys(pr, *b);
+  int64_t e_total = size_keys(pr.keys);
+  cudaEventRecord(P.ev[0], st);
+  if (!pr.keys.empty())
+    P.seed_state.alloc(std::min<int64_t>(static_cast<int64_t>(pr.keys.size()), kSeedChunk) * 2 * kMtN);
+  P.tab_overflow.alloc(1);
+  LT_CUDA(cudaMemsetAsync(P.tab_overflow.p, 0, sizeof(int32_t), st));
+  const size_t early_keys = pr.keys.size();
+  if (early_keys > 0) {
+    P.keys.upload(pr.keys, st);
+    P.E.alloc(std::max<int64_t>(e_total, 1));
+    P.Z.alloc(std::max<int64_t>(e_total, 1));
+    P.h2d_bytes += pr.keys.size() * sizeof(DKey);
+    P.launches_prep += launch_tables(P, static_cast<int>(early_keys), st);
+  }
+  // pass 2: validation and packing in reference order
   for (int64_t i = 0; i < P.n_scen; ++i) {
     pr.pair_begin[i] = static_cast<int64_t>(pr.pair_scen.size());
     prepare_scenario(P, pr, *b, i);
@@ -827,33 +899,30 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   P.max_adapters = (P.max_adapters + 31) / 32 * 32;
   if (pr.lens.empty()) pr.lens.push_back(DLen{1, 0, 1, 0});
   const auto h_prep = hclk::now();
-  cudaEventRecord(P.ev[0], st);
-  // keys: reserve rate_max * dur_max + 8 sigma + slack draws
-  int64_t e_total = 0;
-  for (DKey& k : pr.keys) {
-    const double lam = k.rate_max * k.dur_max;
-    const double capd = lam + 8.0 * std::sqrt(lam) + 32.0;
-    k.cap = static_cast<int32_t>(std::min(capd, 2.0e9));
-    k.e_off = e_total;
-    k.z_off = e_total;
-    e_total += k.cap;
-  }
-  if (!pr.keys.empty())
-    P.seed_state.alloc(std::min<int64_t>(static_cast<int64_t>(pr.keys.size()), kSeedChunk) * 2 * kMtN);
-  P.tab_overflow.alloc(1);
   P.h_decks = pr.decks;
   if (!P.h_decks.empty() && b->n_full_pairs > 0) {
     std::vector<int32_t> fl(b->full_lengths, b->full_lengths + 2 * b->n_full_pairs);
     P.full.upload(fl, st);
   }
-  for (int attempt = 0;; ++attempt) {
+  // (pass 2 found every key pass 1 did, unchanged, unless late_keys)
+  bool relaunch = (pr.late_keys || std::getenv("LT_K0_RELAUNCH")) && !pr.keys.empty();  // (env: test hook)
+  if (relaunch) e_total = size_keys(pr.keys);
+  if (!relaunch && !P.h_decks.empty()) {  // decks of the early tables
     size_decks(P, pr.keys, st);
-    P.keys.upload(pr.keys, st);
-    LT_CUDA(cudaMemsetAsync(P.tab_overflow.p, 0, sizeof(int32_t), st));
-    P.E.alloc(std::max<int64_t>(e_total, 1));
-    P.Z.alloc(std::max<int64_t>(e_total, 1));
-    P.h2d_bytes += pr.keys.size() * sizeof(DKey);
-    if (!pr.keys.empty()) P.launches_prep += launch_tables(P, static_cast<int>(pr.keys.size()), st);
+    P.launches_prep += launch_decks(P, st);
+  }
+  for (int attempt = 0;; ++attempt) {
+    if (relaunch) {
+      P.seed_state.alloc(std::min<int64_t>(static_cast<int64_t>(pr.keys.size()), kSeedChunk) * 2 * kMtN);
+      size_decks(P, pr.keys, st);
+      P.keys.upload(pr.keys, st);
+      LT_CUDA(cudaMemsetAsync(P.tab_overflow.p, 0, sizeof(int32_t), st));
+      P.E.alloc(std::max<int64_t>(e_total, 1));
+      P.Z.alloc(std::max<int64_t>(e_total, 1));
+      P.h2d_bytes += pr.keys.size() * sizeof(DKey);
+      P.launches_prep += launch_tables(P, static_cast<int>(pr.keys.size()), st);
+    }
+    relaunch = true;
     int32_t any = 0;
     LT_CUDA(cudaMemcpyAsync(&any, P.tab_overflow.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     LT_CUDA(cudaStreamSynchronize(st));

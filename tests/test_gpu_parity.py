@@ -441,3 +441,19 @@ def test_engine_variants_match_reference(dev, ref, monkeypatch, variant):
         assert_summaries(g, r)
         for k in gs:
             np.testing.assert_array_equal(gs[k], rs[k], err_msg=k)
+
+
+def test_k0_relaunch_matches_early_launch(dev, monkeypatch):
+    """K0 is launched from the first (key) pass of build_plan; the second pass
+    relaunches it when a key appeared late. Forcing the relaunch (test hook)
+    must give the same arrivals and summaries, Full-mode decks included."""
+    for b, cfg in (W.summary_cases(), W.full_mode_cases()):
+        g1, s1 = dev.simulate_batch(b, cfg, want_states=True, want_digest=True)
+        monkeypatch.setenv("LT_K0_RELAUNCH", "1")
+        g2, s2 = dev.simulate_batch(b, cfg, want_states=True, want_digest=True)
+        monkeypatch.delenv("LT_K0_RELAUNCH")
+        for f in g1.dtype.names:
+            if f not in ("device_cycles", "phase_cycles"):
+                np.testing.assert_array_equal(g1[f], g2[f], err_msg=f)
+        for k in s1:
+            np.testing.assert_array_equal(s1[k], s2[k], err_msg=k)
