@@ -62,6 +62,13 @@ __device__ __forceinline__ void mask_set(uint32_t& w, int a, int lane) {
 __device__ __forceinline__ void mask_clear(uint32_t& w, int a, int lane) {
   if (lane == (a >> 5)) w &= ~(1u << (a & 31));
 }
+// {in, out, next} of a fresh-queue node {in, out, next, adapter}.
+__device__ __forceinline__ int3 node_head(const int4* node, int k) {
+  const int2 xy = *reinterpret_cast<const int2*>(node + k);
+  const int z = reinterpret_cast<const int*>(node + k)[2];
+  return make_int3(xy.x, xy.y, z);
+}
+
 // Lowest set adapter index of a mask, or -1.
 __device__ __forceinline__ int mask_lowest(uint32_t w) {
   const unsigned nz = __ballot_sync(kFull, w != 0);
@@ -215,10 +222,12 @@ struct WarpEngine {
   int32_t* act_key = nullptr;  // scan-local: chain head if the adapter can act, else INT_MAX
   // Lane mode of the fresh scan (<= 32 acting adapters), persistent across
   // scans: lane L owns adapter pl_a (-1: none) whose chain head is pl_k with
-  // node pl_nd {in, out, next, adapter}; pl_sf / pl_cl are its slot-needing /
+  // node fields pl_nd {in, out, next} (loaded without the adapter word, whose
+  // dead register would otherwise be reused while the load is in flight and
+  // stall the warp on it); pl_sf / pl_cl are its slot-needing /
   // claimed flags. built_w is the lane's word of the owned-adapter set.
   int32_t pl_a = -1, pl_k = INT_MAX;
-  int4 pl_nd = make_int4(0, 0, -1, 0);
+  int3 pl_nd = make_int3(0, 0, -1);
   bool pl_sf = false, pl_cl = false, pl_valid = false;
   uint32_t built_w = 0;
   // Fresh admissions of the current iteration (first-token times): lane j
@@ -798,7 +807,7 @@ struct WarpEngine {
           if (lane == fl) {
             pl_a = a;
             pl_k = q_head[a];
-            pl_nd = node[pl_k];
+            pl_nd = node_head(node, pl_k);
             pl_sf = sfa;
           }
           mask_set(built_w, a, lane);
@@ -826,7 +835,7 @@ struct WarpEngine {
           pl_k = q_head[pl_a];
         }
       }
-      if (pl_k != INT_MAX) pl_nd = node[pl_k];
+      if (pl_k != INT_MAX) pl_nd = node_head(node, pl_k);
       pl_sf = mask_bit(slotful_w, pl_a < 0 ? 0 : pl_a);
       built_w = act_w;
       pl_valid = true;
@@ -984,7 +993,7 @@ struct WarpEngine {
           pl_k = INT_MAX;
         } else {
           pl_k = next;
-          pl_nd = node[next];  // in flight until this lane wins again
+          pl_nd = node_head(node, next);  // in flight until this lane wins again
         }
       }
       if (next < 0) mask_clear(built_w, a, lane);
