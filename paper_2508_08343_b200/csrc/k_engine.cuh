@@ -609,7 +609,7 @@ struct WarpEngine {
       bool zero = false;
       if (lane == 0) {
         P.r_phase[rb + idx] = kPreempted;
-        P.r_pre[rb + idx] += 1;
+        atomicAdd(&P.r_pre[rb + idx], 1);  // no return value: nothing waits on the load
         P.r_gen[rb + idx] = gen;
         P.r_last[rb + idx] = clock;
         zero = atomicSub(&run_cnt[a], 1) == 1;
