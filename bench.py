@@ -307,7 +307,8 @@ def impl_gpu(args):
         pb, keep = pinned_copy(batch)
         walls, plan_ms, wait_ms = [], [], []
         h2d = d2h = 0
-        for i in range(max(1, args.e2e_steps) + 1):
+        n_warm = max(1, args.warmup)  # same warm-up as the device-resident leg
+        for i in range(max(1, args.e2e_steps) + n_warm):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             out, _ = dev.simulate_batch(pb, cfg)
@@ -316,7 +317,7 @@ def impl_gpu(args):
             h2d, d2h = int(tm["h2d_bytes"]), int(tm["d2h_bytes"])
             plan_ms.append(tm["plan_ms"])
             wait_ms.append(tm["run_wait_ms"])
-        walls = walls[1:]
+        walls, plan_ms, wait_ms = walls[n_warm:], plan_ms[n_warm:], wait_ms[n_warm:]
         e2e_val = int(out["iterations"].sum()) / statistics.mean(walls)
         if dist:
             tt = torch.tensor([max(walls)], device=f"cuda:{local}", dtype=torch.float64)
@@ -324,7 +325,8 @@ def impl_gpu(args):
             e2e_val = iters_all / float(tt.item())
         e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": 1000 * statistics.mean(walls), "call": "lt_simulate_batch (host pinned buffers)",
-               "plan_ms": statistics.mean(plan_ms[1:]), "run_wait_ms": statistics.mean(wait_ms[1:])}
+               "plan_ms": statistics.mean(plan_ms), "run_wait_ms": statistics.mean(wait_ms),
+               "warmup_calls": n_warm}
         # The reference's compute_metrics always sorts TTFT/ITL for percentiles
         # (metrics.cpp:101-105); sweeps never read them, so the timed device
         # path skips them. Same call with the percentiles (recording pass +
@@ -387,7 +389,7 @@ def main():
     ap.add_argument("--duration", type=float, default=600.0)
     ap.add_argument("--cpu-stride", type=int, default=1, help="cpu_baseline sample: every k-th C2 scenario")
     ap.add_argument("--ref-stride", type=int, default=3, help="--impl reference sample per step")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--sweep-conditions", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -13,6 +13,7 @@
 #include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <thread>
 #include <cmath>
@@ -363,9 +364,10 @@ struct DBuf {
     n = count;
     if (count) p = static_cast<T*>(BlockCache::get().take(count * sizeof(T), &cls));
   }
-  void upload(const std::vector<T>& v, cudaStream_t s) {
-    alloc(v.size());
-    if (!v.empty()) LT_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  void upload(const std::vector<T>& v, cudaStream_t s) { upload(v.data(), v.size(), s); }
+  void upload(const T* src, size_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) LT_CUDA(cudaMemcpyAsync(p, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
   }
 };
 
@@ -376,6 +378,7 @@ struct lt_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;  // second part of a staged plan
+  cudaStream_t stream_up = nullptr;  // packed-scenario uploads, beside K0
   int smem_optin = 0;              // max dynamic shared memory per block (opt-in)
   int sm_count = 0;
   lt_timing timing{};
@@ -387,6 +390,7 @@ struct lt_plan {
   lt_ctx* ctx = nullptr;
   cudaStream_t st = nullptr;  // the stream this plan's work runs on
   cudaEvent_t ev[8]{};        // this plan's timing events
+  cudaEvent_t ev_up = nullptr;  // packed-scenario uploads done (ctx->stream_up)
   // staged plan: parts[0] = the most expensive scenarios (engine started
   // first, one warp per block so the other part's K0/merge kernels share the
   // SMs), parts[1] = the rest, prepared concurrently on a second stream
@@ -399,6 +403,7 @@ struct lt_plan {
     for (cudaEvent_t e : ev)
       if (e) cudaEventDestroy(e);
     if (ev_start) cudaEventDestroy(ev_start);
+    if (ev_up) cudaEventDestroy(ev_up);
     if (ev_join) cudaEventDestroy(ev_join);
   }
   Config cfg;
@@ -475,8 +480,24 @@ namespace {
 // ----------------------------------------------------------------------------
 // Batch preparation
 
+// DAdapter without value-initialisation: the packed array is sized up front
+// for scenarios packed later by several host threads (Prep::deferred).
+struct DAdapterNI : DAdapter {
+  DAdapterNI() {}
+  DAdapterNI(const DAdapter& d) : DAdapter(d) {}
+};
+static_assert(sizeof(DAdapterNI) == sizeof(DAdapter), "layout");
+
 struct Prep {
-  std::vector<DAdapter> adapters;
+  std::vector<DAdapterNI> adapters;
+  // Generated Mean-mode scenarios with ascending adapter ids that passed
+  // validation: their adapter records are packed after the serial pass, in
+  // parallel, into slots reserved in order (scenario, adapter offset, pair offset).
+  struct Deferred {
+    int64_t i, a_off, p_off;
+  };
+  std::vector<Deferred> deferred;
+  bool allow_defer = false;
   std::vector<DLen> lens;
   std::vector<DKey> keys;
   std::vector<int32_t> pair_scen, pair_adp;
@@ -504,6 +525,15 @@ struct Prep {
     seed_index.emplace(seed, static_cast<int32_t>(seeds.size()));
     seeds.emplace_back();
     return seeds.back();
+  }
+  // Key index of (seed, id) or -1, without inserting (safe from several threads).
+  int32_t find_key(uint64_t seed, int64_t id) const {
+    auto it = seed_index.find(seed);
+    if (it == seed_index.end()) return -1;
+    const SeedKeys& sk = seeds[it->second];
+    if (id >= 0 && id < 65536) return id < static_cast<int64_t>(sk.dense.size()) ? sk.dense[id] : -1;
+    auto j = sk.sparse.find(id);
+    return j == sk.sparse.end() ? -1 : j->second;
   }
   // Returns the key index of (seed, id) in `sk`, inserting `fresh` when absent.
   static int32_t find_or_insert(SeedKeys& sk, int64_t id, int32_t fresh, bool* inserted) {
@@ -645,6 +675,20 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
   }
   d.ideal = ideal;
   d.length_param = intern_len(pr, as_dlen(b.lengths[s.length_index], full));
+  if (pr.allow_defer && !scripted && ascending && s.mode != LT_MODE_FULL) {
+    bool simple = true;  // no per-adapter length specs (interning stays serial)
+    for (int k = 0; k < s.n_adapters && simple; ++k) simple = ad[k].length_index < 0;
+    if (simple) {
+      pr.deferred.push_back(Prep::Deferred{i, static_cast<int64_t>(pr.adapters.size()),
+                                           static_cast<int64_t>(pr.pair_scen.size())});
+      pr.adapters.resize(pr.adapters.size() + s.n_adapters);
+      P.adapter_ids.resize(P.adapter_ids.size() + s.n_adapters);
+      pr.pair_scen.resize(pr.pair_scen.size() + s.n_adapters);
+      pr.pair_adp.resize(pr.pair_adp.size() + s.n_adapters);
+      P.max_adapters = std::max(P.max_adapters, s.n_adapters);
+      return;
+    }
+  }
   double cost = 0.0;
   Prep::SeedKeys* sk = scripted ? nullptr : &pr.seed_keys(s.seed);
   for (int k = 0; k < s.n_adapters; ++k) {
@@ -796,6 +840,60 @@ void size_decks(lt_plan& P, const std::vector<DKey>& keys, cudaStream_t st) {
   P.deck_smem = 624 * sizeof(uint32_t) + kMtN * sizeof(uint64_t) + static_cast<size_t>(max_small) * sizeof(int32_t);
 }
 
+// Packs the deferred scenarios' adapter records (the adapter loop of
+// prepare_scenario for generated Mean-mode scenarios with ascending ids) on
+// several host threads. Returns false if a key was missing (never expected:
+// collect_keys saw every such adapter); the caller then repacks serially.
+bool pack_deferred(lt_plan& P, Prep& pr, const lt_workload_batch& b) {
+  const int64_t nd = static_cast<int64_t>(pr.deferred.size());
+  if (nd == 0) return true;
+  std::atomic<bool> ok{true};
+  auto work = [&](int64_t d0, int64_t d1) {
+    for (int64_t d = d0; d < d1; ++d) {
+      const Prep::Deferred& df = pr.deferred[d];
+      const lt_scenario& s = b.scenarios[df.i];
+      const lt_adapter* ad = b.adapters + s.adapter_offset;
+      const lt_length_spec& l = b.lengths[s.length_index];
+      const double out_mean = output_mean(l, b.full_lengths) + 1.0;
+      double cost = 0.0;
+      for (int k = 0; k < s.n_adapters; ++k) {
+        const lt_adapter& a = ad[k];
+        DAdapter x{};
+        x.id = a.adapter_id;
+        x.rank = a.rank;
+        x.rate = a.rate;
+        x.load_lat = (a.rank >= 0 && a.rank < 1024) ? P.cfg.lat_cache[a.rank] : load_latency(P.cfg, a.rank);
+        x.length_param = -1;
+        x.deck = -1;
+        x.key = pr.find_key(s.seed, a.adapter_id);
+        if (x.key < 0) ok = false;
+        pr.adapters[df.a_off + k] = x;
+        P.adapter_ids[df.a_off + k] = a.adapter_id;
+        pr.pair_scen[df.p_off + k] = static_cast<int32_t>(df.i);
+        pr.pair_adp[df.p_off + k] = k;
+        cost += a.rate * s.duration_s * out_mean;
+      }
+      pr.cost[df.i] = cost;
+    }
+  };
+  // the load-latency cache is filled serially first (read-only in the workers)
+  for (const Prep::Deferred& df : pr.deferred) {
+    const lt_scenario& s = b.scenarios[df.i];
+    for (int k = 0; k < s.n_adapters; ++k) load_latency_cached(P.cfg, b.adapters[s.adapter_offset + k].rank);
+  }
+  const int64_t total = pr.deferred.back().a_off + b.scenarios[pr.deferred.back().i].n_adapters -
+                        pr.deferred.front().a_off;
+  const int nt = total < 16384 ? 1 : static_cast<int>(std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency())));
+  if (nt <= 1) {
+    work(0, nd);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) th.emplace_back(work, nd * t / nt, nd * (t + 1) / nt);
+    for (auto& x : th) x.join();
+  }
+  return ok;
+}
+
 // First pass of build_plan: the RNG keys (seed, adapter id) with their
 // largest rate and duration over every generated scenario that can pass the
 // workload screen, so K0 runs on the device while the second pass validates
@@ -886,18 +984,53 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     P.h2d_bytes += pr.keys.size() * sizeof(DKey);
     P.launches_prep += launch_tables(P, static_cast<int>(early_keys), st);
   }
-  // pass 2: validation and packing in reference order
-  for (int64_t i = 0; i < P.n_scen; ++i) {
-    pr.pair_begin[i] = static_cast<int64_t>(pr.pair_scen.size());
-    prepare_scenario(P, pr, *b, i);
-    if (P.errs[i].code != LT_OK) {
-      // drop partially appended pairs of a failed scenario
-      pr.pair_scen.resize(pr.pair_begin[i]);
-      pr.pair_adp.resize(pr.pair_begin[i]);
+  // pass 2: validation and packing in reference order; the adapter records
+  // of plain generated scenarios are packed afterwards on several threads
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    pr.allow_defer = attempt == 0 && !std::getenv("LT_SERIAL_PREP");
+    for (int64_t i = 0; i < P.n_scen; ++i) {
+      pr.pair_begin[i] = static_cast<int64_t>(pr.pair_scen.size());
+      prepare_scenario(P, pr, *b, i);
+      if (P.errs[i].code != LT_OK) {
+        // drop partially appended pairs of a failed scenario
+        pr.pair_scen.resize(pr.pair_begin[i]);
+        pr.pair_adp.resize(pr.pair_begin[i]);
+      }
     }
+    if (pack_deferred(P, pr, *b)) break;
+    // a key was missing: repack everything serially
+    pr.deferred.clear();
+    pr.adapters.clear();
+    P.adapter_ids.clear();
+    pr.pair_scen.clear();
+    pr.pair_adp.clear();
+    pr.lens.clear();
+    pr.len_index.clear();
+    pr.decks.clear();
+    pr.deck_index.clear();
+    P.max_adapters = 0;
   }
   P.max_adapters = (P.max_adapters + 31) / 32 * 32;
   if (pr.lens.empty()) pr.lens.push_back(DLen{1, 0, 1, 0});
+  // The packed scenarios go up on their own stream while K0 runs.
+  {
+    cudaStream_t su = ctx->stream_up;
+    LT_CUDA(cudaEventCreateWithFlags(&P.ev_up, cudaEventDisableTiming));
+    P.scen.upload(P.h_scen, su);
+    P.adapters.upload(pr.adapters.data(), pr.adapters.size(), su);  // (DAdapterNI: DAdapter layout)
+    P.lens.upload(pr.lens, su);
+    P.h2d_bytes += P.h_scen.size() * sizeof(DScen) + pr.adapters.size() * sizeof(DAdapter);
+    std::vector<unsigned long long> base(std::max<int64_t>(P.n_scen, 1), 0ULL);
+    for (int64_t i = 0; i < P.n_scen; ++i)
+      if (!P.h_scen[i].generated && P.h_scen[i].status == LT_OK) base[i] = P.h_scen[i].n_req;
+    P.base_count.upload(base, su);
+    if (!pr.pair_scen.empty()) {
+      P.pair_scen.upload(pr.pair_scen, su);
+      P.pair_adp.upload(pr.pair_adp, su);
+      P.pair_begin.upload(pr.pair_begin, su);
+    }
+    LT_CUDA(cudaEventRecord(P.ev_up, su));
+  }
   const auto h_prep = hclk::now();
   P.h_decks = pr.decks;
   if (!P.h_decks.empty() && b->n_full_pairs > 0) {
@@ -945,23 +1078,11 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   const int64_t n_pairs = static_cast<int64_t>(pr.pair_scen.size());
   P.n_pairs = n_pairs;
   P.n_keys = static_cast<int>(pr.keys.size());
-  P.scen.upload(P.h_scen, st);
-  P.adapters.upload(pr.adapters, st);
-  P.lens.upload(pr.lens, st);
-  P.h2d_bytes += P.h_scen.size() * sizeof(DScen) + pr.adapters.size() * sizeof(DAdapter);
   P.scen_count.alloc(std::max<int64_t>(P.n_scen, 1));
   P.scen_off.alloc(std::max<int64_t>(P.n_scen, 1));
   P.overflow.alloc(1);
-  {
-    std::vector<unsigned long long> base(std::max<int64_t>(P.n_scen, 1), 0ULL);
-    for (int64_t i = 0; i < P.n_scen; ++i)
-      if (!P.h_scen[i].generated && P.h_scen[i].status == LT_OK) base[i] = P.h_scen[i].n_req;
-    P.base_count.upload(base, st);
-  }
+  LT_CUDA(cudaStreamWaitEvent(st, P.ev_up, 0));  // the packed-scenario uploads
   if (n_pairs > 0) {
-    P.pair_scen.upload(pr.pair_scen, st);
-    P.pair_adp.upload(pr.pair_adp, st);
-    P.pair_begin.upload(pr.pair_begin, st);
     P.adp_count.alloc(n_pairs);
     LT_CUDA(cudaMemsetAsync(P.scen_count.p, 0, P.n_scen * sizeof(unsigned long long), st));
     LT_CUDA(cudaMemsetAsync(P.overflow.p, 0, sizeof(int32_t), st));
@@ -1653,7 +1774,18 @@ double lt__host_prep_ms(const lt_workload_batch* b, const lt_server_config* cfg)
   pr.adapters.reserve(b->n_adapters);
   pr.pair_scen.reserve(b->n_adapters);
   pr.pair_adp.reserve(b->n_adapters);
+  const auto t05 = std::chrono::steady_clock::now();
+  collect_keys(pr, *b);
+  const auto t1 = std::chrono::steady_clock::now();
+  pr.allow_defer = !std::getenv("LT_SERIAL_PREP");
   for (int64_t i = 0; i < P.n_scen; ++i) prepare_scenario(P, pr, *b, i);
+  const auto t2 = std::chrono::steady_clock::now();
+  pack_deferred(P, pr, *b);
+  if (std::getenv("LT_HOST_TIMING")) {
+    auto ms = [](auto x, auto y) { return std::chrono::duration<double, std::milli>(y - x).count(); };
+    std::fprintf(stderr, "[lt] host prep: setup %.2f ms, keys %.2f ms, serial pass %.2f ms, parallel packing %.2f ms\n", ms(t0, t05), ms(t05, t1),
+                 ms(t1, t2), ms(t2, std::chrono::steady_clock::now()));
+  }
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
@@ -1744,6 +1876,7 @@ lt_ctx* lt_create(int32_t device, lt_status* status) {
     ctx->smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
     LT_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     LT_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+    LT_CUDA(cudaStreamCreateWithFlags(&ctx->stream_up, cudaStreamNonBlocking));
     for (auto& e : ctx->ev) LT_CUDA(cudaEventCreate(&e));
     return ctx.release();
   } catch (const CudaError& e) {
@@ -1759,6 +1892,7 @@ void lt_destroy(lt_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+  if (ctx->stream_up) cudaStreamDestroy(ctx->stream_up);
   delete ctx;
 }
 
