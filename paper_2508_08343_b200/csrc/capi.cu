@@ -480,6 +480,29 @@ namespace {
 // ----------------------------------------------------------------------------
 // Batch preparation
 
+// Page-locked host memory for the packed arrays uploaded every plan: the
+// copies run as DMA straight from them (no driver staging copy). Prep keeps
+// them per host thread across plans, so the allocation is paid once.
+template <class T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <class U>
+  PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocDefault) != cudaSuccess) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t) { cudaFreeHost(p); }
+  template <class U>
+  bool operator==(const PinnedAlloc<U>&) const { return true; }
+  template <class U>
+  bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+template <class T>
+using PinnedVec = std::vector<T, PinnedAlloc<T>>;
+
 // DAdapter without value-initialisation: the packed array is sized up front
 // for scenarios packed later by several host threads (Prep::deferred).
 struct DAdapterNI : DAdapter {
@@ -487,9 +510,14 @@ struct DAdapterNI : DAdapter {
   DAdapterNI(const DAdapter& d) : DAdapter(d) {}
 };
 static_assert(sizeof(DAdapterNI) == sizeof(DAdapter), "layout");
+struct DKeyNI : DKey {
+  DKeyNI() {}
+  DKeyNI(const DKey& d) : DKey(d) {}
+};
+static_assert(sizeof(DKeyNI) == sizeof(DKey), "layout");
 
 struct Prep {
-  std::vector<DAdapterNI> adapters;
+  PinnedVec<DAdapterNI> adapters;
   // Generated Mean-mode scenarios with ascending adapter ids that passed
   // validation: their adapter records are packed after the serial pass, in
   // parallel, into slots reserved in order (scenario, adapter offset, pair offset).
@@ -499,9 +527,12 @@ struct Prep {
   std::vector<Deferred> deferred;
   bool allow_defer = false;
   std::vector<DLen> lens;
-  std::vector<DKey> keys;
-  std::vector<int32_t> pair_scen, pair_adp;
-  std::vector<int64_t> pair_begin;
+  PinnedVec<DKeyNI> keys;
+  // Scenarios whose seed no other scenario uses, with strictly ascending ids:
+  // their keys are their adapters, at keys[key_base[i] + k] (else -1).
+  std::vector<int64_t> key_base;
+  PinnedVec<int32_t> pair_scen, pair_adp;
+  PinnedVec<int64_t> pair_begin;
   std::unordered_map<std::string, int> len_index;
   // (seed, adapter_id) -> key index. Keys are looked up per seed: a batch has
   // few distinct seeds with many adapters each (sweeps share one seed across
@@ -518,6 +549,32 @@ struct Prep {
   std::vector<double> cost;
   // a key appeared (or grew) after the early K0 launch (collect_keys)
   bool late_keys = false;
+
+  // Empties every table but keeps the vectors' memory (already paged in) for
+  // the next plan on this host thread; very large buffers are released.
+  void reset() {
+    const bool big = keys.capacity() * sizeof(DKey) + adapters.capacity() * sizeof(DAdapter) > (size_t(1536) << 20);
+    if (big) {
+      *this = Prep();
+      return;
+    }
+    adapters.clear();
+    deferred.clear();
+    allow_defer = false;
+    lens.clear();
+    keys.clear();
+    key_base.clear();
+    pair_scen.clear();
+    pair_adp.clear();
+    pair_begin.clear();
+    len_index.clear();
+    seed_index.clear();
+    seeds.clear();
+    decks.clear();
+    deck_index.clear();
+    cost.clear();
+    late_keys = false;
+  }
 
   SeedKeys& seed_keys(uint64_t seed) {
     auto it = seed_index.find(seed);
@@ -690,7 +747,7 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
     }
   }
   double cost = 0.0;
-  Prep::SeedKeys* sk = scripted ? nullptr : &pr.seed_keys(s.seed);
+  Prep::SeedKeys* sk = (scripted || (!pr.key_base.empty() && pr.key_base[i] >= 0)) ? nullptr : &pr.seed_keys(s.seed);
   for (int k = 0; k < s.n_adapters; ++k) {
     const lt_adapter& a = ad[perm[k]];
     DAdapter x{};
@@ -703,8 +760,11 @@ void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t 
     x.deck = -1;
     if (!scripted) {
       bool inserted = false;
-      const int kidx = Prep::find_or_insert(*sk, a.adapter_id, static_cast<int32_t>(pr.keys.size()), &inserted);
-      if (inserted) {
+      const bool own = !pr.key_base.empty() && pr.key_base[i] >= 0;  // (perm is the identity then)
+      const int kidx = own ? static_cast<int>(pr.key_base[i] + k)
+                           : Prep::find_or_insert(*sk, a.adapter_id, static_cast<int32_t>(pr.keys.size()), &inserted);
+      if (own) {
+      } else if (inserted) {
         DKey k{};
         k.seed = s.seed;
         k.id = a.adapter_id;
@@ -817,7 +877,7 @@ int launch_decks(lt_plan& P, cudaStream_t st) {
 }
 
 // Full-mode deck tables: one slot per possible arrival of the deck's key.
-void size_decks(lt_plan& P, const std::vector<DKey>& keys, cudaStream_t st) {
+void size_decks(lt_plan& P, const PinnedVec<DKeyNI>& keys, cudaStream_t st) {
   if (P.h_decks.empty()) return;
   int64_t off = 0, big = 0;
   int max_small = 0;
@@ -865,7 +925,7 @@ bool pack_deferred(lt_plan& P, Prep& pr, const lt_workload_batch& b) {
         x.load_lat = (a.rank >= 0 && a.rank < 1024) ? P.cfg.lat_cache[a.rank] : load_latency(P.cfg, a.rank);
         x.length_param = -1;
         x.deck = -1;
-        x.key = pr.find_key(s.seed, a.adapter_id);
+        x.key = pr.key_base[df.i] >= 0 ? static_cast<int32_t>(pr.key_base[df.i] + k) : pr.find_key(s.seed, a.adapter_id);
         if (x.key < 0) ok = false;
         pr.adapters[df.a_off + k] = x;
         P.adapter_ids[df.a_off + k] = a.adapter_id;
@@ -900,9 +960,57 @@ bool pack_deferred(lt_plan& P, Prep& pr, const lt_workload_batch& b) {
 // and packs the scenarios. Keys of scenarios that fail later only lengthen
 // tables (each table is a prefix-stable draw sequence), never change them.
 void collect_keys(Prep& pr, const lt_workload_batch& b) {
-  for (int64_t i = 0; i < b.n_scenarios; ++i) {
+  const int64_t n = b.n_scenarios;
+  auto screened = [&](const lt_scenario& s) {
+    return s.n_requests < 0 && s.n_adapters > 0 && s.n_adapters <= kMaxAdapters && s.duration_s > 0.0;
+  };
+  // seeds used by exactly one screened scenario with strictly ascending ids
+  // and positive rates: one key per adapter, written in parallel below
+  std::unordered_map<uint64_t, int32_t> uses;
+  uses.reserve(static_cast<size_t>(n) * 2);
+  for (int64_t i = 0; i < n; ++i)
+    if (screened(b.scenarios[i])) ++uses[b.scenarios[i].seed];
+  pr.key_base.assign(n, -1);
+  int64_t base = 0;
+  for (int64_t i = 0; i < n; ++i) {
     const lt_scenario& s = b.scenarios[i];
-    if (s.n_requests >= 0 || s.n_adapters <= 0 || s.n_adapters > kMaxAdapters || s.duration_s <= 0.0) continue;
+    if (!screened(s) || uses[s.seed] != 1) continue;
+    const lt_adapter* ad = b.adapters + s.adapter_offset;
+    bool ok = ad[0].rate > 0.0;
+    for (int k = 1; k < s.n_adapters && ok; ++k) ok = ad[k - 1].adapter_id < ad[k].adapter_id && ad[k].rate > 0.0;
+    if (!ok) continue;
+    pr.key_base[i] = base;
+    base += s.n_adapters;
+  }
+  pr.keys.resize(static_cast<size_t>(base));
+  auto fill = [&](int64_t i0, int64_t i1) {
+    for (int64_t i = i0; i < i1; ++i) {
+      if (pr.key_base[i] < 0) continue;
+      const lt_scenario& s = b.scenarios[i];
+      const lt_adapter* ad = b.adapters + s.adapter_offset;
+      DKey* out = pr.keys.data() + pr.key_base[i];
+      for (int k = 0; k < s.n_adapters; ++k) {
+        DKey key{};
+        key.seed = s.seed;
+        key.id = ad[k].adapter_id;
+        key.rate_max = ad[k].rate;
+        key.dur_max = s.duration_s;
+        out[k] = key;
+      }
+    }
+  };
+  const int nt = base < 16384 ? 1 : static_cast<int>(std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency())));
+  if (nt <= 1) {
+    fill(0, n);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) th.emplace_back(fill, n * t / nt, n * (t + 1) / nt);
+    for (auto& x : th) x.join();
+  }
+  // the rest (shared seeds) deduplicated per (seed, id)
+  for (int64_t i = 0; i < n; ++i) {
+    const lt_scenario& s = b.scenarios[i];
+    if (!screened(s) || pr.key_base[i] >= 0) continue;
     const lt_adapter* ad = b.adapters + s.adapter_offset;
     Prep::SeedKeys& sk = pr.seed_keys(s.seed);
     for (int k = 0; k < s.n_adapters; ++k) {
@@ -927,7 +1035,7 @@ void collect_keys(Prep& pr, const lt_workload_batch& b) {
 }
 
 // Table capacity per key: rate_max * dur_max + 8 sigma + slack draws.
-int64_t size_keys(std::vector<DKey>& keys) {
+int64_t size_keys(PinnedVec<DKeyNI>& keys) {
   int64_t e_total = 0;
   for (DKey& k : keys) {
     const double lam = k.rate_max * k.dur_max;
@@ -960,7 +1068,12 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   using hclk = std::chrono::steady_clock;
   const auto h0 = hclk::now();
   auto hms = [&](hclk::time_point t) { return std::chrono::duration<double, std::milli>(t - h0).count(); };
-  Prep pr;
+  // (the pinned Prep buffers are rewritten below: no upload of an earlier
+  // plan may still read them)
+  LT_CUDA(cudaStreamSynchronize(ctx->stream_up));
+  static thread_local Prep t_prep;
+  Prep& pr = t_prep;
+  pr.reset();
   pr.cost.assign(P.n_scen, 0.0);
   pr.keys.reserve(b->n_adapters);
   P.adapter_ids.reserve(b->n_adapters);
@@ -978,7 +1091,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   LT_CUDA(cudaMemsetAsync(P.tab_overflow.p, 0, sizeof(int32_t), st));
   const size_t early_keys = pr.keys.size();
   if (early_keys > 0) {
-    P.keys.upload(pr.keys, st);
+    P.keys.upload(pr.keys.data(), pr.keys.size(), st);
     P.E.alloc(std::max<int64_t>(e_total, 1));
     P.Z.alloc(std::max<int64_t>(e_total, 1));
     P.h2d_bytes += pr.keys.size() * sizeof(DKey);
@@ -1025,9 +1138,9 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
       if (!P.h_scen[i].generated && P.h_scen[i].status == LT_OK) base[i] = P.h_scen[i].n_req;
     P.base_count.upload(base, su);
     if (!pr.pair_scen.empty()) {
-      P.pair_scen.upload(pr.pair_scen, su);
-      P.pair_adp.upload(pr.pair_adp, su);
-      P.pair_begin.upload(pr.pair_begin, su);
+      P.pair_scen.upload(pr.pair_scen.data(), pr.pair_scen.size(), su);
+      P.pair_adp.upload(pr.pair_adp.data(), pr.pair_adp.size(), su);
+      P.pair_begin.upload(pr.pair_begin.data(), pr.pair_begin.size(), su);
     }
     LT_CUDA(cudaEventRecord(P.ev_up, su));
   }
@@ -1048,7 +1161,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     if (relaunch) {
       P.seed_state.alloc(std::min<int64_t>(static_cast<int64_t>(pr.keys.size()), kSeedChunk) * 2 * kMtN);
       size_decks(P, pr.keys, st);
-      P.keys.upload(pr.keys, st);
+      P.keys.upload(pr.keys.data(), pr.keys.size(), st);
       LT_CUDA(cudaMemsetAsync(P.tab_overflow.p, 0, sizeof(int32_t), st));
       P.E.alloc(std::max<int64_t>(e_total, 1));
       P.Z.alloc(std::max<int64_t>(e_total, 1));
@@ -1767,7 +1880,9 @@ double lt__host_prep_ms(const lt_workload_batch* b, const lt_server_config* cfg)
   P.n_scen = b->n_scenarios;
   P.h_scen.resize(P.n_scen);
   P.errs.resize(P.n_scen);
-  Prep pr;
+  static thread_local Prep t_prep;
+  Prep& pr = t_prep;
+  pr.reset();
   pr.cost.assign(P.n_scen, 0.0);
   pr.keys.reserve(b->n_adapters);
   P.adapter_ids.reserve(b->n_adapters);
