@@ -457,3 +457,24 @@ def test_k0_relaunch_matches_early_launch(dev, monkeypatch):
                 np.testing.assert_array_equal(g1[f], g2[f], err_msg=f)
         for k in s1:
             np.testing.assert_array_equal(s1[k], s2[k], err_msg=k)
+
+
+def test_parallel_host_packing_matches_serial(dev, monkeypatch):
+    """build_plan packs plain generated scenarios on host threads (and writes
+    single-use-seed keys in parallel); the serial packing (LT_SERIAL_PREP) must
+    give identical summaries, states and messages, including batches that mix
+    failing, scripted, Full-mode and shared-seed scenarios."""
+    cases = [W.summary_cases(), W.full_mode_cases(), (W.c2_batch(duration_s=120.0, stride=4), lt.h100_like_config(1))]
+    for b, cfg in cases:
+        g1, s1 = dev.simulate_batch(b, cfg, want_states=True, want_digest=True)
+        m1 = [dev.message(i) for i in range(len(g1))]
+        monkeypatch.setenv("LT_SERIAL_PREP", "1")
+        g2, s2 = dev.simulate_batch(b, cfg, want_states=True, want_digest=True)
+        m2 = [dev.message(i) for i in range(len(g2))]
+        monkeypatch.delenv("LT_SERIAL_PREP")
+        for f in g1.dtype.names:
+            if f not in ("device_cycles", "phase_cycles"):
+                np.testing.assert_array_equal(g1[f], g2[f], err_msg=f)
+        for k in s1:
+            np.testing.assert_array_equal(s1[k], s2[k], err_msg=k)
+        assert m1 == m2
