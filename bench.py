@@ -191,7 +191,8 @@ def cpu_reference_run(sample_stride: int, duration: float, threads: int):
     wall = time.perf_counter() - t0
     iters = int(out["iterations"].sum())
     return {"value": iters / wall, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": (("the whole C2 grid" if sample_stride == 1 else f"every {sample_stride}th C2 scenario")
+            "wall_s": wall,
+            "sample": (("the whole C2 grid" if sample_stride == 1 else f"every {sample_stride}-th C2 scenario")
                        + f" ({len(out)} of 1024 scenarios), run_simulation + compute_metrics (the reference's own "
                        f"TUs, {threads} host threads), {iters} engine-iterations in {wall:.2f} s")}, out, b
 
@@ -201,17 +202,19 @@ def impl_reference(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    vals = []
+    vals, walls = [], []
     for i in range(args.warmup + args.steps):
         cb, _, _ = cpu_reference_run(args.ref_stride, args.duration, threads)
         if i >= args.warmup:
             vals.append(cb["value"])
+            walls.append(cb["wall_s"])
     v = statistics.mean(vals)
     cb["value"] = v
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "sample_stride": args.ref_stride, "duration_s": args.duration},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * statistics.mean(walls),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "sample_stride": args.ref_stride, "duration_s": args.duration,
+                       "step": "one step = the bounded sample (every sample_stride-th C2 scenario)"},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
