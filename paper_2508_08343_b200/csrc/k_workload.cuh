@@ -34,35 +34,44 @@ constexpr size_t kSeedSmem = sizeof(uint32_t) * kSeedThreads * kSeedStride;
 __device__ __forceinline__ void seed_seq_row(uint32_t* b, const uint32_t* v) {
   constexpr int n = 624, p = 306, q = 317, s = 6;
   for (int k = 0; k < n; ++k) b[k] = 0x8b8b8b8bu;
+  // Each step k reads b[k], b[k+p], b[k+q], b[k-1] and writes b[k+p],
+  // b[k+q], b[k] (indices mod n). Step k writes none of b[k+1], b[k+1+p],
+  // b[k+1+q] (q - p = 11), so the next step's three operands are loaded one
+  // step ahead and the updates need no read-modify-write.
   uint32_t prev = b[n - 1];
-  uint32_t x0 = b[0], x1 = b[p];  // operands of the next step, loaded one step ahead
+  uint32_t x0 = b[0], x1 = b[p], x2 = b[q];
   for (int k = 0; k < n; ++k) {    // m = max(s + 1, n) = n
     const int kp = (k + p < n) ? k + p : k + p - n;
     const int kq = (k + q < n) ? k + q : k + q - n;
     const uint32_t r1 = 1664525u * seedseq_T(x0 ^ x1 ^ prev);
-    const int k1 = k + 1 < n ? k + 1 : 0;  // step k+1 reads b[k+1], b[k+1+p]: not written by step k
-    x0 = b[k1];
-    x1 = b[(k1 + p < n) ? k1 + p : k1 + p - n];
     const uint32_t add = (k == 0) ? static_cast<uint32_t>(s) : (k <= s ? static_cast<uint32_t>(k) + v[k - 1]
                                                                           : static_cast<uint32_t>(k));
     const uint32_t r2 = r1 + add;
-    b[kp] += r1;
-    b[kq] += r2;
+    const uint32_t w1 = x1 + r1, w2 = x2 + r2;
+    const int k1 = k + 1 < n ? k + 1 : 0;
+    x0 = b[k1];
+    x1 = b[(k1 + p < n) ? k1 + p : k1 + p - n];
+    x2 = b[(k1 + q < n) ? k1 + q : k1 + q - n];
+    b[kp] = w1;
+    b[kq] = w2;
     b[k] = r2;
     prev = r2;
   }
   x0 = b[0];
   x1 = b[p];
+  x2 = b[q];
   for (int k = 0; k < n; ++k) {  // k + m, m = n: indices repeat modulo n
     const int kp = (k + p < n) ? k + p : k + p - n;
     const int kq = (k + q < n) ? k + q : k + q - n;
     const uint32_t r3 = 1566083941u * seedseq_T(x0 + x1 + prev);
+    const uint32_t r4 = r3 - static_cast<uint32_t>(k);
+    const uint32_t w1 = x1 ^ r3, w2 = x2 ^ r4;
     const int k1 = k + 1 < n ? k + 1 : 0;
     x0 = b[k1];
     x1 = b[(k1 + p < n) ? k1 + p : k1 + p - n];
-    const uint32_t r4 = r3 - static_cast<uint32_t>(k);
-    b[kp] ^= r3;
-    b[kq] ^= r4;
+    x2 = b[(k1 + q < n) ? k1 + q : k1 + q - n];
+    b[kp] = w1;
+    b[kq] = w2;
     b[k] = r4;
     prev = r4;
   }
