@@ -178,7 +178,12 @@ __global__ void __launch_bounds__(128) tables_draw_kernel(DKey* keys, int k0, in
   DKey key = keys[k];
   key.overflow = 0;
   const uint64_t* src = state + static_cast<size_t>(li) * (2 * kMtN);
-  for (int w = lane; w < kMtN; w += 32) st[w] = src[w];
+  // (unrolled: all of a lane's state loads in flight at once)
+#pragma unroll
+  for (int r = 0; r < (kMtN + 31) / 32; ++r) {
+    const int w = lane + 32 * r;
+    if (w < kMtN) st[w] = src[w];
+  }
   __syncwarp();
   // ---- E table (arrivals stream {1, id})
   double* Ek = E + key.e_off;
@@ -186,31 +191,43 @@ __global__ void __launch_bounds__(128) tables_draw_kernel(DKey* keys, int k0, in
   int j = 0, overflow = 0;
   for (bool done = false; !done;) {
     mt64_twist_block(st, lane);
-    for (int w = lane; w < kMtN; w += 32) {
-      const double x = -glibc_log1p<Fma>(-mt64_unit(st[w]));
-      buf[w] = x;
-      qv[w] = x / key.rate_max;
-    }
-    __syncwarp();
-    int take = kMtN, stop = 0;
-    if (lane == 0) {
-      for (int w = 0; w < kMtN; ++w) {
-        if (j + w >= key.cap) {
-          overflow = 1;
-          take = w;
-          stop = 1;
-          break;
-        }
-        t = t + qv[w];
-        if (t >= key.dur_max) {
-          take = w + 1;
-          stop = 1;
-          break;
+    // Transform only the draws the stop rule is expected to reach (the rest of
+    // the window at rate_max plus slack); the rest of the block only if the
+    // running sum has not stopped by then.
+    const double lam = (key.dur_max - __shfl_sync(0xffffffffu, t, 0)) * key.rate_max;
+    int hi = kMtN;
+    if (lam >= 0.0 && lam < static_cast<double>(kMtN)) hi = min(kMtN, static_cast<int>(lam + 4.0 * sqrt(lam) + 16.0));
+    int lo = 0, take = kMtN, stop = 0;
+    for (;;) {
+      for (int w = lo + lane; w < hi; w += 32) {
+        const double x = -glibc_log1p<Fma>(-mt64_unit(st[w]));
+        buf[w] = x;
+        qv[w] = x / key.rate_max;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        for (int w = lo; w < hi; ++w) {
+          if (j + w >= key.cap) {
+            overflow = 1;
+            take = w;
+            stop = 1;
+            break;
+          }
+          t = t + qv[w];
+          if (t >= key.dur_max) {
+            take = w + 1;
+            stop = 1;
+            break;
+          }
         }
       }
+      stop = __shfl_sync(0xffffffffu, stop, 0);
+      if (stop || hi == kMtN) break;
+      lo = hi;
+      hi = kMtN;
     }
     take = __shfl_sync(0xffffffffu, take, 0);
-    done = __shfl_sync(0xffffffffu, stop, 0) != 0;
+    done = stop != 0;
     for (int w = lane; w < take; w += 32) Ek[j + w] = buf[w];
     j += take;
     __syncwarp();
@@ -218,7 +235,11 @@ __global__ void __launch_bounds__(128) tables_draw_kernel(DKey* keys, int k0, in
   overflow = __shfl_sync(0xffffffffu, overflow, 0);
   const int n = overflow ? j : j - 1;  // arrivals strictly inside the window
   // ---- Z table (lengths stream {2, id})
-  for (int w = lane; w < kMtN; w += 32) st[w] = src[kMtN + w];
+#pragma unroll
+  for (int r = 0; r < (kMtN + 31) / 32; ++r) {
+    const int w = lane + 32 * r;
+    if (w < kMtN) st[w] = src[kMtN + w];
+  }
   __syncwarp();
   double2* Zk = Z + key.z_off;
   bool slow = false;
