@@ -9,6 +9,7 @@
 // metrics epilogue and the placement reduction run on the GPU.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
@@ -455,6 +456,10 @@ struct lt_plan {
   // sort-based merge of adapter streams
   DBuf<unsigned long long> pair_excl, sv_in, sv_out;
   DBuf<double> st_in, st_out;
+  DBuf<int32_t> pos_a, pos_b;      // radix merge: positions, sorted by time, then by scenario
+  DBuf<uint32_t> skey_a, skey_b;   // radix merge: scenario of each time-sorted position
+  size_t radix_tmp_bytes = 0;
+  int scen_bits = 1;
   DBuf<int> seg_begin, seg_end;
   DBuf<char> sort_tmp, pscan_tmp;
   size_t sort_tmp_bytes = 0, pscan_tmp_bytes = 0;
@@ -833,6 +838,15 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
   cudaEventElapsedTime(&ms, a, b);
   return ms;
+}
+
+// Arrival merge: one CUB segmented stable sort per scenario, or two global
+// radix sorts for very large batches (measured: equal or slightly slower at
+// C2's 3.6 M and C5's 9 M requests, 4 % faster at C3's 5e8-request chunks).
+// LT_MERGE=radix|segmented overrides.
+bool radix_merge(int64_t n_requests) {
+  if (const char* e = std::getenv("LT_MERGE")) return std::strcmp(e, "radix") == 0;
+  return n_requests >= 50000000;
 }
 
 // Keys seeded and drawn per chunk (the seeded states take 5 KB per key).
@@ -1247,9 +1261,24 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     LT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, P.pscan_tmp_bytes, P.adp_count.p, P.pair_excl.p,
                                           static_cast<int>(n_pairs), st));
     P.pscan_tmp.alloc(std::max<size_t>(P.pscan_tmp_bytes, 1));
-    LT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, P.sort_tmp_bytes, P.st_in.p, P.st_out.p, P.sv_in.p,
-                                                      P.sv_out.p, static_cast<int>(nr), static_cast<int>(P.n_scen),
-                                                      P.seg_begin.p, P.seg_end.p, st));
+    if (radix_merge(nr)) {
+      P.pos_a.alloc(nr);
+      P.pos_b.alloc(nr);
+      P.skey_a.alloc(nr);
+      P.skey_b.alloc(nr);
+      P.scen_bits = 1;
+      while ((int64_t(1) << P.scen_bits) < P.n_scen) ++P.scen_bits;
+      size_t b1 = 0, b2 = 0;
+      LT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, P.st_in.p, P.st_out.p, P.pos_a.p, P.pos_b.p,
+                                              static_cast<int>(nr), 0, 64, st));
+      LT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b2, P.skey_a.p, P.skey_b.p, P.pos_b.p, P.pos_a.p,
+                                              static_cast<int>(nr), 0, P.scen_bits, st));
+      P.sort_tmp_bytes = std::max(b1, b2);
+    } else {
+      LT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, P.sort_tmp_bytes, P.st_in.p, P.st_out.p, P.sv_in.p,
+                                                        P.sv_out.p, static_cast<int>(nr), static_cast<int>(P.n_scen),
+                                                        P.seg_begin.p, P.seg_end.p, st));
+    }
     P.sort_tmp.alloc(std::max<size_t>(P.sort_tmp_bytes, 1));
   }
   // scripted requests
@@ -1418,18 +1447,37 @@ void prepare_requests(lt_plan& P) {
         P.scen.p, P.pair_scen.p, P.pair_adp.p, P.n_pairs, P.pair_begin.p, P.adapters.p, P.keys.p, P.E.p,
         P.adp_count.p, P.pair_excl.p, P.st_in.p, P.sv_in.p);
     after_launch("expand_kernel", st);
-    segments_kernel<<<static_cast<unsigned>((P.n_scen + 255) / 256), 256, 0, st>>>(
-        P.scen.p, static_cast<int>(P.n_scen), P.seg_begin.p, P.seg_end.p);
-    after_launch("segments_kernel", st);
     size_t sb = P.sort_tmp_bytes;
-    LT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(P.sort_tmp.p, sb, P.st_in.p, P.st_out.p, P.sv_in.p,
-                                                      P.sv_out.p, static_cast<int>(std::max<int64_t>(P.total_req, 1)),
-                                                      static_cast<int>(P.n_scen), P.seg_begin.p, P.seg_end.p, st));
-    gather_kernel<<<static_cast<unsigned>((std::max<int64_t>(P.total_req, 1) + 255) / 256), 256, 0, st>>>(
-        P.scen.p, static_cast<int>(P.n_scen), P.total_req, P.adapters.p, P.keys.p, P.lens.p, P.Z.p, P.st_out.p,
-        P.sv_out.p, P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p, P.decks.p, P.deck_tab.p, P.full.p);
+    const int nr = static_cast<int>(std::max<int64_t>(P.total_req, 1));
+    const unsigned gr = static_cast<unsigned>((nr + 255) / 256);
+    const int32_t* perm = nullptr;
+    if (P.pos_a.p) {  // two global stable radix sorts (see scen_key_kernel)
+      iota_kernel<<<gr, 256, 0, st>>>(P.pos_a.p, nr);
+      after_launch("iota_kernel", st);
+      LT_CUDA(cub::DeviceRadixSort::SortPairs(P.sort_tmp.p, sb, P.st_in.p, P.st_out.p, P.pos_a.p, P.pos_b.p, nr, 0,
+                                              64, st));
+      scen_key_kernel<<<gr, 256, 0, st>>>(P.scen.p, static_cast<int>(P.n_scen), nr, P.pos_b.p, P.skey_a.p);
+      after_launch("scen_key_kernel", st);
+      sb = P.sort_tmp_bytes;
+      LT_CUDA(cub::DeviceRadixSort::SortPairs(P.sort_tmp.p, sb, P.skey_a.p, P.skey_b.p, P.pos_b.p, P.pos_a.p, nr, 0,
+                                              P.scen_bits, st));
+      perm = P.pos_a.p;
+      launches += 4;
+    } else {
+      segments_kernel<<<static_cast<unsigned>((P.n_scen + 255) / 256), 256, 0, st>>>(
+          P.scen.p, static_cast<int>(P.n_scen), P.seg_begin.p, P.seg_end.p);
+      after_launch("segments_kernel", st);
+      LT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(P.sort_tmp.p, sb, P.st_in.p, P.st_out.p, P.sv_in.p,
+                                                        P.sv_out.p, nr, static_cast<int>(P.n_scen), P.seg_begin.p,
+                                                        P.seg_end.p, st));
+      launches += 2;
+    }
+    gather_kernel<<<gr, 256, 0, st>>>(P.scen.p, static_cast<int>(P.n_scen), P.total_req, P.adapters.p, P.keys.p,
+                                      P.lens.p, P.Z.p, perm ? P.st_in.p : P.st_out.p, perm ? P.sv_in.p : P.sv_out.p,
+                                      P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p, P.decks.p, P.deck_tab.p, P.full.p,
+                                      perm);
     after_launch("gather_kernel", st);
-    launches += 3;  // + CUB scan and segmented sort (library kernels)
+    launches += 2;  // + CUB scan and sort (library kernels)
   }
   cudaEventRecord(P.ev[3], st);
   P.fresh = false;

@@ -449,6 +449,31 @@ __global__ void segments_kernel(const DScen* scen, int n_scen, int* seg_begin, i
   seg_end[i] = (s.generated && s.status == LT_OK) ? b + s.n_req : b;
 }
 
+// Arrival merge as two stable radix sorts over the whole batch: by time
+// (values: positions 0..n-1), then by the scenario owning each position. The
+// result is each scenario's range ordered by (time, position) -- the stable
+// sort by time within the scenario (workload.cpp:204-207), since positions
+// within a scenario are in (adapter, draw) order.
+__global__ void iota_kernel(int32_t* v, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) v[i] = static_cast<int32_t>(i);
+}
+
+__global__ void scen_key_kernel(const DScen* scen, int n_scen, int64_t n, const int32_t* pos, uint32_t* key) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= n) return;
+  const int64_t p = pos[g];
+  int lo = 0, hi = n_scen - 1;  // last scenario with req_begin <= p
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (scen[mid].req_begin <= p)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  key[g] = static_cast<uint32_t>(lo);
+}
+
 // Sorted (time, adapter, sequence) -> request arrays; lengths from the Z
 // table of the adapter's (seed, id) key (sample_lengths, workload.cpp:162-166).
 // One thread per request of the whole batch; its scenario is found by binary
@@ -459,7 +484,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const DScen* scen, int n_sc
                                                     const unsigned long long* v_sorted, double* r_arr,
                                                     int32_t* r_in, int32_t* r_out, int32_t* r_adp,
                                                     const DDeck* decks, const int32_t* deck_tab,
-                                                    const int32_t* full) {
+                                                    const int32_t* full, const int32_t* perm) {
   const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (g >= total_req) return;
   int lo = 0, hi = n_scen - 1;  // last scenario with req_begin <= g
@@ -472,11 +497,12 @@ __global__ void __launch_bounds__(256) gather_kernel(const DScen* scen, int n_sc
   }
   const DScen& sc = scen[lo];
   if (!sc.generated || sc.status != LT_OK || g >= sc.req_begin + sc.n_req) return;
-  const unsigned long long v = v_sorted[g];
+  const int64_t src = perm ? perm[g] : g;  // (perm: the radix-sorted positions)
+  const unsigned long long v = v_sorted[src];
   const int a = static_cast<int>(v >> 32);
   const int j = static_cast<int>(v & 0xffffffffULL);
   const DAdapter ad = adapters[sc.adapter_begin + a];
-  r_arr[g] = t_sorted[g];
+  r_arr[g] = t_sorted[src];
   r_adp[g] = a;
   if (ad.deck >= 0) {  // Full mode: the shuffled deck's list entry
     const int64_t q = ad.list_off + deck_tab[decks[ad.deck].table_off + j];
