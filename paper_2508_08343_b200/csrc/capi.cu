@@ -1352,7 +1352,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     if (P.engine_variant == 3 && P.warps_per_block == 8) P.warps_per_block = 12;
     const int warps = P.warps_per_block;
     // per SM, below the 227 KB opt-in limit (variant 2: two blocks per SM)
-    const size_t budget = 216 * 1024 / (P.engine_variant == 2 ? 2 : 1);
+    const size_t budget = (static_cast<size_t>(ctx->smem_optin) - 1024) / (P.engine_variant == 2 ? 2 : 1);
     // per warp: adapter tables, retire calendar, then the running-set slots
     // (int4 entry + int32 calendar link each) that fit
     const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter + 2 * kCalBuckets * sizeof(int32_t) +
