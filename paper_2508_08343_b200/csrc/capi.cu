@@ -1462,7 +1462,7 @@ void prepare_requests(lt_plan& P) {
       LT_CUDA(cub::DeviceRadixSort::SortPairs(P.sort_tmp.p, sb, P.skey_a.p, P.skey_b.p, P.pos_b.p, P.pos_a.p, nr, 0,
                                               P.scen_bits, st));
       perm = P.pos_a.p;
-      launches += 4;
+      launches += 2;  // iota, scen_key
     } else {
       segments_kernel<<<static_cast<unsigned>((P.n_scen + 255) / 256), 256, 0, st>>>(
           P.scen.p, static_cast<int>(P.n_scen), P.seg_begin.p, P.seg_end.p);
@@ -1470,14 +1470,14 @@ void prepare_requests(lt_plan& P) {
       LT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(P.sort_tmp.p, sb, P.st_in.p, P.st_out.p, P.sv_in.p,
                                                         P.sv_out.p, nr, static_cast<int>(P.n_scen), P.seg_begin.p,
                                                         P.seg_end.p, st));
-      launches += 2;
+      launches += 1;  // segments
     }
     gather_kernel<<<gr, 256, 0, st>>>(P.scen.p, static_cast<int>(P.n_scen), P.total_req, P.adapters.p, P.keys.p,
                                       P.lens.p, P.Z.p, perm ? P.st_in.p : P.st_out.p, perm ? P.sv_in.p : P.sv_out.p,
                                       P.r_arr.p, P.r_in.p, P.r_out.p, P.r_adp.p, P.decks.p, P.deck_tab.p, P.full.p,
                                       perm);
     after_launch("gather_kernel", st);
-    launches += 2;  // + CUB scan and sort (library kernels)
+    launches += 2;  // expand, gather (own kernels; CUB's scan and sorts not counted)
   }
   cudaEventRecord(P.ev[3], st);
   P.fresh = false;
