@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _abi as A
 from .batch import (ConditionBatch, PackedConfig, PackedGrid, Runner, WorkloadBatch, sim_options)
-from .types import (AdapterSpec, Condition, DatasetProgress, DatasetSpec, DeviceError, ERROR_CLASSES, FrontierPoint, LengthMode,
+from .types import (AdapterSpec, Condition, DatasetProgress, DatasetSpec, DeviceError, ERROR_CLASSES, FrontierPoint, LengthMode, LengthSpec,
                     LoratwinError, MetricsSummary, Phase, PlacementResult, Request, RequestState,
                     ServerConfig, SimOptions, SimulationResult, SweepGrid, SweepOptions, WorkloadSpec)
 
@@ -222,10 +222,55 @@ def run_scripted(requests: Sequence[Request], adapters: Sequence[AdapterSpec], d
     return result_of(out[0], states, 0)
 
 
-def compute_metrics(result: SimulationResult, workload: WorkloadSpec = None,
+def _length_means(spec: LengthSpec):
+    """(input mean, output mean) of a LengthSpec (workload.cpp:29-50, :75-89):
+    Full mode averages the list in order, Mean mode returns the given means."""
+    if spec.mode == LengthMode.Full:
+        if not spec.full_lengths:
+            return 0.0, 0.0
+        s_in = s_out = 0.0
+        for a, b in spec.full_lengths:
+            s_in += float(a)
+            s_out += float(b)
+        n = float(len(spec.full_lengths))
+        return s_in / n, s_out / n
+    return spec.mean_input, spec.mean_output
+
+
+def ideal_throughput(workload: WorkloadSpec, include_input: bool = False) -> float:
+    """metrics.cpp:36-45: Σ over adapters in spec order of rate x mean tokens."""
+    total = 0.0
+    for ad in workload.adapters:
+        mi, mo = _length_means(ad.lengths if ad.lengths is not None else workload.lengths)
+        tokens = mo + mi if include_input else mo
+        total += ad.rate * tokens
+    return total
+
+
+def compute_metrics(result: SimulationResult, workload: WorkloadSpec,
                     ideal_includes_input: bool = False) -> MetricsSummary:
-    """metrics.hpp:49-50 — computed on device in the engine epilogue (K2)."""
-    return result.metrics
+    """metrics.hpp:49-50. Throughput, TTFT and ITL come from the device epilogue
+    (K2, and the percentile pass); the ideal throughput and the starved verdict
+    depend on the caller's workload and flag (metrics.cpp:72, :108-111), so they
+    are recomputed here from `workload`, `ideal_includes_input` and the
+    result's rejected requests, exactly as the reference does."""
+    m = result.metrics
+    ideal = ideal_throughput(workload, ideal_includes_input)
+    if not result.requests and m.degenerate:
+        return MetricsSummary(ideal_throughput_tok_s=ideal, degenerate=True)
+    if not result.requests:
+        raise ValueError("compute_metrics needs the per-request states (run_simulation / run_scripted "
+                         "return them; batched summaries carry the device-computed metrics)")
+    rejected_demand = 0.0
+    for r in result.requests:  # request_id order (metrics.cpp:84-89)
+        if r.phase == Phase.Rejected:
+            rejected_demand += float(r.request.output_tokens) / result.duration_s
+    eff = max(ideal - rejected_demand, 0.0)
+    return MetricsSummary(throughput_tok_s=m.throughput_tok_s, itl_mean_s=m.itl_mean_s, itl_p50_s=m.itl_p50_s,
+                          itl_p99_s=m.itl_p99_s, ttft_mean_s=m.ttft_mean_s, ttft_p50_s=m.ttft_p50_s,
+                          ttft_p99_s=m.ttft_p99_s, ideal_throughput_tok_s=ideal,
+                          starved=m.throughput_tok_s < 0.9 * eff, finished_count=m.finished_count,
+                          rejected_count=m.rejected_count, degenerate=False)
 
 
 def generate_arrivals(workload: WorkloadSpec, mode_override: Optional[LengthMode] = None,

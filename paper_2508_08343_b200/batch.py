@@ -9,7 +9,7 @@ from typing import Callable, Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _abi as A
-from .types import (ERROR_CLASSES, Condition, LengthMode, LengthSpec, LoratwinError, ServerConfig,
+from .types import (ERROR_CLASSES, Condition, LengthMode, LengthSpec, LoratwinError, ServerConfig, UnsupportedError,
                     SweepGrid, SweepOptions, SimOptions, WorkloadSpec, Request)
 
 
@@ -175,9 +175,15 @@ def sim_options(opts: Optional[SimOptions] = None, want_digest: bool = False,
                 libm_variant: int = -1, want_percentiles: bool = False) -> A.lt_sim_options:
     o = A.lt_sim_options()
     opts = opts or SimOptions()
+    if opts.record_iteration_trace:
+        raise UnsupportedError("SimOptions.record_iteration_trace: per-iteration trace rows are not produced by "
+                               "the batched device path (the decision digest covers the same fields)")
     o.check_invariants = int(opts.check_invariants)
     o.want_digest = int(want_digest)
-    o.iteration_cap_override = int(opts.iteration_cap_override or 0)
+    # engine.cpp:75 uses value_or(cap): an override <= 1 truncates after the
+    # first iteration, like 1 (the ABI reads <= 0 as "no override").
+    ov = opts.iteration_cap_override
+    o.iteration_cap_override = 0 if ov is None else max(int(ov), 1)
     o.libm_variant = libm_variant
     o.want_percentiles = int(want_percentiles)
     return o

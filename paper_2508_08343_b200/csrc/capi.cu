@@ -1350,13 +1350,22 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
       P.engine_variant = (v == 2 || v == 3) ? v : 1;
     }
     if (P.engine_variant == 3 && P.warps_per_block == 8) P.warps_per_block = 12;
-    const int warps = P.warps_per_block;
     // per SM, below the 227 KB opt-in limit (variant 2: two blocks per SM)
-    const size_t budget = (static_cast<size_t>(ctx->smem_optin) - 1024) / (P.engine_variant == 2 ? 2 : 1);
+    size_t budget = (static_cast<size_t>(ctx->smem_optin) - 1024) / (P.engine_variant == 2 ? 2 : 1);
     // per warp: adapter tables, retire calendar, then the running-set slots
     // (int4 entry + int32 calendar link each) that fit
     const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter + 2 * kCalBuckets * sizeof(int32_t) +
                             kPqSmem * sizeof(int4);
+    // Every warp's adapter tables must fit in the block: many-adapter batches
+    // (24 B per adapter per warp) leave the occupancy variants and then drop
+    // warps per block until they do (1,024 adapters: 7 warps of 29.7 KB).
+    if (static_cast<size_t>(P.warps_per_block) * adapters > budget && P.engine_variant != 1) {
+      P.engine_variant = 1;
+      P.warps_per_block = std::min(P.warps_per_block, 8);
+      budget = static_cast<size_t>(ctx->smem_optin) - 1024;
+    }
+    while (P.warps_per_block > 1 && static_cast<size_t>(P.warps_per_block) * adapters > budget) --P.warps_per_block;
+    const int warps = P.warps_per_block;
     const size_t per_slot = sizeof(int4) + sizeof(int2);
     const size_t per_warp_max = budget / warps;
     int64_t cap = per_warp_max > adapters ? static_cast<int64_t>((per_warp_max - adapters) / per_slot) : 0;
