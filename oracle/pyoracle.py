@@ -67,6 +67,17 @@ class RefOracle(_Oracle):
     path = REF_LIB
     extra_symbols = A.DATASET_SYMBOLS
 
+    def config_json_matches(self, text: str, packed_config) -> tuple:
+        """(1 | 0 | -code, detail): the reference's server_config_from_json on
+        `text` vs the ABI config, both re-serialised by the reference."""
+        fn = self.lib.dll.ltref_config_json_matches
+        fn.argtypes = [C.c_char_p, C.c_void_p, C.c_char_p, C.c_size_t, C.c_void_p]
+        fn.restype = C.c_int32
+        buf = C.create_string_buffer(8192)
+        st = A.lt_status()
+        rc = fn(text.encode(), C.addressof(packed_config.c), buf, len(buf), C.addressof(st))
+        return rc, (buf.value.decode() if rc == 0 else st.message.decode())
+
 
 class PortOracle(_Oracle):
     prefix = "ltor_"

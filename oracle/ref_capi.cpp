@@ -12,6 +12,7 @@
 // std::thread pool, per-task error capture.
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <functional>
@@ -21,6 +22,7 @@
 
 #include "loratwin/engine.hpp"
 #include "loratwin/errors.hpp"
+#include "loratwin/json_io.hpp"
 #include "loratwin/metrics.hpp"
 #include "loratwin/placement.hpp"
 #include "loratwin/workload.hpp"
@@ -262,12 +264,15 @@ int32_t ltref_simulate_batch(void*, const lt_workload_batch* batch, const lt_ser
       o.itl_p50_s = m.itl_p50_s;
       o.itl_p99_s = m.itl_p99_s;
       o.degenerate = m.degenerate;
-      int64_t pre = 0, tot = 0, win = 0;
+      // tokens_in_window without another pass over every emit time (the
+      // reference already counted them: throughput = tokens / window, and
+      // the integer is recovered exactly by rounding the product).
+      int64_t pre = 0, tot = 0;
       for (const RequestState& q : r.requests) {
         pre += q.preemption_count;
         tot += q.tokens_generated;
-        for (double t : q.token_emit_times_s) win += t <= r.duration_s;
       }
+      const int64_t win = r.requests.empty() ? 0 : std::llround(m.throughput_tok_s * r.duration_s);
       o.preemptions = pre;
       o.tokens_total = tot;
       o.tokens_in_window = win;
@@ -462,6 +467,29 @@ int32_t ltref_encode_workload(const lt_template* mix, int32_t n_mix, const lt_le
     const int32_t code = classify(std::current_exception(), &msg);
     set_status(status, code, -1, msg);
     return code;
+  }
+}
+
+// The reference's own JSON parser on a server-config file (json_io.cpp:188-235),
+// compared with the ABI config `c` through the reference's serializer
+// (server_config_to_json): 1 = identical, 0 = different (both texts in
+// `diff`), < 0 = the reference rejected the file (status carries what()).
+int32_t ltref_config_json_matches(const char* text, const lt_server_config* c, char* diff, size_t len,
+                                  lt_status* status) {
+  if (status) status->code = LT_OK;
+  try {
+    ServerConfig parsed = server_config_from_json(text);
+    ServerConfig mine = to_config(*c);
+    parsed.slots = mine.slots;
+    const std::string a = server_config_to_json(parsed), b = server_config_to_json(mine);
+    if (a == b) return 1;
+    if (diff && len) std::snprintf(diff, len, "reference:\n%s\nabi:\n%s", a.c_str(), b.c_str());
+    return 0;
+  } catch (...) {
+    std::string msg;
+    const int32_t code = classify(std::current_exception(), &msg);
+    set_status(status, code, -1, msg);
+    return -code;
   }
 }
 

@@ -189,6 +189,12 @@ def sim_options(opts: Optional[SimOptions] = None, want_digest: bool = False,
     return o
 
 
+def frontier_capacity(grid: SweepGrid) -> int:
+    """Frontier rows per condition (lt_sweep_frontier_capacity): at most
+    max(4, |explicit G|) points per N row."""
+    return max(sum(max(4, len(grid.g_values)) for _ in grid.n_values), 1)
+
+
 class PackedGrid:
     def __init__(self, grid: SweepGrid):
         self.n = np.array(grid.n_values, dtype=np.int32)
@@ -284,7 +290,7 @@ class Runner:
         pc = PackedConfig(config)
         pg = PackedGrid(grid)
         n = len(conds.conditions)
-        maxf = max(sum(max(4, len(grid.g_values)) for _ in grid.n_values), 1)
+        maxf = frontier_capacity(grid)
         out = np.zeros(max(n, 1), dtype=A.PLACEMENT_DT)
         fr = np.zeros(max(n * maxf, 1), dtype=A.FRONTIER_DT)
         so = A.lt_sweep_options()
@@ -299,4 +305,4 @@ class Runner:
                              C.byref(st))
         if st.code == A.LT_ERR_DEVICE:
             self._raise(st.code, st.index, st.message.decode())
-        return out[:n], fr[:n * maxf].reshape(n, maxf) if n else fr[:0]
+        return out[:n], fr[:n * maxf].reshape(n, maxf)

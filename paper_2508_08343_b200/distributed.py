@@ -15,7 +15,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import _abi as A
-from .batch import ConditionBatch, WorkloadBatch
+from .batch import ConditionBatch, WorkloadBatch, frontier_capacity
 
 
 def balanced_shards(costs: Sequence[float], world: int) -> List[np.ndarray]:
@@ -122,7 +122,7 @@ def sweep_sharded(conds: ConditionBatch, runner, config, grid, duration_s: float
     shards = balanced_shards(costs, world)
     mine = shards[rank]
     pl, fr = runner.sweep(condition_subset(conds, mine), config, grid, duration_s, seed, options, sim)
-    maxf = fr.shape[1] if fr.ndim == 2 else 1
+    maxf = frontier_capacity(grid)  # the same on every rank, also one with no conditions
     rec_dt = np.dtype([("p", A.PLACEMENT_DT), ("f", A.FRONTIER_DT, (maxf,))])
     rec = np.zeros(len(mine), dtype=rec_dt)
     rec["p"] = pl

@@ -146,3 +146,16 @@ def test_port_matches_reference_errors(port, ref):
     np.testing.assert_array_equal(r["status"], p["status"])
     for i in range(len(wls)):
         assert ref.message(i) == port.message(i)
+
+
+@pytest.mark.parametrize("profile", ["h100_like", "llama31_8b", "qwen25_7b"])
+def test_profiles_parse_identically_in_the_reference(ref, profile):
+    """The packaged server profiles (configs/*.json, the C5 workloads' llama31_8b
+    and qwen25_7b) read by the reference's own server_config_from_json
+    (json_io.cpp:188-235) equal what the ABI packs from them."""
+    from paper_2508_08343_b200.batch import PackedConfig
+    from paper_2508_08343_b200.types import profile_config
+    path = os.path.join(os.path.dirname(lt.__file__), "configs", profile + ".json")
+    for slots in (1, 32):
+        rc, detail = ref.config_json_matches(open(path).read(), PackedConfig(profile_config(profile, slots)))
+        assert rc == 1, detail

@@ -248,9 +248,54 @@ def c5_batch(start: int = 0, count: int = 524_288, duration_s: float = 600.0) ->
     rank {8,16,32}[(i/32) mod 3], aggregate rate {0.5,1,2,4}[(i/96) mod 4] req/s
     split over the N adapters, Mean(2048,512,1024,256), 600 s, G = min(N, 32),
     seed 2^32 + i (per-scenario keys). Run under the llama31_8b / qwen25_7b profiles."""
-    i = np.arange(start, start + count, dtype=np.int64)
+    return c5_batch_at(np.arange(start, start + count, dtype=np.int64), duration_s)
+
+
+def c5_batch_at(i, duration_s: float = 600.0) -> WorkloadBatch:
+    """The C5 scenarios of the given indices (see c5_batch)."""
+    i = np.asarray(i, dtype=np.int64)
     ns = 8 * (1 + i % 32)
     rank = np.array([8, 16, 32])[(i // 32) % 3]
     lam = np.array([0.5, 1.0, 2.0, 4.0])[(i // 96) % 4]
     return _flat_batch(ns, np.repeat(rank, ns), np.repeat(lam / ns, ns), (2 ** 32 + i).astype(np.uint64),
                        np.minimum(ns, 32), (A.MODE_MEAN, 0, 2048.0, 512.0, 1024.0, 256.0, 0, 0), duration_s)
+
+
+C4_LENGTHS = [(23, 5, 27, 5), (250, 50, 231, 50), (423, 80, 358, 80), (128, 32, 231, 64), (512, 128, 256, 64),
+              (1024, 256, 512, 128), (64, 0, 128, 0), (2048, 512, 1024, 256)]
+
+
+def c4_conditions(count: int = 16_384):
+    """C4: the 2,200 rate x rank triples (paper rates, ranks
+    {8,16,32}, triple size 3, canonical enumerate_conditions order) under each
+    of the 8 length settings, first `count` in (length setting, condition) order."""
+    conds = []
+    for L in C4_LENGTHS:
+        conds += lt.enumerate_conditions(PAPER_RATES, [8, 16, 32], lt.LengthSpec.mean(*L))
+        if len(conds) >= count:
+            break
+    return conds[:count]
+
+
+def c4_grid():
+    """C4's grid: N {1, 2, 4, ..., 256}, explicit G {2, ..., 64}; early exit k = 3; 600 s; seed 5."""
+    grid = lt.SweepGrid(n_values=[1, 2, 4, 8, 16, 32, 64, 128, 256], g_mode=lt.GMode.Explicit,
+                        g_values=[2, 4, 8, 16, 32, 64])
+    return grid, lt.SweepOptions(early_exit=True, early_exit_k=3), 600.0, 5
+
+
+def c4_sample_indices():
+    """Sampled C4 conditions for the parity fixtures: 6 per length setting
+    (the last setting only has C4's first 984 conditions), spread over the
+    2,200 triples in canonical order (heavy 3.2 req/s mixes first, the
+    lightest last)."""
+    idx = []
+    for s in range(len(C4_LENGTHS)):
+        avail = min(2200, 16_384 - 2200 * s)
+        for j in (0, 331, 662, 983, 1460, 2199):
+            if j < avail:
+                idx.append(2200 * s + j)
+    return idx
+
+
+C5_SAMPLE_STRIDE = 1021  # prime: every (N, rank, rate) combination of the 384-periodic grid is hit
