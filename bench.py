@@ -1,29 +1,45 @@
 #!/usr/bin/env python
 """Benchmark of the batched Digital-Twin sweep (BASELINE.json metric:
-simulated engine-iterations/sec, + placement sweeps/sec) on B200.
+simulated engine-iterations/sec + placement sweeps/sec) on B200.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gpu|reference]
+                  [--workload c2|c3|c4|c5]
 
-Workload (BASELINE configs[1], SURVEY 8d "C2"): 1,024 scenarios = N in
-{8..256 step 8} x rank mode {8,16,32,mixed} x r in {3.2..0.0125}; per-adapter
-rate 8r/N; Mean(250,80,231,80) lengths; 600 s simulated; G = min(N,32); seed
-1234+i; h100_like server. Synthetic (the reference's own generator, on device).
+Workloads (synthetic, built by the reference's own generator on
+device):
+  c2 (default, BASELINE configs[1]) 1,024 scenarios: N in {8..256 step 8} x
+     rank {8,16,32,mixed} x r {3.2..0.0125}; per-adapter rate 8r/N;
+     Mean(250,80,231,80); 600 s; G = min(N,32); seed 1234+i; h100_like.
+  c3 65,536 scenarios: 2,048 rate x rank conditions x N {3..96}; G = min(N,16);
+     shared seed 7.
+  c5 1,048,576 scenarios: 524,288 per profile (llama31_8b, qwen25_7b);
+     N = 8(1 + i mod 32), long I/O Mean(2048,512,1024,256); seed 2^32 + i.
+  c4 16,384 full placement searches (2,200 rate x rank triples x 8 length
+     settings; N {1..256}, explicit G {2..64}, early exit k=3, 600 s, seed 5);
+     metric: placement sweeps/sec.
 
-A step = the whole device pipeline over the batch with inputs resident in HBM:
-K0 RNG tables -> arrival counts -> device scan -> merge -> engine (K1) +
-metrics epilogue (K2). `e2e` = the same metric through the public C-ABI call
-lt_simulate_batch with pinned host buffers (H2D + everything + D2H).
-For N>1 (torchrun, one rank per GPU, NCCL) each rank runs its own replica of
-the grid (seeds shifted by 1024*rank: weak scaling) and the per-scenario
-summaries are all-gathered over NCCL inside the timed step (the path's one
-exchange).
+A step is one pass of the hot path over the whole workload with its inputs
+resident in HBM: K0 RNG tables -> arrival counts -> merge -> engine (K1) +
+metrics epilogue (K2), one plan per <= 65,536 scenarios (c3/c5 plans release
+their regenerated buffers for the next: lt_plan_trim). `e2e` is the same
+metric through the public C-ABI call (lt_simulate_batch / lt_sweep_batch)
+from pinned host buffers, host<->device copies inside.
+
+Multi-GPU (one process per GPU, NCCL; `--gpus N` self-launches torchrun when
+WORLD_SIZE is unset and refuses to run on fewer GPUs): c2 is weak scaling
+(each rank runs its own 1,024-scenario grid, seeds shifted by 1024*rank);
+c3/c4/c5 are strong scaling (the fixed scenario / condition set is sharded
+by estimated cost, LPT). The fixed-size result records are all-gathered over
+NCCL inside the timed step (the path's one exchange).
+
 `--impl reference` times the reference's own CPU implementation
-(oracle/_ref: the unmodified reference TUs) over a bounded sample of the same
-grid on all host cores.
+(oracle/_ref: the unmodified reference TUs) on all host cores over the same
+workload's reference sample (c2: the whole grid).
 """
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import statistics
@@ -39,8 +55,20 @@ import numpy as np  # noqa: E402
 
 METRIC = "simulated engine-iterations/sec + placement sweeps/sec at 1/2/4/8 B200 vs host CPU"
 UNIT = "engine-iterations/s"
-WORKLOAD = ("C2: 1,024-scenario grid, N=8..256 step 8 x rank {8,16,32,mixed} x r {3.2..0.0125}, "
-            "per-adapter rate 8r/N, Mean(250,80,231,80), 600 s simulated, G=min(N,32), seed 1234+i, h100_like")
+SWEEP_UNIT = "conditions/s"
+SM_COUNT = 148
+PLAN_SCENARIOS = 65_536  # scenarios per device-resident plan (c3/c5)
+
+WORKLOADS = {
+    "c2": "C2: 1,024-scenario grid, N=8..256 step 8 x rank {8,16,32,mixed} x r {3.2..0.0125}, per-adapter rate "
+          "8r/N, Mean(250,80,231,80), 600 s simulated, G=min(N,32), seed 1234+i, h100_like",
+    "c3": "C3: 65,536 scenarios = first 2,048 enumerate_conditions(paper rates x ranks {8,16,32}, triple 3) x "
+          "N {3,6..96}, G=min(N,16), Mean(250,80,231,80), 600 s, shared seed 7, h100_like",
+    "c5": "C5: 1,048,576 scenarios = 524,288 per profile (llama31_8b, qwen25_7b), N=8(1+i mod 32), rank "
+          "{8,16,32}, aggregate {0.5,1,2,4} req/s, Mean(2048,512,1024,256), 600 s, G=min(N,32), seed 2^32+i",
+    "c4": "C4: 16,384 placement searches = 2,200 rate x rank triples x 8 length settings (first 16,384), "
+          "N {1..256 x2}, explicit G {2..64}, early exit k=3, 600 s, seed 5, h100_like",
+}
 
 
 def log(*a):
@@ -124,40 +152,174 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm), "source": self.source}
 
 
-def measured_peaks():
-    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
-        if os.path.exists(p):
-            with open(p) as f:
-                d = json.load(f)
-            return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+def measured_hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram bytes per engine launch from the latest committed ncu --set full
-    summary (profiles/r<NN>_engine_ncu.json), if present."""
-    import glob
-
-    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_engine_ncu.json")))
+def ncu_engine_profile(workload: str):
+    """The committed ncu --set full summary of one engine launch of this
+    workload (profiles/r<NN>_engine_ncu_<workload>.json, newest round), which
+    holds the launch's warp-instruction count, engine-iterations and DRAM bytes."""
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_engine_ncu_{workload}.json")))
     if not paths:
-        return None, None
+        return None
     with open(paths[-1]) as f:
         d = json.load(f)
-    m = d.get("metrics", {})
-    brief = {"file": os.path.relpath(paths[-1], ROOT), "workload": d.get("workload"),
-             "kernel_ms": m.get("gpu__time_duration.sum", [None])[0],
-             "issue_active_pct_of_peak": m.get("smsp__issue_active.avg.pct_of_peak_sustained_active", [None])[0],
-             "warp_latency_per_inst": m.get("smsp__average_warp_latency_per_inst_issued.ratio", [None])[0]}
-    return d.get("dram_bytes_per_launch"), brief
+    d["file"] = os.path.relpath(paths[-1], ROOT)
+    return d
 
 
-def c2_batch_for_rank(rank: int, duration: float, stride: int = 1):
+# --- workloads ---------------------------------------------------------------------------------
+
+def sim_parts(workload: str, rank: int = 0):
+    """[(label, WorkloadBatch, ServerConfig)] of a simulate workload."""
+    import paper_2508_08343_b200 as lt
+    from paper_2508_08343_b200.types import profile_config
     from tests import workloads as W
 
-    b = W.c2_batch(duration_s=duration, stride=stride)
-    b.scenarios["seed"] = b.scenarios["seed"] + np.uint64(1024 * rank)
-    return b
+    if workload == "c2":
+        b = W.c2_batch(600.0)
+        b.scenarios["seed"] = b.scenarios["seed"] + np.uint64(1024 * rank)
+        return [("c2", b, lt.h100_like_config(1))]
+    if workload == "c3":
+        return [("c3", W.c3_batch(), lt.h100_like_config(1))]
+    if workload == "c5":
+        b = W.c5_batch(0, 524_288)
+        return [("c5 llama31_8b", b, profile_config("llama31_8b", 1)), ("c5 qwen25_7b", b, profile_config("qwen25_7b", 1))]
+    raise ValueError(workload)
 
+
+def reference_sample(workload: str):
+    """The bounded CPU sample of a workload (the reference arm's step and the
+    GPU arm's cpu_baseline): (parts, description)."""
+    import paper_2508_08343_b200.distributed as D
+    from tests import workloads as W
+
+    if workload == "c2":
+        return sim_parts("c2"), "the whole C2 grid (1,024 scenarios)"
+    if workload == "c3":
+        (lab, b, cfg), = sim_parts("c3")
+        idx = np.arange(0, len(b.scenarios), 61)
+        return [(lab, D.subset(b, idx), cfg)], f"every 61st C3 scenario ({len(idx)} of 65,536)"
+    if workload == "c5":
+        from paper_2508_08343_b200.types import profile_config
+        idx = np.arange(0, 524_288, 1024)
+        out = [(f"c5 {p}", W.c5_batch_at(idx), profile_config(p, 1)) for p in ("llama31_8b", "qwen25_7b")]
+        return out, f"every 1024th C5 scenario per profile ({2 * len(idx)} of 1,048,576)"
+    if workload == "c4":
+        conds = W.c4_conditions()
+        idx = [2200 * s + 983 for s in range(8)]
+        return [conds[i] for i in idx], "8 C4 conditions (the 984th triple of each length setting, of 16,384)"
+    raise ValueError(workload)
+
+
+def sweep_workload():
+    import paper_2508_08343_b200 as lt
+    from tests import workloads as W
+
+    grid, opts, dur, seed = W.c4_grid()
+    return W.c4_conditions(), lt.h100_like_config(1), grid, opts, dur, seed
+
+
+def shard(workload: str, parts, rank: int, world: int):
+    """This rank's share: c2 replicas (weak), else a cost-balanced shard of
+    every part (strong; the same deterministic split on every rank)."""
+    import paper_2508_08343_b200.distributed as D
+
+    if world == 1 or workload == "c2":
+        return parts
+    out = []
+    for lab, b, cfg in parts:
+        mine = D.balanced_shards(D.scenario_costs(b), world)[rank]
+        out.append((lab, D.subset(b, mine), cfg))
+    return out
+
+
+def chunks(batch, max_scenarios: int = PLAN_SCENARIOS, max_requests: float = 2.5e8):
+    """Consecutive scenario ranges of at most `max_scenarios` scenarios and
+    `max_requests` expected requests (Σ rate x duration) each: one plan each."""
+    import paper_2508_08343_b200.distributed as D
+
+    sc, ad = batch.scenarios, batch.adapters
+    rate_cum = np.concatenate([[0.0], np.cumsum(ad["rate"])])
+    lo, hi = sc["adapter_offset"], sc["adapter_offset"] + sc["n_adapters"]
+    req = (rate_cum[hi] - rate_cum[lo]) * sc["duration_s"]
+    cuts, acc, cnt = [0], 0.0, 0
+    for i, r in enumerate(req):
+        if cnt and (cnt >= max_scenarios or acc + r > max_requests):
+            cuts.append(i)
+            acc, cnt = 0.0, 0
+        acc += r
+        cnt += 1
+    cuts.append(len(sc))
+    if len(cuts) == 2:
+        return [batch]
+    return [D.subset(batch, np.arange(a, b)) for a, b in zip(cuts[:-1], cuts[1:])]
+
+
+# --- reference arm -----------------------------------------------------------------------------
+
+def run_reference(workload: str, threads: int):
+    """The reference's own TUs (oracle/_ref) over the workload's bounded
+    sample: run_simulation + compute_metrics (or sweep_optimal for c4) on
+    `threads` host threads. Returns (cpu_baseline dict, outputs)."""
+    import paper_2508_08343_b200 as lt  # noqa: F401
+    from oracle import pyoracle
+    from paper_2508_08343_b200.batch import ConditionBatch, sim_options
+
+    kind = "reference" if pyoracle.available("ref") else "port"
+    orc = pyoracle.RefOracle(threads=threads) if kind == "reference" else pyoracle.PortOracle(threads=threads)
+    sample, desc = reference_sample(workload)
+    if workload == "c4":
+        _, cfg, grid, opts, dur, seed = sweep_workload()
+        t0 = time.perf_counter()
+        pl, fr = orc.sweep(ConditionBatch.from_conditions(sample), cfg, grid, dur, seed, opts, sim_options())
+        wall = time.perf_counter() - t0
+        return {"value": len(sample) / wall, "unit": SWEEP_UNIT, "cores": threads, "kind": kind, "wall_s": wall,
+                "sample": f"{desc}: sweep_optimal (the reference's own TUs, {threads} host threads)"}, [(pl, fr)]
+    outs, iters, wall = [], 0, 0.0
+    for lab, b, cfg in sample:
+        t0 = time.perf_counter()
+        out, _ = orc.simulate(b, cfg, sim_options())
+        wall += time.perf_counter() - t0
+        iters += int(out["iterations"].sum())
+        outs.append(out)
+    return {"value": iters / wall, "unit": UNIT, "cores": threads, "kind": kind, "wall_s": wall,
+            "sample": f"{desc}: run_simulation + compute_metrics (the reference's own TUs, {threads} host "
+                      f"threads), {iters} engine-iterations in {wall:.2f} s"}, outs
+
+
+def impl_reference(args):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    vals, walls = [], []
+    for i in range(args.warmup + args.steps):
+        cb, _ = run_reference(args.workload, threads)
+        log(f"[{time.strftime('%X')}] reference step {i}: {cb['value']:.4g} {cb['unit']} ({cb['wall_s']:.1f} s)")
+        if i >= args.warmup:
+            vals.append(cb["value"])
+            walls.append(cb["wall_s"])
+    v = statistics.mean(vals)
+    cb["value"] = v
+    _, desc = reference_sample(args.workload)
+    line = {"metric": METRIC, "value": v, "unit": cb["unit"], "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * statistics.mean(walls),
+            "higher_is_better": True, "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.workload], "sample": desc,
+                       "same_config": args.workload == "c2",
+                       "step": "one step = the reference sample, on all host cores (rank 0 only)"},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": cb["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --- GPU arm -------------------------------------------------------------------------------------
 
 def pinned_copy(batch):
     """The batch's arrays copied into page-locked host memory (for e2e H2D)."""
@@ -177,70 +339,71 @@ def pinned_copy(batch):
     return pb, pin.keep
 
 
-def cpu_reference_run(sample_stride: int, duration: float, threads: int):
-    """The reference's own CPU implementation over a bounded sample."""
-    import paper_2508_08343_b200 as lt
-    from oracle import pyoracle
-    from paper_2508_08343_b200.batch import sim_options
+def device_view(ptr: int, nbytes: int, local: int):
+    import torch
 
-    kind = "reference" if pyoracle.available("ref") else "port"
-    orc = pyoracle.RefOracle(threads=threads) if kind == "reference" else pyoracle.PortOracle(threads=threads)
-    b = c2_batch_for_rank(0, duration, stride=sample_stride)
-    t0 = time.perf_counter()
-    out, _ = orc.simulate(b, lt.h100_like_config(1), sim_options())
-    wall = time.perf_counter() - t0
-    iters = int(out["iterations"].sum())
-    return {"value": iters / wall, "unit": UNIT, "cores": threads, "kind": kind,
-            "wall_s": wall,
-            "sample": (("the whole C2 grid" if sample_stride == 1 else f"every {sample_stride}-th C2 scenario")
-                       + f" ({len(out)} of 1024 scenarios), run_simulation + compute_metrics (the reference's own "
-                       f"TUs, {threads} host threads), {iters} engine-iterations in {wall:.2f} s")}, out, b
+    class _View:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+    return torch.as_tensor(_View(), device=f"cuda:{local}")
 
 
-def impl_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
-    threads = os.cpu_count() or 1
-    vals, walls = [], []
-    for i in range(args.warmup + args.steps):
-        cb, _, _ = cpu_reference_run(args.ref_stride, args.duration, threads)
-        if i >= args.warmup:
-            vals.append(cb["value"])
-            walls.append(cb["wall_s"])
-    v = statistics.mean(vals)
-    cb["value"] = v
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * statistics.mean(walls),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "sample_stride": args.ref_stride, "duration_s": args.duration,
-                       "step": "one step = the bounded sample (every sample_stride-th C2 scenario)"},
-            "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-    return 0
+def parity_against(cpu_outs, dev, workload: str, sample_parts):
+    """GPU results on the reference sample vs the reference's outputs."""
+    fields = ["status", "iterations", "finished_count", "rejected_count", "preemptions", "load_events",
+              "tokens_in_window", "starved", "final_clock_s", "throughput_tok_s", "ttft_mean_s"]
+    mism, n = 0, 0
+    for (lab, b, cfg), ref_out in zip(sample_parts, cpu_outs):
+        g, _ = dev.simulate_batch(b, cfg)
+        mism += sum(int(np.sum(g[f] != ref_out[f])) for f in fields)
+        n += len(g)
+    return {"scenarios": n, "fields": fields, "mismatches": mism}
 
 
-def sweep_secondary(dev, n_cond: int):
-    """placement sweeps/sec on a C4-shaped sample (explicit G, early exit k=3, 600 s, seed 5)."""
-    import paper_2508_08343_b200 as lt
-    from paper_2508_08343_b200.batch import ConditionBatch
-    from tests import workloads as W
-
-    conds = lt.enumerate_conditions(W.PAPER_RATES, [8, 16, 32], lt.LengthSpec.mean(250, 50, 231, 50))
-    conds = conds[::max(1, len(conds) // n_cond)][:n_cond]
-    grid = lt.SweepGrid(n_values=[1, 2, 4, 8, 16, 32, 64, 128, 256], g_mode=lt.GMode.Explicit,
-                        g_values=[2, 4, 8, 16, 32, 64])
-    cb = ConditionBatch.from_conditions(conds)
-    cfg = lt.h100_like_config(1)
-    opts = lt.SweepOptions(early_exit=True, early_exit_k=3)
-    dev.sweep_batch(cb, cfg, grid, 600.0, 5, opts)  # warm
-    t0 = time.perf_counter()
-    pl, _ = dev.sweep_batch(cb, cfg, grid, 600.0, 5, opts)
-    wall = time.perf_counter() - t0
-    return {"metric": "placement sweeps/sec", "value": len(conds) / wall, "unit": "conditions/s",
-            "conditions": len(conds), "grid": "N {1..256 x2}, explicit G {2..64}, early exit k=3, 600 s, seed 5",
-            "points_simulated": int(pl["points_simulated"].sum()), "wall_s": wall,
-            "note": "end to end through lt_sweep_batch (host buffers)"}
+def issue_roofline(prof, iters_step: int, engine_ms: float, sm_mhz, algo_bytes: float, hbm_peak, hbm_src,
+                   longest_cycles: int, launches_engine: int):
+    """Binding roofline of the engine kernel: issue slots. achieved = warp
+    instructions per engine-iteration (ncu, same workload and build) x this
+    step's iterations / the live engine time; peak = 148 SMs x 4 schedulers x
+    1 warp-instruction per cycle at the sampled SM clock. HBM is reported
+    beside it (SURVEY 8d algorithmic bytes vs the measured peak, and ncu's
+    DRAM bytes)."""
+    clk = (sm_mhz or 1965.0) * 1e6
+    peak = SM_COUNT * 4 * clk
+    r = {"bound": "issue", "unit": "warp-inst/s", "peak": peak, "kernel": "engine_kernel", "achieved": None,
+         "frac": None, "traffic": None, "engine_ms_per_step": engine_ms, "engine_launches_per_step": launches_engine,
+         "peak_note": "148 SMs x 4 SMSPs x 1 issue/cycle at the median sampled SM clock"}
+    if prof:
+        m = prof.get("metrics", {})
+        inst = m.get("smsp__inst_executed.sum", [None])[0]
+        its = prof.get("engine_iterations")
+        if inst and its:
+            per_iter = inst / its
+            r["achieved"] = per_iter * iters_step / (engine_ms / 1e3)
+            r["frac"] = r["achieved"] / peak
+            r["inst_per_iteration"] = per_iter
+        r["traffic"] = prof.get("dram_bytes_per_launch")
+        r["ncu"] = {"file": prof["file"], "workload": prof.get("workload"),
+                    "launch_ms": m.get("gpu__time_duration.sum", [None])[0],
+                    "launch_engine_iterations": its, "launch_warp_instructions": inst,
+                    "issue_active_pct_of_elapsed": m.get("sm__issue_active.avg.pct_of_peak_sustained_elapsed", [None])[0],
+                    "smsp_issue_active_pct_while_resident": m.get("smsp__issue_active.avg.pct_of_peak_sustained_active",
+                                                                  [None])[0],
+                    "warps_active_pct": m.get("sm__warps_active.avg.pct_of_peak_sustained_active", [None])[0],
+                    "cycles_per_issue": m.get("smsp__average_warp_latency_per_inst_issued.ratio", [None])[0]}
+    ach = algo_bytes / (engine_ms / 1e3) / 1e9
+    r["hbm"] = {"achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "peak_source": hbm_src,
+                "algorithmic_bytes_per_step": algo_bytes,
+                "note": "B_iter = 20R+16V+24A+16M+64 per engine-iteration (SURVEY 8d); the event-driven engine never "
+                        "moves these bytes (see traffic)"}
+    if r["traffic"] and launches_engine == 1:
+        r["hbm"]["measured_dram_gbs"] = r["traffic"] / (engine_ms / 1e3) / 1e9
+    # critical path: the longest single engine (one warp, dependent decisions)
+    longest_ms = longest_cycles / clk * 1e3
+    r["critical_path"] = {"longest_engine_ms": longest_ms, "engine_ms": engine_ms,
+                          "ratio": longest_ms / engine_ms if engine_ms else None,
+                          "note": "max over engines of device_cycles / SM clock vs the engine kernel time per "
+                                  "step: ~1 means the step is one engine's latency, not throughput"}
+    return r
 
 
 def impl_gpu(args):
@@ -249,6 +412,8 @@ def impl_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -257,49 +422,66 @@ def impl_gpu(args):
     import paper_2508_08343_b200 as lt
 
     dev = lt.device(local)
-    cfg = lt.h100_like_config(1)
-    batch = c2_batch_for_rank(rank, args.duration)
-    n_scen = len(batch.scenarios)
+    if args.workload == "c4":
+        return impl_gpu_sweeps(args, dev, dist, world, rank, local)
+    parts = shard(args.workload, sim_parts(args.workload, rank), rank, world)
 
-    # CPU baseline (rank 0, N=1 only), bounded sample; its results also spot-check parity.
-    cpu = None
-    parity = None
+    # CPU baseline (rank 0, N=1 only), bounded sample; its results also check parity.
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu, ref_out, ref_b = cpu_reference_run(args.cpu_stride, args.duration, os.cpu_count() or 1)
-        g, _ = dev.simulate_batch(ref_b, cfg)
-        fields = ["status", "iterations", "finished_count", "rejected_count", "preemptions", "load_events",
-                  "tokens_in_window", "starved", "final_clock_s", "throughput_tok_s", "ttft_mean_s"]
-        mism = sum(int(np.sum(g[f] != ref_out[f])) for f in fields)
-        parity = {"scenarios": int(len(g)), "fields": fields, "mismatches": mism, "oracle": cpu["kind"]}
+        cpu, cpu_outs = run_reference(args.workload, os.cpu_count() or 1)
+        sample_parts, _ = reference_sample(args.workload)
+        parity = parity_against(cpu_outs, dev, args.workload, sample_parts)
+        parity["oracle"] = cpu["kind"]
         log("cpu baseline", cpu, "parity", parity)
 
-    log(f"[{time.strftime('%X')}] building plan ({n_scen} scenarios)")
-    plan = dev.plan(batch, cfg)
+    log(f"[{time.strftime('%X')}] building plans")
+    plans = []
+    for lab, b, cfg in parts:
+        for c in chunks(b):
+            p = dev.plan(c, cfg)
+            if args.workload != "c2":
+                p.trim()
+            plans.append(p)
+    n_scen = sum(p.n for p in plans)
+    multi = len(plans) > 1
     stream = torch.cuda.ExternalStream(dev.stream(), device=torch.device("cuda", local))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
-    gathered = None
-    if world > 1:
-        ptr, nbytes = plan.device_summaries()
-
-        class _View:
-            __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
-        mine = torch.as_tensor(_View(), device=f"cuda:{local}")
+    gathered = mine = None
+    if world > 1:  # padded per-rank record buffer for the all-gather
+        nbytes = sum(p.device_summaries()[1] for p in plans)
+        t = torch.tensor([nbytes], device=f"cuda:{local}", dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        mine = torch.zeros(int(t.item()), dtype=torch.uint8, device=f"cuda:{local}")
         gathered = [torch.empty_like(mine) for _ in range(world)]
 
     def step():
-        plan.run()
+        for p in plans:
+            p.run()
+            if multi:
+                p.trim()
         if world > 1:
             with torch.cuda.stream(stream):
+                o = 0
+                for p in plans:
+                    ptr, nb = p.device_summaries()
+                    mine[o:o + nb].copy_(device_view(ptr, nb, local))
+                    o += nb
                 dist.all_gather(gathered, mine)
+
+    def collect():
+        res = [p.results() for p in plans]
+        t = dev.timing()
+        return res, t
 
     for i in range(args.warmup):
         step()
         torch.cuda.synchronize()
-        log(f"[{time.strftime('%X')}] warmup {i} done: {dev.timing()['run_ms']:.1f} ms device pipeline")
-    torch.cuda.synchronize()
-    res = plan.results()
-    iters_rank = int(res["iterations"].sum())
-    bad = int(np.sum(res["status"] != 0))
+        log(f"[{time.strftime('%X')}] warmup {i} done")
+    res, _ = collect()
+    iters_rank = int(sum(int(r["iterations"].sum()) for r in res))
+    longest = int(max(int(r["device_cycles"].max()) for r in res if len(r)))
+    bad = int(sum(int(np.sum(r["status"] != 0)) for r in res))
     clocks = ClockSampler(local)
     clocks.start()
     times, eng, algo, launches = [], [], [], 0
@@ -316,11 +498,15 @@ def impl_gpu(args):
         e1.record(stream)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
-        res_t = plan.results()
-        t = dev.timing()
-        eng.append(t["engine_ms"])
-        algo.append(t["algorithmic_bytes"])
-        launches += int(t["engine_launches"])
+        em, ab = 0.0, 0
+        for p in plans:  # per-plan device timings of this step (CUDA events)
+            p.results()
+            t = dev.timing()
+            em += t["engine_ms"]
+            ab += t["algorithmic_bytes"]
+            launches += int(t["engine_launches"])
+        eng.append(em)
+        algo.append(ab)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -335,86 +521,204 @@ def impl_gpu(args):
         dist.all_reduce(it, op=dist.ReduceOp.SUM)
         iters_all = int(it.item())
     value = iters_all * args.steps / (total_ms / 1000.0)
-    ms_per_step = total_ms / args.steps
+    log(f"[{time.strftime('%X')}] timed steps (ms): {times}")
+    for p in plans:
+        p.close()
 
-    log(f"[{time.strftime('%X')}] timed steps: {times}")
-    # e2e through the public C-ABI call with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        pb, keep = pinned_copy(batch)
-        walls, plan_ms, wait_ms = [], [], []
-        h2d = d2h = 0
-        n_warm = max(1, args.warmup)  # same warm-up as the device-resident leg
-        for i in range(max(1, args.e2e_steps) + n_warm):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            out, _ = dev.simulate_batch(pb, cfg)
-            walls.append(time.perf_counter() - t0)
-            tm = dev.timing()
-            h2d, d2h = int(tm["h2d_bytes"]), int(tm["d2h_bytes"])
-            plan_ms.append(tm["plan_ms"])
-            wait_ms.append(tm["run_wait_ms"])
-        walls, plan_ms, wait_ms = walls[n_warm:], plan_ms[n_warm:], wait_ms[n_warm:]
-        e2e_val = int(out["iterations"].sum()) / statistics.mean(walls)
-        if dist:
-            tt = torch.tensor([max(walls)], device=f"cuda:{local}", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_val = iters_all / float(tt.item())
-        e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": 1000 * statistics.mean(walls), "call": "lt_simulate_batch (host pinned buffers)",
-               "plan_ms": statistics.mean(plan_ms), "run_wait_ms": statistics.mean(wait_ms),
-               "warmup_calls": n_warm}
-        # The reference's compute_metrics always sorts TTFT/ITL for percentiles
-        # (metrics.cpp:101-105); sweeps never read them, so the timed device
-        # path skips them. Same call with the percentiles (recording pass +
-        # segmented sorts), reported beside it:
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        dev.simulate_batch(pb, cfg, want_percentiles=True)
-        e2e["with_percentiles"] = {"value": iters_all / (time.perf_counter() - t0), "unit": UNIT,
-                                   "note": "lt_simulate_batch(want_percentiles=1): full compute_metrics incl. "
-                                           "TTFT/ITL p50/p99, as the CPU reference computes"}
+        e2e = e2e_simulate(args, dev, parts, dist, local, iters_all, world)
+        log(f"[{time.strftime('%X')}] e2e: {e2e}")
 
-    log(f"[{time.strftime('%X')}] e2e: {e2e}")
-    secondary = None
-    if rank == 0 and not args.no_sweeps:
-        try:
-            secondary = sweep_secondary(dev, args.sweep_conditions)
-        except Exception as ex:  # reported, never silently replaced
-            secondary = {"error": repr(ex)}
-
-    peak, peak_kind = measured_peaks()
-    eng_ms = statistics.mean(eng)
-    algo_b = statistics.mean(algo)
-    achieved = algo_b / (eng_ms / 1000.0) / 1e9
-    traffic, ncu = ncu_traffic()
+    hbm_peak, hbm_src = measured_hbm_peak()
+    roof = issue_roofline(ncu_engine_profile(args.workload), iters_rank, statistics.mean(eng), clk["sm_mhz"],
+                          statistics.mean(algo), hbm_peak, hbm_src, longest,
+                          launches_engine=len(plans))
     if rank != 0:
         return 0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "scenarios_per_gpu": n_scen, "duration_s": args.duration,
-                   "engine_iterations_per_step": iters_all, "failed_scenarios": bad,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.workload], "scenarios_per_gpu": n_scen,
+                   "engine_iterations_per_step": iters_all, "failed_scenarios": bad, "plans_per_step": len(plans),
                    "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": f"scenario replicas x{world}, NCCL all-gather of per-scenario records"},
-        "e2e": e2e,
-        "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_kind, "kernel": "engine_kernel",
-                     "algorithmic_bytes_per_launch": algo_b, "kernel_ms": eng_ms,
-                     "note": "B_iter = 20R+16V+24A+16M+64 per engine-iteration (SURVEY 8d); "
-                             "engine is latency/issue-bound (one warp per engine), see profiles/"},
-        "cpu_baseline": cpu, "parity": parity, "clocks": clk, "secondary": secondary,
-        "phase_ms": {k: dev.timing()[k] for k in ("tables_ms", "merge_ms", "engine_ms", "run_ms")},
+                   "parallelism": (f"scenario replicas x{world}" if args.workload == "c2"
+                                   else f"cost-balanced scenario shards over {world} GPU(s)")
+                   + (", NCCL all-gather of the per-scenario records inside the step" if world > 1 else "")},
+        "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "parity": parity,
+        "clocks": clk,
     }
-    if ncu:
-        line["roofline"]["ncu"] = ncu
+    if rank == 0 and args.workload == "c2" and not args.no_sweeps:
+        try:
+            line["secondary"] = sweep_secondary(dev, args.sweep_conditions)
+        except Exception as ex:  # reported, never silently replaced
+            line["secondary"] = {"error": repr(ex)}
     print(json.dumps(line), flush=True)
-    plan.close()
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def e2e_simulate(args, dev, parts, dist, local, iters_all, world):
+    """The same metric through lt_simulate_batch from pinned host buffers
+    (host preparation + H2D + the device pipeline + D2H), per part, after
+    warm-up calls; the CPU-side percentile variant is reported beside it."""
+    import torch
+
+    pinned = [(pinned_copy(b), cfg) for _, b, cfg in parts]
+    walls, plan_ms, wait_ms = [], [], []
+    h2d = d2h = 0
+    n_warm = max(1, args.warmup) if args.workload == "c2" else 1
+    n_steps = max(1, args.e2e_steps) if args.workload == "c2" else 1
+    iters = 0
+    for i in range(n_steps + n_warm):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h2d = d2h = pm = wm = 0
+        iters = 0
+        for (pb, _keep), cfg in pinned:
+            out, _ = dev.simulate_batch(pb, cfg)
+            tm = dev.timing()
+            h2d += int(tm["h2d_bytes"])
+            d2h += int(tm["d2h_bytes"])
+            pm += tm["plan_ms"]
+            wm += tm["run_wait_ms"]
+            iters += int(out["iterations"].sum())
+        walls.append(time.perf_counter() - t0)
+        plan_ms.append(pm)
+        wait_ms.append(wm)
+    walls, plan_ms, wait_ms = walls[n_warm:], plan_ms[n_warm:], wait_ms[n_warm:]
+    wall = statistics.mean(walls)
+    val = iters / wall
+    if dist:
+        tt = torch.tensor([wall], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        val = iters_all / float(tt.item())
+    e2e = {"value": val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "ms_per_step": 1000 * wall, "call": "lt_simulate_batch (host pinned buffers)",
+           "plan_ms": statistics.mean(plan_ms), "run_wait_ms": statistics.mean(wait_ms), "warmup_calls": n_warm,
+           "timed_calls": n_steps}
+    if args.workload == "c2":
+        # compute_metrics always sorts TTFT/ITL for percentiles (metrics.cpp:101-105),
+        # which the CPU reference pays; the same call with them, like for like:
+        (pb, _keep), cfg = pinned[0]
+        pw = []
+        for i in range(1 + max(1, args.e2e_steps)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dev.simulate_batch(pb, cfg, want_percentiles=True)
+            pw.append(time.perf_counter() - t0)
+        wp = statistics.mean(pw[1:])
+        e2e["with_percentiles"] = {"value": iters / wp, "unit": UNIT, "ms_per_step": 1000 * wp,
+                                   "note": "lt_simulate_batch(want_percentiles=1): the full compute_metrics incl. "
+                                           "TTFT/ITL p50/p99, as the CPU reference computes; mean of warmed calls"}
+    return e2e
+
+
+def impl_gpu_sweeps(args, dev, dist, world, rank, local):
+    """c4: placement sweeps/sec through lt_sweep_batch (host condition
+    records in, placements + frontiers out), conditions sharded by cost."""
+    import torch
+
+    import paper_2508_08343_b200.distributed as D
+    from paper_2508_08343_b200.batch import ConditionBatch
+
+    conds, cfg, grid, opts, dur, seed = sweep_workload()
+    cb = ConditionBatch.from_conditions(conds)
+    if world > 1:
+        t = cb.templates
+        costs = [float(t[c["mix_offset"]:c["mix_offset"] + c["mix_count"]]["rate"].mean()) for c in cb.conditions]
+        cb = D.condition_subset(cb, D.balanced_shards(costs, world)[rank])
+    cpu = parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, outs = run_reference("c4", os.cpu_count() or 1)
+        sample, _ = reference_sample("c4")
+        gp, _ = dev.sweep_batch(ConditionBatch.from_conditions(sample), cfg, grid, dur, seed, opts)
+        rp = outs[0][0]
+        fields = ("status", "n_star", "g_star", "all_starved", "frontier_open", "max_throughput_tok_s")
+        parity = {"conditions": len(sample), "fields": list(fields),
+                  "mismatches": int(sum(int(np.sum(gp[f] != rp[f])) for f in fields)), "oracle": cpu["kind"]}
+    for i in range(args.warmup):
+        dev.sweep_batch(cb, cfg, grid, dur, seed, opts)
+        log(f"[{time.strftime('%X')}] warmup {i} done")
+    clocks = ClockSampler(local)
+    clocks.start()
+    walls, launches, pts, iters = [], 0, 0, 0
+    for _ in range(args.steps):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pl, fr = dev.sweep_batch(cb, cfg, grid, dur, seed, opts)
+        if dist:
+            D.all_gather_records(pl, np.arange(len(pl)), len(pl), device=torch.device("cuda", local))
+        torch.cuda.synchronize()
+        walls.append(time.perf_counter() - t0)
+        t = dev.timing()
+        launches += int(t["engine_launches"])
+        pts, iters = int(pl["points_simulated"].sum()), int(pl["iterations"].sum())
+    clk = clocks.stop()
+    wall = sum(walls)
+    if dist:
+        tt = torch.tensor([wall], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        wall = float(tt.item())
+    value = len(conds) * args.steps / wall
+    if rank != 0:
+        return 0
+    line = {"metric": METRIC, "value": value, "unit": SWEEP_UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * wall / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS["c4"], "conditions": len(conds), "points_simulated_per_gpu": pts,
+                       "engine_iterations_per_gpu": iters,
+                       "timing": "wall time of lt_sweep_batch (the sweep's N-row waves are planned on the host per "
+                                 "wave), synchronised; max over ranks"},
+            "e2e": {"value": value, "unit": SWEEP_UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                    "note": "the sweep has no device-resident form: value is already end to end"},
+            "gpu_launches": launches, "cpu_baseline": cpu, "parity": parity, "clocks": clk}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def sweep_secondary(dev, n_cond: int):
+    """placement sweeps/sec on a C4 sample (all 8 length settings; explicit G,
+    early exit k=3, 600 s, seed 5), beside the C2 line."""
+    from paper_2508_08343_b200.batch import ConditionBatch
+
+    conds, cfg, grid, opts, dur, seed = sweep_workload()
+    sel = conds[::max(1, len(conds) // n_cond)][:n_cond]
+    cb = ConditionBatch.from_conditions(sel)
+    dev.sweep_batch(cb, cfg, grid, dur, seed, opts)  # warm
+    t0 = time.perf_counter()
+    pl, _ = dev.sweep_batch(cb, cfg, grid, dur, seed, opts)
+    wall = time.perf_counter() - t0
+    return {"metric": "placement sweeps/sec", "value": len(sel) / wall, "unit": SWEEP_UNIT,
+            "conditions": len(sel), "sample": f"every {max(1, len(conds) // n_cond)}th C4 condition",
+            "points_simulated": int(pl["points_simulated"].sum()), "wall_s": wall,
+            "note": "end to end through lt_sweep_batch (host buffers)"}
+
+
+def self_launch(args) -> int:
+    """--gpus N without torchrun: relaunch as N ranks (one per GPU), or refuse."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} requested but only {have} GPU(s) are visible", file=sys.stderr)
+        return 2
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -423,15 +727,19 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["gpu", "reference"], default="gpu")
-    ap.add_argument("--duration", type=float, default=600.0)
-    ap.add_argument("--cpu-stride", type=int, default=1, help="cpu_baseline sample: every k-th C2 scenario")
-    ap.add_argument("--ref-stride", type=int, default=3, help="--impl reference sample per step")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--sweep-conditions", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweeps", action="store_true")
     args = ap.parse_args()
+    if args.warmup < 0 or args.steps < 1:
+        raise SystemExit("bench.py: --steps >= 1 and --warmup >= 0")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "reference":  # rank 0 alone runs it
+            return impl_reference(args)
+        return self_launch(args)
     if args.impl == "reference":
         return impl_reference(args)
     return impl_gpu(args)

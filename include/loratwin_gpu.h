@@ -407,6 +407,14 @@ void lt_plan_destroy(lt_plan* plan);
 /* Device address of the plan's lt_sim_summary array (for device-side
  * collectives, e.g. an NCCL all-gather of per-scenario records). */
 int32_t lt_plan_summaries_device(lt_plan* plan, void** ptr, int64_t* bytes);
+/* Returns the plan's regenerated buffers (RNG tables, per-request arrays,
+ * merge scratch, engine workspace) to the context's block cache; the
+ * summaries stay. The next lt_plan_run re-acquires and regenerates them, so
+ * a chain of trimmed plans run on one context needs the device memory of the
+ * largest, not of all (stream order makes the reuse safe). Per-request states
+ * are unavailable from lt_plan_results until the next run. Plans holding
+ * scripted requests are not trimmed. */
+int32_t lt_plan_trim(lt_plan* plan);
 
 #ifdef __cplusplus
 }

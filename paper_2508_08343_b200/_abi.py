@@ -217,6 +217,7 @@ SIGNATURES = {
     "plan_results": (C.c_int32, [C.c_void_p, C.c_void_p, C.POINTER(lt_request_states), C.POINTER(lt_status)]),
     "plan_destroy": (None, [C.c_void_p]),
     "plan_summaries_device": (C.c_int32, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "plan_trim": (C.c_int32, [C.c_void_p]),
 }
 
 # Symbols the oracle libraries must export (same meaning, other prefix).

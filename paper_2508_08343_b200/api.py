@@ -121,6 +121,10 @@ class Plan:
             raise DeviceError(st.message.decode())
         return out[:self.n]
 
+    def trim(self):
+        """lt_plan_trim: release the regenerated buffers until the next run."""
+        self.dev.lib.plan_trim(self.h)
+
     def device_summaries(self):
         """(device pointer, bytes) of the lt_sim_summary array this plan writes."""
         p = C.c_void_p()

@@ -478,6 +478,11 @@ struct lt_plan {
   int64_t h2d_bytes = 0;
   int64_t launches_prep = 0;
   int64_t launches_run = 0;
+  // lt_plan_trim: the per-request arrays, RNG tables, merge buffers and
+  // engine workspace go back to the block cache between runs (sizes kept)
+  bool has_scripted = false;  // scripted requests live in r_*: never trimmed
+  bool trimmed = false;
+  std::vector<size_t> trimmed_sizes;
 };
 
 namespace {
@@ -1301,6 +1306,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
       }
       where.push_back(i);
     }
+    P.has_scripted = !where.empty();
     int64_t cursor = 0;
     for (int64_t i : where) {
       const int64_t n = P.h_scen[i].n_req;
@@ -1416,6 +1422,57 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   return plan.release();
 }
 
+// Buffers a run regenerates from the plan's inputs (K0 tables, request
+// arrays, merge scratch, engine workspace): what lt_plan_trim releases.
+template <typename F>
+void for_transient(lt_plan& P, F&& f) {
+  f(P.seed_state);
+  f(P.E);
+  f(P.Z);
+  f(P.r_arr);
+  f(P.r_first);
+  f(P.r_last);
+  f(P.r_in);
+  f(P.r_out);
+  f(P.r_adp);
+  f(P.r_gen);
+  f(P.r_pre);
+  f(P.r_phase);
+  f(P.ws_run);
+  f(P.ws_pq);
+  f(P.ws_node);
+  f(P.ws_ov);
+  f(P.ws_link);
+  f(P.pair_excl);
+  f(P.st_in);
+  f(P.st_out);
+  f(P.sv_in);
+  f(P.sv_out);
+  f(P.pos_a);
+  f(P.pos_b);
+  f(P.skey_a);
+  f(P.skey_b);
+  f(P.sort_tmp);
+}
+
+void trim_plan(lt_plan& P) {
+  if (P.trimmed || P.has_scripted) return;
+  P.trimmed_sizes.clear();
+  for_transient(P, [&](auto& b) {
+    P.trimmed_sizes.push_back(b.n);
+    b.release();
+  });
+  P.trimmed = true;
+  P.fresh = false;  // the next run regenerates the tables
+}
+
+void untrim_plan(lt_plan& P) {
+  if (!P.trimmed) return;
+  size_t k = 0;
+  for_transient(P, [&](auto& b) { b.alloc(P.trimmed_sizes[k++]); });
+  P.trimmed = false;
+}
+
 // K0 + merge: (re)generates every request of every generated scenario.
 void prepare_requests(lt_plan& P) {
   lt_ctx* ctx = P.ctx;
@@ -1519,6 +1576,7 @@ void run_percentiles(lt_plan& P, EngineParams E);
 void run_plan(lt_plan& P) {
   lt_ctx* ctx = P.ctx;
   cudaStream_t st = P.st;
+  untrim_plan(P);
   prepare_requests(P);
   reset_state(P);
   EngineParams E{};
@@ -1641,6 +1699,7 @@ void fetch_results(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {
   std::vector<int8_t> phase;
   std::vector<int32_t> gen, pre, in, outv, adp;
   std::vector<double> first, last, arr;
+  if (states && P.trimmed) throw CudaError{"lt_plan_results: per-request states were released by lt_plan_trim"};
   if (states) {
     const int64_t n = P.total_req;
     phase.resize(n);
@@ -2127,6 +2186,14 @@ int32_t lt_plan_results(lt_plan* plan, lt_sim_summary* out, lt_request_states* s
     set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
     return LT_ERR_DEVICE;
   }
+}
+
+int32_t lt_plan_trim(lt_plan* plan) {
+  if (!plan) return LT_ERR_VALIDATION;
+  if (plan->parts[0]) return LT_OK;  // staged plans keep their buffers
+  cudaSetDevice(plan->ctx->device);
+  trim_plan(*plan);
+  return LT_OK;
 }
 
 int32_t lt_plan_summaries_device(lt_plan* plan, void** ptr, int64_t* bytes) {

@@ -274,6 +274,32 @@ def test_plan_rerun_is_deterministic(dev):
         np.testing.assert_array_equal(a[f], c[f], err_msg=f)
 
 
+def test_trimmed_plan_chain_reruns_identically(dev):
+    """lt_plan_trim: plans run one after another, each releasing its
+    regenerated buffers to the block cache for the next, give the results of
+    untrimmed runs (tables, requests and workspace regenerated from inputs)."""
+    from paper_2508_08343_b200.types import profile_config
+    parts = [(W.c2_batch(duration_s=120.0, stride=16), lt.h100_like_config(1)),
+             (W.c5_batch_at(np.arange(0, 524_288, 8191)), profile_config("llama31_8b", 1)),
+             (W.c5_batch_at(np.arange(7, 524_288, 8191)), profile_config("qwen25_7b", 1))]
+    plans = [dev.plan(b, c, want_digest=True) for b, c in parts]
+    first = []
+    for p in plans:
+        p.run()
+        first.append(p.results())
+        p.trim()
+    for _ in range(2):
+        for p, a in zip(plans, first):
+            p.run()
+            c = p.results()
+            p.trim()
+            for f in a.dtype.names:
+                if f != "device_cycles":
+                    np.testing.assert_array_equal(a[f], c[f], err_msg=f)
+    for p in plans:
+        p.close()
+
+
 def test_derived_lat_step_fixture(dev):
     """derived_values.json: lat_step = 0.075455 for R=10, W=5, g=4, n=8, a=1 and one 0.05 s rank-8 load."""
     from tests.test_oracle import derived_values_case

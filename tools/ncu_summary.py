@@ -1,7 +1,9 @@
 """Summarise one `ncu --set full` capture of the engine kernel into
 profiles/<tag>_engine_ncu.json (read back by bench.py for roofline.traffic).
 
-    python tools/ncu_summary.py <report.ncu-rep> <out.json> <workload text> <command text>
+    python tools/ncu_summary.py <report.ncu-rep> <out.json> <workload text> <command text> [iters.json]
+
+iters.json (tools/profile_engine.py) adds the profiled launch's engine-iterations.
 """
 import csv
 import io
@@ -32,5 +34,9 @@ d = {"kernel": "engine_kernel", "command": command, "workload": workload,
      "metrics": {k: (g(k), u[h.index(k)]) for k in keys if k in h},
      "stalls_per_issue": {n[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]: g(n)
                           for n in stall if g(n) > 0.001}}
+if len(sys.argv) > 5:
+    it = json.load(open(sys.argv[5]))
+    d["engine_iterations"] = it["engine_iterations"]
+    d["plan"] = it["plan"]
 json.dump(d, open(outp, "w"), indent=1)
 print(json.dumps(d, indent=1))
