@@ -1067,14 +1067,124 @@ int64_t size_keys(PinnedVec<DKeyNI>& keys) {
   return e_total;
 }
 
+// Engine launch shape of a plan (order, variant, warps, shared memory,
+// persistent grid, workspace) from the per-scenario cost estimates and the
+// plan's request counts (max_req, total_req) and max_adapters.
+void size_engine(lt_plan& P, const std::vector<double>& cost, int max_run_cap) {
+  lt_ctx* ctx = P.ctx;
+  cudaStream_t st = P.st;
+  // engine order: most expensive first
+  P.h_order.resize(P.n_scen);
+  for (int64_t i = 0; i < P.n_scen; ++i) P.h_order[i] = static_cast<int32_t>(i);
+  std::stable_sort(P.h_order.begin(), P.h_order.end(),
+                   [&](int32_t x, int32_t y) { return cost[x] > cost[y]; });
+  P.order.upload(P.h_order, st);
+  P.counter.alloc(1);
+  P.out.alloc(std::max<int64_t>(P.n_scen, 1));
+  // occupancy-sized persistent grid: 8 warps per block, one block per SM
+  // (the engine kernel runs at ~200 registers). Per warp: the adapter tables
+  // plus as much of the running set as fits in shared memory.
+  {
+    // engine_kernel<1> (~200 registers, 8 warps per SM) is the default: the
+    // longest engines set every batch's time, even C3's 65,536 (3.25 s vs
+    // 3.93 s with engine_kernel<2>: <=128 registers with spills, 16 warps per
+    // SM, half the shared memory per warp). LT_ENGINE_VARIANT=2 selects it.
+    // Variant 3: 12 warps per block (<= 170 registers), one block per SM.
+    // Batches whose mean work per warp slot exceeds their longest engine are
+    // throughput-bound (C3 / C5 chunks: 12% / 17% faster with 12 warps);
+    // one-round batches are set by their longest engines, which run ~7%
+    // faster at the latency variant's register budget (C2).
+    // LT_ENGINE_VARIANT overrides.
+    P.engine_variant = 1;
+    if (P.warps_per_block == 8 && P.n_scen > 0) {
+      double total = 0.0, longest = 0.0;
+      for (int64_t i = 0; i < P.n_scen; ++i) {
+        total += cost[i];
+        longest = std::max(longest, cost[i]);
+      }
+      if (total / (static_cast<double>(ctx->sm_count) * 8.0) > longest) P.engine_variant = 3;
+    }
+    if (const char* env = std::getenv("LT_ENGINE_VARIANT")) {
+      const int v = std::atoi(env);
+      P.engine_variant = (v == 2 || v == 3) ? v : 1;
+    }
+    if (P.engine_variant == 3 && P.warps_per_block == 8) P.warps_per_block = 12;
+    // per SM, below the 227 KB opt-in limit (variant 2: two blocks per SM)
+    size_t budget = (static_cast<size_t>(ctx->smem_optin) - 1024) / (P.engine_variant == 2 ? 2 : 1);
+    // per warp: adapter tables, retire calendar, then the running-set slots
+    // (int4 entry + int32 calendar link each) that fit
+    const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter + 2 * kCalBuckets * sizeof(int32_t) +
+                            kPqSmem * sizeof(int4);
+    // Every warp's adapter tables must fit in the block: many-adapter batches
+    // (24 B per adapter per warp) leave the occupancy variants and then drop
+    // warps per block until they do (1,024 adapters: 7 warps of 29.7 KB).
+    if (static_cast<size_t>(P.warps_per_block) * adapters > budget && P.engine_variant != 1) {
+      P.engine_variant = 1;
+      P.warps_per_block = std::min(P.warps_per_block, 8);
+      budget = static_cast<size_t>(ctx->smem_optin) - 1024;
+    }
+    while (P.warps_per_block > 1 && static_cast<size_t>(P.warps_per_block) * adapters > budget) --P.warps_per_block;
+    const int warps = P.warps_per_block;
+    const size_t per_slot = sizeof(int4) + sizeof(int2);
+    const size_t per_warp_max = budget / warps;
+    int64_t cap = per_warp_max > adapters ? static_cast<int64_t>((per_warp_max - adapters) / per_slot) : 0;
+    cap = std::min<int64_t>(cap, max_run_cap) / 32 * 32;
+    P.run_cap = static_cast<int32_t>(cap);
+    P.smem_per_warp = static_cast<int32_t>(adapters + static_cast<size_t>(cap) * per_slot);
+    P.block = warps * 32;
+    P.smem = static_cast<size_t>(P.smem_per_warp) * warps;
+  }
+  // The device's opt-in maximum (a constant, so plans built concurrently on
+  // other host threads never lower it under each other) and the max-shared
+  // carveout, so blocks of a staged plan's two parts (and the K0 seed kernel)
+  // can share an SM.
+  const void* ek = P.engine_variant == 2   ? reinterpret_cast<const void*>(engine_kernel<256, 2>)
+                   : P.engine_variant == 3 ? reinterpret_cast<const void*>(engine_kernel<384, 1>)
+                                           : reinterpret_cast<const void*>(engine_kernel<256, 1>);
+  LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_optin));
+  LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+  int per_sm = 0;
+  LT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ek, P.block, P.smem));
+  per_sm = std::max(per_sm, 1);
+  // at least one block per SM while there are scenarios for them (the first
+  // round spreads the heaviest engines one per SM)
+  const int64_t want = std::max<int64_t>((P.n_scen + P.block / 32 - 1) / (P.block / 32),
+                                         std::min<int64_t>(P.n_scen, ctx->sm_count));
+  P.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(ctx->sm_count) * per_sm)));
+  P.ws_stride = std::max<int64_t>(P.max_req, 1);
+  {
+    // Workspace per persistent warp slot (slots x longest scenario) or per
+    // scenario (at its request offset), whichever is smaller.
+    const int64_t slots = int64_t(P.grid) * (P.block / 32);
+    const int64_t per_slot = slots * P.ws_stride;
+    const int64_t per_scen = std::max<int64_t>(P.total_req, 1);
+    P.ws_per_scenario = per_scen < per_slot;
+    const int64_t entries = P.ws_per_scenario ? per_scen : per_slot;
+    P.ws_run.alloc(entries);
+    P.ws_pq.alloc(entries);
+    P.ws_node.alloc(entries);
+    P.ws_link.alloc(entries);
+    P.ws_ov.alloc(entries);
+  }
+}
+
+// Adapter records the batch's scenarios reference (a chunk of a larger batch
+// shares the caller's adapter array, so b->n_adapters would over-reserve).
+int64_t batch_adapters(const lt_workload_batch* b) {
+  int64_t n = 0;
+  for (int64_t i = 0; i < b->n_scenarios; ++i) n += std::max<int32_t>(b->scenarios[i].n_adapters, 0);
+  return std::min<int64_t>(n, b->n_adapters);
+}
+
 // Builds a plan: validation, RNG tables, counting, merge, request arrays,
 // workspace. Leaves everything resident; returns nullptr + status on error.
 lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_config* cfg,
-                    const lt_sim_options* opts, int warps_per_block = 8, int max_run_cap = 1024) {
+                    const lt_sim_options* opts, int warps_per_block = 8, int max_run_cap = 1024,
+                    cudaStream_t stream = nullptr) {
   auto plan = std::make_unique<lt_plan>();
   lt_plan& P = *plan;
   P.ctx = ctx;
-  P.st = ctx->stream;
+  P.st = stream ? stream : ctx->stream;
   for (cudaEvent_t& e : P.ev) LT_CUDA(cudaEventCreate(&e));
   P.warps_per_block = warps_per_block;
   cudaStream_t st = P.st;
@@ -1094,11 +1204,12 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   Prep& pr = t_prep;
   pr.reset();
   pr.cost.assign(P.n_scen, 0.0);
-  pr.keys.reserve(b->n_adapters);
-  P.adapter_ids.reserve(b->n_adapters);
-  pr.adapters.reserve(b->n_adapters);
-  pr.pair_scen.reserve(b->n_adapters);
-  pr.pair_adp.reserve(b->n_adapters);
+  const int64_t n_ad = batch_adapters(b);
+  pr.keys.reserve(n_ad);
+  P.adapter_ids.reserve(n_ad);
+  pr.adapters.reserve(n_ad);
+  pr.pair_scen.reserve(n_ad);
+  pr.pair_adp.reserve(n_ad);
   pr.pair_begin.resize(P.n_scen);
   // pass 1 + early K0 (seed_seq and table draws; Full-mode decks follow pass 2)
   collect_keys(pr, *b);
@@ -1320,99 +1431,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     P.h2d_bytes += cursor * 20;
     LT_CUDA(cudaStreamSynchronize(st));
   }
-  // engine order: most expensive first
-  P.h_order.resize(P.n_scen);
-  for (int64_t i = 0; i < P.n_scen; ++i) P.h_order[i] = static_cast<int32_t>(i);
-  std::stable_sort(P.h_order.begin(), P.h_order.end(),
-                   [&](int32_t x, int32_t y) { return pr.cost[x] > pr.cost[y]; });
-  P.order.upload(P.h_order, st);
-  P.counter.alloc(1);
-  P.out.alloc(std::max<int64_t>(P.n_scen, 1));
-  // occupancy-sized persistent grid: 8 warps per block, one block per SM
-  // (the engine kernel runs at ~200 registers). Per warp: the adapter tables
-  // plus as much of the running set as fits in shared memory.
-  {
-    // engine_kernel<1> (~200 registers, 8 warps per SM) is the default: the
-    // longest engines set every batch's time, even C3's 65,536 (3.25 s vs
-    // 3.93 s with engine_kernel<2>: <=128 registers with spills, 16 warps per
-    // SM, half the shared memory per warp). LT_ENGINE_VARIANT=2 selects it.
-    // Variant 3: 12 warps per block (<= 170 registers), one block per SM.
-    // Batches whose mean work per warp slot exceeds their longest engine are
-    // throughput-bound (C3 / C5 chunks: 12% / 17% faster with 12 warps);
-    // one-round batches are set by their longest engines, which run ~7%
-    // faster at the latency variant's register budget (C2).
-    // LT_ENGINE_VARIANT overrides.
-    P.engine_variant = 1;
-    if (warps_per_block == 8 && P.n_scen > 0) {
-      double total = 0.0, longest = 0.0;
-      for (int64_t i = 0; i < P.n_scen; ++i) {
-        total += pr.cost[i];
-        longest = std::max(longest, pr.cost[i]);
-      }
-      if (total / (static_cast<double>(ctx->sm_count) * 8.0) > longest) P.engine_variant = 3;
-    }
-    if (const char* env = std::getenv("LT_ENGINE_VARIANT")) {
-      const int v = std::atoi(env);
-      P.engine_variant = (v == 2 || v == 3) ? v : 1;
-    }
-    if (P.engine_variant == 3 && P.warps_per_block == 8) P.warps_per_block = 12;
-    // per SM, below the 227 KB opt-in limit (variant 2: two blocks per SM)
-    size_t budget = (static_cast<size_t>(ctx->smem_optin) - 1024) / (P.engine_variant == 2 ? 2 : 1);
-    // per warp: adapter tables, retire calendar, then the running-set slots
-    // (int4 entry + int32 calendar link each) that fit
-    const size_t adapters = static_cast<size_t>(P.max_adapters) * kSmemPerAdapter + 2 * kCalBuckets * sizeof(int32_t) +
-                            kPqSmem * sizeof(int4);
-    // Every warp's adapter tables must fit in the block: many-adapter batches
-    // (24 B per adapter per warp) leave the occupancy variants and then drop
-    // warps per block until they do (1,024 adapters: 7 warps of 29.7 KB).
-    if (static_cast<size_t>(P.warps_per_block) * adapters > budget && P.engine_variant != 1) {
-      P.engine_variant = 1;
-      P.warps_per_block = std::min(P.warps_per_block, 8);
-      budget = static_cast<size_t>(ctx->smem_optin) - 1024;
-    }
-    while (P.warps_per_block > 1 && static_cast<size_t>(P.warps_per_block) * adapters > budget) --P.warps_per_block;
-    const int warps = P.warps_per_block;
-    const size_t per_slot = sizeof(int4) + sizeof(int2);
-    const size_t per_warp_max = budget / warps;
-    int64_t cap = per_warp_max > adapters ? static_cast<int64_t>((per_warp_max - adapters) / per_slot) : 0;
-    cap = std::min<int64_t>(cap, max_run_cap) / 32 * 32;
-    P.run_cap = static_cast<int32_t>(cap);
-    P.smem_per_warp = static_cast<int32_t>(adapters + static_cast<size_t>(cap) * per_slot);
-    P.block = warps * 32;
-    P.smem = static_cast<size_t>(P.smem_per_warp) * warps;
-  }
-  // The device's opt-in maximum (a constant, so plans built concurrently on
-  // other host threads never lower it under each other) and the max-shared
-  // carveout, so blocks of a staged plan's two parts (and the K0 seed kernel)
-  // can share an SM.
-  const void* ek = P.engine_variant == 2   ? reinterpret_cast<const void*>(engine_kernel<256, 2>)
-                   : P.engine_variant == 3 ? reinterpret_cast<const void*>(engine_kernel<384, 1>)
-                                           : reinterpret_cast<const void*>(engine_kernel<256, 1>);
-  LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_optin));
-  LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-  int per_sm = 0;
-  LT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ek, P.block, P.smem));
-  per_sm = std::max(per_sm, 1);
-  // at least one block per SM while there are scenarios for them (the first
-  // round spreads the heaviest engines one per SM)
-  const int64_t want = std::max<int64_t>((P.n_scen + P.block / 32 - 1) / (P.block / 32),
-                                         std::min<int64_t>(P.n_scen, ctx->sm_count));
-  P.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(ctx->sm_count) * per_sm)));
-  P.ws_stride = std::max<int64_t>(P.max_req, 1);
-  {
-    // Workspace per persistent warp slot (slots x longest scenario) or per
-    // scenario (at its request offset), whichever is smaller.
-    const int64_t slots = int64_t(P.grid) * (P.block / 32);
-    const int64_t per_slot = slots * P.ws_stride;
-    const int64_t per_scen = std::max<int64_t>(P.total_req, 1);
-    P.ws_per_scenario = per_scen < per_slot;
-    const int64_t entries = P.ws_per_scenario ? per_scen : per_slot;
-    P.ws_run.alloc(entries);
-    P.ws_pq.alloc(entries);
-    P.ws_node.alloc(entries);
-    P.ws_link.alloc(entries);
-    P.ws_ov.alloc(entries);
-  }
+  size_engine(P, pr.cost, max_run_cap);
   LT_CUDA(cudaStreamSynchronize(st));
   P.tables_ms = elapsed(P.ev[0], P.ev[1]);
   P.fresh = true;
@@ -1571,14 +1590,8 @@ void reset_state(lt_plan& P) {
   LT_CUDA(cudaMemsetAsync(P.counter.p, 0, sizeof(int32_t), st));
 }
 
-void run_percentiles(lt_plan& P, EngineParams E);
-
-void run_plan(lt_plan& P) {
-  lt_ctx* ctx = P.ctx;
-  cudaStream_t st = P.st;
-  untrim_plan(P);
-  prepare_requests(P);
-  reset_state(P);
+// Kernel parameters of a plan's engine pass.
+EngineParams engine_params(const lt_plan& P) {
   EngineParams E{};
   E.scen = P.scen.p;
   E.order = P.order.p;
@@ -1614,6 +1627,18 @@ void run_plan(lt_plan& P) {
   E.priority = P.cfg.raw.loaded_adapter_priority;
   E.want_digest = P.want_digest;
   E.out = P.out.p;
+  return E;
+}
+
+void run_percentiles(lt_plan& P, EngineParams E);
+
+void run_plan(lt_plan& P) {
+  lt_ctx* ctx = P.ctx;
+  cudaStream_t st = P.st;
+  untrim_plan(P);
+  prepare_requests(P);
+  reset_state(P);
+  const EngineParams E = engine_params(P);
   cudaEventRecord(P.ev[4], st);
   if (P.n_scen > 0) {
     launch_engine(P, E, st);
@@ -2000,11 +2025,12 @@ double lt__host_prep_ms(const lt_workload_batch* b, const lt_server_config* cfg)
   Prep& pr = t_prep;
   pr.reset();
   pr.cost.assign(P.n_scen, 0.0);
-  pr.keys.reserve(b->n_adapters);
-  P.adapter_ids.reserve(b->n_adapters);
-  pr.adapters.reserve(b->n_adapters);
-  pr.pair_scen.reserve(b->n_adapters);
-  pr.pair_adp.reserve(b->n_adapters);
+  const int64_t n_ad = batch_adapters(b);
+  pr.keys.reserve(n_ad);
+  P.adapter_ids.reserve(n_ad);
+  pr.adapters.reserve(n_ad);
+  pr.pair_scen.reserve(n_ad);
+  pr.pair_adp.reserve(n_ad);
   const auto t05 = std::chrono::steady_clock::now();
   collect_keys(pr, *b);
   const auto t1 = std::chrono::steady_clock::now();
@@ -2245,19 +2271,27 @@ int32_t lt_simulate_batch(lt_ctx* ctx, const lt_workload_batch* batch, const lt_
   const auto t0 = clk::now();
   ok_status(status);
   // Device memory is bounded by splitting the batch into consecutive chunks of
-  // at most kChunkRequests estimated requests (~100 B of device state each).
-  double kChunkRequests = 5.0e8;
+  // at most kChunkScenarios scenarios and kChunkRequests estimated requests
+  // (~100 B of device state each). Chunks are pipelined on two streams: the
+  // host validates and packs chunk c+1 (and launches its tables) while the
+  // device runs chunk c, then collects chunk c.
+  double kChunkRequests = 2.5e8;
+  int64_t kChunkScenarios = 65536;
   if (const char* env = std::getenv("LT_CHUNK_REQUESTS")) kChunkRequests = std::max(1.0, std::atof(env));
+  if (const char* env = std::getenv("LT_CHUNK_SCENARIOS")) kChunkScenarios = std::max(1, std::atoi(env));
   const int64_t n = batch->n_scenarios;
   std::vector<int64_t> cuts{0};
   double acc = 0.0;
+  int64_t cnt = 0;
   for (int64_t i = 0; i < n; ++i) {
     const double e = est_requests(batch, i);
-    if (acc > 0.0 && acc + e > kChunkRequests) {
+    if (cnt > 0 && (acc + e > kChunkRequests || cnt >= kChunkScenarios)) {
       cuts.push_back(i);
       acc = 0.0;
+      cnt = 0;
     }
     acc += e;
+    ++cnt;
   }
   cuts.push_back(n);
   double plan_ms = 0.0;
@@ -2265,67 +2299,86 @@ int32_t lt_simulate_batch(lt_ctx* ctx, const lt_workload_batch* batch, const lt_
   if (cuts.size() <= 2) {
     rc = simulate_one(ctx, batch, config, options, out, states, status, &plan_ms);
   } else {
-    std::vector<std::string> msgs(n);
-    lt_timing tsum{};
-    int64_t req_off = 0;
-    lt_status first{};
-    first.code = LT_OK;
-    for (size_t c = 0; c + 1 < cuts.size(); ++c) {
-      const int64_t c0 = cuts[c], nc = cuts[c + 1] - c0;
-      lt_workload_batch sub = *batch;
-      sub.scenarios = batch->scenarios + c0;
-      sub.n_scenarios = nc;
-      lt_request_states sst;
-      lt_request_states* sp = nullptr;
-      if (states) {
-        sst = *states;
-        sst.capacity = std::max<int64_t>(states->capacity - req_off, 0);
-        sst.req_offset = states->req_offset ? states->req_offset + c0 : nullptr;
-        auto shift = [&](auto*& p) {
-          if (p) p += req_off;
-        };
-        shift(sst.phase);
-        shift(sst.tokens_generated);
-        shift(sst.first_token_time_s);
-        shift(sst.completion_time_s);
-        shift(sst.preemption_count);
-        shift(sst.adapter_id);
-        shift(sst.input_tokens);
-        shift(sst.output_tokens);
-        shift(sst.arrival_time_s);
-        sp = &sst;
+    try {
+      cudaSetDevice(ctx->device);
+      std::vector<std::string> msgs(n);
+      lt_timing tsum{};
+      int64_t req_off = 0;
+      lt_status first{};
+      first.code = LT_OK;
+      // collects chunk [c0, c0 + nc) of plan P into the caller's arrays
+      auto finish = [&](lt_plan& P, int64_t c0, int64_t nc) {
+        lt_request_states sst;
+        lt_request_states* sp = nullptr;
+        if (states) {
+          sst = *states;
+          sst.capacity = std::max<int64_t>(states->capacity - req_off, 0);
+          sst.req_offset = states->req_offset ? states->req_offset + c0 : nullptr;
+          auto shift = [&](auto*& q) {
+            if (q) q += req_off;
+          };
+          shift(sst.phase);
+          shift(sst.tokens_generated);
+          shift(sst.first_token_time_s);
+          shift(sst.completion_time_s);
+          shift(sst.preemption_count);
+          shift(sst.adapter_id);
+          shift(sst.input_tokens);
+          shift(sst.output_tokens);
+          shift(sst.arrival_time_s);
+          sp = &sst;
+        }
+        fetch_results(P, out + c0, sp);
+        lt_status st{};
+        const int32_t r = first_error(ctx, out + c0, nc, &st);
+        const int64_t base = req_off;
+        for (int64_t i = 0; i < nc; ++i) {
+          msgs[c0 + i] = ctx->messages[i];
+          if (states && states->req_offset) states->req_offset[c0 + i] += base;
+          req_off += out[c0 + i].n_requests;
+        }
+        if (r != LT_OK && first.code == LT_OK) {
+          first = st;
+          first.index += c0;
+          rc = r;
+        }
+        const lt_timing& t = ctx->timing;
+        tsum.tables_ms += t.tables_ms;
+        tsum.merge_ms += t.merge_ms;
+        tsum.engine_ms += t.engine_ms;
+        tsum.d2h_ms += t.d2h_ms;
+        tsum.run_ms += t.run_ms;
+        tsum.h2d_bytes += t.h2d_bytes;
+        tsum.d2h_bytes += t.d2h_bytes;
+        tsum.engine_launches += t.engine_launches;
+        tsum.algorithmic_bytes += t.algorithmic_bytes;
+      };
+      std::unique_ptr<lt_plan> prev;
+      int64_t prev_c0 = 0, prev_nc = 0;
+      for (size_t c = 0; c + 1 < cuts.size(); ++c) {
+        const int64_t c0 = cuts[c], nc = cuts[c + 1] - c0;
+        lt_workload_batch sub = *batch;
+        sub.scenarios = batch->scenarios + c0;
+        sub.n_scenarios = nc;
+        const auto tb = clk::now();
+        std::unique_ptr<lt_plan> plan(
+            build_plan(ctx, &sub, config, options, 8, 1024, (c & 1) ? ctx->stream2 : ctx->stream));
+        plan_ms += std::chrono::duration<double, std::milli>(clk::now() - tb).count();
+        run_plan(*plan);
+        if (prev) finish(*prev, prev_c0, prev_nc);
+        prev = std::move(plan);
+        prev_c0 = c0;
+        prev_nc = nc;
       }
-      lt_status st{};
-      const int32_t r = simulate_one(ctx, &sub, config, options, out + c0, sp, &st, &plan_ms);
-      if (r == LT_ERR_DEVICE && st.index < 0) {  // the chunk itself failed
-        if (status) *status = st;
-        return r;
-      }
-      const int64_t base = req_off;
-      for (int64_t i = 0; i < nc; ++i) {
-        msgs[c0 + i] = ctx->messages[i];
-        if (states && states->req_offset) states->req_offset[c0 + i] += base;
-        req_off += out[c0 + i].n_requests;
-      }
-      if (r != LT_OK && first.code == LT_OK) {
-        first = st;
-        first.index += c0;
-        rc = r;
-      }
-      const lt_timing& t = ctx->timing;
-      tsum.tables_ms += t.tables_ms;
-      tsum.merge_ms += t.merge_ms;
-      tsum.engine_ms += t.engine_ms;
-      tsum.d2h_ms += t.d2h_ms;
-      tsum.run_ms += t.run_ms;
-      tsum.h2d_bytes += t.h2d_bytes;
-      tsum.d2h_bytes += t.d2h_bytes;
-      tsum.engine_launches += t.engine_launches;
-      tsum.algorithmic_bytes += t.algorithmic_bytes;
+      finish(*prev, prev_c0, prev_nc);
+      prev.reset();
+      ctx->messages = std::move(msgs);
+      ctx->timing = tsum;
+      if (status && rc != LT_OK) *status = first;
+    } catch (const CudaError& e) {
+      set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
+      return LT_ERR_DEVICE;
     }
-    ctx->messages = std::move(msgs);
-    ctx->timing = tsum;
-    if (status && rc != LT_OK) *status = first;
   }
   ctx->timing.total_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
   ctx->timing.plan_ms = plan_ms;

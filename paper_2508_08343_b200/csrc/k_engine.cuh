@@ -892,9 +892,12 @@ struct WarpEngine {
     // turnover scan of a slot-starved engine).
     int lk = INT_MAX, la = -1;
     bool direct = false;
-    if (LT_LIKELY(lane_mode)) {
-      enter_lane_mode(act_w);
-    } else {
+    // enter_lane_mode has one call site, at the head of the event loop (it is
+    // large: a second inlined copy for the mid-scan switch doubled the scan's
+    // code and its instruction-cache footprint)
+    bool enter = lane_mode;
+    uint32_t enter_w = act_w;
+    if (LT_UNLIKELY(!lane_mode)) {
       LT_STAT(2);
       direct = P.priority && !mass && !__any_sync(kFull, blocked_w != 0);
       if (!direct) {
@@ -905,6 +908,10 @@ struct WarpEngine {
     }
     int stop_id = INT_MAX;
     for (;;) {
+      if (enter) {
+        enter_lane_mode(enter_w);
+        enter = false;
+      }
       int id, a;
       bool sf, cl;
       int4 nd;  // {in, out, next, adapter}
@@ -1013,9 +1020,9 @@ struct WarpEngine {
             __syncwarp();
             const uint32_t aw = nonempty_w & ~blocked_w & ~(slotful_w & ~claimed_w);
             if (__reduce_add_sync(kFull, __popc(aw)) <= 32) {  // only claimed chains act now
-              enter_lane_mode(aw);
+              enter_w = aw;
+              enter = true;
               lane_mode = true;
-              __syncwarp();
               continue;
             }
             if (direct) {
@@ -1121,7 +1128,7 @@ struct WarpEngine {
 // 32 shuffles are independent and only the adds form a chain.
 __device__ __forceinline__ double ordered_add(double acc, double v, bool f) {
   const double x = f ? v : 0.0;
-#pragma unroll 8
+#pragma unroll 1
   for (int k = 0; k < 32; ++k) acc = acc + __shfl_sync(kFull, x, k);
   return acc;
 }
