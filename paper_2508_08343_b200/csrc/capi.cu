@@ -1566,9 +1566,10 @@ void prepare_requests(lt_plan& P) {
   }
   cudaEventRecord(P.ev[3], st);
   P.fresh = false;
-  P.launches_run = launches + 1;
+  P.launches_run = launches + 2;  // + engine, metrics (launch_engine)
 }
 
+// K1 (the engine kernel) then K2 (metrics_kernel) over the plan's scenarios.
 void launch_engine(lt_plan& P, const EngineParams& E, cudaStream_t st) {
   if (P.engine_variant == 2)
     engine_kernel<256, 2><<<P.grid, P.block, P.smem, st>>>(E);
@@ -1576,6 +1577,9 @@ void launch_engine(lt_plan& P, const EngineParams& E, cudaStream_t st) {
     engine_kernel<384, 1><<<P.grid, P.block, P.smem, st>>>(E);
   else
     engine_kernel<256, 1><<<P.grid, P.block, P.smem, st>>>(E);
+  after_launch("engine_kernel", st);
+  metrics_kernel<<<static_cast<unsigned>((P.n_scen + 7) / 8), 256, 0, st>>>(
+      E.scen, E.n_scen, E.r_phase, E.r_first, E.r_arr, E.r_last, E.r_out, E.r_gen, E.out);
 }
 
 // Per-request engine state before an engine pass.
@@ -1642,7 +1646,7 @@ void run_plan(lt_plan& P) {
   cudaEventRecord(P.ev[4], st);
   if (P.n_scen > 0) {
     launch_engine(P, E, st);
-    after_launch("engine_kernel", st);
+    after_launch("metrics_kernel", st);
   }
   cudaEventRecord(P.ev[5], st);
   if (P.want_pct && P.n_scen > 0) run_percentiles(P, E);
@@ -1692,7 +1696,7 @@ void run_percentiles(lt_plan& P, EngineParams E) {
   E.rec_d = P.rec_d.p;
   E.rec_c = P.rec_c.p;
   launch_engine(P, E, st);
-  after_launch("engine_kernel(record)", st);
+  after_launch("metrics_kernel(record)", st);
   ttft_keys_kernel<<<static_cast<unsigned>((nr + 255) / 256), 256, 0, st>>>(P.r_arr.p, P.r_first.p, nr,
                                                                             P.ttft_keys.p);
   after_launch("ttft_keys_kernel", st);
@@ -1712,7 +1716,7 @@ void run_percentiles(lt_plan& P, EngineParams E) {
       P.scen.p, static_cast<int>(n), P.ttft_sorted.p, P.rec_off.p, P.rec_len.p, P.rec_d_sorted.p,
       P.rec_c_sorted.p, P.out.p);
   after_launch("percentile_kernel", st);
-  P.launches_run += 4;
+  P.launches_run += 5;  // engine + metrics (recording pass), ttft keys, percentiles
 }
 
 void fetch_results(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {

@@ -185,6 +185,122 @@ __device__ __noinline__ void act_keys(int32_t* act_key, const int32_t* q_head, i
   }
 }
 
+// Running-set tiers of one engine (shared-memory slots < run_cap, HBM beyond).
+struct RunTiers {
+  int4* runs;
+  int4* run;
+  int2* links;
+  int2* linkg;
+  int32_t* cal;
+  int32_t* cmin;
+  int run_cap;
+};
+
+// Stable compaction of the live running entries, then the retire calendar
+// rebuilt for the new slots (next links by atomic head exchange, then each
+// node's successor learns its predecessor). Rare, so out of line: it keeps
+// the engine loop's instruction footprint small. Returns the new length.
+__device__ __noinline__ int compact_running(RunTiers t, int R_end, int lane) {
+  auto get = [&](int pos) { return pos < t.run_cap ? t.runs[pos] : t.run[pos]; };
+  auto lk = [&](int pos) -> int2& { return pos < t.run_cap ? t.links[pos] : t.linkg[pos]; };
+  int w = 0;
+  for (int base = 0; base < R_end; base += 32) {
+    const int i = base + lane;
+    const int4 e = (i < R_end) ? get(i) : make_int4(-1, INT_MAX, 0, 0);
+    const unsigned lm = __ballot_sync(kFull, e.x >= 0);
+    if (e.x >= 0) {
+      const int d = w + __popc(lm & lanemask_lt());
+      if (d < t.run_cap)
+        t.runs[d] = e;
+      else
+        t.run[d] = e;
+    }
+    w += __popc(lm);
+    __syncwarp();
+  }
+  for (int b = lane; b < kCalBuckets; b += 32) {
+    t.cal[b] = -1;
+    t.cmin[b] = INT_MAX;
+  }
+  __syncwarp();
+  for (int i = lane; i < w; i += 32) {
+    const int fin = get(i).y;
+    lk(i) = make_int2(atomicExch(&t.cal[fin & (kCalBuckets - 1)], i), -1);
+    atomicMin(&t.cmin[fin & (kCalBuckets - 1)], fin);
+  }
+  __syncwarp();
+  for (int i = lane; i < w; i += 32) {
+    const int nx = lk(i).x;
+    if (nx >= 0) lk(nx).y = i;
+  }
+  __syncwarp();
+  return w;
+}
+
+// Preempted-queue ring (shared-memory slots < kPqSmem, HBM beyond).
+struct PqRing {
+  int4* pqs;
+  int4* pq;
+  int pq_h;
+  int pq_cap;
+};
+
+// A preempted request inserted into waiting_preempted ordered by (arrival,
+// request_id) (kv_scheduler.cpp:206-215) at a position inside the queue: the
+// backward scan for the first entry that does not sort after it, then the
+// tail shifted by one (back to front). Out of line: the append / prepend
+// cases cover every victim of generated workloads.
+__device__ __noinline__ void pq_insert_middle(PqRing q, int Wp, int4 ent, bool ids_sorted, const double* arr,
+                                              int lane) {
+  auto slot = [&](int i) {
+    const int j = q.pq_h + i;
+    return j >= q.pq_cap ? j - q.pq_cap : j;
+  };
+  auto get = [&](int i) {
+    const int j = slot(i);
+    return j < kPqSmem ? q.pqs[j] : q.pq[j];
+  };
+  auto put = [&](int i, int4 e) {
+    const int j = slot(i);
+    if (j < kPqSmem)
+      q.pqs[j] = e;
+    else
+      q.pq[j] = e;
+  };
+  const int idx = ent.x;
+  const double a_idx = arr[idx];
+  int pos = 0;
+  for (int hi = Wp; hi > 0; hi -= 32) {
+    const int i = hi - 32 + lane;
+    bool greater = false;  // entry i sorts after the victim
+    if (i >= 0) {
+      const int j = get(i).x;
+      if (ids_sorted) {
+        greater = idx < j;
+      } else {
+        const double aj = arr[j];
+        greater = (a_idx < aj) || (a_idx == aj && idx < j);
+      }
+    }
+    const unsigned notg = __ballot_sync(kFull, i >= 0 && !greater);
+    if (notg) {
+      pos = hi - 32 + (31 - __clz(notg)) + 1;
+      break;
+    }
+  }
+  for (int hi = Wp; hi > pos; hi -= 32) {
+    const int lo = max(pos, hi - 32);
+    const int i = lo + lane;
+    int4 e;
+    if (i < hi) e = get(i);
+    __syncwarp();
+    if (i < hi) put(i + 1, e);
+    __syncwarp();
+  }
+  if (lane == 0) put(pos, ent);
+  __syncwarp();
+}
+
 struct WarpEngine {
 #ifdef LT_SCAN_STATS
   // diagnostics build: fresh scans, stop-cache hits, non-lane scans,
@@ -444,36 +560,9 @@ struct WarpEngine {
   }
 
   // Stable compaction of the live entries (amortised: only when tombstones
-  // outnumber live entries), then the calendar is rebuilt for the new slots.
+  // outnumber live entries), out of line (compact_running).
   __device__ __forceinline__ void compact() {
-    int w = 0;
-    for (int base = 0; base < R_end; base += 32) {
-      const int i = base + lane;
-      const int4 e = (i < R_end) ? run_get(i) : make_int4(-1, INT_MAX, 0, 0);
-      const unsigned lm = __ballot_sync(kFull, e.x >= 0);
-      if (e.x >= 0) run_put(w + __popc(lm & lanemask_lt()), e);
-      w += __popc(lm);
-    }
-    __syncwarp();
-    R_end = w;
-    for (int b = lane; b < kCalBuckets; b += 32) {
-      cal[b] = -1;
-      cmin[b] = INT_MAX;
-    }
-    __syncwarp();
-    // next links by atomic head exchange, then each node's successor learns
-    // its predecessor (one writer per node)
-    for (int i = lane; i < R_end; i += 32) {
-      const int fin = run_get(i).y;
-      lk_put(i, make_int2(atomicExch(&cal[fin & (kCalBuckets - 1)], i), -1));
-      atomicMin(&cmin[fin & (kCalBuckets - 1)], fin);
-    }
-    __syncwarp();
-    for (int i = lane; i < R_end; i += 32) {
-      const int nx = lk_get(i).x;
-      if (nx >= 0) lk_prev(nx, i);
-    }
-    __syncwarp();
+    R_end = compact_running(RunTiers{runs, run, links, linkg, cal, cmin, run_cap}, R_end, lane);
   }
 
   // complete_finished (kv_scheduler.cpp:238-259): the retirees of this
@@ -555,37 +644,7 @@ struct WarpEngine {
         return;
       }
     }
-    const double arr = P.r_arr[rb + idx];
-    // scan backwards for the first entry that is not greater
-    int pos = 0;
-    for (int hi = Wp; hi > 0; hi -= 32) {
-      const int i = hi - 32 + lane;
-      bool greater = false;  // entry i sorts after the victim
-      if (i >= 0) {
-        const int j = pq_get(i).x;
-        greater = ids_sorted ? idx < j : [&] {
-          const double aj = P.r_arr[rb + j];
-          return (arr < aj) || (arr == aj && idx < j);
-        }();
-      }
-      const unsigned notg = __ballot_sync(kFull, i >= 0 && !greater);
-      if (notg) {
-        pos = hi - 32 + (31 - __clz(notg)) + 1;
-        break;
-      }
-    }
-    // shift [pos, Wp) right by one, back to front
-    for (int hi = Wp; hi > pos; hi -= 32) {
-      const int lo = max(pos, hi - 32);
-      const int i = lo + lane;
-      int4 e;
-      if (i < hi) e = pq_get(i);
-      __syncwarp();
-      if (i < hi) pq_put(i + 1, e);
-      __syncwarp();
-    }
-    if (lane == 0) pq_put(pos, ent);
-    __syncwarp();
+    pq_insert_middle(PqRing{pqs, pq, pq_h, pq_cap}, Wp, ent, ids_sorted, P.r_arr + rb, lane);
     ++Wp;
   }
 
@@ -799,6 +858,7 @@ struct WarpEngine {
       if (LT_UNLIKELY(n_add > 8)) {
         rebuild = true;
       } else {
+#pragma unroll 1
         for (int k = 0; k < n_add; ++k) {
           const int a = mask_lowest(add);
           mask_clear(add, a, lane);
@@ -1121,17 +1181,6 @@ struct WarpEngine {
     return true;
   }
 };
-
-// Ordered (sequential) FP sum of the 32 lanes' values, lane 0 first: the
-// reference's std::accumulate order (metrics.cpp:29-32, :86-105). Unflagged
-// lanes add +0.0, which leaves a non-negative accumulator unchanged, so the
-// 32 shuffles are independent and only the adds form a chain.
-__device__ __forceinline__ double ordered_add(double acc, double v, bool f) {
-  const double x = f ? v : 0.0;
-#pragma unroll 1
-  for (int k = 0; k < 32; ++k) acc = acc + __shfl_sync(kFull, x, k);
-  return acc;
-}
 
 __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_warp) {
   const long long t_start = clock64();
@@ -1490,51 +1539,10 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   o.sum_arrivals = E.sum_a;
   o.sum_moves = E.sum_m;
 
-  // K2: compute_metrics (metrics.cpp:70-113), sums in request_id order.
-  if (E.status == LT_OK) {
-    if (E.n_req == 0) {
-      o.degenerate = 1;
-    } else {
-      const double window = E.duration;
-      double rej_demand = 0.0, ttft_sum = 0.0, itl_sum = 0.0;
-      long long nrej = 0, nfin = 0, nttft = 0, nitl = 0;
-      for (int base = 0; base < E.n_req; base += 32) {
-        const int i = base + lane;
-        const bool v = i < E.n_req;
-        int8_t ph = kWaiting;
-        double first = 0.0, arr = 0.0, last = 0.0;
-        int outv = 0, gen = 0;
-        if (v) {
-          ph = P.r_phase[E.rb + i];
-          first = P.r_first[E.rb + i];
-          arr = P.r_arr[E.rb + i];
-          last = P.r_last[E.rb + i];
-          outv = P.r_out[E.rb + i];
-          gen = (ph == kFinished) ? outv : P.r_gen[E.rb + i];
-          if (ph == kFinished) P.r_gen[E.rb + i] = outv;
-        }
-        __syncwarp();
-        const bool is_rej = v && ph == kRejected;
-        const bool has_first = v && first == first;
-        const bool has_itl = v && gen >= 2;
-        nrej += __popc(__ballot_sync(kFull, is_rej));
-        nfin += __popc(__ballot_sync(kFull, v && ph == kFinished));
-        nttft += __popc(__ballot_sync(kFull, has_first));
-        if (__any_sync(kFull, is_rej)) rej_demand = ordered_add(rej_demand, static_cast<double>(outv) / window, is_rej);
-        ttft_sum = ordered_add(ttft_sum, first - arr, has_first);
-        itl_sum = ordered_add(itl_sum, last - first, has_itl);
-        nitl += warp_sum_ll(has_itl ? gen - 1 : 0);
-      }
-      o.rejected_count = nrej;
-      o.finished_count = nfin;
-      o.throughput_tok_s = static_cast<double>(E.tok_win) / window;
-      o.ttft_mean_s = nttft ? ttft_sum / static_cast<double>(nttft) : 0.0;
-      o.itl_mean_s = nitl ? itl_sum / static_cast<double>(nitl) : 0.0;
-      const double eff_raw = sc.ideal - rej_demand;
-      const double eff = (eff_raw < 0.0) ? 0.0 : eff_raw;
-      o.starved = o.throughput_tok_s < 0.9 * eff;
-    }
-  }
+  // Throughput (metrics.cpp:96); the rest of compute_metrics -- counts, the
+  // ordered TTFT / ITL / rejected-demand sums and the starved verdict -- is
+  // metrics_kernel (K2), launched after this kernel.
+  if (E.status == LT_OK && E.n_req > 0) o.throughput_tok_s = static_cast<double>(E.tok_win) / E.duration;
   LT_PH(5);
 #ifdef LT_PHASE_PROF
   for (int k = 0; k < 6; ++k) o.phase_cycles[k] = ph[k];

@@ -18,6 +18,82 @@
 
 namespace lt {
 
+// K2 compute_metrics (metrics.cpp:70-113) of every engine, after K1: one
+// warp per scenario walks its requests in request_id order, 32 at a time
+// (coalesced). Counts are ballots; the three FP64 sums (rejected demand
+// out/window, TTFT first - arrival, ITL last - first: the telescoped per-
+// request sum, SURVEY 7 hard part 8) are the reference's sequential
+// accumulate: each block's 32 terms are broadcast by shuffles and added in
+// lane order, the three chains interleaved. Unflagged lanes add +0.0, which
+// leaves the (non-negative) accumulators unchanged. Finished requests get
+// their final token count (gen = out). Kept out of the engine kernel: its
+// code would sit in the engine's instruction footprint, and its serial add
+// chains at the end of every engine's critical path.
+__global__ void __launch_bounds__(256) metrics_kernel(const DScen* scen, int n_scen, const int8_t* r_phase,
+                                                     const double* r_first, const double* r_arr,
+                                                     const double* r_last, const int32_t* r_out, int32_t* r_gen,
+                                                     lt_sim_summary* out) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int s = static_cast<int>((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5);
+  if (s >= n_scen) return;
+  if (out[s].status != LT_OK) return;
+  const DScen sc = scen[s];
+  const int64_t n = sc.n_req;
+  if (n == 0) {
+    if (lane == 0) out[s].degenerate = 1;
+    return;
+  }
+  const int64_t rb = sc.req_begin;
+  const double window = sc.duration;
+  double rej = 0.0, ttft = 0.0, itl = 0.0;
+  long long nrej = 0, nfin = 0, nttft = 0, nitl = 0;
+  for (int64_t base = 0; base < n; base += 32) {
+    const int64_t i = base + lane;
+    const bool v = i < n;
+    int8_t ph = kWaiting;
+    double first = 0.0, arr = 0.0, last = 0.0;
+    int outv = 0, gen = 0;
+    if (v) {
+      ph = r_phase[rb + i];
+      first = r_first[rb + i];
+      arr = r_arr[rb + i];
+      last = r_last[rb + i];
+      outv = r_out[rb + i];
+      gen = (ph == kFinished) ? outv : r_gen[rb + i];
+      if (ph == kFinished) r_gen[rb + i] = outv;
+    }
+    const bool is_rej = v && ph == kRejected;
+    const bool has_first = v && first == first;
+    const bool has_itl = v && gen >= 2;
+    nrej += __popc(__ballot_sync(full, is_rej));
+    nfin += __popc(__ballot_sync(full, v && ph == kFinished));
+    nttft += __popc(__ballot_sync(full, has_first));
+    long long g1 = has_itl ? gen - 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) g1 += __shfl_xor_sync(full, g1, o);
+    nitl += g1;
+    const double x0 = is_rej ? static_cast<double>(outv) / window : 0.0;
+    const double x1 = has_first ? first - arr : 0.0;
+    const double x2 = has_itl ? last - first : 0.0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      rej = rej + __shfl_sync(full, x0, k);
+      ttft = ttft + __shfl_sync(full, x1, k);
+      itl = itl + __shfl_sync(full, x2, k);
+    }
+  }
+  if (lane == 0) {
+    lt_sim_summary& o = out[s];
+    o.rejected_count = nrej;
+    o.finished_count = nfin;
+    o.ttft_mean_s = nttft ? ttft / static_cast<double>(nttft) : 0.0;
+    o.itl_mean_s = nitl ? itl / static_cast<double>(nitl) : 0.0;
+    const double eff_raw = sc.ideal - rej;
+    const double eff = (eff_raw < 0.0) ? 0.0 : eff_raw;
+    o.starved = o.throughput_tok_s < 0.9 * eff;
+  }
+}
+
 __global__ void ttft_keys_kernel(const double* r_arr, const double* r_first, int64_t n, double* keys) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
