@@ -12,6 +12,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include <algorithm>
 #include <atomic>
@@ -1067,6 +1069,54 @@ int64_t size_keys(PinnedVec<DKeyNI>& keys) {
   return e_total;
 }
 
+// Request arrays and merge scratch for P.total_req requests of P.n_pairs
+// (scenario, adapter) streams over P.n_scen scenarios.
+void alloc_requests(lt_plan& P) {
+  cudaStream_t st = P.st;
+  const int64_t nr = std::max<int64_t>(P.total_req, 1);
+  P.r_arr.alloc(nr);
+  P.r_in.alloc(nr);
+  P.r_out.alloc(nr);
+  P.r_adp.alloc(nr);
+  P.r_phase.alloc(nr);
+  P.r_gen.alloc(nr);
+  P.r_first.alloc(nr);
+  P.r_last.alloc(nr);
+  P.r_pre.alloc(nr);
+  if (P.total_req >= (int64_t(1) << 31)) throw CudaError{"batch too large: more than 2^31 requests in one plan"};
+  if (P.n_pairs > 0) {
+    P.pair_excl.alloc(P.n_pairs);
+    P.st_in.alloc(nr);
+    P.st_out.alloc(nr);
+    P.sv_in.alloc(nr);
+    P.sv_out.alloc(nr);
+    P.seg_begin.alloc(P.n_scen);
+    P.seg_end.alloc(P.n_scen);
+    LT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, P.pscan_tmp_bytes, P.adp_count.p, P.pair_excl.p,
+                                          static_cast<int>(P.n_pairs), st));
+    P.pscan_tmp.alloc(std::max<size_t>(P.pscan_tmp_bytes, 1));
+    if (radix_merge(nr)) {
+      P.pos_a.alloc(nr);
+      P.pos_b.alloc(nr);
+      P.skey_a.alloc(nr);
+      P.skey_b.alloc(nr);
+      P.scen_bits = 1;
+      while ((int64_t(1) << P.scen_bits) < P.n_scen) ++P.scen_bits;
+      size_t b1 = 0, b2 = 0;
+      LT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, P.st_in.p, P.st_out.p, P.pos_a.p, P.pos_b.p,
+                                              static_cast<int>(nr), 0, 64, st));
+      LT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b2, P.skey_a.p, P.skey_b.p, P.pos_b.p, P.pos_a.p,
+                                              static_cast<int>(nr), 0, P.scen_bits, st));
+      P.sort_tmp_bytes = std::max(b1, b2);
+    } else {
+      LT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, P.sort_tmp_bytes, P.st_in.p, P.st_out.p, P.sv_in.p,
+                                                        P.sv_out.p, static_cast<int>(nr), static_cast<int>(P.n_scen),
+                                                        P.seg_begin.p, P.seg_end.p, st));
+    }
+    P.sort_tmp.alloc(std::max<size_t>(P.sort_tmp_bytes, 1));
+  }
+}
+
 // Engine launch shape of a plan (order, variant, warps, shared memory,
 // persistent grid, workspace) from the per-scenario cost estimates and the
 // plan's request counts (max_req, total_req) and max_adapters.
@@ -1355,48 +1405,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   }
   P.total_req = off;
   P.scen.upload(P.h_scen, st);
-  const int64_t nr = std::max<int64_t>(P.total_req, 1);
-  P.r_arr.alloc(nr);
-  P.r_in.alloc(nr);
-  P.r_out.alloc(nr);
-  P.r_adp.alloc(nr);
-  P.r_phase.alloc(nr);
-  P.r_gen.alloc(nr);
-  P.r_first.alloc(nr);
-  P.r_last.alloc(nr);
-  P.r_pre.alloc(nr);
-  if (P.total_req >= (int64_t(1) << 31)) throw CudaError{"batch too large: more than 2^31 requests in one plan"};
-  if (n_pairs > 0) {
-    P.pair_excl.alloc(n_pairs);
-    P.st_in.alloc(nr);
-    P.st_out.alloc(nr);
-    P.sv_in.alloc(nr);
-    P.sv_out.alloc(nr);
-    P.seg_begin.alloc(P.n_scen);
-    P.seg_end.alloc(P.n_scen);
-    LT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, P.pscan_tmp_bytes, P.adp_count.p, P.pair_excl.p,
-                                          static_cast<int>(n_pairs), st));
-    P.pscan_tmp.alloc(std::max<size_t>(P.pscan_tmp_bytes, 1));
-    if (radix_merge(nr)) {
-      P.pos_a.alloc(nr);
-      P.pos_b.alloc(nr);
-      P.skey_a.alloc(nr);
-      P.skey_b.alloc(nr);
-      P.scen_bits = 1;
-      while ((int64_t(1) << P.scen_bits) < P.n_scen) ++P.scen_bits;
-      size_t b1 = 0, b2 = 0;
-      LT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, P.st_in.p, P.st_out.p, P.pos_a.p, P.pos_b.p,
-                                              static_cast<int>(nr), 0, 64, st));
-      LT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b2, P.skey_a.p, P.skey_b.p, P.pos_b.p, P.pos_a.p,
-                                              static_cast<int>(nr), 0, P.scen_bits, st));
-      P.sort_tmp_bytes = std::max(b1, b2);
-    } else {
-      LT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, P.sort_tmp_bytes, P.st_in.p, P.st_out.p, P.sv_in.p,
-                                                        P.sv_out.p, static_cast<int>(nr), static_cast<int>(P.n_scen),
-                                                        P.seg_begin.p, P.seg_end.p, st));
-    }
-    P.sort_tmp.alloc(std::max<size_t>(P.sort_tmp_bytes, 1));
-  }
+  alloc_requests(P);
   // scripted requests
   {
     std::vector<double> arr;
@@ -1492,6 +1501,8 @@ void untrim_plan(lt_plan& P) {
   P.trimmed = false;
 }
 
+int64_t merge_requests(lt_plan& P);
+
 // K0 + merge: (re)generates every request of every generated scenario.
 void prepare_requests(lt_plan& P) {
   lt_ctx* ctx = P.ctx;
@@ -1522,6 +1533,17 @@ void prepare_requests(lt_plan& P) {
     launches += 2;
   }
   cudaEventRecord(P.ev[2], st);
+  launches += merge_requests(P);
+  cudaEventRecord(P.ev[3], st);
+  P.fresh = false;
+  P.launches_run = launches + 2;  // + engine, metrics (launch_engine)
+}
+
+// Arrival merge of the counted streams: per-pair times (expand), stable sort
+// by time per scenario, gather into the request arrays. Returns own launches.
+int64_t merge_requests(lt_plan& P) {
+  cudaStream_t st = P.st;
+  int64_t launches = 0;
   if (P.n_pairs > 0) {
     // sort-based merge: unsorted times per (scenario, adapter), stable
     // segmented sort by time, gather into request arrays
@@ -1564,9 +1586,7 @@ void prepare_requests(lt_plan& P) {
     after_launch("gather_kernel", st);
     launches += 2;  // expand, gather (own kernels; CUB's scan and sorts not counted)
   }
-  cudaEventRecord(P.ev[3], st);
-  P.fresh = false;
-  P.launches_run = launches + 2;  // + engine, metrics (launch_engine)
+  return launches;
 }
 
 // K1 (the engine kernel) then K2 (metrics_kernel) over the plan's scenarios.
@@ -2008,6 +2028,8 @@ void fetch_staged(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {
 }
 
 }  // namespace
+
+#include "host_sweep.h"
 
 // ============================================================================
 // C-ABI
@@ -2511,14 +2533,19 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
         rows.push_back(r);
       }
     }
-    // Conditions -> grid-point scenarios (instantiate_condition, placement.cpp:139-157):
-    // adapter ids 1..N with (rank, rate) = mix[(id-1) % |mix|]; every point of a
-    // condition reads a prefix of the condition's n_max-adapter block.
-    std::vector<lt_adapter> adapters;
-    std::vector<int64_t> cond_base(n_cond, -1);
-    std::vector<int64_t> cond_ab(n_cond, -1);
+    // Condition validation (sweep_optimal, placement.cpp:186-188); grid
+    // points of valid conditions are numbered row-major per condition.
+    SweepSetup S;
+    S.batch = batch;
+    S.rows = rows;
+    S.g_list = g_list;
+    S.per_cond = per_cond;
+    S.n_max = n_max;
+    S.duration = duration_s;
+    S.seed = seed;
+    S.options = options;
+    S.cond_base.assign(n_cond, -1);
     std::vector<HostErr> cond_err(n_cond);
-    int64_t n_points = 0;
     for (int64_t c = 0; c < n_cond; ++c) {
       const lt_condition& cd = batch->conditions[c];
       HostErr& e = cond_err[c];
@@ -2531,134 +2558,33 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
         e.set(LT_ERR_VALIDATION, "condition.mix: must be non-empty");
         continue;
       }
-      cond_ab[c] = static_cast<int64_t>(adapters.size());
-      for (int i = 0; i < n_max; ++i) {
-        const lt_template& t = batch->templates[cd.mix_offset + (i % cd.mix_count)];
-        lt_adapter a{};
-        a.adapter_id = i + 1;
-        a.rank = t.rank;
-        a.rate = t.rate;
-        a.length_index = -1;
-        adapters.push_back(a);
-      }
-      cond_base[c] = n_points;
-      n_points += per_cond;
+      S.cond_base[c] = S.n_points;
+      S.n_points += per_cond;
     }
-    // Rows are simulated in waves, exactly as sweep_optimal consumes them
-    // (placement.cpp:204-245): wave r holds row r of every condition that has
-    // neither stopped early nor failed, so the device simulates the same grid
-    // points as the reference. Waves are chunked by estimated work.
-    std::vector<lt_sim_summary> pts(std::max<int64_t>(n_points, 1));
-    std::vector<std::string> pt_msg(std::max<int64_t>(n_points, 1));
-    std::vector<char> active(n_cond, 0);
-    std::vector<double> best(n_cond, -1.0);
-    std::vector<int> stall(n_cond, 0);
-    for (int64_t c = 0; c < n_cond; ++c) active[c] = cond_base[c] >= 0;
+    const std::vector<int64_t>& cond_base = S.cond_base;
     lt_sim_options so{};
     if (sim_options) so = *sim_options;
     so.want_digest = 0;
-    double engine_ms = 0, tables_ms = 0, merge_ms = 0, run_ms = 0;
-    int64_t launches = 0, algo = 0;
-    // estimated requests per device batch: a whole row in one batch lets its
-    // longest engines run side by side (lt_simulate_batch bounds memory itself)
-    const double budget = 5.0e8;
-    for (size_t ni = 0; ni < rows.size(); ++ni) {
-      const SweepRow& r = rows[ni];
-      std::vector<int64_t> conds;
-      for (int64_t c = 0; c < n_cond; ++c)
-        if (active[c]) conds.push_back(c);
-      size_t ci = 0;
-      while (ci < conds.size()) {
-        std::vector<lt_scenario> scen;
-        std::vector<int64_t> pidx;
-        double est = 0.0;
-        while (ci < conds.size() && (scen.empty() || est < budget)) {
-          const int64_t c = conds[ci++];
-          const lt_condition& cd = batch->conditions[c];
-          double rate_sum = 0.0;
-          for (int i = 0; i < r.n; ++i) rate_sum += batch->templates[cd.mix_offset + (i % cd.mix_count)].rate;
-          for (int gi = 0; gi < r.g_count; ++gi) {
-            lt_scenario s{};
-            s.adapter_offset = cond_ab[c];
-            s.n_adapters = r.n;
-            s.length_index = cd.length_index;
-            s.duration_s = duration_s;
-            s.seed = seed;
-            s.slots = g_list[r.g_offset + gi];
-            s.mode = options->mode;
-            s.n_requests = -1;
-            scen.push_back(s);
-            pidx.push_back(cond_base[c] + r.point_offset + gi);
-            est += rate_sum * duration_s;
-          }
-        }
-        lt_workload_batch wb{};
-        wb.scenarios = scen.data();
-        wb.n_scenarios = static_cast<int64_t>(scen.size());
-        wb.adapters = adapters.data();
-        wb.n_adapters = static_cast<int64_t>(adapters.size());
-        wb.lengths = batch->lengths;
-        wb.n_lengths = batch->n_lengths;
-        wb.full_lengths = batch->full_lengths;
-        wb.n_full_pairs = batch->n_full_pairs;
-        std::unique_ptr<lt_plan> plan(build_plan(ctx, &wb, config, &so));
-        run_plan(*plan);
-        std::vector<lt_sim_summary> part(scen.size());
-        fetch_results(*plan, part.data(), nullptr);
-        for (size_t k = 0; k < scen.size(); ++k) {
-          pts[pidx[k]] = part[k];
-          pt_msg[pidx[k]] = ctx->messages[k];
-        }
-        if (std::getenv("LT_HOST_TIMING")) {
-          int64_t it = 0, itmax = 0, cyc = 0;
-          for (const lt_sim_summary& q : part) {
-            it += q.iterations;
-            itmax = std::max<int64_t>(itmax, q.iterations);
-            cyc = std::max<int64_t>(cyc, q.device_cycles);
-          }
-          std::fprintf(stderr, "[lt] sweep row N=%d: %zu points, engine %.1f ms, iterations %lld (max %lld), "
-                       "longest engine %.1f Mcycles\n", r.n, scen.size(), ctx->timing.engine_ms,
-                       static_cast<long long>(it), static_cast<long long>(itmax), cyc / 1e6);
-        }
-        engine_ms += ctx->timing.engine_ms;
-        tables_ms += ctx->timing.tables_ms;
-        merge_ms += ctx->timing.merge_ms;
-        run_ms += ctx->timing.run_ms;
-        launches += ctx->timing.engine_launches;
-        algo += ctx->timing.algorithmic_bytes;
-      }
-      // mirror of the reduction's control flow: which conditions continue
-      for (int64_t c : conds) {
-        bool improved = false, err = false;
-        for (int gi = 0; gi < r.g_count; ++gi) {
-          const lt_sim_summary& p = pts[cond_base[c] + r.point_offset + gi];
-          if (p.status != LT_OK) err = true;
-          if (!p.starved && p.throughput_tok_s > best[c]) {
-            best[c] = p.throughput_tok_s;
-            improved = true;
-          }
-        }
-        if (err) {
-          active[c] = 0;
-          continue;
-        }
-        if (options->early_exit) {
-          stall[c] = improved ? 0 : stall[c] + 1;
-          if (stall[c] >= options->early_exit_k && ni + 1 < rows.size()) active[c] = 0;
-        }
-      }
-    }
+    Config probe;
+    load_config(probe, config, &so);
+    SweepTiming tm;
+    DBuf<lt_sim_summary> d_pts;
+    std::unordered_map<int64_t, std::string> point_msg;
+    if (grid_ok && sweep_device_eligible(S, probe))
+      sweep_waves_device(ctx, S, config, so, d_pts, point_msg, tm);
+    else
+      sweep_waves_host(ctx, S, config, so, d_pts, point_msg, tm);
+    double engine_ms = tm.engine_ms, tables_ms = tm.tables_ms, merge_ms = tm.merge_ms, run_ms = tm.run_ms;
+    int64_t launches = tm.launches, algo = tm.algo;
     ctx->messages.assign(n_cond, std::string());
     DBuf<SweepRow> d_rows;
     DBuf<int32_t> d_g;
     DBuf<int64_t> d_base;
-    DBuf<lt_sim_summary> d_pts;
     DBuf<lt_placement> d_out;
     DBuf<lt_frontier_point> d_front;
     d_rows.upload(rows, st);
     d_g.upload(g_list, st);
     d_base.upload(cond_base, st);
-    d_pts.upload(pts, st);
     d_out.alloc(std::max<int64_t>(n_cond, 1));
     d_front.alloc(std::max<int64_t>(n_cond * max_frontier, 1));
     cudaEventRecord(ctx->ev[5], st);
@@ -2690,7 +2616,8 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
         p.status_b = cond_err[c].b;
         msg = cond_err[c].msg;
       } else if (p.status != LT_OK) {
-        msg = pt_msg[p.status_point];
+        auto it = point_msg.find(p.status_point);
+        msg = it != point_msg.end() ? it->second : render(p.status, p.status_kind, p.status_a, p.status_b);
       }
       ctx->messages[c] = msg;
       if (p.status != LT_OK && rc == LT_OK) {

@@ -525,3 +525,42 @@ def test_radix_merge_matches_segmented_merge(dev, monkeypatch):
         for k in s1:
             np.testing.assert_array_equal(s1[k], s2[k], err_msg=k)
         assert m1 == m2
+
+
+def _sweep_error_config():
+    """h100_like with no slot cost for rank 32 (ConfigError in the Engine ctor),
+    a budget that makes G = 64 infeasible at rank 16 (ConfigError), and no
+    load latency for rank 16 (ConfigError at its first load): every error a
+    sweep point can hit."""
+    cfg = lt.h100_like_config(1)
+    cfg.memory = lt.MemoryModel(total_kv_budget=60_000, kv_bytes_per_token=1.0, slot_cost_table={8: 800, 16: 1600})
+    cfg.load = lt.LoadLatencyTable(cpu_load_seconds={8: 0.04, 32: 0.12})
+    return cfg
+
+
+@pytest.mark.parametrize("host_waves", [False, True])
+def test_sweep_waves_errors_and_early_exit_match_reference(dev, ref, monkeypatch, host_waves):
+    """lt_sweep_batch's device waves (conditions instantiated on the device,
+    early exit decided on the device) and its host waves (LT_SWEEP_HOST=1)
+    against the reference's sweep_optimal: placements, frontiers, and the
+    lowest-index point error of each condition with its exact message."""
+    if host_waves:
+        monkeypatch.setenv("LT_SWEEP_HOST", "1")
+    conds = lt.enumerate_conditions([3.2, 0.4, 0.05, 0.0125], [8, 16, 32], lt.LengthSpec.mean(250, 50, 231, 50),
+                                    triple_size=2, condition_stride=2)
+    grid = lt.SweepGrid(n_values=[1, 2, 4, 16, 64], g_mode=lt.GMode.Explicit, g_values=[2, 8, 32, 64])
+    opts = lt.SweepOptions(early_exit=True, early_exit_k=2)
+    for cfg in (_sweep_error_config(), lt.h100_like_config(1)):
+        cb = ConditionBatch.from_conditions(conds)
+        gp, gf = dev.sweep_batch(cb, cfg, grid, 90.0, 11, opts)
+        rp, rf = ref.sweep(cb, cfg, grid, 90.0, 11, opts, sim_options())
+        for f in ("status", "n_star", "g_star", "all_starved", "frontier_open", "frontier_count",
+                  "max_throughput_tok_s", "points_simulated"):
+            np.testing.assert_array_equal(gp[f], rp[f], err_msg=f)
+        for i in range(len(conds)):
+            n = int(gp[i]["frontier_count"])
+            if gp[i]["status"] == 0:
+                np.testing.assert_array_equal(gf[i][:n], rf[i][:n])
+            else:
+                assert dev.message(i) == ref.message(i), i
+    assert set(gp["status"]) == {0}
