@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define LT_ABI_VERSION 1
+#define LT_ABI_VERSION 2
 
 /* Exception classes of errors.hpp, plus two conditions of this library. */
 enum lt_code {
@@ -307,6 +307,11 @@ typedef struct lt_timing {
   int64_t algorithmic_bytes; /* B_iter summed over the engine launches */
   double plan_ms;    /* host wall time of building the plan (validation, packing, sizing passes) */
   double run_wait_ms; /* host wall time from lt_plan_run to results copied back */
+  /* multi-device contexts: device phases above are the slowest member's */
+  double gather_ms;     /* wall time of the cross-device gather + the one copy back (sweeps) */
+  int64_t gather_bytes; /* bytes moved between devices by that gather */
+  int32_t devices;      /* members that ran the call (0 for a single-device context) */
+  int32_t _pad;
 } lt_timing;
 
 int32_t lt_abi_version(void);
@@ -316,6 +321,23 @@ int32_t lt_host_libm_variant(void);
 void lt_format_status(int32_t code, int32_t kind, int64_t a, int64_t b, char* buf, size_t len);
 
 lt_ctx* lt_create(int32_t device, lt_status* status);
+
+/* Multi-device context (SURVEY 8b `lt_create(device_mask)`, 8e). Replaces the
+ * reference's thread pool over conditions (run_parallel, placement.cpp:65-96,
+ * as generate_dataset uses it at :492-522) with the GPUs of one box:
+ * lt_simulate_batch / lt_sweep_batch / lt_generate_dataset on it shard the
+ * scenarios / conditions by estimated cost (LPT) over one member context per
+ * entry, run the members on their own host threads, and gather the sweeps'
+ * per-condition placements + frontiers to the first device (NCCL send/recv
+ * when the devices are distinct, peer copies otherwise) before one copy back.
+ * Results, statuses and messages are those of the single-device call.
+ * lt_create_devices may repeat a device (members then share that GPU);
+ * plans and lt_generate_arrivals_batch run on the first member. */
+lt_ctx* lt_create_devices(const int32_t* devices, int32_t n_devices, lt_status* status);
+lt_ctx* lt_create_mask(uint64_t device_mask, lt_status* status); /* bit d = CUDA device d */
+int32_t lt_device_count(lt_ctx* ctx);
+enum lt_gather_transport { LT_GATHER_NONE = 0, LT_GATHER_NCCL = 1, LT_GATHER_PEER = 2 };
+int32_t lt_gather_transport(lt_ctx* ctx);
 void lt_destroy(lt_ctx* ctx);
 /* The cudaStream_t (as void*) all work of this context runs on. */
 void* lt_stream(lt_ctx* ctx);

@@ -7,7 +7,7 @@ from .types import (AdapterSpec, AdapterTemplate, Condition, ConfigError, Device
                     SweepGrid, SweepOptions, UnsupportedError, ValidationError, WorkloadSpec, enumerate_conditions,
                     h100_like_config, instantiate_condition)
 from .batch import ConditionBatch, WorkloadBatch
-from .api import (Device, Plan, compute_metrics, condition_hash, device, encode_workload, generate_arrivals,
+from .api import (Device, Plan, device_group, compute_metrics, condition_hash, device, encode_workload, generate_arrivals,
                   generate_dataset, ideal_throughput, load_library, run_scripted, run_simulation, sweep_conditions, sweep_optimal)
 
 __version__ = "0.1.0"

@@ -11,13 +11,14 @@ import os
 
 import numpy as np
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # enum lt_code
 LT_OK, LT_ERR_VALIDATION, LT_ERR_CONFIG, LT_ERR_SIMULATION, LT_ERR_INTERNAL, LT_ERR_UNSUPPORTED, LT_ERR_DEVICE = range(7)
 MODE_FULL, MODE_MEAN = 0, 1
 SOURCE_CPU, SOURCE_DISK = 0, 1
 G_GEOMETRIC, G_EXPLICIT = 0, 1
+GATHER_NONE, GATHER_NCCL, GATHER_PEER = 0, 1, 2
 
 
 class lt_status(C.Structure):
@@ -158,7 +159,8 @@ class lt_timing(C.Structure):
                 ("engine_ms", C.c_double), ("reduce_ms", C.c_double), ("d2h_ms", C.c_double),
                 ("total_ms", C.c_double), ("run_ms", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("engine_launches", C.c_int64), ("algorithmic_bytes", C.c_int64), ("plan_ms", C.c_double),
-                ("run_wait_ms", C.c_double)]
+                ("run_wait_ms", C.c_double), ("gather_ms", C.c_double), ("gather_bytes", C.c_int64),
+                ("devices", C.c_int32), ("_pad", C.c_int32)]
 
 
 # numpy views with the exact C layouts (numpy honours ctypes field offsets)
@@ -189,6 +191,10 @@ SIGNATURES = {
     "host_libm_variant": (C.c_int32, []),
     "format_status": (None, [C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_char_p, C.c_size_t]),
     "create": (C.c_void_p, [C.c_int32, C.POINTER(lt_status)]),
+    "create_devices": (C.c_void_p, [C.POINTER(C.c_int32), C.c_int32, C.POINTER(lt_status)]),
+    "create_mask": (C.c_void_p, [C.c_uint64, C.POINTER(lt_status)]),
+    "device_count": (C.c_int32, [C.c_void_p]),
+    "gather_transport": (C.c_int32, [C.c_void_p]),
     "destroy": (None, [C.c_void_p]),
     "stream": (C.c_void_p, [C.c_void_p]),
     "last_timing": (C.c_int32, [C.c_void_p, C.POINTER(lt_timing)]),

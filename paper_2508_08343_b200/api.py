@@ -42,16 +42,30 @@ def load_library() -> A.Lib:
 
 
 class Device:
-    """One lt_ctx (one B200, one CUDA stream)."""
+    """One lt_ctx: one B200 (lt_create), or several (lt_create_devices: the
+    batch calls shard scenarios / conditions across them and gather the
+    sweeps' placements to the first device)."""
 
-    def __init__(self, index: int = 0):
+    def __init__(self, index: int = 0, devices: Optional[Sequence[int]] = None):
         self.lib = load_library()
         st = A.lt_status()
-        self.ctx = self.lib.create(index, C.byref(st))
+        if devices is None:
+            self.ctx = self.lib.create(index, C.byref(st))
+        else:
+            arr = (C.c_int32 * len(devices))(*devices)
+            self.ctx = self.lib.create_devices(arr, len(devices), C.byref(st))
         if not self.ctx:
             raise DeviceError(st.message.decode())
-        self.index = index
+        self.index = index if devices is None else devices[0]
+        self.devices = [index] if devices is None else list(devices)
         self.runner = Runner(self.lib, self.ctx, self.message)
+
+    def device_count(self) -> int:
+        return self.lib.device_count(self.ctx)
+
+    def gather_transport(self) -> str:
+        return {A.GATHER_NONE: "none", A.GATHER_NCCL: "nccl", A.GATHER_PEER: "peer"}[
+            self.lib.gather_transport(self.ctx)]
 
     def message(self, i: int) -> str:
         buf = C.create_string_buffer(512)
@@ -142,6 +156,11 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+def device_group(devices: Sequence[int]) -> Device:
+    """A multi-device context over `devices` (a device may repeat)."""
+    return Device(devices=devices)
 
 
 def device(index: int = 0) -> Device:

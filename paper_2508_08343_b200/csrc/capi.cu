@@ -298,9 +298,10 @@ struct BlockCache {
     while (c < bytes) c <<= 1;  // power-of-two classes bound waste at 2x
     return c;
   }
-  void* take(size_t bytes, size_t* got) {
+  void* take(size_t bytes, size_t* got, int* device) {
     int dev = 0;
     cudaGetDevice(&dev);
+    *device = dev;
     const size_t cls = size_class(bytes);
     {
       std::lock_guard<std::mutex> lk(mu);
@@ -324,9 +325,7 @@ struct BlockCache {
     *got = cls;
     return p;
   }
-  void give(void* p, size_t cls) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  void give(void* p, size_t cls, int dev) {
     std::lock_guard<std::mutex> lk(mu);
     free_blocks.emplace(std::make_pair(dev, cls), p);
   }
@@ -348,12 +347,13 @@ struct DBuf {
   T* p = nullptr;
   size_t n = 0;
   size_t cls = 0;
+  int dev = 0;  // the block goes back to its own device's free list, whichever thread releases it
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) BlockCache::get().give(p, cls);
+    if (p) BlockCache::get().give(p, cls, dev);
     p = nullptr;
     n = 0;
     cls = 0;
@@ -365,7 +365,7 @@ struct DBuf {
     }
     release();
     n = count;
-    if (count) p = static_cast<T*>(BlockCache::get().take(count * sizeof(T), &cls));
+    if (count) p = static_cast<T*>(BlockCache::get().take(count * sizeof(T), &cls, &dev));
   }
   void upload(const std::vector<T>& v, cudaStream_t s) { upload(v.data(), v.size(), s); }
   void upload(const T* src, size_t count, cudaStream_t s) {
@@ -380,12 +380,17 @@ struct lt_ctx {
   std::vector<std::string> messages;  // per scenario / condition of the last call
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t stream2 = nullptr;  // second part of a staged plan
+  cudaStream_t stream2 = nullptr;  // every other chunk of a chunked lt_simulate_batch
   cudaStream_t stream_up = nullptr;  // packed-scenario uploads, beside K0
   int smem_optin = 0;              // max dynamic shared memory per block (opt-in)
   int sm_count = 0;
   lt_timing timing{};
   cudaEvent_t ev[8]{};
+  // multi-device context (lt_create_devices): one single-device member per
+  // entry; the group's own streams are the first member's
+  std::vector<lt_ctx*> members;
+  std::vector<void*> comms;  // ncclComm_t per member (LT_GATHER_NCCL)
+  int32_t transport = LT_GATHER_NONE;
 };
 
 // A prepared batch: everything the kernels need, resident in HBM.
@@ -394,20 +399,11 @@ struct lt_plan {
   cudaStream_t st = nullptr;  // the stream this plan's work runs on
   cudaEvent_t ev[8]{};        // this plan's timing events
   cudaEvent_t ev_up = nullptr;  // packed-scenario uploads done (ctx->stream_up)
-  // staged plan: parts[0] = the most expensive scenarios (engine started
-  // first, one warp per block so the other part's K0/merge kernels share the
-  // SMs), parts[1] = the rest, prepared concurrently on a second stream
-  std::unique_ptr<lt_plan> parts[2];
-  std::vector<int64_t> part_idx[2];
-  DBuf<int64_t> part_map[2];
-  cudaEvent_t ev_start = nullptr, ev_join = nullptr;
   int warps_per_block = 8;
   ~lt_plan() {
     for (cudaEvent_t e : ev)
       if (e) cudaEventDestroy(e);
-    if (ev_start) cudaEventDestroy(ev_start);
     if (ev_up) cudaEventDestroy(ev_up);
-    if (ev_join) cudaEventDestroy(ev_join);
   }
   Config cfg;
   int64_t n_scen = 0;
@@ -1186,8 +1182,8 @@ void size_engine(lt_plan& P, const std::vector<double>& cost, int max_run_cap) {
   }
   // The device's opt-in maximum (a constant, so plans built concurrently on
   // other host threads never lower it under each other) and the max-shared
-  // carveout, so blocks of a staged plan's two parts (and the K0 seed kernel)
-  // can share an SM.
+  // carveout, so an engine block and the K0 seed kernel of the next chunk can
+  // share an SM.
   const void* ek = P.engine_variant == 2   ? reinterpret_cast<const void*>(engine_kernel<256, 2>)
                    : P.engine_variant == 3 ? reinterpret_cast<const void*>(engine_kernel<384, 1>)
                                            : reinterpret_cast<const void*>(engine_kernel<256, 1>);
@@ -1841,195 +1837,24 @@ int32_t first_error(lt_ctx* ctx, const lt_sim_summary* out, int64_t n, lt_status
   return LT_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Staged plans: the few most expensive engines set the step time (one warp
-// each, ~10^4 dependent iterations), while everything else -- the K0 tables
-// and the arrival merge of the other scenarios, and their shorter engines --
-// can run beside them. A staged plan builds two plans: part 0 holds the
-// most expensive scenarios and launches its engine with one warp per block
-// (small blocks leave shared memory for the other part's kernels), part 1
-// the rest on a second stream. Outputs are scattered back to batch order.
-
-__global__ void scatter_summaries(const lt_sim_summary* src, const int64_t* map, int64_t n, lt_sim_summary* dst) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) dst[map[i]] = src[i];
-}
-
-bool want_staged(lt_ctx* ctx, const lt_workload_batch* b, const lt_sim_options* opts) {
-  if (opts && opts->want_percentiles) return false;  // the recording pass synchronises the host
-  // Opt-in (LT_STAGED=1). Measured on C2 (1,024 engines): the expensive part's
-  // own K0 is not small (3.4 ms) and the two parts' engines slow each other on
-  // shared SMs, so the step got slower (47.7 vs 37.8 ms); kept for batches
-  // whose preparation dwarfs their few long engines.
-  (void)ctx;
-  if (const char* env = std::getenv("LT_STAGED")) return std::atoi(env) != 0 && b->n_scenarios >= 2;
-  return false;
-}
-
-lt_plan* build_staged(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_config* cfg,
-                      const lt_sim_options* opts) {
-  const int64_t n = b->n_scenarios;
-  std::vector<double> cost(n, 0.0);
-  for (int64_t i = 0; i < n; ++i) {
-    const lt_scenario& s = b->scenarios[i];
-    if (s.n_requests >= 0) {
-      cost[i] = static_cast<double>(s.n_requests);
-      continue;
-    }
-    for (int32_t k = 0; k < s.n_adapters; ++k) cost[i] += b->adapters[s.adapter_offset + k].rate * s.duration_s;
+// Requests a scenario can generate: the Poisson mean of every adapter plus
+// 8 sigma and slack (the same bound that sizes the RNG tables), or the
+// scripted list.
+double est_requests(const lt_workload_batch* b, int64_t i) {
+  const lt_scenario& s = b->scenarios[i];
+  if (s.n_requests >= 0) return static_cast<double>(s.n_requests);
+  double e = 0.0;
+  for (int32_t k = 0; k < s.n_adapters; ++k) {
+    const double lam = std::max(b->adapters[s.adapter_offset + k].rate, 0.0) * std::max(s.duration_s, 0.0);
+    e += lam + 8.0 * std::sqrt(lam) + 32.0;
   }
-  std::vector<int64_t> order(n);
-  for (int64_t i = 0; i < n; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return cost[x] > cost[y]; });
-  const int64_t na = std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count, n / 4));
-  std::vector<char> in_a(n, 0);
-  for (int64_t k = 0; k < na; ++k) in_a[order[k]] = 1;
-  auto plan = std::make_unique<lt_plan>();
-  lt_plan& P = *plan;
-  P.ctx = ctx;
-  P.st = ctx->stream;
-  P.n_scen = n;
-  for (int64_t i = 0; i < n; ++i) P.part_idx[in_a[i] ? 0 : 1].push_back(i);
-  for (int g = 0; g < 2; ++g) {
-    std::vector<lt_scenario> sc;
-    for (int64_t i : P.part_idx[g]) sc.push_back(b->scenarios[i]);
-    lt_workload_batch sub = *b;
-    sub.scenarios = sc.data();
-    sub.n_scenarios = static_cast<int64_t>(sc.size());
-    int rc_b = 1024;
-    if (const char* env = std::getenv("LT_STAGED_B_RUNCAP")) rc_b = std::atoi(env);
-    P.parts[g].reset(build_plan(ctx, &sub, cfg, opts, g == 0 ? 1 : 8, g == 0 ? 1024 : rc_b));
-    P.part_map[g].upload(P.part_idx[g], ctx->stream);
-  }
-  P.parts[1]->st = ctx->stream2;
-  P.out.alloc(n);
-  LT_CUDA(cudaEventCreate(&P.ev_start));
-  LT_CUDA(cudaEventCreate(&P.ev_join));
-  LT_CUDA(cudaStreamSynchronize(ctx->stream));
-  return plan.release();
-}
-
-void run_staged(lt_plan& P) {
-  cudaStream_t s1 = P.ctx->stream, s2 = P.parts[1]->st;
-  LT_CUDA(cudaEventRecord(P.ev_start, s1));
-  LT_CUDA(cudaStreamWaitEvent(s2, P.ev_start, 0));
-  run_plan(*P.parts[0]);  // expensive engines first ...
-  run_plan(*P.parts[1]);  // ... the rest prepared and simulated beside them
-  LT_CUDA(cudaEventRecord(P.parts[1]->ev[7], s2));
-  LT_CUDA(cudaStreamWaitEvent(s1, P.parts[1]->ev[7], 0));
-  for (int g = 0; g < 2; ++g) {
-    const int64_t m = P.parts[g]->n_scen;
-    if (m == 0) continue;
-    scatter_summaries<<<static_cast<unsigned>((m + 255) / 256), 256, 0, s1>>>(P.parts[g]->out.p, P.part_map[g].p, m,
-                                                                           P.out.p);
-    after_launch("scatter_summaries", s1);
-  }
-  LT_CUDA(cudaEventRecord(P.ev_join, s1));
-}
-
-void fetch_staged(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {
-  lt_ctx* ctx = P.ctx;
-  const int64_t n = P.n_scen;
-  std::vector<std::string> msgs(n);
-  // per part: summaries, messages and (optionally) request states in part order
-  struct PartStates {
-    std::vector<int64_t> off;
-    std::vector<int8_t> phase;
-    std::vector<int32_t> gen, pre, aid, in, outv;
-    std::vector<double> first, comp, arr;
-  } ps[2];
-  std::vector<lt_sim_summary> po[2];
-  lt_timing tsum{};
-  for (int g = 0; g < 2; ++g) {
-    lt_plan& Q = *P.parts[g];
-    po[g].resize(std::max<int64_t>(Q.n_scen, 1));
-    lt_request_states qs{};
-    if (states) {
-      PartStates& q = ps[g];
-      const int64_t r = std::max<int64_t>(Q.total_req, 1);
-      q.off.resize(std::max<int64_t>(Q.n_scen, 1));
-      q.phase.resize(r);
-      q.gen.resize(r);
-      q.pre.resize(r);
-      q.aid.resize(r);
-      q.in.resize(r);
-      q.outv.resize(r);
-      q.first.resize(r);
-      q.comp.resize(r);
-      q.arr.resize(r);
-      qs.capacity = Q.total_req;
-      qs.req_offset = q.off.data();
-      qs.phase = q.phase.data();
-      qs.tokens_generated = q.gen.data();
-      qs.first_token_time_s = q.first.data();
-      qs.completion_time_s = q.comp.data();
-      qs.preemption_count = q.pre.data();
-      qs.adapter_id = q.aid.data();
-      qs.input_tokens = q.in.data();
-      qs.output_tokens = q.outv.data();
-      qs.arrival_time_s = q.arr.data();
-    }
-    fetch_results(Q, po[g].data(), states ? &qs : nullptr);
-    for (int64_t i = 0; i < Q.n_scen; ++i) {
-      out[P.part_idx[g][i]] = po[g][i];
-      msgs[P.part_idx[g][i]] = ctx->messages[i];
-    }
-    const lt_timing& t = ctx->timing;
-    tsum.tables_ms = std::max(tsum.tables_ms, t.tables_ms);
-    tsum.merge_ms = std::max(tsum.merge_ms, t.merge_ms);
-    tsum.h2d_bytes += t.h2d_bytes;
-    tsum.d2h_bytes += t.d2h_bytes;
-    tsum.engine_launches += t.engine_launches;
-  }
-  if (states) {  // request states back in batch order
-    std::vector<std::pair<int, int64_t>> where(n);
-    for (int g = 0; g < 2; ++g)
-      for (int64_t i = 0; i < static_cast<int64_t>(P.part_idx[g].size()); ++i) where[P.part_idx[g][i]] = {g, i};
-    int64_t off = 0;
-    for (int64_t k = 0; k < n; ++k) {
-      const auto [g, i] = where[k];
-      const PartStates& q = ps[g];
-      if (states->req_offset) states->req_offset[k] = off;
-      const int64_t b0 = q.off[i];
-      for (int64_t r = 0; r < out[k].n_requests; ++r, ++off) {
-        if (off >= states->capacity) continue;
-        const int64_t j = b0 + r;
-        if (states->phase) states->phase[off] = q.phase[j];
-        if (states->tokens_generated) states->tokens_generated[off] = q.gen[j];
-        if (states->first_token_time_s) states->first_token_time_s[off] = q.first[j];
-        if (states->completion_time_s) states->completion_time_s[off] = q.comp[j];
-        if (states->preemption_count) states->preemption_count[off] = q.pre[j];
-        if (states->adapter_id) states->adapter_id[off] = q.aid[j];
-        if (states->input_tokens) states->input_tokens[off] = q.in[j];
-        if (states->output_tokens) states->output_tokens[off] = q.outv[j];
-        if (states->arrival_time_s) states->arrival_time_s[off] = q.arr[j];
-      }
-    }
-  }
-  ctx->messages = std::move(msgs);
-  if (std::getenv("LT_HOST_TIMING")) {
-    lt_plan &A = *P.parts[0], &B = *P.parts[1];
-    std::fprintf(stderr,
-                 "[lt] staged: A prep %.2f engine %.2f..%.2f ms | B prep %.2f..%.2f engine %.2f..%.2f ms | join %.2f\n",
-                 elapsed(P.ev_start, A.ev[4]), elapsed(P.ev_start, A.ev[4]), elapsed(P.ev_start, A.ev[5]),
-                 elapsed(P.ev_start, B.ev[0]), elapsed(P.ev_start, B.ev[3]), elapsed(P.ev_start, B.ev[4]),
-                 elapsed(P.ev_start, B.ev[5]), elapsed(P.ev_start, P.ev_join));
-  }
-  tsum.run_ms = elapsed(P.ev_start, P.ev_join);
-  tsum.engine_ms = elapsed(P.parts[0]->ev[4], P.ev_join);  // first engine launch .. both parts done
-  tsum.engine_launches += 2;
-  int64_t bytes = 0;
-  for (int64_t i = 0; i < n; ++i) {
-    const lt_sim_summary& o = out[i];
-    bytes += 20 * o.sum_running + 16 * o.sum_visited + 24 * o.sum_arrivals + 16 * o.sum_moves + 64 * o.iterations;
-  }
-  tsum.algorithmic_bytes = bytes;
-  ctx->timing = tsum;
+  return e;
 }
 
 }  // namespace
 
 #include "host_sweep.h"
+#include "host_group.h"
 
 // ============================================================================
 // C-ABI
@@ -2168,8 +1993,85 @@ lt_ctx* lt_create(int32_t device, lt_status* status) {
   }
 }
 
+lt_ctx* lt_create_devices(const int32_t* devices, int32_t n_devices, lt_status* status) {
+  ok_status(status);
+  if (!devices || n_devices <= 0) {
+    set_status(status, LT_ERR_VALIDATION, LT_K_MESSAGE, -1, n_devices, 0, "lt_create_devices: no devices given");
+    return nullptr;
+  }
+  if (n_devices == 1) return lt_create(devices[0], status);
+  auto g = std::make_unique<lt_ctx>();
+  auto fail = [&](lt_ctx* grp) {
+    for (lt_ctx* m : grp->members) lt_destroy(m);
+    grp->members.clear();
+    return nullptr;
+  };
+  for (int32_t i = 0; i < n_devices; ++i) {
+    lt_ctx* m = lt_create(devices[i], status);
+    if (!m) return fail(g.get());
+    g->members.push_back(m);
+  }
+  lt_ctx* m0 = g->members[0];
+  g->device = m0->device;
+  g->stream = m0->stream;
+  g->sm_count = m0->sm_count;
+  g->smem_optin = m0->smem_optin;
+  // NCCL needs distinct devices (one communicator rank per GPU); repeated
+  // entries (one GPU split into several members) gather with peer copies.
+  std::set<int32_t> distinct(devices, devices + n_devices);
+  const char* env = std::getenv("LT_GATHER");
+  const bool want_peer = env && std::string(env) == "peer";
+  g->transport = LT_GATHER_PEER;
+  if (!want_peer && static_cast<int32_t>(distinct.size()) == n_devices && NcclApi::get().ok) {
+    std::vector<ncclComm_t> comms(n_devices);
+    const ncclResult_t r = NcclApi::get().CommInitAll(comms.data(), n_devices, devices);
+    if (r == ncclSuccess) {
+      g->comms.assign(comms.begin(), comms.end());
+      g->transport = LT_GATHER_NCCL;
+    }
+  }
+  if (g->transport == LT_GATHER_PEER) {
+    for (size_t i = 1; i < g->members.size(); ++i) {
+      int can = 0;
+      const int d = g->members[i]->device;
+      if (d != m0->device && cudaDeviceCanAccessPeer(&can, m0->device, d) == cudaSuccess && can) {
+        cudaSetDevice(m0->device);
+        cudaDeviceEnablePeerAccess(d, 0);  // already enabled is fine
+        cudaGetLastError();
+      }
+    }
+  }
+  return g.release();
+}
+
+lt_ctx* lt_create_mask(uint64_t device_mask, lt_status* status) {
+  std::vector<int32_t> devs;
+  for (int d = 0; d < 64; ++d)
+    if (device_mask >> d & 1) devs.push_back(d);
+  if (devs.empty()) {
+    ok_status(status);
+    set_status(status, LT_ERR_VALIDATION, LT_K_MESSAGE, -1, 0, 0, "lt_create_mask: empty device mask");
+    return nullptr;
+  }
+  return lt_create_devices(devs.data(), static_cast<int32_t>(devs.size()), status);
+}
+
+int32_t lt_device_count(lt_ctx* ctx) {
+  if (!ctx) return 0;
+  return ctx->members.empty() ? 1 : static_cast<int32_t>(ctx->members.size());
+}
+
+int32_t lt_gather_transport(lt_ctx* ctx) { return ctx ? ctx->transport : LT_GATHER_NONE; }
+
 void lt_destroy(lt_ctx* ctx) {
   if (!ctx) return;
+  if (!ctx->members.empty()) {  // a group: its streams belong to the members
+    for (void* c : ctx->comms)
+      if (c) NcclApi::get().CommDestroy(static_cast<ncclComm_t>(c));
+    for (lt_ctx* m : ctx->members) lt_destroy(m);
+    delete ctx;
+    return;
+  }
   cudaSetDevice(ctx->device);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -2200,9 +2102,9 @@ int32_t lt_last_timing(lt_ctx* ctx, lt_timing* out) {
 lt_plan* lt_plan_simulate(lt_ctx* ctx, const lt_workload_batch* batch, const lt_server_config* config,
                           const lt_sim_options* options, lt_status* status) {
   ok_status(status);
+  if (!ctx->members.empty()) ctx = ctx->members[0];  // a plan lives on one device
   try {
     cudaSetDevice(ctx->device);
-    if (want_staged(ctx, batch, options)) return build_staged(ctx, batch, config, options);
     return build_plan(ctx, batch, config, options);
   } catch (const CudaError& e) {
     set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
@@ -2214,10 +2116,7 @@ int32_t lt_plan_run(lt_plan* plan, lt_status* status) {
   ok_status(status);
   try {
     cudaSetDevice(plan->ctx->device);
-    if (plan->parts[0])
-      run_staged(*plan);
-    else
-      run_plan(*plan);
+    run_plan(*plan);
     return LT_OK;
   } catch (const CudaError& e) {
     set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
@@ -2229,10 +2128,7 @@ int32_t lt_plan_results(lt_plan* plan, lt_sim_summary* out, lt_request_states* s
   ok_status(status);
   try {
     cudaSetDevice(plan->ctx->device);
-    if (plan->parts[0])
-      fetch_staged(*plan, out, states);
-    else
-      fetch_results(*plan, out, states);
+    fetch_results(*plan, out, states);
     return first_error(plan->ctx, out, plan->n_scen, status);
   } catch (const CudaError& e) {
     set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
@@ -2242,7 +2138,6 @@ int32_t lt_plan_results(lt_plan* plan, lt_sim_summary* out, lt_request_states* s
 
 int32_t lt_plan_trim(lt_plan* plan) {
   if (!plan) return LT_ERR_VALIDATION;
-  if (plan->parts[0]) return LT_OK;  // staged plans keep their buffers
   cudaSetDevice(plan->ctx->device);
   trim_plan(*plan);
   return LT_OK;
@@ -2276,26 +2171,13 @@ static int32_t simulate_one(lt_ctx* ctx, const lt_workload_batch* batch, const l
   return rc;
 }
 
-// Requests a scenario can generate: the Poisson mean of every adapter plus
-// 8 sigma and slack (the same bound that sizes the RNG tables), or the
-// scripted list.
-static double est_requests(const lt_workload_batch* b, int64_t i) {
-  const lt_scenario& s = b->scenarios[i];
-  if (s.n_requests >= 0) return static_cast<double>(s.n_requests);
-  double e = 0.0;
-  for (int32_t k = 0; k < s.n_adapters; ++k) {
-    const double lam = std::max(b->adapters[s.adapter_offset + k].rate, 0.0) * std::max(s.duration_s, 0.0);
-    e += lam + 8.0 * std::sqrt(lam) + 32.0;
-  }
-  return e;
-}
-
 int32_t lt_simulate_batch(lt_ctx* ctx, const lt_workload_batch* batch, const lt_server_config* config,
                           const lt_sim_options* options, lt_sim_summary* out, lt_request_states* states,
                           lt_status* status) {
+  ok_status(status);
+  if (!ctx->members.empty()) return group_simulate(ctx, batch, config, options, out, states, status);
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
-  ok_status(status);
   // Device memory is bounded by splitting the batch into consecutive chunks of
   // at most kChunkScenarios scenarios and kChunkRequests estimated requests
   // (~100 B of device state each). Chunks are pipelined on two streams: the
@@ -2416,6 +2298,12 @@ int32_t lt_generate_arrivals_batch(lt_ctx* ctx, const lt_workload_batch* batch, 
                                    lt_request* out, int64_t capacity, int64_t* offsets, int64_t* counts,
                                    lt_status* status) {
   ok_status(status);
+  if (!ctx->members.empty()) {  // a data-format call: the first device does it
+    const int32_t rc = lt_generate_arrivals_batch(ctx->members[0], batch, options, out, capacity, offsets, counts, status);
+    ctx->messages = ctx->members[0]->messages;
+    ctx->timing = ctx->members[0]->timing;
+    return rc;
+  }
   lt_server_config cfg{};
   // generate_arrivals needs no server config; a permissive one keeps the
   // engine-level checks out of the way.
@@ -2487,155 +2375,30 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
                        lt_placement* out, lt_frontier_point* frontier, int32_t max_frontier,
                        lt_status* status) {
   ok_status(status);
+  if (!ctx->members.empty())
+    return group_sweep(ctx, batch, config, grid, duration_s, seed, options, sim_options, out, frontier, max_frontier,
+                       status);
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t n_cond = batch->n_conditions;
   ctx->messages.assign(n_cond, std::string());
   try {
-    cudaSetDevice(ctx->device);
+    SweepRun R;
+    sweep_run(ctx, batch, config, grid, duration_s, seed, options, sim_options, max_frontier, R);
     cudaStream_t st = ctx->stream;
-    // SweepGrid::validate (placement.cpp:169-183)
-    HostErr grid_err;
-    bool grid_ok = true;
-    if (grid->n_count <= 0) {
-      grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.n_values: must be non-empty");
-    } else {
-      for (int i = 0; i < grid->n_count && grid_ok; ++i) {
-        if (grid->n_values[i] < 1)
-          grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.n_values: entries must be >= 1");
-        else if (i > 0 && grid->n_values[i] <= grid->n_values[i - 1])
-          grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.n_values: must be strictly ascending");
-      }
-      if (grid_ok && grid->g_mode == LT_G_EXPLICIT) {
-        if (grid->g_count <= 0)
-          grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.g_values: must be non-empty in explicit mode");
-        for (int i = 0; i < grid->g_count && grid_ok; ++i)
-          if (grid->g_values[i] < 1) grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.g_values: entries must be >= 1");
-      }
-    }
-    // rows: SweepGrid::g_candidates (placement.cpp:159-167)
-    std::vector<SweepRow> rows;
-    std::vector<int32_t> g_list;
-    int32_t per_cond = 0;
-    int n_max = 1;
-    if (grid_ok) {
-      for (int i = 0; i < grid->n_count; ++i) {
-        const int n = grid->n_values[i];
-        n_max = std::max(n_max, n);
-        std::set<int> gs;
-        if (grid->g_mode == LT_G_GEOMETRIC) {
-          for (int g : {8, n / 4, n / 2, n}) gs.insert(std::clamp(g, 1, n));
-        } else {
-          for (int k = 0; k < grid->g_count; ++k) gs.insert(std::clamp(grid->g_values[k], 1, n));
-        }
-        SweepRow r{n, static_cast<int32_t>(gs.size()), static_cast<int32_t>(g_list.size()), per_cond};
-        for (int g : gs) g_list.push_back(g);
-        per_cond += r.g_count;
-        rows.push_back(r);
-      }
-    }
-    // Condition validation (sweep_optimal, placement.cpp:186-188); grid
-    // points of valid conditions are numbered row-major per condition.
-    SweepSetup S;
-    S.batch = batch;
-    S.rows = rows;
-    S.g_list = g_list;
-    S.per_cond = per_cond;
-    S.n_max = n_max;
-    S.duration = duration_s;
-    S.seed = seed;
-    S.options = options;
-    S.cond_base.assign(n_cond, -1);
-    std::vector<HostErr> cond_err(n_cond);
-    for (int64_t c = 0; c < n_cond; ++c) {
-      const lt_condition& cd = batch->conditions[c];
-      HostErr& e = cond_err[c];
-      if (!grid_ok) {
-        e = grid_err;
-        continue;
-      }
-      if (!validate_lengths(batch->lengths[cd.length_index], batch->full_lengths, "condition.lengths", &e)) continue;
-      if (cd.mix_count <= 0) {
-        e.set(LT_ERR_VALIDATION, "condition.mix: must be non-empty");
-        continue;
-      }
-      S.cond_base[c] = S.n_points;
-      S.n_points += per_cond;
-    }
-    const std::vector<int64_t>& cond_base = S.cond_base;
-    lt_sim_options so{};
-    if (sim_options) so = *sim_options;
-    so.want_digest = 0;
-    Config probe;
-    load_config(probe, config, &so);
-    SweepTiming tm;
-    DBuf<lt_sim_summary> d_pts;
-    std::unordered_map<int64_t, std::string> point_msg;
-    if (grid_ok && sweep_device_eligible(S, probe))
-      sweep_waves_device(ctx, S, config, so, d_pts, point_msg, tm);
-    else
-      sweep_waves_host(ctx, S, config, so, d_pts, point_msg, tm);
-    double engine_ms = tm.engine_ms, tables_ms = tm.tables_ms, merge_ms = tm.merge_ms, run_ms = tm.run_ms;
-    int64_t launches = tm.launches, algo = tm.algo;
-    ctx->messages.assign(n_cond, std::string());
-    DBuf<SweepRow> d_rows;
-    DBuf<int32_t> d_g;
-    DBuf<int64_t> d_base;
-    DBuf<lt_placement> d_out;
-    DBuf<lt_frontier_point> d_front;
-    d_rows.upload(rows, st);
-    d_g.upload(g_list, st);
-    d_base.upload(cond_base, st);
-    d_out.alloc(std::max<int64_t>(n_cond, 1));
-    d_front.alloc(std::max<int64_t>(n_cond * max_frontier, 1));
-    cudaEventRecord(ctx->ev[5], st);
-    if (n_cond > 0 && !rows.empty()) {
-      sweep_reduce_kernel<<<static_cast<unsigned>((n_cond + 127) / 128), 128, 0, st>>>(
-          static_cast<int>(n_cond), d_rows.p, static_cast<int>(rows.size()), d_g.p, per_cond, d_base.p,
-          d_pts.p, options->early_exit, options->early_exit_k, max_frontier, d_out.p, d_front.p);
-      after_launch("sweep_reduce_kernel", st);
-      ++launches;
-    }
     cudaEventRecord(ctx->ev[6], st);
     if (n_cond > 0) {
-      LT_CUDA(cudaMemcpyAsync(out, d_out.p, n_cond * sizeof(lt_placement), cudaMemcpyDeviceToHost, st));
-      LT_CUDA(cudaMemcpyAsync(frontier, d_front.p, n_cond * max_frontier * sizeof(lt_frontier_point),
+      LT_CUDA(cudaMemcpyAsync(out, R.d_out.p, n_cond * sizeof(lt_placement), cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(frontier, R.d_front.p, n_cond * max_frontier * sizeof(lt_frontier_point),
                               cudaMemcpyDeviceToHost, st));
     }
     cudaEventRecord(ctx->ev[7], st);
     LT_CUDA(cudaStreamSynchronize(st));
-    int32_t rc = LT_OK;
-    for (int64_t c = 0; c < n_cond; ++c) {
-      lt_placement& p = out[c];
-      std::string msg;
-      if (cond_base[c] < 0) {
-        std::memset(&p, 0, sizeof(p));
-        p.status_point = -1;
-        p.status = cond_err[c].code;
-        p.status_kind = cond_err[c].kind;
-        p.status_a = cond_err[c].a;
-        p.status_b = cond_err[c].b;
-        msg = cond_err[c].msg;
-      } else if (p.status != LT_OK) {
-        auto it = point_msg.find(p.status_point);
-        msg = it != point_msg.end() ? it->second : render(p.status, p.status_kind, p.status_a, p.status_b);
-      }
-      ctx->messages[c] = msg;
-      if (p.status != LT_OK && rc == LT_OK) {
-        rc = p.status;
-        set_status(status, p.status, p.status_kind, c, p.status_a, p.status_b, msg);
-      }
-    }
-    lt_timing& t = ctx->timing;
-    t.tables_ms = tables_ms;
-    t.merge_ms = merge_ms;
-    t.engine_ms = engine_ms;
-    t.reduce_ms = elapsed(ctx->ev[5], ctx->ev[6]);
-    t.d2h_ms = elapsed(ctx->ev[6], ctx->ev[7]);
-    t.run_ms = run_ms;
-    t.engine_launches = launches;
-    t.algorithmic_bytes = algo;
-    t.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    return rc;
+    std::vector<lt_placement*> rows(n_cond);
+    for (int64_t c = 0; c < n_cond; ++c) rows[c] = out + c;
+    sweep_statuses(R, rows.data(), ctx->messages.data());
+    sweep_timing(ctx, R, elapsed(ctx->ev[6], ctx->ev[7]));
+    ctx->timing.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return first_condition_error(ctx, out, n_cond, status);
   } catch (const CudaError& e) {
     set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
     return LT_ERR_DEVICE;

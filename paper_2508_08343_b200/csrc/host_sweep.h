@@ -471,3 +471,173 @@ void sweep_waves_device(lt_ctx* ctx, const SweepSetup& S, const lt_server_config
   // engine work and messages of the points that failed on the device: K3 reads the table
   (void)point_msg;
 }
+
+// One lt_sweep_batch call up to K3, with the placements and frontiers left on
+// ctx's device (d_out, d_front): the single-device call copies them back, a
+// multi-device context gathers every member's rows to its first device first.
+struct SweepRun {
+  int64_t n_cond = 0;
+  std::vector<HostErr> cond_err;   // validation failures (cond_base < 0)
+  std::vector<int64_t> cond_base;  // first grid point of condition c, -1: failed validation
+  std::unordered_map<int64_t, std::string> point_msg;
+  DBuf<lt_placement> d_out;
+  DBuf<lt_frontier_point> d_front;
+  SweepTiming tm;
+  double reduce_ms = 0.0;
+};
+
+void sweep_run(lt_ctx* ctx, const lt_condition_batch* batch, const lt_server_config* config,
+               const lt_sweep_grid* grid, double duration_s, uint64_t seed, const lt_sweep_options* options,
+               const lt_sim_options* sim_options, int32_t max_frontier, SweepRun& R) {
+  const int64_t n_cond = batch->n_conditions;
+  R.n_cond = n_cond;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  // SweepGrid::validate (placement.cpp:169-183)
+  HostErr grid_err;
+  bool grid_ok = true;
+  if (grid->n_count <= 0) {
+    grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.n_values: must be non-empty");
+  } else {
+    for (int i = 0; i < grid->n_count && grid_ok; ++i) {
+      if (grid->n_values[i] < 1)
+        grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.n_values: entries must be >= 1");
+      else if (i > 0 && grid->n_values[i] <= grid->n_values[i - 1])
+        grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.n_values: must be strictly ascending");
+    }
+    if (grid_ok && grid->g_mode == LT_G_EXPLICIT) {
+      if (grid->g_count <= 0)
+        grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.g_values: must be non-empty in explicit mode");
+      for (int i = 0; i < grid->g_count && grid_ok; ++i)
+        if (grid->g_values[i] < 1) grid_ok = grid_err.set(LT_ERR_VALIDATION, "grid.g_values: entries must be >= 1");
+    }
+  }
+  // rows: SweepGrid::g_candidates (placement.cpp:159-167)
+  std::vector<SweepRow> rows;
+  std::vector<int32_t> g_list;
+  int32_t per_cond = 0;
+  int n_max = 1;
+  if (grid_ok) {
+    for (int i = 0; i < grid->n_count; ++i) {
+      const int n = grid->n_values[i];
+      n_max = std::max(n_max, n);
+      std::set<int> gs;
+      if (grid->g_mode == LT_G_GEOMETRIC) {
+        for (int g : {8, n / 4, n / 2, n}) gs.insert(std::clamp(g, 1, n));
+      } else {
+        for (int k = 0; k < grid->g_count; ++k) gs.insert(std::clamp(grid->g_values[k], 1, n));
+      }
+      SweepRow r{n, static_cast<int32_t>(gs.size()), static_cast<int32_t>(g_list.size()), per_cond};
+      for (int g : gs) g_list.push_back(g);
+      per_cond += r.g_count;
+      rows.push_back(r);
+    }
+  }
+  // Condition validation (sweep_optimal, placement.cpp:186-188); grid
+  // points of valid conditions are numbered row-major per condition.
+  SweepSetup S;
+  S.batch = batch;
+  S.rows = rows;
+  S.g_list = g_list;
+  S.per_cond = per_cond;
+  S.n_max = n_max;
+  S.duration = duration_s;
+  S.seed = seed;
+  S.options = options;
+  S.cond_base.assign(n_cond, -1);
+  R.cond_err.assign(n_cond, HostErr());
+  for (int64_t c = 0; c < n_cond; ++c) {
+    const lt_condition& cd = batch->conditions[c];
+    HostErr& e = R.cond_err[c];
+    if (!grid_ok) {
+      e = grid_err;
+      continue;
+    }
+    if (!validate_lengths(batch->lengths[cd.length_index], batch->full_lengths, "condition.lengths", &e)) continue;
+    if (cd.mix_count <= 0) {
+      e.set(LT_ERR_VALIDATION, "condition.mix: must be non-empty");
+      continue;
+    }
+    S.cond_base[c] = S.n_points;
+    S.n_points += per_cond;
+  }
+  R.cond_base = S.cond_base;
+  lt_sim_options so{};
+  if (sim_options) so = *sim_options;
+  so.want_digest = 0;
+  Config probe;
+  load_config(probe, config, &so);
+  DBuf<lt_sim_summary> d_pts;
+  if (grid_ok && sweep_device_eligible(S, probe))
+    sweep_waves_device(ctx, S, config, so, d_pts, R.point_msg, R.tm);
+  else
+    sweep_waves_host(ctx, S, config, so, d_pts, R.point_msg, R.tm);
+  DBuf<SweepRow> d_rows;
+  DBuf<int32_t> d_g;
+  DBuf<int64_t> d_base;
+  d_rows.upload(rows, st);
+  d_g.upload(g_list, st);
+  d_base.upload(R.cond_base, st);
+  R.d_out.alloc(std::max<int64_t>(n_cond, 1));
+  R.d_front.alloc(std::max<int64_t>(n_cond * max_frontier, 1));
+  // rows past a condition's frontier_count read as zeros, not stale cache blocks
+  LT_CUDA(cudaMemsetAsync(R.d_front.p, 0, R.d_front.n * sizeof(lt_frontier_point), st));
+  cudaEventRecord(ctx->ev[5], st);
+  if (n_cond > 0 && !rows.empty()) {
+    sweep_reduce_kernel<<<static_cast<unsigned>((n_cond + 127) / 128), 128, 0, st>>>(
+        static_cast<int>(n_cond), d_rows.p, static_cast<int>(rows.size()), d_g.p, per_cond, d_base.p, d_pts.p,
+        options->early_exit, options->early_exit_k, max_frontier, R.d_out.p, R.d_front.p);
+    after_launch("sweep_reduce_kernel", st);
+    ++R.tm.launches;
+  }
+  cudaEventRecord(ctx->ev[6], st);
+  LT_CUDA(cudaStreamSynchronize(st));  // K3's inputs are released on return
+  R.reduce_ms = elapsed(ctx->ev[5], ctx->ev[6]);
+}
+
+// Status and reference message of every condition of R from its placement
+// row as copied back (rows[c] = condition c of R's batch; messages[c] gets
+// the text).
+void sweep_statuses(const SweepRun& R, lt_placement* const* rows, std::string* messages) {
+  for (int64_t c = 0; c < R.n_cond; ++c) {
+    lt_placement& p = *rows[c];
+    std::string msg;
+    if (R.cond_base[c] < 0) {
+      std::memset(&p, 0, sizeof(p));
+      p.status_point = -1;
+      p.status = R.cond_err[c].code;
+      p.status_kind = R.cond_err[c].kind;
+      p.status_a = R.cond_err[c].a;
+      p.status_b = R.cond_err[c].b;
+      msg = R.cond_err[c].msg;
+    } else if (p.status != LT_OK) {
+      auto it = R.point_msg.find(p.status_point);
+      msg = it != R.point_msg.end() ? it->second : render(p.status, p.status_kind, p.status_a, p.status_b);
+    }
+    messages[c] = std::move(msg);
+  }
+}
+
+void sweep_timing(lt_ctx* ctx, const SweepRun& R, double d2h_ms) {
+  lt_timing& t = ctx->timing;
+  t.tables_ms = R.tm.tables_ms;
+  t.merge_ms = R.tm.merge_ms;
+  t.engine_ms = R.tm.engine_ms;
+  t.reduce_ms = R.reduce_ms;
+  t.d2h_ms = d2h_ms;
+  t.run_ms = R.tm.run_ms;
+  t.engine_launches = R.tm.launches;
+  t.algorithmic_bytes = R.tm.algo;
+}
+
+// The call-level status of a sweep: the lowest failing condition
+// (placement.cpp:93-95).
+int32_t first_condition_error(lt_ctx* ctx, const lt_placement* out, int64_t n, lt_status* status) {
+  for (int64_t c = 0; c < n; ++c) {
+    if (out[c].status != LT_OK) {
+      set_status(status, out[c].status, out[c].status_kind, c, out[c].status_a, out[c].status_b, ctx->messages[c]);
+      return out[c].status;
+    }
+  }
+  return LT_OK;
+}

@@ -27,6 +27,19 @@ def test_library_exports_every_declared_symbol():
     assert lib.abi_version() == A.ABI_VERSION
 
 
+def test_device_group_argument_errors_without_a_gpu():
+    import ctypes as C
+
+    lib = lt.load_library()
+    st = A.lt_status()
+    assert not lib.create_devices(None, 0, C.byref(st))
+    assert st.code == A.LT_ERR_VALIDATION and b"no devices" in st.message
+    st = A.lt_status()
+    assert not lib.create_mask(0, C.byref(st))
+    assert st.code == A.LT_ERR_VALIDATION and b"empty device mask" in st.message
+    assert lib.device_count(None) == 0 and lib.gather_transport(None) == A.GATHER_NONE
+
+
 def test_library_is_sm100a():
     out = subprocess.run(["cuobjdump", "--list-elf", B.LIB], capture_output=True, text=True).stdout
     assert "sm_100a" in out
