@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define LT_ABI_VERSION 2
+#define LT_ABI_VERSION 3
 
 /* Exception classes of errors.hpp, plus two conditions of this library. */
 enum lt_code {
@@ -358,6 +358,55 @@ int32_t lt_generate_arrivals_batch(lt_ctx* ctx, const lt_workload_batch* batch,
 int32_t lt_simulate_batch(lt_ctx* ctx, const lt_workload_batch* batch,
                           const lt_server_config* config, const lt_sim_options* options,
                           lt_sim_summary* out, lt_request_states* states, lt_status* status);
+
+/* ---- Full simulation report ----------------------------
+ * What run_simulation / run_scripted return beyond the summary: the
+ * IterationTraceRow trace (engine.hpp:39-47, engine.cpp:137-140), the
+ * LoadEvent list (adapter_cache.hpp:28-34, engine.cpp:141) and every
+ * request's token_emit_times_s (kv_scheduler.hpp:30-41, engine.cpp:132),
+ * i.e. the inputs of simulation_report_json (json_io.cpp:608-687). */
+typedef struct lt_trace_row {
+  double time_s;   /* clock at the start of the iteration */
+  int64_t iteration;
+  int32_t r_running, r_waiting, a_running, loads;
+  double lat_step_s;
+} lt_trace_row;
+
+typedef struct lt_load_event {
+  double time_s;
+  int32_t adapter_id;
+  int32_t rank;
+  int32_t source; /* enum lt_load_source */
+  int32_t _pad;
+  double latency_s;
+} lt_load_event;
+
+/* Caller-owned output rows. Scenario s's trace is trace[trace_offset[s] ..
+ * + summary.iterations), its loads loads[load_offset[s] .. + load_events);
+ * request row j (lt_request_states order) emitted at emit_times[emit_offset[j]
+ * .. + tokens_generated). Rows past a capacity are not written (the counts
+ * still are), so a first lt_simulate_batch call can size the buffers. */
+typedef struct lt_report {
+  lt_trace_row* trace;
+  int64_t trace_capacity;
+  int64_t* trace_offset; /* n_scenarios entries */
+  lt_load_event* loads;
+  int64_t load_capacity;
+  int64_t* load_offset;  /* n_scenarios entries */
+  double* emit_times;
+  int64_t emit_capacity;
+  int64_t* emit_offset;  /* one per request row (states->capacity entries) */
+} lt_report;
+
+/* lt_simulate_batch plus the full report: a second engine pass over the same
+ * batch records the trace rows, load events and every admission / preemption
+ * (the request's running stints); the emit times are expanded on the device
+ * from the stints and the per-iteration emit times. One device plan (no
+ * chunking): meant for report-sized batches. `states` is required. */
+int32_t lt_simulate_report(lt_ctx* ctx, const lt_workload_batch* batch,
+                           const lt_server_config* config, const lt_sim_options* options,
+                           lt_sim_summary* out, lt_request_states* states, lt_report* report,
+                           lt_status* status);
 
 /* sweep_optimal for every condition: frontier rows of condition c are
  * frontier[c * max_frontier ...]. lt_sweep_frontier_capacity gives the

@@ -204,83 +204,103 @@ int32_t ltref_generate_arrivals_batch(void*, const lt_workload_batch* batch, con
   return status ? status->code : 0;
 }
 
-int32_t ltref_simulate_batch(void*, const lt_workload_batch* batch, const lt_server_config* config,
-                             const lt_sim_options* options, lt_sim_summary* out,
-                             lt_request_states* states, lt_status* status) {
+}  // extern "C"
+
+namespace {
+
+// One scenario through the reference's own run_simulation / run_scripted.
+SimulationResult run_one(const lt_workload_batch* batch, std::size_t i, const ServerConfig& base,
+                         const lt_sim_options* options, bool trace, WorkloadSpec* w_out, ServerConfig* cfg_out) {
+  const lt_scenario& s = batch->scenarios[i];
+  ServerConfig cfg = base;
+  if (s.slots > 0) cfg.slots = s.slots;
+  SimOptions opt;
+  opt.record_iteration_trace = trace;
+  opt.check_invariants = options && options->check_invariants;
+  if (options && options->iteration_cap_override > 0) opt.iteration_cap_override = options->iteration_cap_override;
+  WorkloadSpec w = to_workload(*batch, s);
+  SimulationResult r;
+  if (s.n_requests >= 0) {
+    std::vector<Request> rr;
+    rr.reserve(static_cast<std::size_t>(s.n_requests));
+    for (int64_t k = 0; k < s.n_requests; ++k) {
+      const lt_request& q = batch->requests[s.request_offset + k];
+      Request x;
+      x.request_id = q.request_id;
+      x.adapter_id = q.adapter_id;
+      x.arrival_time_s = q.arrival_time_s;
+      x.input_tokens = q.input_tokens;
+      x.output_tokens = q.output_tokens;
+      rr.push_back(x);
+    }
+    r = run_scripted(rr, w.adapters, w.duration_s, cfg, opt);
+  } else {
+    r = run_simulation(w, cfg, static_cast<LengthMode>(s.mode), opt);
+  }
+  *w_out = std::move(w);
+  *cfg_out = cfg;
+  return r;
+}
+
+void fill_summary(const SimulationResult& r, const MetricsSummary& m, bool trace, lt_sim_summary& o) {
+  o.n_requests = static_cast<int64_t>(r.requests.size());
+  o.iterations = r.iterations;
+  o.final_clock_s = r.final_clock_s;
+  o.duration_s = r.duration_s;
+  o.truncated = r.truncated;
+  o.slots = r.slots;
+  o.served_adapters = r.served_adapters;
+  o.kv_capacity_tokens = r.kv_capacity_tokens;
+  o.starved = m.starved;
+  o.finished_count = m.finished_count;
+  o.rejected_count = m.rejected_count;
+  o.load_events = static_cast<int64_t>(r.load_events.size());
+  o.throughput_tok_s = m.throughput_tok_s;
+  o.ideal_throughput_tok_s = m.ideal_throughput_tok_s;
+  o.ttft_mean_s = m.ttft_mean_s;
+  o.itl_mean_s = m.itl_mean_s;
+  o.ttft_p50_s = m.ttft_p50_s;
+  o.ttft_p99_s = m.ttft_p99_s;
+  o.itl_p50_s = m.itl_p50_s;
+  o.itl_p99_s = m.itl_p99_s;
+  o.degenerate = m.degenerate;
+  // tokens_in_window without another pass over every emit time (the
+  // reference already counted them: throughput = tokens / window, and the
+  // integer is recovered exactly by rounding the product).
+  int64_t pre = 0, tot = 0;
+  for (const RequestState& q : r.requests) {
+    pre += q.preemption_count;
+    tot += q.tokens_generated;
+  }
+  const int64_t win = r.requests.empty() ? 0 : std::llround(m.throughput_tok_s * r.duration_s);
+  o.preemptions = pre;
+  o.tokens_total = tot;
+  o.tokens_in_window = win;
+  if (trace) {
+    o.digest = digest_of(r);
+    for (const IterationTraceRow& t : r.iteration_trace) o.sum_running += t.r_running;
+  }
+}
+
+// Runs every scenario on the pool; errors become statuses (lowest index
+// first in *status), results are kept when `keep` is non-null.
+void simulate_all(const lt_workload_batch* batch, const lt_server_config* config, const lt_sim_options* options,
+                  bool trace, lt_sim_summary* out, std::vector<SimulationResult>* keep, lt_status* status) {
   const std::size_t n = static_cast<std::size_t>(batch->n_scenarios);
   const ServerConfig base = to_config(*config);
   std::vector<std::exception_ptr> errors(n);
-  std::vector<SimulationResult> keep(states ? n : 0);
+  if (keep) keep->assign(n, SimulationResult());
   g_messages.assign(n, std::string());
   run_pool(n, [&](std::size_t i) {
     lt_sim_summary& o = out[i];
     std::memset(&o, 0, sizeof(o));
     try {
-      const lt_scenario& s = batch->scenarios[i];
-      ServerConfig cfg = base;
-      if (s.slots > 0) cfg.slots = s.slots;
-      SimOptions opt;
-      opt.record_iteration_trace = options && options->want_digest;
-      opt.check_invariants = options && options->check_invariants;
-      if (options && options->iteration_cap_override > 0) opt.iteration_cap_override = options->iteration_cap_override;
-      WorkloadSpec w = to_workload(*batch, s);
-      SimulationResult r;
-      if (s.n_requests >= 0) {
-        std::vector<Request> rr;
-        rr.reserve(static_cast<std::size_t>(s.n_requests));
-        for (int64_t k = 0; k < s.n_requests; ++k) {
-          const lt_request& q = batch->requests[s.request_offset + k];
-          Request x;
-          x.request_id = q.request_id;
-          x.adapter_id = q.adapter_id;
-          x.arrival_time_s = q.arrival_time_s;
-          x.input_tokens = q.input_tokens;
-          x.output_tokens = q.output_tokens;
-          rr.push_back(x);
-        }
-        r = run_scripted(rr, w.adapters, w.duration_s, cfg, opt);
-      } else {
-        r = run_simulation(w, cfg, static_cast<LengthMode>(s.mode), opt);
-      }
+      WorkloadSpec w;
+      ServerConfig cfg;
+      SimulationResult r = run_one(batch, i, base, options, trace, &w, &cfg);
       const MetricsSummary m = compute_metrics(r, w, cfg.ideal_includes_input);
-      o.n_requests = static_cast<int64_t>(r.requests.size());
-      o.iterations = r.iterations;
-      o.final_clock_s = r.final_clock_s;
-      o.duration_s = r.duration_s;
-      o.truncated = r.truncated;
-      o.slots = r.slots;
-      o.served_adapters = r.served_adapters;
-      o.kv_capacity_tokens = r.kv_capacity_tokens;
-      o.starved = m.starved;
-      o.finished_count = m.finished_count;
-      o.rejected_count = m.rejected_count;
-      o.load_events = static_cast<int64_t>(r.load_events.size());
-      o.throughput_tok_s = m.throughput_tok_s;
-      o.ideal_throughput_tok_s = m.ideal_throughput_tok_s;
-      o.ttft_mean_s = m.ttft_mean_s;
-      o.itl_mean_s = m.itl_mean_s;
-      o.ttft_p50_s = m.ttft_p50_s;
-      o.ttft_p99_s = m.ttft_p99_s;
-      o.itl_p50_s = m.itl_p50_s;
-      o.itl_p99_s = m.itl_p99_s;
-      o.degenerate = m.degenerate;
-      // tokens_in_window without another pass over every emit time (the
-      // reference already counted them: throughput = tokens / window, and
-      // the integer is recovered exactly by rounding the product).
-      int64_t pre = 0, tot = 0;
-      for (const RequestState& q : r.requests) {
-        pre += q.preemption_count;
-        tot += q.tokens_generated;
-      }
-      const int64_t win = r.requests.empty() ? 0 : std::llround(m.throughput_tok_s * r.duration_s);
-      o.preemptions = pre;
-      o.tokens_total = tot;
-      o.tokens_in_window = win;
-      if (opt.record_iteration_trace) {
-        o.digest = digest_of(r);
-        for (const IterationTraceRow& t : r.iteration_trace) o.sum_running += t.r_running;
-      }
-      if (states) keep[i] = std::move(r);
+      fill_summary(r, m, trace, o);
+      if (keep) (*keep)[i] = std::move(r);
     } catch (...) {
       errors[i] = std::current_exception();
     }
@@ -295,25 +315,77 @@ int32_t ltref_simulate_batch(void*, const lt_workload_batch* batch, const lt_ser
     out[i].status_kind = LT_K_MESSAGE;
     if (status && status->code == LT_OK) set_status(status, code, static_cast<int64_t>(i), msg);
   }
-  if (states) {
-    int64_t off = 0;
-    for (std::size_t i = 0; i < n; ++i) {
-      if (states->req_offset) states->req_offset[i] = off;
-      for (const RequestState& q : keep[i].requests) {
-        if (off < states->capacity) {
-          if (states->phase) states->phase[off] = static_cast<int8_t>(q.phase);
-          if (states->tokens_generated) states->tokens_generated[off] = q.tokens_generated;
-          if (states->first_token_time_s)
-            states->first_token_time_s[off] = q.first_token_time_s ? *q.first_token_time_s : NAN;
-          if (states->completion_time_s) states->completion_time_s[off] = q.completion_time_s;
-          if (states->preemption_count) states->preemption_count[off] = q.preemption_count;
-          if (states->adapter_id) states->adapter_id[off] = q.request.adapter_id;
-          if (states->input_tokens) states->input_tokens[off] = q.request.input_tokens;
-          if (states->output_tokens) states->output_tokens[off] = q.request.output_tokens;
-          if (states->arrival_time_s) states->arrival_time_s[off] = q.request.arrival_time_s;
-        }
-        ++off;
+}
+
+void write_states(const std::vector<SimulationResult>& keep, lt_request_states* states) {
+  int64_t off = 0;
+  for (std::size_t i = 0; i < keep.size(); ++i) {
+    if (states->req_offset) states->req_offset[i] = off;
+    for (const RequestState& q : keep[i].requests) {
+      if (off < states->capacity) {
+        if (states->phase) states->phase[off] = static_cast<int8_t>(q.phase);
+        if (states->tokens_generated) states->tokens_generated[off] = q.tokens_generated;
+        if (states->first_token_time_s)
+          states->first_token_time_s[off] = q.first_token_time_s ? *q.first_token_time_s : NAN;
+        if (states->completion_time_s) states->completion_time_s[off] = q.completion_time_s;
+        if (states->preemption_count) states->preemption_count[off] = q.preemption_count;
+        if (states->adapter_id) states->adapter_id[off] = q.request.adapter_id;
+        if (states->input_tokens) states->input_tokens[off] = q.request.input_tokens;
+        if (states->output_tokens) states->output_tokens[off] = q.request.output_tokens;
+        if (states->arrival_time_s) states->arrival_time_s[off] = q.request.arrival_time_s;
       }
+      ++off;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ltref_simulate_batch(void*, const lt_workload_batch* batch, const lt_server_config* config,
+                             const lt_sim_options* options, lt_sim_summary* out,
+                             lt_request_states* states, lt_status* status) {
+  std::vector<SimulationResult> keep;
+  simulate_all(batch, config, options, options && options->want_digest, out, states ? &keep : nullptr, status);
+  if (states) write_states(keep, states);
+  return status ? status->code : 0;
+}
+
+// The full SimulationResult (trace rows, load events, token emit times) in
+// the lt_report layout of lt_simulate_report.
+int32_t ltref_simulate_report(void*, const lt_workload_batch* batch, const lt_server_config* config,
+                              const lt_sim_options* options, lt_sim_summary* out, lt_request_states* states,
+                              lt_report* report, lt_status* status) {
+  std::vector<SimulationResult> keep;
+  simulate_all(batch, config, options, true, out, &keep, status);
+  if (!(options && options->want_digest))
+    for (int64_t i = 0; i < batch->n_scenarios; ++i) out[i].digest = 0, out[i].sum_running = 0;
+  write_states(keep, states);
+  int64_t to = 0, lo = 0, row = 0, eo = 0;
+  for (std::size_t i = 0; i < keep.size(); ++i) {
+    const SimulationResult& r = keep[i];
+    if (report->trace_offset) report->trace_offset[i] = to;
+    if (report->load_offset) report->load_offset[i] = lo;
+    for (const IterationTraceRow& t : r.iteration_trace) {
+      if (to < report->trace_capacity && report->trace)
+        report->trace[to] = lt_trace_row{t.time_s, t.iteration, t.r_running, t.r_waiting, t.a_running, t.loads,
+                                         t.lat_step_s};
+      ++to;
+    }
+    for (const LoadEvent& e : r.load_events) {
+      if (lo < report->load_capacity && report->loads)
+        report->loads[lo] = lt_load_event{e.time_s, e.adapter_id, e.rank, static_cast<int32_t>(e.source), 0,
+                                          e.latency_s};
+      ++lo;
+    }
+    for (const RequestState& q : r.requests) {
+      if (row < states->capacity && report->emit_offset) report->emit_offset[row] = eo;
+      for (double t : q.token_emit_times_s) {
+        if (eo < report->emit_capacity && report->emit_times) report->emit_times[eo] = t;
+        ++eo;
+      }
+      ++row;
     }
   }
   return status ? status->code : 0;

@@ -11,7 +11,7 @@ import os
 
 import numpy as np
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # enum lt_code
 LT_OK, LT_ERR_VALIDATION, LT_ERR_CONFIG, LT_ERR_SIMULATION, LT_ERR_INTERNAL, LT_ERR_UNSUPPORTED, LT_ERR_DEVICE = range(7)
@@ -163,6 +163,22 @@ class lt_timing(C.Structure):
                 ("devices", C.c_int32), ("_pad", C.c_int32)]
 
 
+class lt_trace_row(C.Structure):
+    _fields_ = [("time_s", C.c_double), ("iteration", C.c_int64), ("r_running", C.c_int32),
+                ("r_waiting", C.c_int32), ("a_running", C.c_int32), ("loads", C.c_int32), ("lat_step_s", C.c_double)]
+
+
+class lt_load_event(C.Structure):
+    _fields_ = [("time_s", C.c_double), ("adapter_id", C.c_int32), ("rank", C.c_int32), ("source", C.c_int32),
+                ("_pad", C.c_int32), ("latency_s", C.c_double)]
+
+
+class lt_report(C.Structure):
+    _fields_ = [("trace", C.c_void_p), ("trace_capacity", C.c_int64), ("trace_offset", C.c_void_p),
+                ("loads", C.c_void_p), ("load_capacity", C.c_int64), ("load_offset", C.c_void_p),
+                ("emit_times", C.c_void_p), ("emit_capacity", C.c_int64), ("emit_offset", C.c_void_p)]
+
+
 # numpy views with the exact C layouts (numpy honours ctypes field offsets)
 SCENARIO_DT = np.dtype(lt_scenario)
 ADAPTER_DT = np.dtype(lt_adapter)
@@ -173,6 +189,8 @@ TEMPLATE_DT = np.dtype(lt_template)
 CONDITION_DT = np.dtype(lt_condition)
 FRONTIER_DT = np.dtype(lt_frontier_point)
 PLACEMENT_DT = np.dtype(lt_placement)
+TRACE_DT = np.dtype(lt_trace_row)
+LOAD_EVENT_DT = np.dtype(lt_load_event)
 
 assert SCENARIO_DT.itemsize == 56 and ADAPTER_DT.itemsize == 24 and REQUEST_DT.itemsize == 32
 assert LENGTH_DT.itemsize == 56
@@ -205,6 +223,9 @@ SIGNATURES = {
     "simulate_batch": (C.c_int32, [C.c_void_p, C.POINTER(lt_workload_batch),
                                    C.POINTER(lt_server_config), C.POINTER(lt_sim_options),
                                    C.c_void_p, C.POINTER(lt_request_states), C.POINTER(lt_status)]),
+    "simulate_report": (C.c_int32, [C.c_void_p, C.POINTER(lt_workload_batch), C.POINTER(lt_server_config),
+                                    C.POINTER(lt_sim_options), C.c_void_p, C.POINTER(lt_request_states),
+                                    C.POINTER(lt_report), C.POINTER(lt_status)]),
     "sweep_frontier_capacity": (C.c_int32, [C.POINTER(lt_sweep_grid)]),
     "sweep_batch": (C.c_int32, [C.c_void_p, C.POINTER(lt_condition_batch), C.POINTER(lt_server_config),
                                 C.POINTER(lt_sweep_grid), C.c_double, C.c_uint64,

@@ -19,7 +19,8 @@ import numpy as np
 from . import _abi as A
 from .batch import (ConditionBatch, PackedConfig, PackedGrid, Runner, WorkloadBatch, sim_options)
 from .types import (AdapterSpec, Condition, DatasetProgress, DatasetSpec, DeviceError, ERROR_CLASSES, FrontierPoint, LengthMode, LengthSpec,
-                    LoratwinError, MetricsSummary, Phase, PlacementResult, Request, RequestState,
+                    IterationTraceRow, LoadEvent, LoadSource, LoratwinError, MetricsSummary, Phase, PlacementResult,
+                    Request, RequestState,
                     ServerConfig, SimOptions, SimulationResult, SweepGrid, SweepOptions, WorkloadSpec)
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
@@ -94,6 +95,14 @@ class Device:
         only with want_percentiles (sweeps never read them)."""
         return self.runner.simulate(batch, config, sim_options(options, want_digest, libm_variant, want_percentiles),
                                     want_states)
+
+    def simulate_report(self, batch: WorkloadBatch, config: ServerConfig, options: Optional[SimOptions] = None,
+                        want_digest: bool = False, libm_variant: int = -1, want_percentiles: bool = False):
+        """lt_simulate_report: (summaries, request states, report) where the
+        report holds the trace rows, load events and per-request emit times
+        (numpy arrays with their per-scenario / per-request offsets)."""
+        return self.runner.report(batch, config, sim_options(options, want_digest, libm_variant, want_percentiles,
+                                                             report=True))
 
     def generate_arrivals_batch(self, batch: WorkloadBatch, libm_variant: int = -1):
         return self.runner.generate_arrivals(batch, sim_options(None, False, libm_variant))
@@ -187,13 +196,31 @@ def metrics_of(row) -> MetricsSummary:
                           rejected_count=int(row["rejected_count"]), degenerate=bool(row["degenerate"]))
 
 
-def result_of(row, states, i: int) -> SimulationResult:
+def result_of(row, states, i: int, report=None, want_trace: bool = False) -> SimulationResult:
     reqs: List[RequestState] = []
+    loads: List[LoadEvent] = []
+    trace: List[IterationTraceRow] = []
+    if report is not None:
+        lo = int(report["load_offset"][i])
+        for e in report["loads"][lo:lo + int(row["load_events"])]:
+            loads.append(LoadEvent(time_s=float(e["time_s"]), adapter_id=int(e["adapter_id"]), rank=int(e["rank"]),
+                                   source=LoadSource(int(e["source"])), latency_s=float(e["latency_s"])))
+        if want_trace:
+            to = int(report["trace_offset"][i])
+            for t in report["trace"][to:to + int(row["iterations"])]:
+                trace.append(IterationTraceRow(time_s=float(t["time_s"]), iteration=int(t["iteration"]),
+                                               r_running=int(t["r_running"]), r_waiting=int(t["r_waiting"]),
+                                               a_running=int(t["a_running"]), lat_step_s=float(t["lat_step_s"]),
+                                               loads=int(t["loads"])))
     if states is not None:
         off = int(states["req_offset"][i])
         for k in range(int(row["n_requests"])):
             j = off + k
             first = float(states["first_token_time_s"][j])
+            emits: List[float] = []
+            if report is not None:
+                eo = int(report["emit_offset"][j])
+                emits = report["emit_times"][eo:eo + int(states["tokens_generated"][j])].tolist()
             reqs.append(RequestState(
                 request=Request(request_id=k, adapter_id=int(states["adapter_id"][j]),
                                 arrival_time_s=float(states["arrival_time_s"][j]),
@@ -202,13 +229,14 @@ def result_of(row, states, i: int) -> SimulationResult:
                 phase=Phase(int(states["phase"][j])), tokens_generated=int(states["tokens_generated"][j]),
                 first_token_time_s=None if math.isnan(first) else first,
                 completion_time_s=float(states["completion_time_s"][j]),
-                preemption_count=int(states["preemption_count"][j])))
+                preemption_count=int(states["preemption_count"][j]), token_emit_times_s=emits))
     return SimulationResult(requests=reqs, iterations=int(row["iterations"]), final_clock_s=float(row["final_clock_s"]),
                             duration_s=float(row["duration_s"]), truncated=bool(row["truncated"]),
                             slots=int(row["slots"]), served_adapters=int(row["served_adapters"]),
                             kv_capacity_tokens=int(row["kv_capacity_tokens"]), load_events=int(row["load_events"]),
                             preemptions=int(row["preemptions"]), tokens_in_window=int(row["tokens_in_window"]),
-                            digest=int(row["digest"]), metrics=metrics_of(row))
+                            digest=int(row["digest"]), metrics=metrics_of(row), load_event_list=loads,
+                            iteration_trace=trace)
 
 
 def placement_of(row, frontier_rows) -> PlacementResult:
@@ -227,9 +255,9 @@ def run_simulation(workload: WorkloadSpec, config: ServerConfig, mode: LengthMod
     """engine.hpp:70-71 — one engine on the B200 (result + device-computed metrics)."""
     dev = dev or device()
     batch = WorkloadBatch.from_workloads([workload], mode=mode)
-    out, states = dev.simulate_batch(batch, config, options, want_states=True, want_percentiles=True)
+    out, states, rep = dev.simulate_report(batch, config, options, want_percentiles=True)
     raise_for(out[0], dev.message(0))
-    return result_of(out[0], states, 0)
+    return result_of(out[0], states, 0, rep, bool(options and options.record_iteration_trace))
 
 
 def run_scripted(requests: Sequence[Request], adapters: Sequence[AdapterSpec], duration_s: float,
@@ -240,9 +268,9 @@ def run_scripted(requests: Sequence[Request], adapters: Sequence[AdapterSpec], d
     w = WorkloadSpec(adapters=list(adapters), duration_s=duration_s)
     w.lengths.mean_input = w.lengths.mean_output = 1.0  # unused by scripted runs
     batch = WorkloadBatch.from_workloads([w], scripted=[list(requests)])
-    out, states = dev.simulate_batch(batch, config, options, want_states=True, want_percentiles=True)
+    out, states, rep = dev.simulate_report(batch, config, options, want_percentiles=True)
     raise_for(out[0], dev.message(0))
-    return result_of(out[0], states, 0)
+    return result_of(out[0], states, 0, rep, bool(options and options.record_iteration_trace))
 
 
 def _length_means(spec: LengthSpec):

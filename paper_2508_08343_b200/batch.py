@@ -172,12 +172,13 @@ class ConditionBatch:
 
 
 def sim_options(opts: Optional[SimOptions] = None, want_digest: bool = False,
-                libm_variant: int = -1, want_percentiles: bool = False) -> A.lt_sim_options:
+                libm_variant: int = -1, want_percentiles: bool = False,
+                report: bool = False) -> A.lt_sim_options:
     o = A.lt_sim_options()
     opts = opts or SimOptions()
-    if opts.record_iteration_trace:
-        raise UnsupportedError("SimOptions.record_iteration_trace: per-iteration trace rows are not produced by "
-                               "the batched device path (the decision digest covers the same fields)")
+    if opts.record_iteration_trace and not report:
+        raise UnsupportedError("SimOptions.record_iteration_trace: trace rows come from the report call "
+                               "(Device.simulate_report / run_simulation), not from simulate_batch")
     o.check_invariants = int(opts.check_invariants)
     o.want_digest = int(want_digest)
     # engine.cpp:75 uses value_or(cap): an override <= 1 truncates after the
@@ -258,6 +259,43 @@ class Runner:
         if st.code == A.LT_ERR_DEVICE:
             self._raise(st.code, st.index, st.message.decode())
         return out[:n], states
+
+    def report(self, batch: WorkloadBatch, config: ServerConfig, options: A.lt_sim_options):
+        """lt_simulate_report: summaries, request states and the full report
+        (trace rows, load events, per-request emit times). A first
+        lt_simulate_batch call sizes the buffers."""
+        out, states = self.simulate(batch, config, options, want_states=True)
+        n = len(batch.scenarios)
+        ok = out["status"] == A.LT_OK
+        n_ld = int(out["load_events"].sum()) if n else 0
+        n_em = int(out["tokens_total"][ok].sum()) if n else 0
+        cap = len(states["phase"])
+        rep = {"trace": np.zeros(max(int(out["iterations"].sum()) if n else 0, 1), dtype=A.TRACE_DT),
+               "trace_offset": np.zeros(max(n, 1), dtype=np.int64),
+               "loads": np.zeros(max(n_ld, 1), dtype=A.LOAD_EVENT_DT),
+               "load_offset": np.zeros(max(n, 1), dtype=np.int64),
+               "emit_times": np.zeros(max(n_em, 1), dtype=np.float64),
+               "emit_offset": np.zeros(max(cap, 1), dtype=np.int64)}
+        rc = A.lt_report()
+        rc.trace, rc.trace_capacity, rc.trace_offset = rep["trace"].ctypes.data, len(rep["trace"]), \
+            rep["trace_offset"].ctypes.data
+        rc.loads, rc.load_capacity, rc.load_offset = rep["loads"].ctypes.data, len(rep["loads"]), \
+            rep["load_offset"].ctypes.data
+        rc.emit_times, rc.emit_capacity, rc.emit_offset = rep["emit_times"].ctypes.data, len(rep["emit_times"]), \
+            rep["emit_offset"].ctypes.data
+        states_c = A.lt_request_states()
+        states_c.capacity = cap
+        states_c.req_offset = A.ptr(states["req_offset"])
+        for name, _ in REQUEST_STATE_FIELDS:
+            setattr(states_c, name, A.ptr(states[name]))
+        pc = PackedConfig(config)
+        cb = batch.c_struct()
+        st = A.lt_status()
+        self.lib.simulate_report(self.ctx, C.byref(cb), C.byref(pc.c), C.byref(options), out.ctypes.data,
+                                 C.byref(states_c), C.byref(rc), C.byref(st))
+        if st.code == A.LT_ERR_DEVICE:
+            self._raise(st.code, st.index, st.message.decode())
+        return out[:n], states, rep
 
     def _count_requests(self, batch: WorkloadBatch, options) -> int:
         sc = batch.scenarios

@@ -34,6 +34,7 @@
 
 #include "k_engine.cuh"
 #include "k_metrics.cuh"
+#include "k_report.cuh"
 #include "k_sweep.cuh"
 #include "k_workload.cuh"
 #include "loratwin_gpu.h"
@@ -1735,6 +1736,128 @@ void run_percentiles(lt_plan& P, EngineParams E) {
   P.launches_run += 5;  // engine + metrics (recording pass), ttft keys, percentiles
 }
 
+// lt_simulate_report's second engine pass (engine_kernel<256, 1, true>),
+// sized by the first pass's counts, and the emit-time expansion
+// (k_report.cuh). The rows stay on the device in R until copied out.
+struct ReportRun {
+  std::vector<int64_t> tr_off, ld_off, ld_len;
+  int64_t n_tr = 0, n_ld = 0, n_log = 0, n_emit = 0;
+  DBuf<int64_t> d_tr_off, d_ld_off, d_sl_off, tokens, emit_off;
+  DBuf<double> tr_time, tr_lat, emit;
+  DBuf<int4> tr_rwal;
+  DBuf<lt_trace_row> trace;
+  DBuf<DLoadEvent> ld;
+  DBuf<int2> sl_log;
+  DBuf<int32_t> sl_cnt, iters, iters_sorted;
+  DBuf<uint32_t> keys, keys_sorted;
+  DBuf<char> tmp;
+};
+
+void run_report(lt_plan& P, ReportRun& R) {
+  cudaStream_t st = P.st;
+  const int64_t n = P.n_scen;
+  const int64_t nr = std::max<int64_t>(P.total_req, 1);
+  std::vector<lt_sim_summary> h(n);
+  LT_CUDA(cudaMemcpyAsync(h.data(), P.out.p, n * sizeof(lt_sim_summary), cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaStreamSynchronize(st));
+  // rows per scenario: a trace row per iteration, the load events, and at
+  // most one stint-log entry per first admission, re-admission and
+  // preemption. A scenario that fails in the engine still writes the rows of
+  // its completed iterations, plus the loads of the failing call (<= N).
+  R.tr_off.resize(n);
+  R.ld_off.resize(n);
+  R.ld_len.resize(n);
+  std::vector<int64_t> sl_off(n);
+  int64_t n_sl = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    R.tr_off[i] = R.n_tr;
+    R.ld_off[i] = R.n_ld;
+    sl_off[i] = n_sl;
+    R.ld_len[i] = h[i].load_events;
+    R.n_tr += h[i].iterations;
+    R.n_ld += h[i].load_events + (h[i].status != LT_OK ? h[i].served_adapters : 0);
+    n_sl += P.h_scen[i].n_req + 2 * h[i].preemptions;
+  }
+  if (n_sl >= (int64_t(1) << 31) || P.total_req >= (int64_t(1) << 32) - 1)
+    throw CudaError{"lt_simulate_report: batch too large for one report (2^31 stint entries)"};
+  R.n_log = n_sl;
+  R.d_tr_off.upload(R.tr_off, st);
+  R.d_ld_off.upload(R.ld_off, st);
+  R.d_sl_off.upload(sl_off, st);
+  R.tr_time.alloc(std::max<int64_t>(R.n_tr, 1));
+  R.tr_lat.alloc(std::max<int64_t>(R.n_tr, 1));
+  R.tr_rwal.alloc(std::max<int64_t>(R.n_tr, 1));
+  R.ld.alloc(std::max<int64_t>(R.n_ld, 1));
+  R.sl_log.alloc(std::max<int64_t>(n_sl, 1));
+  R.sl_cnt.alloc(std::max<int64_t>(n, 1));
+  LT_CUDA(cudaMemsetAsync(R.sl_cnt.p, 0, R.sl_cnt.n * sizeof(int32_t), st));
+  reset_state(P);
+  EngineParams E = engine_params(P);
+  E.tr_off = R.d_tr_off.p;
+  E.tr_time = R.tr_time.p;
+  E.tr_lat = R.tr_lat.p;
+  E.tr_rwal = R.tr_rwal.p;
+  E.ld_off = R.d_ld_off.p;
+  E.ld = R.ld.p;
+  E.sl_off = R.d_sl_off.p;
+  E.sl_log = R.sl_log.p;
+  E.sl_cnt = R.sl_cnt.p;
+  // the plan's warp layout, at most 8 warps per block (the report kernel is
+  // the latency variant's code)
+  const int warps = std::min(P.block / 32, 8);
+  const void* rk = reinterpret_cast<const void*>(engine_kernel<256, 1, true>);
+  LT_CUDA(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, P.ctx->smem_optin));
+  engine_kernel<256, 1, true><<<P.grid, warps * 32, static_cast<size_t>(P.smem_per_warp) * warps, st>>>(E);
+  after_launch("engine_kernel(report)", st);
+  metrics_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, st>>>(E.scen, E.n_scen, E.r_phase, E.r_first, E.r_arr,
+                                                                     E.r_last, E.r_out, E.r_gen, E.out);
+  after_launch("metrics_kernel(report)", st);
+  // trace rows as lt_trace_row
+  R.trace.alloc(std::max<int64_t>(R.n_tr, 1));
+  if (R.n_tr > 0) {
+    trace_pack_kernel<<<static_cast<unsigned>((R.n_tr + 255) / 256), 256, 0, st>>>(
+        R.d_tr_off.p, static_cast<int>(n), R.n_tr, R.tr_time.p, R.tr_lat.p, R.tr_rwal.p, R.trace.p);
+    after_launch("trace_pack_kernel", st);
+  }
+  // emit times: stint log grouped by request (stable), then expanded
+  R.keys.alloc(std::max<int64_t>(n_sl, 1));
+  R.keys_sorted.alloc(std::max<int64_t>(n_sl, 1));
+  R.iters.alloc(std::max<int64_t>(n_sl, 1));
+  R.iters_sorted.alloc(std::max<int64_t>(n_sl, 1));
+  LT_CUDA(cudaMemsetAsync(R.keys.p, 0xff, R.keys.n * sizeof(uint32_t), st));
+  stint_keys_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, st>>>(P.scen.p, static_cast<int>(n), R.d_sl_off.p,
+                                                                        R.sl_cnt.p, R.sl_log.p, R.keys.p, R.iters.p);
+  after_launch("stint_keys_kernel", st);
+  R.tokens.alloc(nr);
+  R.emit_off.alloc(nr);
+  request_tokens_kernel<<<static_cast<unsigned>((nr + 255) / 256), 256, 0, st>>>(
+      P.scen.p, static_cast<int>(n), P.out.p, P.r_phase.p, P.r_gen.p, P.r_out.p, P.total_req, R.tokens.p);
+  after_launch("request_tokens_kernel", st);
+  size_t b1 = 0, b2 = 0;
+  LT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, R.keys.p, R.keys_sorted.p, R.iters.p, R.iters_sorted.p,
+                                          static_cast<int>(std::max<int64_t>(n_sl, 1)), 0, 32, st));
+  LT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b2, R.tokens.p, R.emit_off.p, static_cast<int>(nr), st));
+  R.tmp.alloc(std::max<size_t>(std::max(b1, b2), 1));
+  LT_CUDA(cub::DeviceRadixSort::SortPairs(R.tmp.p, b1, R.keys.p, R.keys_sorted.p, R.iters.p, R.iters_sorted.p,
+                                          static_cast<int>(std::max<int64_t>(n_sl, 1)), 0, 32, st));
+  LT_CUDA(cub::DeviceScan::ExclusiveSum(R.tmp.p, b2, R.tokens.p, R.emit_off.p, static_cast<int>(nr), st));
+  int64_t last_off = 0, last_tok = 0;
+  if (P.total_req > 0) {
+    LT_CUDA(cudaMemcpyAsync(&last_off, R.emit_off.p + P.total_req - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaMemcpyAsync(&last_tok, R.tokens.p + P.total_req - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  }
+  LT_CUDA(cudaStreamSynchronize(st));
+  R.n_emit = last_off + last_tok;
+  R.emit.alloc(std::max<int64_t>(R.n_emit, 1));
+  if (P.total_req > 0) {
+    emit_times_kernel<<<static_cast<unsigned>((P.total_req + 255) / 256), 256, 0, st>>>(
+        P.scen.p, static_cast<int>(n), P.total_req, R.keys_sorted.p, R.iters_sorted.p, n_sl, R.tokens.p,
+        R.emit_off.p, R.d_tr_off.p, R.tr_time.p, R.tr_lat.p, R.emit.p);
+    after_launch("emit_times_kernel", st);
+  }
+  P.launches_run += 7;
+}
+
 void fetch_results(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {
   lt_ctx* ctx = P.ctx;
   cudaStream_t st = P.st;
@@ -2292,6 +2415,83 @@ int32_t lt_simulate_batch(lt_ctx* ctx, const lt_workload_batch* batch, const lt_
   ctx->timing.plan_ms = plan_ms;
   ctx->timing.run_wait_ms = ctx->timing.total_ms - plan_ms;
   return rc;
+}
+
+int32_t lt_simulate_report(lt_ctx* ctx, const lt_workload_batch* batch, const lt_server_config* config,
+                           const lt_sim_options* options, lt_sim_summary* out, lt_request_states* states,
+                           lt_report* report, lt_status* status) {
+  ok_status(status);
+  if (!states || !report) {
+    set_status(status, LT_ERR_VALIDATION, LT_K_MESSAGE, -1, 0, 0, "lt_simulate_report: states and report are required");
+    return LT_ERR_VALIDATION;
+  }
+  if (!ctx->members.empty()) {  // one plan: the first device
+    const int32_t rc = lt_simulate_report(ctx->members[0], batch, config, options, out, states, report, status);
+    ctx->messages = ctx->members[0]->messages;
+    ctx->timing = ctx->members[0]->timing;
+    return rc;
+  }
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  try {
+    cudaSetDevice(ctx->device);
+    std::unique_ptr<lt_plan> plan(build_plan(ctx, batch, config, options));
+    lt_plan& P = *plan;
+    const double plan_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+    const int want_pct = P.want_pct;
+    P.want_pct = 0;  // the report pass rewrites the summaries: percentiles last
+    run_plan(P);
+    ReportRun R;
+    if (P.n_scen > 0) {
+      run_report(P, R);
+      if (want_pct) run_percentiles(P, engine_params(P));
+    }
+    fetch_results(P, out, states);
+    cudaStream_t st = P.st;
+    const int64_t n = P.n_scen;
+    // trace rows (dense: iterations per scenario)
+    for (int64_t i = 0; i < n; ++i) {
+      if (report->trace_offset) report->trace_offset[i] = R.tr_off[i];
+    }
+    const int64_t nt = std::min<int64_t>(R.n_tr, std::max<int64_t>(report->trace_capacity, 0));
+    if (nt > 0 && report->trace)
+      LT_CUDA(cudaMemcpyAsync(report->trace, R.trace.p, nt * sizeof(lt_trace_row), cudaMemcpyDeviceToHost, st));
+    // emit times, one offset per request row (device request order = row order)
+    const int64_t nr = std::min<int64_t>(P.total_req, std::max<int64_t>(states->capacity, 0));
+    if (nr > 0 && report->emit_offset)
+      LT_CUDA(cudaMemcpyAsync(report->emit_offset, R.emit_off.p, nr * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    const int64_t ne = std::min<int64_t>(R.n_emit, std::max<int64_t>(report->emit_capacity, 0));
+    if (ne > 0 && report->emit_times)
+      LT_CUDA(cudaMemcpyAsync(report->emit_times, R.emit.p, ne * sizeof(double), cudaMemcpyDeviceToHost, st));
+    std::vector<DLoadEvent> ld(R.n_ld);
+    if (R.n_ld > 0) LT_CUDA(cudaMemcpyAsync(ld.data(), R.ld.p, R.n_ld * sizeof(DLoadEvent), cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    // load events, dense in scenario order (the device rows of a failed
+    // scenario carry slack for its failing call)
+    int64_t lo = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (report->load_offset) report->load_offset[i] = lo;
+      for (int64_t k = 0; k < R.ld_len[i]; ++k, ++lo) {
+        if (lo >= report->load_capacity || !report->loads) continue;
+        const DLoadEvent& e = ld[R.ld_off[i] + k];
+        lt_load_event& o = report->loads[lo];
+        o.time_s = e.time;
+        o.adapter_id = e.adapter_id;
+        o.rank = e.rank;
+        o.source = P.cfg.raw.load_source;
+        o._pad = 0;
+        o.latency_s = e.latency;
+      }
+    }
+    ctx->timing.d2h_bytes += nt * static_cast<int64_t>(sizeof(lt_trace_row)) + ne * 8 + nr * 8 +
+                             R.n_ld * static_cast<int64_t>(sizeof(DLoadEvent));
+    ctx->timing.total_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+    ctx->timing.plan_ms = plan_ms;
+    return first_error(ctx, out, n, status);
+  } catch (const CudaError& e) {
+    set_status(status, LT_ERR_DEVICE, LT_K_MESSAGE, -1, 0, 0, e.what);
+    return LT_ERR_DEVICE;
+  }
 }
 
 int32_t lt_generate_arrivals_batch(lt_ctx* ctx, const lt_workload_batch* batch, const lt_sim_options* options,

@@ -327,6 +327,9 @@ struct WarpEngine {
   // --- scan-local SlotPlan state
   uint32_t evicted_w = 0, blocked_w = 0;
   int32_t free_slots = 0;
+  // --- report pass: bases of this scenario's load-event and stint-log rows
+  int64_t ld_base = 0, sl_base = 0;
+  int32_t sl_n = 0;
   // --- pointers
   int64_t rb = 0, ab = 0;
   int lane = 0;
@@ -649,6 +652,7 @@ struct WarpEngine {
   }
 
   // decode_step_alloc (kv_scheduler.cpp:183-236).
+  template <bool kRep>
   __device__ __forceinline__ bool alloc(const EngineParams& P) {
     if (R == 0) return true;
     int64_t demand = R;
@@ -672,7 +676,9 @@ struct WarpEngine {
         P.r_gen[rb + idx] = gen;
         P.r_last[rb + idx] = clock;
         zero = atomicSub(&run_cnt[a], 1) == 1;
+        if constexpr (kRep) P.sl_log[sl_base + sl_n] = make_int2(idx, iter);
       }
+      if constexpr (kRep) ++sl_n;
       zero = __shfl_sync(kFull, zero, 0);
       release_adapter(a, zero);
       const bool over = static_cast<int64_t>(in) + gen + 1 > cap;
@@ -1131,6 +1137,7 @@ struct WarpEngine {
 
   // SlotCache::ensure_loaded (adapter_cache.cpp:40-78) with needed = the
   // running batch's adapters (engine.cpp:108-114). Returns Σ load latency.
+  template <bool kRep>
   __device__ __forceinline__ bool ensure_loaded(const EngineParams& P, double* loads_sum, int* loads_cnt) {
     const uint32_t needed_w = claimed_w;
     const int n_needed = __reduce_add_sync(kFull, __popc(needed_w));
@@ -1162,6 +1169,9 @@ struct WarpEngine {
         return false;
       }
       sum = sum + ll;
+      if constexpr (kRep) {
+        if (lane == 0) P.ld[ld_base + loads_n + cnt] = DLoadEvent{clock, ll, ad.id, ad.rank};
+      }
       ++cnt;
       mask_clear(missing_w, a, lane);
     }
@@ -1182,6 +1192,7 @@ struct WarpEngine {
   }
 };
 
+template <bool kRep>
 __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_warp) {
   const long long t_start = clock64();
 #ifdef LT_PHASE_PROF
@@ -1277,6 +1288,12 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   double next_arr = __shfl_sync(kFull, pf_t, 0);  // arrival time of request `ingest`
   const int64_t rec_base = P.record ? P.rec_off[s] : 0;
   int64_t rec_n = 0;
+  int64_t tr_base = 0;
+  if constexpr (kRep) {
+    tr_base = P.tr_off[s];
+    E.ld_base = P.ld_off[s];
+    E.sl_base = P.sl_off[s];
+  }
 
   while (true) {
     __syncwarp();
@@ -1353,7 +1370,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     LT_PH(0);
     if (E.R > 0) E.retire(P);
     LT_PH(1);
-    if (!E.alloc(P)) break;
+    if (!E.template alloc<kRep>(P)) break;
     LT_PH(2);
     const int r_before = E.R_end;
     const int w_before = E.Wp + E.Wf, rcount_before = E.R;
@@ -1375,6 +1392,15 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     }
     __syncwarp();
     LT_PH(4);
+    if constexpr (kRep) {  // stint log: this iteration's admissions, in running-set order
+      for (int base = r_before; base < E.R_end; base += 32) {
+        const int i = base + lane;
+        const int4 e = i < E.R_end ? E.run_get(i) : make_int4(-1, 0, 0, 0);
+        const unsigned m = __ballot_sync(kFull, e.x >= 0);
+        if (e.x >= 0) P.sl_log[E.sl_base + E.sl_n + __popc(m & lanemask_lt())] = make_int2(e.x, E.iter);
+        E.sl_n += __popc(m);
+      }
+    }
     if (E.R == 0) {
       if (E.Wp + E.Wf != 0) {
         E.fail(LT_ERR_INTERNAL, LT_K_ADMISSION_STUCK, 0, 0);
@@ -1384,7 +1410,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     }
     double loads = 0.0;
     int nl = 0;
-    if (!E.ensure_loaded(P, &loads, &nl)) break;
+    if (!E.template ensure_loaded<kRep>(P, &loads, &nl)) break;
     E.loads_n += nl;
     // lat_step (estimators.cpp:110-139), no contraction (--fmad=false).
     const int W = E.Wp + E.Wf;
@@ -1398,6 +1424,13 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     const double adapters = (A == 0) ? 1.0 : P.k6 * static_cast<double>(A) + P.k7;
     const double lat = sched + loads + model * adapters;
     const double emit = E.clock + lat;
+    if constexpr (kRep) {  // IterationTraceRow (engine.cpp:137-140)
+      if (lane == 0) {
+        P.tr_time[tr_base + E.iter] = E.clock;
+        P.tr_lat[tr_base + E.iter] = lat;
+        P.tr_rwal[tr_base + E.iter] = make_int4(E.R, W, A, nl);
+      }
+    }
     if (LT_UNLIKELY(P.record)) {  // ITL multiset of compute_metrics (metrics.cpp:92-105)
       const int64_t r0 = rec_base + rec_n;
       if (lane == 0) {
@@ -1491,6 +1524,13 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
             P.rec_d[rec_base + rec_n + n] = clk - start;
             P.rec_c[rec_base + rec_n + n] = E.R;
           }
+          if constexpr (kRep) {
+            if (lane == 0) {
+              P.tr_time[tr_base + E.iter + n] = start;
+              P.tr_lat[tr_base + E.iter + n] = lat_q;
+              P.tr_rwal[tr_base + E.iter + n] = make_int4(E.R, W, A, 0);
+            }
+          }
           win += (clk <= E.duration);
           ++n;
           if (LT_UNLIKELY(P.want_digest)) {
@@ -1552,6 +1592,9 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
 #endif
   o.device_cycles = clock64() - t_start;
   if (lane == 0) P.out[s] = o;
+  if constexpr (kRep) {
+    if (lane == 0) P.sl_cnt[s] = E.sl_n;
+  }
 }
 
 // Persistent kernel: each warp pulls scenarios (cost-descending order) from a
@@ -1559,7 +1602,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
 // one 8-warp block per SM, the shortest per-engine latency (the batch's
 // longest engines set its time). kMinBlocks = 2: <= 128 registers, 16 warps
 // per SM, for batches with many rounds of engines per warp (throughput).
-template <int kThreads, int kMinBlocks>
+template <int kThreads, int kMinBlocks, bool kRep = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(EngineParams P) {
   extern __shared__ __align__(16) char smem[];
   const int warp = threadIdx.x >> 5;
@@ -1576,7 +1619,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(EnginePara
   const int first = rank * gridDim.x + blockIdx.x;
   // (one call site: engine_run is inlined once)
   for (int k = first; k < P.n_scen;) {
-    engine_run(P, P.order[k], slot, mine);
+    engine_run<kRep>(P, P.order[k], slot, mine);
     int nk = 0;
     if ((threadIdx.x & 31) == 0) nk = atomicAdd(P.counter, 1) + gridDim.x * warps;
     k = __shfl_sync(kFull, nk, 0);

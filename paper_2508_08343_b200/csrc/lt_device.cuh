@@ -61,6 +61,15 @@ struct DAdapter {
   int64_t list_off; // Full mode: first (in, out) pair of the adapter's length list
 };
 
+// LoadEvent (adapter_cache.hpp:28-34) as the report pass writes it; the
+// source is the config's default_source for every event (engine.cpp:113-114).
+struct DLoadEvent {
+  double time;
+  double latency;
+  int32_t adapter_id;
+  int32_t rank;
+};
+
 // Full-mode length deck of one (RNG key, list size D): the lengths stream
 // {2, id} shuffles the deck once, then again every D requests
 // (workload.cpp:149-161). tab[table_off + j] is the list index of arrival j.
@@ -125,6 +134,20 @@ struct EngineParams {
   const int64_t* rec_off;
   double* rec_d;
   int32_t* rec_c;
+  // report pass (lt_simulate_report, engine_kernel<.., true>): trace row k of
+  // scenario s at tr_off[s] + k (engine.cpp:137-140), its load events at
+  // ld_off[s] in emission order (:141), and a stint log at sl_off[s]: one
+  // {request, iteration} per admission and per preemption, in the order they
+  // happen (a request's entries alternate admit / preempt); sl_cnt[s] = entries
+  const int64_t* tr_off;
+  double* tr_time;
+  double* tr_lat;
+  int4* tr_rwal;  // {R, W, A, loads}
+  const int64_t* ld_off;
+  DLoadEvent* ld;
+  const int64_t* sl_off;
+  int2* sl_log;
+  int32_t* sl_cnt;
 };
 
 }  // namespace lt

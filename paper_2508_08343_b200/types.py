@@ -195,13 +195,35 @@ class SimOptions:  # engine.hpp:29-35
 
 
 @dataclass
-class RequestState:  # kv_scheduler.hpp:30-41 (token emit vectors are not materialised)
+class RequestState:  # kv_scheduler.hpp:30-41
     request: Request
     phase: Phase
     tokens_generated: int
     first_token_time_s: Optional[float]
     completion_time_s: float
     preemption_count: int
+    # filled by the report call (run_simulation / run_scripted / simulate_report)
+    token_emit_times_s: List[float] = field(default_factory=list)
+
+
+@dataclass
+class LoadEvent:  # adapter_cache.hpp:28-34
+    time_s: float
+    adapter_id: int
+    rank: int
+    source: "LoadSource"
+    latency_s: float
+
+
+@dataclass
+class IterationTraceRow:  # engine.hpp:37-45
+    time_s: float
+    iteration: int
+    r_running: int
+    r_waiting: int
+    a_running: int
+    lat_step_s: float
+    loads: int
 
 
 @dataclass
@@ -235,6 +257,11 @@ class SimulationResult:  # engine.hpp:47-64
     tokens_in_window: int
     digest: int
     metrics: MetricsSummary
+    # SimulationResult.load_events / iteration_trace of the reference (the
+    # count above keeps the name load_events); filled by the report call,
+    # iteration_trace only with SimOptions.record_iteration_trace
+    load_event_list: List[LoadEvent] = field(default_factory=list)
+    iteration_trace: List[IterationTraceRow] = field(default_factory=list)
 
 
 @dataclass
