@@ -21,6 +21,7 @@ from paper_2508_08343_b200.batch import Runner
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_LIB = os.path.join(HERE, "_ref", "libloratwin_ref.so")
 PORT_LIB = os.path.join(HERE, "_ref", "libloratwin_oracle.so")
+SHIM_CHECK = os.path.join(HERE, "_ref", "gpu_backend_check")
 REFERENCE_SRC = "/root/reference/proj/core"
 
 
@@ -30,7 +31,7 @@ def build(target: str = "all") -> None:
     if "restate" in targets and not os.path.exists(os.path.join(HERE, "restate.c")):
         targets.remove("restate")
     if target == "all" and os.path.isdir(REFERENCE_SRC):
-        targets.append("ref")
+        targets += ["ref", "shim"]  # shim: the reference-side binding + its check (needs the GPU library built)
     if targets:
         subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 

@@ -74,6 +74,12 @@ def build_native(force: bool = False) -> None:
         if force or _stale(out, deps):
             subprocess.run([cxx, "-std=c++17", "-O2", "-ffp-contract=off", "-DLT_NO_CONTRACT", "-I" + CSRC,
                             src, "-o", out], check=True)
+    # the same ports compiled for the device (sm_100a, --fmad=false), checked
+    # against the host glibc on the GPU box (tests/test_gpu_robustness.py)
+    src = os.path.join(NATIVE, "libm_device.cu")
+    out = os.path.join(NATIVE_BIN, "libm_device")
+    if force or _stale(out, [src] + glob.glob(os.path.join(CSRC, "*.h"))):
+        subprocess.run([nvcc()] + NVCC_FLAGS[:-2] + ["-I" + CSRC, src, "-o", out, "-lpthread"], check=True)
 
 
 def build_oracle() -> None:

@@ -2445,6 +2445,10 @@ int32_t lt_simulate_report(lt_ctx* ctx, const lt_workload_batch* batch, const lt
     if (P.n_scen > 0) {
       run_report(P, R);
       if (want_pct) run_percentiles(P, engine_params(P));
+      // the exact ITL mean from the emit times, after every pass that rewrites the summaries
+      itl_exact_kernel<<<static_cast<unsigned>((P.n_scen + 127) / 128), 128, 0, P.st>>>(
+          P.scen.p, static_cast<int>(P.n_scen), P.out.p, R.tokens.p, R.emit_off.p, R.emit.p);
+      after_launch("itl_exact_kernel", P.st);
     }
     fetch_results(P, out, states);
     cudaStream_t st = P.st;

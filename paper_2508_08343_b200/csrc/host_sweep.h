@@ -301,7 +301,7 @@ void sweep_waves_device(lt_ctx* ctx, const SweepSetup& S, const lt_server_config
     }
   }
   cudaEventRecord(W.ev[1], st);
-  tm.tables_ms += elapsed(W.ev[0], W.ev[1]);
+  bool tables_timed = false;  // read once the first wave has synchronised the stream
   // point table and the per-condition early-exit state
   d_pts.alloc(std::max<int64_t>(S.n_points, 1));
   DBuf<int64_t> d_base;
@@ -440,6 +440,10 @@ void sweep_waves_device(lt_ctx* ctx, const SweepSetup& S, const lt_server_config
       after_launch("wave_scatter_kernel", st);
       tm.launches += 3;
       LT_CUDA(cudaStreamSynchronize(st));
+      if (!tables_timed) {
+        tm.tables_ms += elapsed(W.ev[0], W.ev[1]);
+        tables_timed = true;
+      }
       tm.engine_ms += elapsed(W.ev[4], W.ev[5]);
       tm.merge_ms += elapsed(W.ev[2], W.ev[3]);
       tm.run_ms += elapsed(W.ev[2], W.ev[5]);

@@ -208,6 +208,7 @@ __device__ __noinline__ int compact_running(RunTiers t, int R_end, int lane) {
     const int i = base + lane;
     const int4 e = (i < R_end) ? get(i) : make_int4(-1, INT_MAX, 0, 0);
     const unsigned lm = __ballot_sync(kFull, e.x >= 0);
+    __syncwarp();  // every lane's read of this chunk precedes the stores into it
     if (e.x >= 0) {
       const int d = w + __popc(lm & lanemask_lt());
       if (d < t.run_cap)
@@ -560,6 +561,7 @@ struct WarpEngine {
       }
       R_end = lo;
     }
+    __syncwarp();  // the slots read above may be rewritten by lane 0's next append
   }
 
   // Stable compaction of the live entries (amortised: only when tombstones
@@ -586,6 +588,7 @@ struct WarpEngine {
         const int a = e.z & kAdapterMask;
         released += static_cast<long long>(e.w) - (idx == waived ? 1 : 0);
         const int left = run_cnt[a] - 1;
+        __syncwarp();  // every lane has read run_cnt[a] and slot p before lane 0 rewrites them
         if (lane == 0) {
           P.r_phase[rb + idx] = kFinished;
           P.r_last[rb + idx] = clock;  // completion == the final emit (engine.cpp:134)
@@ -907,6 +910,7 @@ struct WarpEngine {
       pl_valid = true;
     }
     pl_cl = mask_bit(claimed_w, pl_a < 0 ? 0 : pl_a);  // claims/releases since the last scan
+    __syncwarp();  // chain heads read above are rewritten by lane 0 as the scan admits
   }
 
   __device__ __forceinline__ void nonlane_best(bool direct, int* bkey, int* ba) const {
@@ -1325,6 +1329,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         const int a = __shfl_sync(kFull, a_l, src);
         const int id = E.ingest + src;
         const int t = E.q_tail[a];
+        __syncwarp();  // every lane has read q_tail[a] before lane 0 rewrites it
         if (lane == 0) {
           if (t < 0)
             E.q_head[a] = id;

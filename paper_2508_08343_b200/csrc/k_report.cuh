@@ -114,4 +114,27 @@ __global__ void __launch_bounds__(256) emit_times_kernel(const DScen* scen, int 
   }
 }
 
+// compute_metrics' ITL mean from the materialised emit times, in the
+// reference's order: requests in id order, each request's gaps in emit order,
+// one sequential sum (std::accumulate over the flattened list, metrics.cpp:
+// 29-32, :92-94) -- bit-exact where the engine epilogue's per-request sums
+// are within 1e-9. One thread per scenario.
+__global__ void __launch_bounds__(128) itl_exact_kernel(const DScen* scen, int n_scen, lt_sim_summary* out,
+                                                       const int64_t* tokens, const int64_t* emit_off,
+                                                       const double* emit) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_scen || out[s].status != LT_OK || scen[s].n_req == 0) return;
+  double sum = 0.0;
+  int64_t cnt = 0;
+  const int64_t g0 = scen[s].req_begin;
+  for (int64_t g = g0; g < g0 + scen[s].n_req; ++g) {
+    const double* e = emit + emit_off[g];
+    for (int64_t i = 1; i < tokens[g]; ++i) {
+      sum += e[i] - e[i - 1];
+      ++cnt;
+    }
+  }
+  out[s].itl_mean_s = cnt ? sum / static_cast<double>(cnt) : 0.0;
+}
+
 }  // namespace lt

@@ -40,6 +40,24 @@ def test_device_group_argument_errors_without_a_gpu():
     assert lib.device_count(None) == 0 and lib.gather_transport(None) == A.GATHER_NONE
 
 
+def test_reference_side_binding_builds_and_reports_no_device():
+    """integration/gpu_backend.cpp (the shim INTEGRATION.md describes),
+    compiled against the reference's own headers and linked with its TUs and
+    libloratwin_gpu.so; without a GPU the library's LT_ERR_DEVICE status
+    comes back as the reference's InternalError."""
+    from oracle import pyoracle
+
+    if not os.path.exists(pyoracle.SHIM_CHECK):
+        if not os.path.isdir(pyoracle.REFERENCE_SRC):
+            pytest.skip("built only where /root/reference exists")
+        pyoracle.build("shim")
+    p = subprocess.run([pyoracle.SHIM_CHECK], capture_output=True, text=True, timeout=120)
+    if p.returncode == 0:
+        pytest.skip("a GPU is visible: tests/test_gpu_report.py runs the full check")
+    assert p.returncode == 3, p.stdout + p.stderr
+    assert p.stdout.startswith("no-device: ")
+
+
 def test_library_is_sm100a():
     out = subprocess.run(["cuobjdump", "--list-elf", B.LIB], capture_output=True, text=True).stdout
     assert "sm_100a" in out

@@ -25,7 +25,8 @@ def assert_reports_equal(dev, ref, batch, cfg, where=""):
     opts = sim_options(None, False, -1, False, report=True)
     g, gs, gr = dev.runner.report(batch, cfg, opts)
     r, rs, rr = ref.report(batch, cfg, opts)
-    for f in ("status", "iterations", "load_events", "tokens_total", "preemptions", "final_clock_s"):
+    for f in ("status", "iterations", "load_events", "tokens_total", "preemptions", "final_clock_s",
+              "throughput_tok_s", "ttft_mean_s", "itl_mean_s"):  # the report path's ITL mean is exact
         np.testing.assert_array_equal(g[f], r[f], err_msg=where + f)
     for k in gs:
         np.testing.assert_array_equal(gs[k], rs[k], err_msg=where + k)
@@ -109,3 +110,20 @@ def test_run_simulation_returns_full_result(dev, ref):
     # throughput = emits inside the window / duration (metrics.cpp:96)
     emits = sum(sum(1 for t in r.token_emit_times_s if t <= wl.duration_s) for r in res.requests)
     assert res.metrics.throughput_tok_s == emits / wl.duration_s
+
+
+def test_reference_side_binding_prints_identical_reports():
+    """The reference's own code through integration/gpu_backend.cpp: its
+    simulation_report_json / placement_result_to_json print byte-identical
+    documents for the GPU results and for its own run_simulation /
+    run_scripted / sweep_optimal (oracle/_ref/gpu_backend_check, built with
+    the oracle where /root/reference exists)."""
+    import subprocess
+
+    from oracle import pyoracle
+
+    if not os.path.exists(pyoracle.SHIM_CHECK):
+        pytest.skip("oracle/_ref/gpu_backend_check not built (needs /root/reference at build time)")
+    p = subprocess.run([pyoracle.SHIM_CHECK], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-2000:]
+    assert p.stdout.startswith("ok: ")
