@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define LT_ABI_VERSION 3
+#define LT_ABI_VERSION 4
 
 /* Exception classes of errors.hpp, plus two conditions of this library. */
 enum lt_code {
@@ -464,6 +464,57 @@ uint64_t lt_condition_hash(const lt_template* mix, int32_t n_mix, const lt_lengt
 /* encode_workload (placement.cpp:117-137): the 16 features. */
 int32_t lt_encode_workload(const lt_template* mix, int32_t n_mix, const lt_length_spec* lengths,
                            const int32_t* full_lengths, double* features16, lt_status* status);
+
+/* ---- Placement-model training on the device -------------
+ * train_tree / train_forest / train_placement_model and ForestModel::predict
+ * (predictor.hpp:41-118, predictor.cpp:202-269). Features are the 16
+ * WorkloadFeatures values per row (row-major, n_rows x 16); trees come back
+ * as the reference's node vectors (preorder, nodes[0] the root). */
+typedef struct lt_tree_params { /* TreeParams */
+  int32_t max_depth;
+  int32_t min_leaf;
+  int32_t feature_subset; /* features considered per node, 1..16 */
+  int32_t _pad;
+} lt_tree_params;
+
+typedef struct lt_forest_params { /* ForestParams */
+  int32_t n_trees;
+  int32_t bootstrap;
+  lt_tree_params tree;
+} lt_forest_params;
+
+typedef struct lt_tree_node { /* TreeNode */
+  int32_t feature_index; /* -1: leaf */
+  int32_t left, right;
+  int32_t _pad;
+  double threshold;
+  double value;
+  int64_t coverage;
+} lt_tree_node;
+
+/* train_tree(x, y, params, seed, tree_tag): node_count[0] nodes at nodes[0..]. */
+int32_t lt_train_tree(lt_ctx* ctx, const double* x, int64_t n_rows, const double* y,
+                      const lt_tree_params* params, uint64_t seed, uint64_t tree_tag,
+                      lt_tree_node* nodes, int64_t node_capacity, int32_t* node_count,
+                      lt_status* status);
+
+/* train_forest for each of n_targets targets (y: n_targets rows of n_rows;
+ * target_tags: PredictTarget 0 throughput, 1 n_star, 2 g_star) over the same
+ * features -- train_placement_model is the three targets at once. Tree t of
+ * target g is tree g * n_trees + t, its nodes at nodes[node_offset[..]] with
+ * node_count[..] entries. All trees grow on the device in one call. */
+int32_t lt_train_forests(lt_ctx* ctx, const double* x, int64_t n_rows, const double* y,
+                         const int32_t* target_tags, int32_t n_targets, const lt_forest_params* params,
+                         uint64_t seed, lt_tree_node* nodes, int64_t node_capacity,
+                         int64_t* node_offset, int32_t* node_count, lt_status* status);
+
+/* ForestModel::predict of n_targets forests of n_trees trees each (the
+ * lt_train_forests layout) for n_rows feature rows: out[g * n_rows + i]; a
+ * negative target tag gives predict_raw (the plain mean of the trees). */
+int32_t lt_predict_forests(lt_ctx* ctx, const lt_tree_node* nodes, int64_t n_nodes,
+                           const int64_t* node_offset, int32_t n_trees, const int32_t* target_tags,
+                           int32_t n_targets, const double* x, int64_t n_rows, double* out,
+                           lt_status* status);
 
 /* Resident-input form for timing the device path alone: upload once, run
  * many times with inputs already in HBM, read results back once. */

@@ -66,7 +66,7 @@ class _Oracle(Runner):
 class RefOracle(_Oracle):
     prefix = "ltref_"
     path = REF_LIB
-    extra_symbols = A.DATASET_SYMBOLS + ["simulate_report"]
+    extra_symbols = A.DATASET_SYMBOLS + ["simulate_report"] + A.PREDICTOR_SYMBOLS
 
     def config_json_matches(self, text: str, packed_config) -> tuple:
         """(1 | 0 | -code, detail): the reference's server_config_from_json on

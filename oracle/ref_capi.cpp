@@ -566,3 +566,134 @@ int32_t ltref_config_json_matches(const char* text, const lt_server_config* c, c
 }
 
 }  // extern "C"
+
+// ---- predictor (predictor.cpp:202-269): the reference's own training ------
+#include "loratwin/predictor.hpp"
+
+namespace {
+
+std::vector<WorkloadFeatures> to_features(const double* x, int64_t n) {
+  std::vector<WorkloadFeatures> v(static_cast<std::size_t>(n));
+  for (int64_t i = 0; i < n; ++i)
+    for (std::size_t f = 0; f < kNumFeatures; ++f) v[i].values[f] = x[i * kNumFeatures + f];
+  return v;
+}
+
+TreeParams to_tree_params(const lt_tree_params& p) {
+  TreeParams t;
+  t.max_depth = p.max_depth;
+  t.min_leaf = static_cast<std::size_t>(p.min_leaf < 0 ? 0 : p.min_leaf);
+  t.feature_subset = static_cast<std::size_t>(p.feature_subset < 0 ? 0 : p.feature_subset);
+  return t;
+}
+
+int32_t put_trees(const std::vector<const DecisionTree*>& trees, lt_tree_node* nodes, int64_t cap,
+                  int64_t* offset, int32_t* count) {
+  int64_t off = 0;
+  for (std::size_t t = 0; t < trees.size(); ++t) {
+    if (offset) offset[t] = off;
+    if (count) count[t] = static_cast<int32_t>(trees[t]->nodes.size());
+    for (const TreeNode& n : trees[t]->nodes) {
+      if (off < cap && nodes)
+        nodes[off] = lt_tree_node{n.feature_index, n.left, n.right, 0, n.threshold, n.value,
+                                  static_cast<int64_t>(n.coverage)};
+      ++off;
+    }
+  }
+  return off <= cap ? LT_OK : LT_ERR_VALIDATION;
+}
+
+int32_t predictor_error(lt_status* st) {
+  std::string msg;
+  const int32_t code = classify(std::current_exception(), &msg);
+  set_status(st, code, -1, msg);
+  return code;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ltref_train_tree(void*, const double* x, int64_t n_rows, const double* y, const lt_tree_params* params,
+                         uint64_t seed, uint64_t tree_tag, lt_tree_node* nodes, int64_t cap, int32_t* count,
+                         lt_status* status) {
+  if (status) status->code = LT_OK;
+  try {
+    const DecisionTree t = train_tree(to_features(x, n_rows), std::vector<double>(y, y + n_rows),
+                                      to_tree_params(*params), seed, tree_tag);
+    return put_trees({&t}, nodes, cap, nullptr, count);
+  } catch (...) {
+    return predictor_error(status);
+  }
+}
+
+int32_t ltref_train_forests(void*, const double* x, int64_t n_rows, const double* y, const int32_t* tags,
+                            int32_t n_targets, const lt_forest_params* params, uint64_t seed, lt_tree_node* nodes,
+                            int64_t cap, int64_t* offset, int32_t* count, lt_status* status) {
+  if (status) status->code = LT_OK;
+  try {
+    ForestParams fp;
+    fp.n_trees = params->n_trees;
+    fp.bootstrap = params->bootstrap != 0;
+    fp.tree = to_tree_params(params->tree);
+    const std::vector<WorkloadFeatures> xf = to_features(x, n_rows);
+    std::vector<ForestModel> forests;
+    for (int32_t g = 0; g < n_targets; ++g)
+      forests.push_back(train_forest(xf, std::vector<double>(y + g * n_rows, y + (g + 1) * n_rows),
+                                     static_cast<PredictTarget>(tags[g]), fp, seed));
+    std::vector<const DecisionTree*> trees;
+    for (const ForestModel& f : forests)
+      for (const DecisionTree& t : f.trees) trees.push_back(&t);
+    return put_trees(trees, nodes, cap, offset, count);
+  } catch (...) {
+    return predictor_error(status);
+  }
+}
+
+int32_t ltref_predict_forests(void*, const lt_tree_node* nodes, int64_t, const int64_t* offset, int32_t n_trees,
+                              const int32_t* tags, int32_t n_targets, const double* x, int64_t n_rows, double* out,
+                              lt_status* status) {
+  if (status) status->code = LT_OK;
+  try {
+    const std::vector<WorkloadFeatures> xf = to_features(x, n_rows);
+    for (int32_t g = 0; g < n_targets; ++g) {
+      ForestModel m;
+      m.target = static_cast<PredictTarget>(tags[g] < 0 ? 0 : tags[g]);
+      for (int32_t t = 0; t < n_trees; ++t) {
+        const int64_t o = offset[g * n_trees + t];
+        DecisionTree d;
+        // node count: up to the next tree's offset is not known here; walk the preorder vector
+        std::vector<int64_t> stack{0};
+        int64_t maxk = 0;
+        while (!stack.empty()) {
+          const int64_t k = stack.back();
+          stack.pop_back();
+          maxk = std::max(maxk, k);
+          if (nodes[o + k].feature_index >= 0) {
+            stack.push_back(nodes[o + k].left);
+            stack.push_back(nodes[o + k].right);
+          }
+        }
+        for (int64_t k = 0; k <= maxk; ++k) {
+          const lt_tree_node& n = nodes[o + k];
+          TreeNode tn;
+          tn.feature_index = n.feature_index;
+          tn.threshold = n.threshold;
+          tn.left = n.left;
+          tn.right = n.right;
+          tn.value = n.value;
+          tn.coverage = static_cast<std::size_t>(n.coverage);
+          d.nodes.push_back(tn);
+        }
+        m.trees.push_back(std::move(d));
+      }
+      for (int64_t i = 0; i < n_rows; ++i)
+        out[g * n_rows + i] = tags[g] < 0 ? m.predict_raw(xf[i]) : m.predict(xf[i]);
+    }
+    return LT_OK;
+  } catch (...) {
+    return predictor_error(status);
+  }
+}
+
+}  // extern "C"

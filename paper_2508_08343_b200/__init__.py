@@ -10,4 +10,7 @@ from .batch import ConditionBatch, WorkloadBatch
 from .api import (Device, Plan, device_group, compute_metrics, condition_hash, device, encode_workload, generate_arrivals,
                   generate_dataset, ideal_throughput, load_library, run_scripted, run_simulation, sweep_conditions, sweep_optimal)
 
+from .predictor import (DatasetRow, DecisionTree, ForestModel, ForestParams, PlacementModel, PredictTarget, TreeNode,
+                        TreeParams, train_forest, train_placement_model, train_tree)
+
 __version__ = "0.1.0"

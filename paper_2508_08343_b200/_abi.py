@@ -11,7 +11,7 @@ import os
 
 import numpy as np
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # enum lt_code
 LT_OK, LT_ERR_VALIDATION, LT_ERR_CONFIG, LT_ERR_SIMULATION, LT_ERR_INTERNAL, LT_ERR_UNSUPPORTED, LT_ERR_DEVICE = range(7)
@@ -179,6 +179,20 @@ class lt_report(C.Structure):
                 ("emit_times", C.c_void_p), ("emit_capacity", C.c_int64), ("emit_offset", C.c_void_p)]
 
 
+class lt_tree_params(C.Structure):
+    _fields_ = [("max_depth", C.c_int32), ("min_leaf", C.c_int32), ("feature_subset", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class lt_forest_params(C.Structure):
+    _fields_ = [("n_trees", C.c_int32), ("bootstrap", C.c_int32), ("tree", lt_tree_params)]
+
+
+class lt_tree_node(C.Structure):
+    _fields_ = [("feature_index", C.c_int32), ("left", C.c_int32), ("right", C.c_int32), ("_pad", C.c_int32),
+                ("threshold", C.c_double), ("value", C.c_double), ("coverage", C.c_int64)]
+
+
 # numpy views with the exact C layouts (numpy honours ctypes field offsets)
 SCENARIO_DT = np.dtype(lt_scenario)
 ADAPTER_DT = np.dtype(lt_adapter)
@@ -191,6 +205,7 @@ FRONTIER_DT = np.dtype(lt_frontier_point)
 PLACEMENT_DT = np.dtype(lt_placement)
 TRACE_DT = np.dtype(lt_trace_row)
 LOAD_EVENT_DT = np.dtype(lt_load_event)
+TREE_NODE_DT = np.dtype(lt_tree_node)
 
 assert SCENARIO_DT.itemsize == 56 and ADAPTER_DT.itemsize == 24 and REQUEST_DT.itemsize == 32
 assert LENGTH_DT.itemsize == 56
@@ -226,6 +241,13 @@ SIGNATURES = {
     "simulate_report": (C.c_int32, [C.c_void_p, C.POINTER(lt_workload_batch), C.POINTER(lt_server_config),
                                     C.POINTER(lt_sim_options), C.c_void_p, C.POINTER(lt_request_states),
                                     C.POINTER(lt_report), C.POINTER(lt_status)]),
+    "train_tree": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(lt_tree_params), C.c_uint64,
+                               C.c_uint64, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(lt_status)]),
+    "train_forests": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32,
+                                  C.POINTER(lt_forest_params), C.c_uint64, C.c_void_p, C.c_int64, C.c_void_p,
+                                  C.c_void_p, C.POINTER(lt_status)]),
+    "predict_forests": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
+                                    C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(lt_status)]),
     "sweep_frontier_capacity": (C.c_int32, [C.POINTER(lt_sweep_grid)]),
     "sweep_batch": (C.c_int32, [C.c_void_p, C.POINTER(lt_condition_batch), C.POINTER(lt_server_config),
                                 C.POINTER(lt_sweep_grid), C.c_double, C.c_uint64,
@@ -251,6 +273,8 @@ SIGNATURES = {
 ORACLE_SYMBOLS = ["generate_arrivals_batch", "simulate_batch", "sweep_batch"]
 # ... and the dataset entry points (the compiled reference only)
 DATASET_SYMBOLS = ["generate_dataset", "condition_hash", "encode_workload"]
+# ... and the predictor entry points (the compiled reference only)
+PREDICTOR_SYMBOLS = ["train_tree", "train_forests", "predict_forests"]
 
 
 class Lib:

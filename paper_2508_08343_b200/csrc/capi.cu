@@ -34,6 +34,7 @@
 
 #include "k_engine.cuh"
 #include "k_metrics.cuh"
+#include "k_predict.cuh"
 #include "k_report.cuh"
 #include "k_sweep.cuh"
 #include "k_workload.cuh"
@@ -2611,3 +2612,4 @@ int32_t lt_sweep_batch(lt_ctx* ctx, const lt_condition_batch* batch, const lt_se
 
 }  // extern "C"
 #include "host_dataset.h"
+#include "host_predict.h"

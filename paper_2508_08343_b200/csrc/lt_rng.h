@@ -97,6 +97,26 @@ LT_HD void rng_stream_init(Mt64& e, uint64_t seed, uint64_t a, uint64_t b) {
   mt64_seed_seq(e, w, 6);
 }
 
+// RngStream(seed, {a, b, c}) (rng.hpp:35-46): the predictor's bootstrap
+// {kBootstrap, target, tree} and feature-subset {kFeatureSubset, tree_tag,
+// node} streams (predictor.cpp:142-143, :227-233).
+LT_HD void rng_stream_init3(Mt64& e, uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+  uint32_t w[8] = {static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32),
+                   static_cast<uint32_t>(a),    static_cast<uint32_t>(a >> 32),
+                   static_cast<uint32_t>(b),    static_cast<uint32_t>(b >> 32),
+                   static_cast<uint32_t>(c),    static_cast<uint32_t>(c >> 32)};
+  mt64_seed_seq(e, w, 8);
+}
+
+// uniform_below (rng.hpp:76-82): rejection sampling, then modulo.
+LT_HD uint64_t uniform_below(Mt64& e, uint64_t bound) {
+  if (bound <= 1) return 0;
+  const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+  uint64_t draw = mt64_next(e);
+  while (draw >= limit) draw = mt64_next(e);
+  return draw % bound;
+}
+
 // uniform01 (rng.hpp:51): 53 random bits, exact.
 LT_HD double uniform01(Mt64& e) { return static_cast<double>(mt64_next(e) >> 11) * 0x1.0p-53; }
 
