@@ -1196,7 +1196,7 @@ struct WarpEngine {
   }
 };
 
-template <bool kRep>
+template <bool kRep, bool kQuietUnroll>
 __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_warp) {
   const long long t_start = clock64();
 #ifdef LT_PHASE_PROF
@@ -1522,6 +1522,24 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         const double lat_q = sched + model * adapters;  // loads == 0
         double clk = E.clock, start = E.clock;
         int n = 0, win = 0;
+        if (kQuietUnroll && !kRep && !P.record && !P.want_digest && lat_q >= 0.0) {
+          // Four iterations per loop test: the adds are the reference's, one
+          // after the other; the clock only grows, so t_next above the clock
+          // before the block's last add covers the block's other tests.
+          // (Throughput variants only: C3 / C5 engines -3 %, the latency
+          // variant's C2 critical path +0.6 %.)
+          while (n + 4 <= n_max) {
+            const double c1 = clk + lat_q;
+            const double c2 = c1 + lat_q;
+            const double c3 = c2 + lat_q;
+            if (!(t_next > c3)) break;
+            const double c4 = c3 + lat_q;
+            win += (c1 <= E.duration) + (c2 <= E.duration) + (c3 <= E.duration) + (c4 <= E.duration);
+            start = c3;
+            clk = c4;
+            n += 4;
+          }
+        }
         while (n < n_max && t_next > clk) {
           start = clk;
           clk = clk + lat_q;
@@ -1624,7 +1642,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(EnginePara
   const int first = rank * gridDim.x + blockIdx.x;
   // (one call site: engine_run is inlined once)
   for (int k = first; k < P.n_scen;) {
-    engine_run<kRep>(P, P.order[k], slot, mine);
+    engine_run<kRep, (kThreads > 256 || kMinBlocks > 1)>(P, P.order[k], slot, mine);
     int nk = 0;
     if ((threadIdx.x & 31) == 0) nk = atomicAdd(P.counter, 1) + gridDim.x * warps;
     k = __shfl_sync(kFull, nk, 0);

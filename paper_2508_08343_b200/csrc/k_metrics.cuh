@@ -48,21 +48,34 @@ __global__ void __launch_bounds__(256) metrics_kernel(const DScen* scen, int n_s
   const double window = sc.duration;
   double rej = 0.0, ttft = 0.0, itl = 0.0;
   long long nrej = 0, nfin = 0, nttft = 0, nitl = 0;
-  for (int64_t base = 0; base < n; base += 32) {
-    const int64_t i = base + lane;
-    const bool v = i < n;
-    int8_t ph = kWaiting;
-    double first = 0.0, arr = 0.0, last = 0.0;
-    int outv = 0, gen = 0;
-    if (v) {
+  // the next block's loads are issued before this block's ordered sums (the
+  // sums are one dependent add chain; the loads would otherwise wait on it)
+  auto load = [&](int64_t i, int8_t& ph, double& first, double& arr, double& last, int& outv, int& gen) {
+    ph = kWaiting;
+    first = arr = last = 0.0;
+    outv = gen = 0;
+    if (i < n) {
       ph = r_phase[rb + i];
       first = r_first[rb + i];
       arr = r_arr[rb + i];
       last = r_last[rb + i];
       outv = r_out[rb + i];
-      gen = (ph == kFinished) ? outv : r_gen[rb + i];
-      if (ph == kFinished) r_gen[rb + i] = outv;
+      gen = r_gen[rb + i];
     }
+  };
+  int8_t nph;
+  double nfirst, narr, nlast;
+  int nout, ngen;
+  load(lane, nph, nfirst, narr, nlast, nout, ngen);
+  for (int64_t base = 0; base < n; base += 32) {
+    const int64_t i = base + lane;
+    const bool v = i < n;
+    const int8_t ph = nph;
+    const double first = nfirst, arr = narr, last = nlast;
+    const int outv = nout;
+    const int gen = (ph == kFinished) ? outv : ngen;
+    if (v && ph == kFinished) r_gen[rb + i] = outv;
+    load(i + 32, nph, nfirst, narr, nlast, nout, ngen);
     const bool is_rej = v && ph == kRejected;
     const bool has_first = v && first == first;
     const bool has_itl = v && gen >= 2;

@@ -157,6 +157,7 @@ __global__ void split_keys_kernel(const DNode* nodes, int n_nodes, const DNodeOu
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (r >= rows) return;
   const int a = node_of_row(nodes, n_nodes, r);
+  if (out[a].leaf) return;  // not in any sort segment: its ord rows are stale after a swap
   const DNode nd = nodes[a];
   const int f = out[a].cand[k];
   const int32_t row = src[static_cast<int64_t>(nd.job) * n + ord[r]];
