@@ -31,50 +31,71 @@ constexpr int kSeedThreads = 90;  // 90 rows x 625 words = 225 KB: three warps' 
 constexpr int kSeedStride = 625;
 constexpr size_t kSeedSmem = sizeof(uint32_t) * kSeedThreads * kSeedStride;
 
-__device__ __forceinline__ void seed_seq_row(uint32_t* b, const uint32_t* v) {
-  constexpr int n = 624, p = 306, q = 317, s = 6;
-  for (int k = 0; k < n; ++k) b[k] = 0x8b8b8b8bu;
-  // Each step k reads b[k], b[k+p], b[k+q], b[k-1] and writes b[k+p],
-  // b[k+q], b[k] (indices mod n). Step k writes none of b[k+1], b[k+1+p],
-  // b[k+1+q] (q - p = 11), so the next step's three operands are loaded one
-  // step ahead and the updates need no read-modify-write.
-  uint32_t prev = b[n - 1];
+// Steps [k0, k1) of one std::seed_seq::generate pass over the row, in a
+// range where none of the touched indices wraps: the offsets of b[k+p],
+// b[k+q] and of the next step's operands b[k+1], b[k+1+p], b[k+1+q] are
+// compile-time constants (OP, OQ, O1, O1P, O1Q: the index minus k, already
+// reduced mod n), so every access is one shared-memory op at an immediate
+// offset and a step is the dependent chain plus three loads and three
+// stores. Step k writes none of b[k+1], b[k+1+p], b[k+1+q] (q - p = 11), so
+// the next step's operands are loaded one step ahead and the updates are
+// plain stores. kFirst: the first loop (k < m = n); else the second
+// (k + m, indices repeat modulo n). kV: steps 0..s, whose add term reads v.
+template <bool kFirst, bool kV, int OP, int OQ, int O1, int O1P, int O1Q>
+__device__ __forceinline__ void seed_seq_steps(uint32_t* b, int k0, int k1, uint32_t& x0, uint32_t& x1,
+                                               uint32_t& x2, uint32_t& prev, const uint32_t* v) {
+  constexpr int s = 6;
+#pragma unroll 4
+  for (int k = k0; k < k1; ++k) {
+    uint32_t* bk = b + k;
+    uint32_t r, w1, w2;
+    if (kFirst) {
+      const uint32_t r1 = 1664525u * seedseq_T(x0 ^ x1 ^ prev);
+      uint32_t add = static_cast<uint32_t>(k);
+      if (kV) add = (k == 0) ? static_cast<uint32_t>(s) : static_cast<uint32_t>(k) + v[k - 1];
+      r = r1 + add;
+      w1 = x1 + r1;
+      w2 = x2 + r;
+    } else {
+      const uint32_t r3 = 1566083941u * seedseq_T(x0 + x1 + prev);
+      r = r3 - static_cast<uint32_t>(k);
+      w1 = x1 ^ r3;
+      w2 = x2 ^ r;
+    }
+    x0 = bk[O1];
+    x1 = bk[O1P];
+    x2 = bk[O1Q];
+    bk[OP] = w1;
+    bk[OQ] = w2;
+    bk[0] = r;
+    prev = r;
+  }
+}
+
+template <bool kFirst>
+__device__ __forceinline__ void seed_seq_pass(uint32_t* b, uint32_t& prev, const uint32_t* v) {
+  constexpr int n = 624, p = 306, q = 317;
   uint32_t x0 = b[0], x1 = b[p], x2 = b[q];
-  for (int k = 0; k < n; ++k) {    // m = max(s + 1, n) = n
-    const int kp = (k + p < n) ? k + p : k + p - n;
-    const int kq = (k + q < n) ? k + q : k + q - n;
-    const uint32_t r1 = 1664525u * seedseq_T(x0 ^ x1 ^ prev);
-    const uint32_t add = (k == 0) ? static_cast<uint32_t>(s) : (k <= s ? static_cast<uint32_t>(k) + v[k - 1]
-                                                                          : static_cast<uint32_t>(k));
-    const uint32_t r2 = r1 + add;
-    const uint32_t w1 = x1 + r1, w2 = x2 + r2;
-    const int k1 = k + 1 < n ? k + 1 : 0;
-    x0 = b[k1];
-    x1 = b[(k1 + p < n) ? k1 + p : k1 + p - n];
-    x2 = b[(k1 + q < n) ? k1 + q : k1 + q - n];
-    b[kp] = w1;
-    b[kq] = w2;
-    b[k] = r2;
-    prev = r2;
+  // wrap points: k+1+q at k = 306, k+q at 307, k+1+p at 317, k+p at 318, k+1 at 623
+  if (kFirst) {
+    seed_seq_steps<true, true, p, q, 1, 1 + p, 1 + q>(b, 0, 7, x0, x1, x2, prev, v);  // 0 <= k <= s
+    seed_seq_steps<true, false, p, q, 1, 1 + p, 1 + q>(b, 7, 306, x0, x1, x2, prev, v);
+  } else {
+    seed_seq_steps<false, false, p, q, 1, 1 + p, 1 + q>(b, 0, 306, x0, x1, x2, prev, v);
   }
-  x0 = b[0];
-  x1 = b[p];
-  x2 = b[q];
-  for (int k = 0; k < n; ++k) {  // k + m, m = n: indices repeat modulo n
-    const int kp = (k + p < n) ? k + p : k + p - n;
-    const int kq = (k + q < n) ? k + q : k + q - n;
-    const uint32_t r3 = 1566083941u * seedseq_T(x0 + x1 + prev);
-    const uint32_t r4 = r3 - static_cast<uint32_t>(k);
-    const uint32_t w1 = x1 ^ r3, w2 = x2 ^ r4;
-    const int k1 = k + 1 < n ? k + 1 : 0;
-    x0 = b[k1];
-    x1 = b[(k1 + p < n) ? k1 + p : k1 + p - n];
-    x2 = b[(k1 + q < n) ? k1 + q : k1 + q - n];
-    b[kp] = w1;
-    b[kq] = w2;
-    b[k] = r4;
-    prev = r4;
-  }
+  seed_seq_steps<kFirst, false, p, q, 1, 1 + p, 1 + q - n>(b, 306, 307, x0, x1, x2, prev, v);
+  seed_seq_steps<kFirst, false, p, q - n, 1, 1 + p, 1 + q - n>(b, 307, 317, x0, x1, x2, prev, v);
+  seed_seq_steps<kFirst, false, p, q - n, 1, 1 + p - n, 1 + q - n>(b, 317, 318, x0, x1, x2, prev, v);
+  seed_seq_steps<kFirst, false, p - n, q - n, 1, 1 + p - n, 1 + q - n>(b, 318, 623, x0, x1, x2, prev, v);
+  seed_seq_steps<kFirst, false, p - n, q - n, 1 - n, 1 + p - n, 1 + q - n>(b, 623, 624, x0, x1, x2, prev, v);
+}
+
+__device__ __forceinline__ void seed_seq_row(uint32_t* b, const uint32_t* v) {
+  constexpr int n = 624;
+  for (int k = 0; k < n; ++k) b[k] = 0x8b8b8b8bu;
+  uint32_t prev = b[n - 1];
+  seed_seq_pass<true>(b, prev, v);   // m = max(s + 1, n) = n
+  seed_seq_pass<false>(b, prev, v);  // k + m, m = n: indices repeat modulo n
   // [rand.eng.mers] seed(q): an all-zero state (top w-r bits of x[0]) -> 2^(w-1)
   if ((b[1] == 0u) && ((b[0] & 0x80000000u) == 0u)) {
     bool zero = true;
