@@ -473,6 +473,7 @@ struct lt_plan {
   size_t smem = 0;
   int32_t run_cap = 0, smem_per_warp = 0;
   int engine_variant = 1;  // engine_kernel<1> (latency) or <2> (occupancy)
+  int pair_g = 32;         // lanes per (scenario, adapter) pair in count / expand (pair_group)
   int want_digest = 0;
   double tables_ms = 0, h2d_ms = 0;
   int64_t h2d_bytes = 0;
@@ -845,6 +846,47 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+void launch_count(const lt_plan& P, cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>((P.n_pairs * P.pair_g + 255) / 256);
+  if (P.pair_g == 4)
+    count_kernel<4><<<grid, 256, 0, st>>>(P.scen.p, P.pair_scen.p, P.pair_adp.p, P.n_pairs, P.adapters.p, P.keys.p,
+                                          P.E.p, P.adp_count.p, P.scen_count.p, P.overflow.p);
+  else
+    count_kernel<32><<<grid, 256, 0, st>>>(P.scen.p, P.pair_scen.p, P.pair_adp.p, P.n_pairs, P.adapters.p, P.keys.p,
+                                           P.E.p, P.adp_count.p, P.scen_count.p, P.overflow.p);
+  after_launch("count_kernel", st);
+}
+
+void launch_expand(const lt_plan& P, cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>((P.n_pairs * P.pair_g + 255) / 256);
+  if (P.pair_g == 4)
+    expand_kernel<4><<<grid, 256, 0, st>>>(P.scen.p, P.pair_scen.p, P.pair_adp.p, P.n_pairs, P.pair_begin.p,
+                                           P.adapters.p, P.keys.p, P.E.p, P.adp_count.p, P.pair_excl.p, P.st_in.p,
+                                           P.sv_in.p);
+  else
+    expand_kernel<32><<<grid, 256, 0, st>>>(P.scen.p, P.pair_scen.p, P.pair_adp.p, P.n_pairs, P.pair_begin.p,
+                                            P.adapters.p, P.keys.p, P.E.p, P.adp_count.p, P.pair_excl.p, P.st_in.p,
+                                            P.sv_in.p);
+  after_launch("expand_kernel", st);
+}
+
+// Mean expected arrivals per (scenario, adapter) pair of a batch, from up to
+// 4,096 evenly spaced scenarios (it only picks count / expand's lanes per pair).
+double mean_pair_draws(const lt_workload_batch* b) {
+  const int64_t n = b->n_scenarios;
+  const int64_t step = std::max<int64_t>(1, n / 4096);
+  double draws = 0.0;
+  int64_t pairs = 0;
+  for (int64_t i = 0; i < n; i += step) {
+    const lt_scenario& s = b->scenarios[i];
+    if (s.n_requests >= 0) continue;
+    for (int32_t k = 0; k < s.n_adapters; ++k)
+      draws += std::max(b->adapters[s.adapter_offset + k].rate, 0.0) * std::max(s.duration_s, 0.0);
+    pairs += s.n_adapters;
+  }
+  return pairs ? draws / static_cast<double>(pairs) : 1e9;
+}
+
 // Arrival merge: one CUB segmented stable sort per scenario, or two global
 // radix sorts for very large batches (measured: equal or slightly slower at
 // C2's 3.6 M and C5's 9 M requests, 4 % faster at C3's 5e8-request chunks).
@@ -855,7 +897,17 @@ bool radix_merge(int64_t n_requests) {
 }
 
 // Keys seeded and drawn per chunk (the seeded states take 5 KB per key).
-constexpr int64_t kSeedChunk = 1 << 18;
+constexpr int64_t kSeedChunk = 1 << 18;  // keys per seed_kernel + tables_draw_kernel pair (upper bound)
+// Keys per launch pair: the 2.5 KB MT states a seed_kernel launch writes are
+// read back by the draw kernel right after, so a launch's states should fit
+// in L2 instead of going to HBM and back. LT_SEED_CHUNK overrides.
+int64_t seed_chunk() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("LT_SEED_CHUNK");
+    return e ? std::max<int64_t>(1, std::min<int64_t>(std::atoll(e), kSeedChunk)) : kSeedChunk;
+  }();
+  return v;
+}
 
 int launch_decks(lt_plan& P, cudaStream_t st);
 
@@ -867,8 +919,9 @@ int launch_tables(lt_plan& P, int nk, cudaStream_t st) {
   LT_CUDA(cudaFuncSetAttribute(seed_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared));
   int launches = 0;
-  for (int64_t k0 = 0; k0 < nk; k0 += kSeedChunk) {
-    const int n = static_cast<int>(std::min<int64_t>(kSeedChunk, nk - k0));
+  const int64_t chunk = seed_chunk();
+  for (int64_t k0 = 0; k0 < nk; k0 += chunk) {
+    const int n = static_cast<int>(std::min<int64_t>(chunk, nk - k0));
     seed_kernel<<<(2 * n + kSeedThreads - 1) / kSeedThreads, kSeedThreads, kSeedSmem, st>>>(
         P.keys.p, static_cast<int>(k0), n, P.seed_state.p);
     after_launch("seed_kernel", st);
@@ -1377,10 +1430,8 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     P.adp_count.alloc(n_pairs);
     LT_CUDA(cudaMemsetAsync(P.scen_count.p, 0, P.n_scen * sizeof(unsigned long long), st));
     LT_CUDA(cudaMemsetAsync(P.overflow.p, 0, sizeof(int32_t), st));
-    count_kernel<<<static_cast<unsigned>((n_pairs + 7) / 8), 256, 0, st>>>(
-        P.scen.p, P.pair_scen.p, P.pair_adp.p, n_pairs, P.adapters.p, P.keys.p, P.E.p, P.adp_count.p,
-        P.scen_count.p, P.overflow.p);
-    after_launch("count_kernel", st);
+    P.pair_g = pair_group(mean_pair_draws(b));
+    launch_count(P, st);
     ++P.launches_prep;
     std::vector<unsigned long long> counts(P.n_scen);
     int32_t ovf = 0;
@@ -1516,10 +1567,7 @@ void prepare_requests(lt_plan& P) {
     LT_CUDA(cudaMemcpyAsync(P.scen_count.p, P.base_count.p, P.n_scen * sizeof(unsigned long long),
                             cudaMemcpyDeviceToDevice, st));
     if (P.n_pairs > 0) {
-      count_kernel<<<static_cast<unsigned>((P.n_pairs + 7) / 8), 256, 0, st>>>(
-          P.scen.p, P.pair_scen.p, P.pair_adp.p, P.n_pairs, P.adapters.p, P.keys.p, P.E.p, P.adp_count.p,
-          P.scen_count.p, P.overflow.p);
-      after_launch("count_kernel", st);
+      launch_count(P, st);
       ++launches;
     }
     size_t tb = P.scan_tmp_bytes;
@@ -1548,10 +1596,7 @@ int64_t merge_requests(lt_plan& P) {
     size_t tb = P.pscan_tmp_bytes;
     LT_CUDA(cub::DeviceScan::ExclusiveSum(P.pscan_tmp.p, tb, P.adp_count.p, P.pair_excl.p,
                                           static_cast<int>(P.n_pairs), st));
-    expand_kernel<<<static_cast<unsigned>((P.n_pairs + 7) / 8), 256, 0, st>>>(
-        P.scen.p, P.pair_scen.p, P.pair_adp.p, P.n_pairs, P.pair_begin.p, P.adapters.p, P.keys.p, P.E.p,
-        P.adp_count.p, P.pair_excl.p, P.st_in.p, P.sv_in.p);
-    after_launch("expand_kernel", st);
+    launch_expand(P, st);
     size_t sb = P.sort_tmp_bytes;
     const int nr = static_cast<int>(std::max<int64_t>(P.total_req, 1));
     const unsigned gr = static_cast<unsigned>((nr + 255) / 256);

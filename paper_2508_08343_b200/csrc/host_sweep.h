@@ -399,10 +399,8 @@ void sweep_waves_device(lt_ctx* ctx, const SweepSetup& S, const lt_server_config
       after_launch("wave_pairs_kernel", st);
       LT_CUDA(cudaMemsetAsync(W.scen_count.p, 0, W.n_scen * sizeof(unsigned long long), st));
       LT_CUDA(cudaMemsetAsync(W.overflow.p, 0, sizeof(int32_t), st));
-      count_kernel<<<static_cast<unsigned>((W.n_pairs + 7) / 8), 256, 0, st>>>(
-          W.scen.p, W.pair_scen.p, W.pair_adp.p, W.n_pairs, W.adapters.p, W.keys.p, W.E.p, W.adp_count.p,
-          W.scen_count.p, W.overflow.p);
-      after_launch("count_kernel", st);
+      W.pair_g = pair_group(W.n_pairs ? est / static_cast<double>(W.n_pairs) : 1e9);
+      launch_count(W, st);
       tm.launches += 2;
       std::vector<unsigned long long> counts(W.n_scen);
       int32_t ovf = 0;

@@ -125,11 +125,15 @@ __global__ void __launch_bounds__(kSeedThreads) seed_kernel(const DKey* keys, in
     seed_seq_row(sb + tid * kSeedStride, v);
   }
   __syncthreads();
+  // copy-out row by row, the block's threads over a row's words
+  // (conflict-free reads, coalesced writes, no per-word index division)
   const int ns = min(kSeedThreads, n_streams - base);
   uint32_t* dst = reinterpret_cast<uint32_t*>(state) + static_cast<size_t>(base) * 2 * kMtN;
-  for (int idx = tid; idx < ns * 2 * kMtN; idx += kSeedThreads) {
-    const int sidx = idx / (2 * kMtN);
-    dst[idx] = sb[sidx * kSeedStride + (idx - sidx * 2 * kMtN)];
+  for (int r = 0; r < ns; ++r) {
+    const uint32_t* src = sb + r * kSeedStride;
+    uint32_t* out = dst + static_cast<size_t>(r) * 2 * kMtN;
+#pragma unroll
+    for (int j = tid; j < 2 * kMtN; j += kSeedThreads) out[j] = src[j];
   }
 }
 
@@ -366,18 +370,22 @@ __global__ void __launch_bounds__(32) deck_kernel(const DKey* keys, const DDeck*
   }
 }
 
-// Arrivals of one (scenario, adapter): count t < duration (workload.cpp:179-183).
-// One warp per pair: the table loads and divisions E_j / rate of 32 draws run
-// in parallel; the running sum t is the reference's sequential chain, one add
-// per draw in draw order, broadcast by shuffles.
+// Arrivals of every (scenario, adapter) pair: the reference's t += E/rate
+// loop (workload.cpp:179-183) with G lanes per pair: G table loads and
+// divisions in parallel, the sum one add per draw in draw order, fed by
+// shuffles. G = 32 for pairs with many draws (one pair per warp), G = 4 for
+// sparse ones (eight pairs per warp: their dependent metadata loads overlap).
+template <int G>
 __global__ void __launch_bounds__(256) count_kernel(const DScen* scen, const int32_t* pair_scen,
                                                     const int32_t* pair_adp, int64_t n_pairs,
                                                     const DAdapter* adapters, const DKey* keys, const double* E,
                                                     int32_t* adp_count, unsigned long long* scen_count,
                                                     int32_t* overflow) {
   const int lane = threadIdx.x & 31;
-  const int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-  if (p >= n_pairs) return;
+  const int g = lane % G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - g));
+  const int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / G;
+  if (p >= n_pairs) return;  // whole groups leave together
   const int si = pair_scen[p];
   const double duration = scen[si].duration;
   const DAdapter ad = adapters[scen[si].adapter_begin + pair_adp[p]];
@@ -386,32 +394,35 @@ __global__ void __launch_bounds__(256) count_kernel(const DScen* scen, const int
   const int len = key.e_len;
   double t = 0.0;
   int count = -1;
-  for (int j0 = 0; count < 0; j0 += 32) {
+  for (int j0 = 0; count < 0; j0 += G) {
     if (j0 >= len) {  // table exhausted before the window closed
-      if (lane == 0) atomicExch(overflow, 1);
+      if (g == 0) atomicExch(overflow, 1);
       count = len;
       break;
     }
-    const int j = j0 + lane;
+    const int j = j0 + g;
     const double q = (j < len) ? Ek[j] / ad.rate : 0.0;
-    int hit = 32;
+    int hit = G;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      t = t + __shfl_sync(0xffffffffu, q, k);
-      if (hit == 32 && t >= duration) hit = k;
+    for (int k = 0; k < G; ++k) {
+      t = t + __shfl_sync(gmask, q, k, G);
+      if (hit == G && t >= duration) hit = k;
     }
-    if (hit < 32) {
+    if (hit < G) {
       count = j0 + hit;
-    } else if (j0 + 32 > len) {
-      if (lane == 0) atomicExch(overflow, 1);
+    } else if (j0 + G > len) {
+      if (g == 0) atomicExch(overflow, 1);
       count = len;
     }
   }
-  if (lane == 0) {
+  if (g == 0) {
     adp_count[p] = count;
     atomicAdd(&scen_count[si], static_cast<unsigned long long>(count));
   }
 }
+
+// Lanes per pair for a batch: sparse pairs (few expected draws) share warps.
+inline int pair_group(double mean_draws) { return mean_draws < 24.0 ? 4 : 32; }
 
 // Request offsets of every scenario from the device exclusive scan.
 __global__ void set_offsets_kernel(DScen* scen, int n_scen, const unsigned long long* count,
@@ -426,7 +437,8 @@ __global__ void set_offsets_kernel(DScen* scen, int n_scen, const unsigned long 
 // slot of the scenario segment; a stable segmented sort by time then realises
 // the reference's stable_sort by (time, adapter_id, sequence)
 // (workload.cpp:204-207): pairs are laid out in adapter-id order. One warp
-// per pair, the same sequential sum as count_kernel.
+// group of G lanes per pair, the same sequential sum as count_kernel.
+template <int G>
 __global__ void __launch_bounds__(256) expand_kernel(const DScen* scen, const int32_t* pair_scen,
                                                      const int32_t* pair_adp, int64_t n_pairs,
                                                      const int64_t* pair_begin, const DAdapter* adapters,
@@ -434,7 +446,9 @@ __global__ void __launch_bounds__(256) expand_kernel(const DScen* scen, const in
                                                      const unsigned long long* pair_excl, double* t_out,
                                                      unsigned long long* v_out) {
   const int lane = threadIdx.x & 31;
-  const int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int g = lane % G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - g));
+  const int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / G;
   if (p >= n_pairs) return;
   const int si = pair_scen[p];
   const DScen& s = scen[si];
@@ -444,14 +458,14 @@ __global__ void __launch_bounds__(256) expand_kernel(const DScen* scen, const in
   const int64_t off = s.req_begin + static_cast<int64_t>(pair_excl[p] - pair_excl[pair_begin[si]]);
   const int n = adp_count[p];
   double t = 0.0;
-  for (int j0 = 0; j0 < n; j0 += 32) {
-    const int j = j0 + lane;
+  for (int j0 = 0; j0 < n; j0 += G) {
+    const int j = j0 + g;
     const double q = (j < n) ? Ek[j] / ad.rate : 0.0;
     double mine = 0.0;
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      t = t + __shfl_sync(0xffffffffu, q, u);
-      if (u == lane) mine = t;
+    for (int u = 0; u < G; ++u) {
+      t = t + __shfl_sync(gmask, q, u, G);
+      if (u == g) mine = t;
     }
     if (j < n) {
       t_out[off + j] = mine;
