@@ -7,6 +7,9 @@ simulated engine-iterations/sec + placement sweeps/sec) on B200.
 
 Workloads (synthetic, built by the reference's own generator on
 device):
+  c1 (BASELINE configs[0]) one Digital Twin run: 8 adapters rank 16 at 0.2 req/s,
+     Mean(250,50,231,50), 3600 s, G = 8, seed 1, llama31_8b -- one engine, so
+     its time is one warp's latency (reported, not a throughput case).
   c2 (default, BASELINE configs[1]) 1,024 scenarios: N in {8..256 step 8} x
      rank {8,16,32,mixed} x r {3.2..0.0125}; per-adapter rate 8r/N;
      Mean(250,80,231,80); 600 s; G = min(N,32); seed 1234+i; h100_like.
@@ -60,6 +63,8 @@ SM_COUNT = 148
 PLAN_SCENARIOS = 65_536  # scenarios per device-resident plan (c3/c5)
 
 WORKLOADS = {
+    "c1": "C1: single Digital Twin run, llama31_8b profile, 8 LoRA adapters rank 16, 0.2 req/s each (Poisson), "
+          "Mean(250,50,231,50), 3600 s simulated, G=8, seed 1 (BASELINE configs[0], latency of one engine)",
     "c2": "C2: 1,024-scenario grid, N=8..256 step 8 x rank {8,16,32,mixed} x r {3.2..0.0125}, per-adapter rate "
           "8r/N, Mean(250,80,231,80), 600 s simulated, G=min(N,32), seed 1234+i, h100_like",
     "c3": "C3: 65,536 scenarios = first 2,048 enumerate_conditions(paper rates x ranks {8,16,32}, triple 3) x "
@@ -181,6 +186,12 @@ def sim_parts(workload: str, rank: int = 0):
     from paper_2508_08343_b200.types import profile_config
     from tests import workloads as W
 
+    if workload == "c1":
+        from paper_2508_08343_b200.batch import WorkloadBatch
+        from paper_2508_08343_b200.types import profile_config
+        wl = lt.WorkloadSpec(adapters=[lt.AdapterSpec(i, 16, 0.2) for i in range(1, 9)],
+                             lengths=lt.LengthSpec.mean(250, 50, 231, 50), duration_s=3600.0, seed=1 + 1024 * rank)
+        return [("c1", WorkloadBatch.from_workloads([wl], slots=[8]), profile_config("llama31_8b", 8))]
     if workload == "c2":
         b = W.c2_batch(600.0)
         b.scenarios["seed"] = b.scenarios["seed"] + np.uint64(1024 * rank)
@@ -199,6 +210,8 @@ def reference_sample(workload: str):
     import paper_2508_08343_b200.distributed as D
     from tests import workloads as W
 
+    if workload == "c1":
+        return sim_parts("c1"), "the C1 run itself (1 scenario, one reference thread)"
     if workload == "c2":
         return sim_parts("c2"), "the whole C2 grid (1,024 scenarios)"
     if workload == "c3":
@@ -230,7 +243,7 @@ def shard(workload: str, parts, rank: int, world: int):
     every part (strong; the same deterministic split on every rank)."""
     import paper_2508_08343_b200.distributed as D
 
-    if world == 1 or workload == "c2":
+    if world == 1 or workload in ("c1", "c2"):
         return parts
     out = []
     for lab, b, cfg in parts:
@@ -309,10 +322,10 @@ def impl_reference(args):
     _, desc = reference_sample(args.workload)
     line = {"metric": METRIC, "value": v, "unit": cb["unit"], "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * statistics.mean(walls),
-            "higher_is_better": True, "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "weak" if args.workload in ("c1", "c2") else "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.workload], "sample": desc,
-                       "same_config": args.workload == "c2",
+                       "same_config": args.workload in ("c1", "c2"),
                        "step": "one step = the reference sample, on all host cores (rank 0 only)"},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": cb["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -440,7 +453,7 @@ def impl_gpu(args):
     for lab, b, cfg in parts:
         for c in chunks(b):
             p = dev.plan(c, cfg)
-            if args.workload != "c2":
+            if args.workload not in ("c1", "c2"):
                 p.trim()
             plans.append(p)
     n_scen = sum(p.n for p in plans)
@@ -539,12 +552,12 @@ def impl_gpu(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak" if args.workload in ("c1", "c2") else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload], "scenarios_per_gpu": n_scen,
                    "engine_iterations_per_step": iters_all, "failed_scenarios": bad, "plans_per_step": len(plans),
                    "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": (f"scenario replicas x{world}" if args.workload == "c2"
+                   "parallelism": (f"scenario replicas x{world}" if args.workload in ("c1", "c2")
                                    else f"cost-balanced scenario shards over {world} GPU(s)")
                    + (", NCCL all-gather of the per-scenario records inside the step" if world > 1 else "")},
         "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "parity": parity,
@@ -570,8 +583,8 @@ def e2e_simulate(args, dev, parts, dist, local, iters_all, world):
     pinned = [(pinned_copy(b), cfg) for _, b, cfg in parts]
     walls, plan_ms, wait_ms = [], [], []
     h2d = d2h = 0
-    n_warm = max(1, args.warmup) if args.workload == "c2" else 1
-    n_steps = max(1, args.e2e_steps) if args.workload == "c2" else 1
+    n_warm = max(1, args.warmup) if args.workload in ("c1", "c2") else 1
+    n_steps = max(1, args.e2e_steps) if args.workload in ("c1", "c2") else 1
     iters = 0
     for i in range(n_steps + n_warm):
         torch.cuda.synchronize()
