@@ -55,9 +55,10 @@ void grow_trees(lt_ctx* ctx, const double* x, int32_t n, const double* y, int32_
   const int64_t total = static_cast<int64_t>(J) * n;
   DBuf<double> d_x, d_y;
   DBuf<DTreeJob> d_jobs;
-  DBuf<int32_t> src, perm, ord, ord2, tmp, seg_begin, seg_end;
-  DBuf<uint64_t> keys, keys2;
-  DBuf<double> psum, psumsq;
+  DBuf<int32_t> src, perm, ord, tmp, seg_end;
+  DBuf<uint64_t> keys, keys2, np1, np2;
+  DBuf<uint32_t> nkey, nkey2;
+  DBuf<double> psum, psumsq, xbuf;
   DBuf<DNode> d_nodes;
   DBuf<DNodeOut> d_out;
   DBuf<char> sort_tmp;
@@ -68,13 +69,17 @@ void grow_trees(lt_ctx* ctx, const double* x, int32_t n, const double* y, int32_
   src.alloc(std::max<int64_t>(total, 1));
   perm.alloc(std::max<int64_t>(total, 1));
   ord.alloc(std::max<int64_t>(total, 1));
-  ord2.alloc(std::max<int64_t>(total, 1));
   tmp.alloc(std::max<int64_t>(total, 1));
   keys.alloc(std::max<int64_t>(total, 1));
   keys2.alloc(std::max<int64_t>(total, 1));
+  np1.alloc(std::max<int64_t>(total, 1));
+  np2.alloc(std::max<int64_t>(total, 1));
+  nkey.alloc(std::max<int64_t>(total, 1));
+  nkey2.alloc(std::max<int64_t>(total, 1));
+  xbuf.alloc(std::max<int64_t>(total, 1));
   psum.alloc(std::max<int64_t>(2 * total, 1));  // a step's rows + one entry per node (<= rows)
   psumsq.alloc(std::max<int64_t>(2 * total, 1));
-  tree_rows_kernel<<<(J + 63) / 64, 64, 0, st>>>(d_jobs.p, J, n, seed, src.p, perm.p);
+  tree_rows_kernel<<<(J + 3) / 4, 128, 0, st>>>(d_jobs.p, J, n, seed, src.p, perm.p);
   after_launch("tree_rows_kernel", st);
   int64_t launches = 1;
   const bool dfs = prm.feature_subset < kNumFeatures;
@@ -113,30 +118,31 @@ void grow_trees(lt_ctx* ctx, const double* x, int32_t n, const double* y, int32_
     const int A = static_cast<int>(act.size());
     d_nodes.upload(act, st);
     d_out.alloc(A);
-    std::vector<int32_t> sb(A);
-    for (int a = 0; a < A; ++a) sb[a] = act[a].off;
-    seg_begin.upload(sb, st);
     seg_end.alloc(A);
-    node_begin_kernel<<<(A + 63) / 64, 64, 0, st>>>(d_nodes.p, A, d_jobs.p, n, d_y.p, src.p, perm.p, prm.max_depth,
-                                                    prm.min_leaf, prm.feature_subset, seed, ord.p, seg_end.p, d_out.p);
+    node_begin_kernel<<<(A + 7) / 8, 256, 0, st>>>(d_nodes.p, A, d_jobs.p, n, d_y.p, src.p, perm.p, prm.max_depth,
+                                                   prm.min_leaf, prm.feature_subset, seed, ord.p, seg_end.p, d_out.p);
     after_launch("node_begin_kernel", st);
     ++launches;
-    size_t need = 0;
-    LT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, need, keys.p, keys2.p, ord.p, ord2.p,
-                                                      static_cast<int>(rows), A, seg_begin.p, seg_end.p, st));
-    sort_tmp.alloc(std::max<size_t>(need, 1));
+    int node_bits = 1;
+    while ((1 << node_bits) < A) ++node_bits;
+    const int R = static_cast<int>(rows);
+    size_t need1 = 0, need2 = 0;
+    LT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need1, keys.p, keys2.p, np1.p, np2.p, R, 0, 64, st));
+    LT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need2, nkey.p, nkey2.p, tmp.p, ord.p, R, 0, node_bits, st));
+    sort_tmp.alloc(std::max<size_t>(std::max(need1, need2), 1));
+    const unsigned rg = static_cast<unsigned>((rows + 255) / 256);
     for (int k = 0; k < m; ++k) {
-      split_keys_kernel<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, st>>>(
-          d_nodes.p, A, d_out.p, k, n, d_x.p, src.p, ord.p, rows, keys.p);
+      split_keys_kernel<<<rg, 256, 0, st>>>(d_nodes.p, A, d_out.p, k, n, d_x.p, src.p, ord.p, rows, keys.p, np1.p);
       after_launch("split_keys_kernel", st);
-      size_t b = need;
-      LT_CUDA(cub::DeviceSegmentedSort::StableSortPairs(sort_tmp.p, b, keys.p, keys2.p, ord.p, ord2.p,
-                                                        static_cast<int>(rows), A, seg_begin.p, seg_end.p, st));
-      std::swap(ord.p, ord2.p);
+      size_t b1 = need1, b2 = need2;
+      LT_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp.p, b1, keys.p, keys2.p, np1.p, np2.p, R, 0, 64, st));
+      node_keys_kernel<<<rg, 256, 0, st>>>(np2.p, rows, nkey.p, tmp.p);
+      after_launch("node_keys_kernel", st);
+      LT_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp.p, b2, nkey.p, nkey2.p, tmp.p, ord.p, R, 0, node_bits, st));
       split_eval_kernel<<<(A + 7) / 8, 256, 0, st>>>(d_nodes.p, A, d_out.p, k, n, prm.min_leaf, d_x.p, d_y.p,
-                                                     d_jobs.p, src.p, ord.p, psum.p, psumsq.p);
+                                                     d_jobs.p, src.p, ord.p, xbuf.p, psum.p, psumsq.p);
       after_launch("split_eval_kernel", st);
-      launches += 3;
+      launches += 5;
     }
     node_finish_kernel<<<(A + 7) / 8, 256, 0, st>>>(d_nodes.p, A, d_out.p, n, d_x.p, src.p, perm.p, tmp.p);
     after_launch("node_finish_kernel", st);

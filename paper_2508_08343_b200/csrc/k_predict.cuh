@@ -10,9 +10,10 @@
 //                      targets in its row order (grow, predictor.cpp:97-103),
 //                      the leaf test, the candidate features (all, or the
 //                      {kFeatureSubset, tree_tag, node} shuffle, :138-147);
-//   per candidate k:   split_keys_kernel + a stable segmented sort: the
-//                      node's order re-sorted stably by feature f_k, exactly
-//                      the reference's chain of std::stable_sort calls on one
+//   per candidate k:   split_keys_kernel + two stable radix sorts (by the
+//                      feature, then by the node): each node's order
+//                      re-sorted stably by feature f_k, exactly the
+//                      reference's chain of std::stable_sort calls on one
 //                      `order` vector (:156-159) -- ties keep the previous
 //                      feature's order, then row order;
 //                      split_eval_kernel: the sequential prefix sums (:160-
@@ -26,6 +27,7 @@
 
 #include <cstdint>
 
+#include "k_workload.cuh"  // mt64_twist_block, mt64_temper
 #include "lt_rng.h"
 
 namespace lt {
@@ -69,41 +71,88 @@ __device__ __forceinline__ uint64_t orderable(double x) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
 }
 
-// Bootstrap draws (or the identity) and the root order of every job. One
-// thread per job: the resample is one sequential stream (:227-233).
-__global__ void tree_rows_kernel(const DTreeJob* jobs, int n_jobs, int32_t n, uint64_t seed, int32_t* src,
-                                 int32_t* perm) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+// Bootstrap draws (or the identity) and the root order of every job
+// (train_forest, :227-233): j = uniform_below(n) per row from the tree's
+// {kBootstrap, target, tree} stream. One warp per job: lane 0 seeds the
+// stream, the warp twists 312 state words at a time and every lane tempers
+// and reduces its own words. uniform_below rejects draws >= 2^64 - 2^64 mod n
+// (a shift of every later draw); a block holding one (probability ~n / 2^64)
+// sends the job to lane 0's sequential replay of the reference's loop.
+__global__ void __launch_bounds__(128) tree_rows_kernel(const DTreeJob* jobs, int n_jobs, int32_t n, uint64_t seed,
+                                                        int32_t* src, int32_t* perm) {
+  __shared__ uint64_t st_all[4][kMtN];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 4 + warp;
   if (j >= n_jobs) return;
-  int32_t* s = src + static_cast<int64_t>(j) * n;
+  int32_t* sj = src + static_cast<int64_t>(j) * n;
   int32_t* p = perm + static_cast<int64_t>(j) * n;
-  if (jobs[j].bootstrap) {
+  for (int32_t i = lane; i < n; i += 32) p[i] = i;
+  if (!jobs[j].bootstrap) {
+    for (int32_t i = lane; i < n; i += 32) sj[i] = i;
+    return;
+  }
+  uint64_t* st = st_all[warp];
+  const uint64_t bound = static_cast<uint64_t>(n);
+  const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+  if (lane == 0) {
     Mt64 e;
     rng_stream_init3(e, seed, 3 /* stream_id::kBootstrap */, jobs[j].boot_tag, jobs[j].boot_index);
-    for (int32_t i = 0; i < n; ++i) s[i] = static_cast<int32_t>(uniform_below(e, static_cast<uint64_t>(n)));
-  } else {
-    for (int32_t i = 0; i < n; ++i) s[i] = i;
+    for (int w = 0; w < kMtN; ++w) st[w] = e.x[w];
   }
-  for (int32_t i = 0; i < n; ++i) p[i] = i;
+  __syncwarp();
+  bool replay = false;
+  for (int32_t i0 = 0; i0 < n && !replay; i0 += kMtN) {
+    mt64_twist_block(st, lane);
+    bool rej = false;
+    for (int w = lane; w < kMtN && i0 + w < n; w += 32) {
+      const uint64_t z = mt64_temper(st[w]);
+      rej |= z >= limit;
+      sj[i0 + w] = static_cast<int32_t>(z % bound);
+    }
+    replay = __any_sync(0xffffffffu, rej);
+  }
+  if (replay && lane == 0) {
+    Mt64 e;
+    rng_stream_init3(e, seed, 3, jobs[j].boot_tag, jobs[j].boot_index);
+    for (int32_t i = 0; i < n; ++i) sj[i] = static_cast<int32_t>(uniform_below(e, bound));
+  }
 }
 
-// grow() up to best_split (predictor.cpp:93-107, :138-147). One thread per node.
+// grow() up to best_split (predictor.cpp:93-107, :138-147). One warp per node.
 __global__ void node_begin_kernel(const DNode* nodes, int n_nodes, const DTreeJob* jobs, int32_t n, const double* y,
                                   const int32_t* src, const int32_t* perm, int max_depth, int min_leaf, int subset,
                                   uint64_t seed, int32_t* ord, int32_t* seg_end, DNodeOut* out) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (a >= n_nodes) return;
   const DNode nd = nodes[a];
   const DTreeJob jb = jobs[nd.job];
   const int32_t* s = src + static_cast<int64_t>(nd.job) * n;
   const int32_t* p = perm + static_cast<int64_t>(nd.job) * n + nd.begin;
   const double* yy = y + static_cast<int64_t>(jb.y_index) * n;
+  // the ordered sums of grow() (:97-103) over the node's row order: 32
+  // targets per round gathered by the lanes, broadcast by shuffles into one
+  // chain (every lane runs it; lane 0's result is kept)
   double sum = 0.0, sumsq = 0.0;
-  for (int32_t i = 0; i < nd.len; ++i) {
-    const double v = yy[s[p[i]]];
-    sum += v;
-    sumsq += v * v;
+  for (int32_t base = 0; base < nd.len; base += 32) {
+    const int32_t i = base + lane;
+    double v = 0.0;
+    if (i < nd.len) {
+      const int32_t pi = p[i];
+      ord[nd.off + i] = pi;  // the node's order starts as its row order (`order(idx)`, :153)
+      v = yy[s[pi]];
+    }
+    const int32_t lim = nd.len - base;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const double w = __shfl_sync(0xffffffffu, v, k);
+      if (k < lim) {
+        sum += w;
+        sumsq += w * w;
+      }
+    }
   }
+  if (lane != 0) return;
   const double cnt = static_cast<double>(nd.len);
   DNodeOut o;
   o.mean = sum / cnt;
@@ -135,8 +184,6 @@ __global__ void node_begin_kernel(const DNode* nodes, int n_nodes, const DTreeJo
     }
   }
   out[a] = o;
-  // the node's order starts as its row order (`order(idx)`, :153)
-  for (int32_t i = 0; i < nd.len; ++i) ord[nd.off + i] = p[i];
   seg_end[a] = o.leaf ? nd.off : nd.off + nd.len;
 }
 
@@ -150,18 +197,38 @@ __device__ __forceinline__ int node_of_row(const DNode* nodes, int n_nodes, int6
   return lo;
 }
 
-// Sort keys of candidate k for every row of the step's split nodes.
+// Sort keys of candidate k for every row of the step's nodes: the feature
+// value (orderable bits) and, as the value, {node, position}. A stable radix
+// sort by the feature, then a stable one by the node (node_keys_kernel),
+// leaves every node's rows contiguous, in feature order, ties in the
+// previous order -- the reference's std::stable_sort of the node's `order`.
+// Leaf nodes' rows ride along (their order is never read).
 __global__ void split_keys_kernel(const DNode* nodes, int n_nodes, const DNodeOut* out, int k, int32_t n,
                                   const double* x, const int32_t* src, const int32_t* ord, int64_t rows,
-                                  uint64_t* keys) {
+                                  uint64_t* keys, uint64_t* node_pos) {
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (r >= rows) return;
   const int a = node_of_row(nodes, n_nodes, r);
-  if (out[a].leaf) return;  // not in any sort segment: its ord rows are stale after a swap
+  const int32_t pos = ord[r];
+  node_pos[r] = (static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(pos);
+  if (out[a].leaf) {
+    keys[r] = 0;
+    return;
+  }
   const DNode nd = nodes[a];
   const int f = out[a].cand[k];
-  const int32_t row = src[static_cast<int64_t>(nd.job) * n + ord[r]];
+  const int32_t row = src[static_cast<int64_t>(nd.job) * n + pos];
   keys[r] = orderable(x[static_cast<int64_t>(row) * kNumFeatures + f]);
+}
+
+// After the sort by feature: the node of each row as the key of the second
+// (stable) sort, the position as its value.
+__global__ void node_keys_kernel(const uint64_t* node_pos, int64_t rows, uint32_t* node_key, int32_t* pos) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  const uint64_t v = node_pos[r];
+  node_key[r] = static_cast<uint32_t>(v >> 32);
+  pos[r] = static_cast<int32_t>(static_cast<uint32_t>(v));
 }
 
 // best_split's scan of candidate k (predictor.cpp:160-180), one warp per node:
@@ -171,7 +238,7 @@ __global__ void split_keys_kernel(const DNode* nodes, int n_nodes, const DNodeOu
 // candidate order, as the reference's nested loops do.
 __global__ void split_eval_kernel(const DNode* nodes, int n_nodes, DNodeOut* out, int k, int32_t n, int min_leaf,
                                   const double* x, const double* y, const DTreeJob* jobs, const int32_t* src,
-                                  const int32_t* ord, double* psum, double* psumsq) {
+                                  const int32_t* ord, double* xbuf, double* psum, double* psumsq) {
   const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (a >= n_nodes) return;
@@ -184,25 +251,56 @@ __global__ void split_eval_kernel(const DNode* nodes, int n_nodes, DNodeOut* out
   const int32_t* od = ord + nd.off;
   double* ps = psum + nd.off + a;  // len + 1 entries per node
   double* pq = psumsq + nd.off + a;
+  double* xb = xbuf + nd.off;
+  // The two prefix-sum chains in the sorted order (:160-163): 32 values per
+  // round, one per lane (independent gathers, the next round's in flight),
+  // broadcast by shuffles; every lane runs the same chain and keeps its own
+  // element's prefixes for a coalesced store.
+  const int32_t len = nd.len;
+  auto gather = [&](int32_t i, double& v, double& xv) {
+    if (i < len) {
+      const int64_t row = s[od[i]];
+      v = yy[row];
+      xv = x[row * kNumFeatures + f];
+    }
+  };
+  double nv = 0.0, nx = 0.0;
+  gather(lane, nv, nx);
+  double s1 = 0.0, s2 = 0.0;
   if (lane == 0) {
-    double s1 = 0.0, s2 = 0.0;
     ps[0] = 0.0;
     pq[0] = 0.0;
-    for (int32_t i = 0; i < nd.len; ++i) {
-      const double v = yy[s[od[i]]];
-      s1 = s1 + v;
-      s2 = s2 + v * v;
-      ps[i + 1] = s1;
-      pq[i + 1] = s2;
+  }
+  for (int32_t base = 0; base < len; base += 32) {
+    const double v = nv;
+    const int32_t i = base + lane;
+    if (i < len) xb[i] = nx;
+    gather(i + 32, nv, nx);
+    double m1 = 0.0, m2 = 0.0;
+    const int32_t lim = len - base;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const double w = __shfl_sync(0xffffffffu, v, k);
+      if (k < lim) {
+        s1 = s1 + w;
+        s2 = s2 + w * w;
+      }
+      if (k == lane) {
+        m1 = s1;
+        m2 = s2;
+      }
+    }
+    if (i < len) {
+      ps[i + 1] = m1;
+      pq[i + 1] = m2;
     }
   }
   __syncwarp();
-  const int32_t len = nd.len;
   double best = INFINITY;
   int32_t best_s = INT32_MAX;
   for (int32_t sp = min_leaf + lane; sp + min_leaf <= len; sp += 32) {
-    const double lo = x[static_cast<int64_t>(s[od[sp - 1]]) * kNumFeatures + f];
-    const double hi = x[static_cast<int64_t>(s[od[sp]]) * kNumFeatures + f];
+    const double lo = xb[sp - 1];
+    const double hi = xb[sp];
     if (!(lo < hi)) continue;
     const double ls = static_cast<double>(sp), rs = static_cast<double>(len - sp);
     const double left_sse = pq[sp] - ps[sp] * ps[sp] / ls;
@@ -225,8 +323,8 @@ __global__ void split_eval_kernel(const DNode* nodes, int n_nodes, DNodeOut* out
     }
   }
   if (lane == 0 && best_s != INT32_MAX && best < o.best_sse) {
-    const double lo = x[static_cast<int64_t>(s[od[best_s - 1]]) * kNumFeatures + f];
-    const double hi = x[static_cast<int64_t>(s[od[best_s]]) * kNumFeatures + f];
+    const double lo = xb[best_s - 1];
+    const double hi = xb[best_s];
     o.best_sse = best;
     o.feature = f;
     o.threshold = lo + (hi - lo) / 2.0;
