@@ -65,7 +65,13 @@ enum lt_status_kind {
   LT_K_MESSAGE = 9,            /* free-form, message holds the text */
   LT_K_SLOT_OVERFLOW = 10,     /* adapter_cache.cpp:45-48   a = needed, b = slots */
   LT_K_NO_EVICTABLE = 11,      /* adapter_cache.cpp:64-66   a = adapter_id */
-  LT_K_VALIDATION_MSG = 12     /* host validation; message holds the text */
+  LT_K_VALIDATION_MSG = 12,    /* host validation; message holds the text */
+  /* check_invariants (kv_scheduler.cpp:261-290): InternalError texts */
+  LT_K_NOT_RUNNING = 13,       /* a = request_id: "request a in the batch but not Running" */
+  LT_K_PAST_OUTPUT = 14,       /* a = request_id: "request a generated past its output length" */
+  LT_K_LEDGER_BALANCE = 15,    /* a = holds, b = ledger: "KV ledger out of balance: ..." */
+  LT_K_LEDGER_OVER = 16,       /* "KV ledger over capacity" */
+  LT_K_QUEUE_PHASE = 17        /* "non-preempted request in the preempted queue" */
 };
 
 typedef struct lt_status {
@@ -162,7 +168,8 @@ typedef struct lt_workload_batch {
 
 /* SimOptions (engine.hpp:29-35) plus device knobs. */
 typedef struct lt_sim_options {
-  int32_t check_invariants;      /* accepted; the device path checks its ledger always */
+  int32_t check_invariants;      /* the reference's scheduler invariants, checked every simulated iteration
+                                    (a checked engine build; InternalError on a violation) */
   int32_t want_digest;           /* fold each iteration's decisions into summary.digest */
   int64_t iteration_cap_override; /* <= 0: none */
   int32_t libm_variant;          /* -1: match the host glibc; 0: generic build; 1: FMA build */

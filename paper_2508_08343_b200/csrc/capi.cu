@@ -443,6 +443,7 @@ struct lt_plan {
   DBuf<lt_sim_summary> out;
   // percentiles (want_percentiles): recording pass + segmented sorts
   int want_pct = 0;
+  int want_check = 0;  // SimOptions.check_invariants: the checked engine build (engine_kernel<256,1,true>)
   DBuf<int64_t> rec_off, rec_len;
   DBuf<double> rec_d, rec_d_sorted, ttft_keys, ttft_sorted;
   DBuf<int32_t> rec_c, rec_c_sorted, pct_seg_b, pct_seg_e, pct_rseg_b, pct_rseg_e;
@@ -1292,6 +1293,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   load_config(P.cfg, cfg, opts);
   P.want_digest = opts ? opts->want_digest : 0;
   P.want_pct = opts ? opts->want_percentiles : 0;
+  P.want_check = opts ? opts->check_invariants : 0;
   P.n_scen = b->n_scenarios;
   P.h_scen.resize(P.n_scen);
   P.errs.resize(P.n_scen);
@@ -1632,9 +1634,20 @@ int64_t merge_requests(lt_plan& P) {
   return launches;
 }
 
+// The report / checked engine build (engine_kernel<256,1,true>) on the plan's
+// warp layout, at most 8 warps per block.
+void launch_engine_checked(lt_plan& P, const EngineParams& E, cudaStream_t st) {
+  const int warps = std::min(P.block / 32, 8);
+  const void* rk = reinterpret_cast<const void*>(engine_kernel<256, 1, true>);
+  LT_CUDA(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, P.ctx->smem_optin));
+  engine_kernel<256, 1, true><<<P.grid, warps * 32, static_cast<size_t>(P.smem_per_warp) * warps, st>>>(E);
+}
+
 // K1 (the engine kernel) then K2 (metrics_kernel) over the plan's scenarios.
 void launch_engine(lt_plan& P, const EngineParams& E, cudaStream_t st) {
-  if (P.engine_variant == 2)
+  if (E.check_invariants)
+    launch_engine_checked(P, E, st);
+  else if (P.engine_variant == 2)
     engine_kernel<256, 2><<<P.grid, P.block, P.smem, st>>>(E);
   else if (P.engine_variant == 3)
     engine_kernel<384, 1><<<P.grid, P.block, P.smem, st>>>(E);
@@ -1694,6 +1707,9 @@ EngineParams engine_params(const lt_plan& P) {
   E.priority = P.cfg.raw.loaded_adapter_priority;
   E.want_digest = P.want_digest;
   E.out = P.out.p;
+  E.check_invariants = P.want_check;
+  const char* inject = std::getenv("LT_INVARIANT_INJECT");  // test hook: a ledger fault at this iteration
+  E.inject_iteration = inject ? std::atoll(inject) : -1;
   return E;
 }
 
@@ -1848,12 +1864,8 @@ void run_report(lt_plan& P, ReportRun& R) {
   E.sl_off = R.d_sl_off.p;
   E.sl_log = R.sl_log.p;
   E.sl_cnt = R.sl_cnt.p;
-  // the plan's warp layout, at most 8 warps per block (the report kernel is
-  // the latency variant's code)
-  const int warps = std::min(P.block / 32, 8);
-  const void* rk = reinterpret_cast<const void*>(engine_kernel<256, 1, true>);
-  LT_CUDA(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, P.ctx->smem_optin));
-  engine_kernel<256, 1, true><<<P.grid, warps * 32, static_cast<size_t>(P.smem_per_warp) * warps, st>>>(E);
+  E.report = 1;
+  launch_engine_checked(P, E, st);
   after_launch("engine_kernel(report)", st);
   metrics_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, st>>>(E.scen, E.n_scen, E.r_phase, E.r_first, E.r_arr,
                                                                      E.r_last, E.r_out, E.r_gen, E.out);
@@ -2119,6 +2131,22 @@ void lt_format_status(int32_t code, int32_t kind, int64_t a, int64_t b, char* bu
     case LT_K_SLOT_OVERFLOW:
       std::snprintf(buf, len, "SlotCache: running batch needs %lld adapters but only %lld slots exist (admission bug)",
                     static_cast<long long>(a), static_cast<long long>(b));
+      return;
+    case LT_K_NOT_RUNNING:
+      std::snprintf(buf, len, "request %lld in the batch but not Running", static_cast<long long>(a));
+      return;
+    case LT_K_PAST_OUTPUT:
+      std::snprintf(buf, len, "request %lld generated past its output length", static_cast<long long>(a));
+      return;
+    case LT_K_LEDGER_BALANCE:
+      std::snprintf(buf, len, "KV ledger out of balance: holds sum to %lld, ledger says %lld",
+                    static_cast<long long>(a), static_cast<long long>(b));
+      return;
+    case LT_K_LEDGER_OVER:
+      std::snprintf(buf, len, "KV ledger over capacity");
+      return;
+    case LT_K_QUEUE_PHASE:
+      std::snprintf(buf, len, "non-preempted request in the preempted queue");
       return;
     case LT_K_NO_EVICTABLE:
       std::snprintf(buf, len, "SlotCache: no evictable slot for adapter %lld (admission bug)",

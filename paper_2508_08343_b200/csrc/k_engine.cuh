@@ -679,7 +679,7 @@ struct WarpEngine {
         P.r_gen[rb + idx] = gen;
         P.r_last[rb + idx] = clock;
         zero = atomicSub(&run_cnt[a], 1) == 1;
-        if constexpr (kRep) P.sl_log[sl_base + sl_n] = make_int2(idx, iter);
+        if (kRep && P.report) P.sl_log[sl_base + sl_n] = make_int2(idx, iter);
       }
       if constexpr (kRep) ++sl_n;
       zero = __shfl_sync(kFull, zero, 0);
@@ -1141,6 +1141,53 @@ struct WarpEngine {
 
   // SlotCache::ensure_loaded (adapter_cache.cpp:40-78) with needed = the
   // running batch's adapters (engine.cpp:108-114). Returns Σ load latency.
+  // SimOptions.check_invariants (the debug engine build, kRep): the
+  // reference's check_scheduler_invariants (kv_scheduler.cpp:261-290) on the
+  // device state before the emit -- every running request Running and short
+  // of its output, the ledger equal to the holds (in + generated + the
+  // reserved next token, less a waived final reservation) and within
+  // capacity, every preempted-queue entry Preempted. The first violation, in
+  // the reference's order, fails the engine with its InternalError text.
+  __device__ __forceinline__ bool check_invariants(const EngineParams& P) {
+    long long held = 0;
+    int bad_phase = INT_MAX, bad_gen = INT_MAX;  // lowest running-set slot of each kind
+    for (int base = 0; base < R_end; base += 32) {
+      const int i = base + lane;
+      if (i >= R_end) continue;
+      const int4 e = run_get(i);
+      if (e.x < 0) continue;
+      const int rem = e.y - iter;  // tokens left: the request has generated out - rem
+      held += static_cast<long long>(e.w) - rem + 1 - (e.x == waived ? 1 : 0);
+      if (P.r_phase[rb + e.x] != kRunning && i < bad_phase) bad_phase = i;
+      if (rem < 1 && i < bad_gen) bad_gen = i;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) held += __shfl_xor_sync(kFull, held, d);
+    const int first_phase = __reduce_min_sync(kFull, static_cast<unsigned>(bad_phase));
+    const int first_gen = __reduce_min_sync(kFull, static_cast<unsigned>(bad_gen));
+    const int first = first_phase < first_gen ? first_phase : first_gen;
+    if (first != INT_MAX) {
+      const int4 e = run_get(first);
+      fail(LT_ERR_INTERNAL, first == first_phase ? LT_K_NOT_RUNNING : LT_K_PAST_OUTPUT, e.x, 0);
+      return false;
+    }
+    if (held != used) {
+      fail(LT_ERR_INTERNAL, LT_K_LEDGER_BALANCE, held, used);
+      return false;
+    }
+    if (used > cap) {
+      fail(LT_ERR_INTERNAL, LT_K_LEDGER_OVER, 0, 0);
+      return false;
+    }
+    bool bad_pq = false;
+    for (int i = lane; i < Wp; i += 32) bad_pq |= P.r_phase[rb + pq_get(i).x] != kPreempted;
+    if (__any_sync(kFull, bad_pq)) {
+      fail(LT_ERR_INTERNAL, LT_K_QUEUE_PHASE, 0, 0);
+      return false;
+    }
+    return true;
+  }
+
   template <bool kRep>
   __device__ __forceinline__ bool ensure_loaded(const EngineParams& P, double* loads_sum, int* loads_cnt) {
     const uint32_t needed_w = claimed_w;
@@ -1173,9 +1220,7 @@ struct WarpEngine {
         return false;
       }
       sum = sum + ll;
-      if constexpr (kRep) {
-        if (lane == 0) P.ld[ld_base + loads_n + cnt] = DLoadEvent{clock, ll, ad.id, ad.rank};
-      }
+      if (kRep && P.report && lane == 0) P.ld[ld_base + loads_n + cnt] = DLoadEvent{clock, ll, ad.id, ad.rank};
       ++cnt;
       mask_clear(missing_w, a, lane);
     }
@@ -1293,7 +1338,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   const int64_t rec_base = P.record ? P.rec_off[s] : 0;
   int64_t rec_n = 0;
   int64_t tr_base = 0;
-  if constexpr (kRep) {
+  if (kRep && P.report) {
     tr_base = P.tr_off[s];
     E.ld_base = P.ld_off[s];
     E.sl_base = P.sl_off[s];
@@ -1397,7 +1442,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     }
     __syncwarp();
     LT_PH(4);
-    if constexpr (kRep) {  // stint log: this iteration's admissions, in running-set order
+    if (kRep && P.report) {  // stint log: this iteration's admissions, in running-set order
       for (int base = r_before; base < E.R_end; base += 32) {
         const int i = base + lane;
         const int4 e = i < E.R_end ? E.run_get(i) : make_int4(-1, 0, 0, 0);
@@ -1412,6 +1457,10 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         break;
       }
       continue;
+    }
+    if (kRep && P.check_invariants) {  // check_invariants_pre_emit (engine.cpp:105, :168-183)
+      if (LT_UNLIKELY(P.inject_iteration == E.iter)) E.used += 1;  // test hook: a ledger fault
+      if (!E.check_invariants(P)) break;
     }
     double loads = 0.0;
     int nl = 0;
@@ -1429,7 +1478,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     const double adapters = (A == 0) ? 1.0 : P.k6 * static_cast<double>(A) + P.k7;
     const double lat = sched + loads + model * adapters;
     const double emit = E.clock + lat;
-    if constexpr (kRep) {  // IterationTraceRow (engine.cpp:137-140)
+    if (kRep && P.report) {  // IterationTraceRow (engine.cpp:137-140)
       if (lane == 0) {
         P.tr_time[tr_base + E.iter] = E.clock;
         P.tr_lat[tr_base + E.iter] = lat;
@@ -1547,7 +1596,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
             P.rec_d[rec_base + rec_n + n] = clk - start;
             P.rec_c[rec_base + rec_n + n] = E.R;
           }
-          if constexpr (kRep) {
+          if (kRep && P.report) {
             if (lane == 0) {
               P.tr_time[tr_base + E.iter + n] = start;
               P.tr_lat[tr_base + E.iter + n] = lat_q;
@@ -1615,9 +1664,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
 #endif
   o.device_cycles = clock64() - t_start;
   if (lane == 0) P.out[s] = o;
-  if constexpr (kRep) {
-    if (lane == 0) P.sl_cnt[s] = E.sl_n;
-  }
+  if (kRep && P.report && lane == 0) P.sl_cnt[s] = E.sl_n;
 }
 
 // Persistent kernel: each warp pulls scenarios (cost-descending order) from a

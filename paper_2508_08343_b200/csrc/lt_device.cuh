@@ -148,6 +148,9 @@ struct EngineParams {
   const int64_t* sl_off;
   int2* sl_log;
   int32_t* sl_cnt;
+  int32_t report;            // the report pass writes the rows above
+  int32_t check_invariants;  // SimOptions.check_invariants: checked engine pass
+  int64_t inject_iteration;  // test hook (LT_INVARIANT_INJECT): ledger fault at this iteration, -1 none
 };
 
 }  // namespace lt

@@ -18,6 +18,7 @@ import pytest
 import paper_2508_08343_b200 as lt
 from paper_2508_08343_b200 import _abi as A
 from paper_2508_08343_b200.batch import WorkloadBatch, sim_options
+from tests import workloads as W
 from tests.conftest import ROOT
 
 pytestmark = pytest.mark.gpu
@@ -75,3 +76,40 @@ def test_many_adapter_batch_on_occupancy_variant(dev, ref, monkeypatch):
     r, _ = ref.simulate(batch, cfg, sim_options(None, True))
     for f in FIELDS:
         np.testing.assert_array_equal(g[f], r[f], err_msg=f)
+
+
+def test_check_invariants_passes_and_changes_nothing(dev, ref):
+    """SimOptions.check_invariants runs the checked engine build (the
+    reference's check_scheduler_invariants before every emit): clean runs
+    give the unchecked results, fuzz engines with preemption included."""
+    batch, cfg = W.summary_cases()
+    a, sa = dev.simulate_batch(batch, cfg, want_states=True, want_digest=True)
+    b, sb = dev.simulate_batch(batch, cfg, lt.SimOptions(check_invariants=True), want_states=True, want_digest=True)
+    for f in FIELDS + ("status", "rejected_count"):
+        np.testing.assert_array_equal(a[f], b[f], err_msg=f)
+    for k in sa:
+        np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
+    for seed in range(12):
+        ads, reqs, fcfg = W.scripted_fuzz(seed, n_requests=40 + seed % 50, n_adapters=1 + seed % 6)
+        fb = WorkloadBatch.from_workloads([W.scripted_workload(ads, 6.0)], scripted=[reqs])
+        g, _ = dev.simulate_batch(fb, fcfg, lt.SimOptions(check_invariants=True), want_digest=True)
+        r, _ = ref.simulate(fb, fcfg, sim_options(lt.SimOptions(check_invariants=True), True))
+        for f in ("status", "iterations", "digest", "preemptions"):
+            assert g[f][0] == r[f][0], (seed, f)
+
+
+def test_check_invariants_reports_a_ledger_fault(dev, monkeypatch):
+    """A ledger fault injected on the device (test hook) is caught by the
+    checked build and reported with the reference's InternalError text."""
+    batch, cfg = W.summary_cases()
+    monkeypatch.setenv("LT_INVARIANT_INJECT", "3")
+    out, _ = dev.simulate_batch(batch, cfg, lt.SimOptions(check_invariants=True))
+    hit = [i for i in range(len(out)) if int(out["status"][i]) == A.LT_ERR_INTERNAL]
+    assert hit, "no engine reported the injected fault"
+    msg = dev.message(hit[0])
+    assert msg.startswith("KV ledger out of balance: holds sum to "), msg
+    held, ledger = [int(t.strip(",")) for t in msg.split() if t.strip(",").isdigit()]
+    assert ledger == held + 1
+    monkeypatch.delenv("LT_INVARIANT_INJECT")
+    clean, _ = dev.simulate_batch(batch, cfg, lt.SimOptions(check_invariants=True))
+    assert (clean["status"] == A.LT_OK).sum() >= (out["status"] == A.LT_OK).sum()
