@@ -42,24 +42,44 @@ def nvcc() -> str:
 
 
 def build_gpu(force: bool = False, verbose: bool = False, prof: bool = False, stats: bool = False) -> str:
-    """libloratwin_gpu.so; prof=True builds libloratwin_gpu_prof.so with the
+    """libloratwin_gpu.so from csrc/*.cu: every translation unit (the host /
+    C-ABI code in capi.cu and one engine build per engine_*.cu) compiled in
+    parallel, then linked. prof=True builds libloratwin_gpu_prof.so with the
     per-phase cycle counters (-DLT_PHASE_PROF) used by tools/diag_phase.py,
     stats=True libloratwin_gpu_stats.so with scan counters (-DLT_SCAN_STATS)."""
-    lib = LIB.replace(".so", "_prof.so") if prof else (LIB.replace(".so", "_stats.so") if stats else LIB)
+    tag = "_prof" if prof else ("_stats" if stats else "")
+    lib = LIB.replace(".so", tag + ".so")
     deps = glob.glob(os.path.join(CSRC, "*")) + [os.path.join(INCLUDE, "loratwin_gpu.h")]
     if not force and not _stale(lib, deps):
         return lib
-    os.makedirs(os.path.dirname(lib), exist_ok=True)
-    cmd = [nvcc()] + NVCC_FLAGS + (["-DLT_PHASE_PROF"] if prof else []) + (["-DLT_SCAN_STATS"] if stats else []) + [
-        "-I" + INCLUDE, "-I" + CSRC, "-shared", "-o", lib, os.path.join(CSRC, "capi.cu")]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(os.path.dirname(lib), "obj" + tag)
+    os.makedirs(objdir, exist_ok=True)
+    extra = (["-DLT_PHASE_PROF"] if prof else []) + (["-DLT_SCAN_STATS"] if stats else [])
+    units = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    procs = []
+    for u in units:
+        obj = os.path.join(objdir, os.path.basename(u).replace(".cu", ".o"))
+        cmd = [nvcc()] + NVCC_FLAGS + extra + ["-I" + INCLUDE, "-I" + CSRC, "-c", "-o", obj, u]
+        procs.append((u, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    log = []
+    failed = False
+    for u, obj, p in procs:
+        out, err = p.communicate()
+        log.append(f"== {os.path.basename(u)}\n{out}{err}")
+        if p.returncode != 0:
+            failed = True
+            sys.stderr.write(out + err)
+    if failed:
+        raise RuntimeError("nvcc failed building libloratwin_gpu.so")
+    res = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib]
+                         + [obj for _, obj, _ in procs], capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libloratwin_gpu.so")
-    with open(os.path.join(os.path.dirname(lib), "ptxas" + ("_prof" if prof else "_stats" if stats else "") + ".log"), "w") as f:
-        f.write(res.stderr)
+        raise RuntimeError("nvcc failed linking libloratwin_gpu.so")
+    with open(os.path.join(os.path.dirname(lib), "ptxas" + tag + ".log"), "w") as f:
+        f.write("\n".join(log))
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("\n".join(log))
     return lib
 
 

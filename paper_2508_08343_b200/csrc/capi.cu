@@ -32,7 +32,7 @@
 #include <unordered_map>
 #include <vector>
 
-#include "k_engine.cuh"
+#include "engine_launch.h"
 #include "k_metrics.cuh"
 #include "k_predict.cuh"
 #include "k_report.cuh"
@@ -1240,9 +1240,7 @@ void size_engine(lt_plan& P, const std::vector<double>& cost, int max_run_cap) {
   // other host threads never lower it under each other) and the max-shared
   // carveout, so an engine block and the K0 seed kernel of the next chunk can
   // share an SM.
-  const void* ek = P.engine_variant == 2   ? reinterpret_cast<const void*>(engine_kernel<256, 2>)
-                   : P.engine_variant == 3 ? reinterpret_cast<const void*>(engine_kernel<384, 1>)
-                                           : reinterpret_cast<const void*>(engine_kernel<256, 1>);
+  const void* ek = engine_kernel_fn(P.engine_variant);
   LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_optin));
   LT_CUDA(cudaFuncSetAttribute(ek, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
   int per_sm = 0;
@@ -1556,7 +1554,6 @@ int64_t merge_requests(lt_plan& P);
 
 // K0 + merge: (re)generates every request of every generated scenario.
 void prepare_requests(lt_plan& P) {
-  lt_ctx* ctx = P.ctx;
   cudaStream_t st = P.st;
   cudaEventRecord(P.ev[0], st);
   // K0: RNG tables, arrival counts and request offsets are recomputed on
@@ -1638,21 +1635,19 @@ int64_t merge_requests(lt_plan& P) {
 // warp layout, at most 8 warps per block.
 void launch_engine_checked(lt_plan& P, const EngineParams& E, cudaStream_t st) {
   const int warps = std::min(P.block / 32, 8);
-  const void* rk = reinterpret_cast<const void*>(engine_kernel<256, 1, true>);
-  LT_CUDA(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, P.ctx->smem_optin));
-  engine_kernel<256, 1, true><<<P.grid, warps * 32, static_cast<size_t>(P.smem_per_warp) * warps, st>>>(E);
+  LT_CUDA(cudaFuncSetAttribute(engine_kernel_fn(kEngineChecked), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               P.ctx->smem_optin));
+  launch_engine_build(kEngineChecked, static_cast<unsigned>(P.grid), static_cast<unsigned>(warps * 32),
+                      static_cast<size_t>(P.smem_per_warp) * warps, st, E);
 }
 
 // K1 (the engine kernel) then K2 (metrics_kernel) over the plan's scenarios.
 void launch_engine(lt_plan& P, const EngineParams& E, cudaStream_t st) {
   if (E.check_invariants)
     launch_engine_checked(P, E, st);
-  else if (P.engine_variant == 2)
-    engine_kernel<256, 2><<<P.grid, P.block, P.smem, st>>>(E);
-  else if (P.engine_variant == 3)
-    engine_kernel<384, 1><<<P.grid, P.block, P.smem, st>>>(E);
   else
-    engine_kernel<256, 1><<<P.grid, P.block, P.smem, st>>>(E);
+    launch_engine_build(P.engine_variant, static_cast<unsigned>(P.grid), static_cast<unsigned>(P.block), P.smem, st,
+                        E);
   after_launch("engine_kernel", st);
   metrics_kernel<<<static_cast<unsigned>((P.n_scen + 7) / 8), 256, 0, st>>>(
       E.scen, E.n_scen, E.r_phase, E.r_first, E.r_arr, E.r_last, E.r_out, E.r_gen, E.out);
@@ -1716,7 +1711,6 @@ EngineParams engine_params(const lt_plan& P) {
 void run_percentiles(lt_plan& P, EngineParams E);
 
 void run_plan(lt_plan& P) {
-  lt_ctx* ctx = P.ctx;
   cudaStream_t st = P.st;
   untrim_plan(P);
   prepare_requests(P);

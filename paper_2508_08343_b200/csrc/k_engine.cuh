@@ -37,14 +37,6 @@ constexpr unsigned kFull = 0xffffffffu;
 // stalls show up (ncu no_instruction); rare paths are kept out of line.
 #define LT_UNLIKELY(x) __builtin_expect(!!(x), 0)
 #define LT_LIKELY(x) __builtin_expect(!!(x), 1)
-// per-warp shared memory per adapter: last_used f64 + run_cnt, q_head, q_tail,
-// act_key (i32)
-constexpr int kSmemPerAdapter = 8 + 4 * 4;
-// Retire calendar: running entries are linked into bucket (retire iteration
-// mod kCalBuckets); the bucket of the current iteration holds every retiree.
-constexpr int kCalBuckets = 512;
-// Preempted-queue slots kept in shared memory (the rest in HBM).
-constexpr int kPqSmem = 64;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -91,7 +83,7 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
 // LRU victim: argmin over set bits of `cand` of (last_used, adapter_id);
 // dense index order == adapter_id order. Adapters needed by the previous
 // ensure_loaded call still carry last_used == prev_now (lazy refresh).
-__device__ __noinline__ int lru_victim(uint32_t cand, uint32_t prev_needed, double prev_now,
+static __device__ __noinline__ int lru_victim(uint32_t cand, uint32_t prev_needed, double prev_now,
                                           const double* last_used, int lane) {
   double best = DBL_MAX;
   int best_a = INT_MAX;
@@ -133,7 +125,7 @@ __device__ __forceinline__ uint64_t fold64(uint64_t h, uint64_t w) {
 // Non-lane-mode helpers of the fresh scan (rare: more than 32 adapters can
 // act), kept out of line so the hot loop stays compact in the instruction cache.
 // Lane-local minimum of act_key over this lane's adapters a = lane + 32 m.
-__device__ __noinline__ int2 lane_best(const int32_t* act_key, int N, int lane) {
+static __device__ __noinline__ int2 lane_best(const int32_t* act_key, int N, int lane) {
   int best = INT_MAX, bi = -1;
 #pragma unroll 1
   for (int a = lane; a < N; a += 32) {
@@ -148,7 +140,7 @@ __device__ __noinline__ int2 lane_best(const int32_t* act_key, int N, int lane) 
 
 // Lane-local minimum chain head over this lane's adapters a = lane + 32 m
 // (q_head -1, an empty chain, compares above every id).
-__device__ __noinline__ int2 lane_best_head(const int32_t* q_head, int N, int lane) {
+static __device__ __noinline__ int2 lane_best_head(const int32_t* q_head, int N, int lane) {
   int best = INT_MAX, bi = -1;
 #pragma unroll 1
   for (int a = lane; a < N; a += 32) {
@@ -163,7 +155,7 @@ __device__ __noinline__ int2 lane_best_head(const int32_t* q_head, int N, int la
 
 // act_key for every adapter (round-robin layout: lane owns a = lane + 32 m,
 // whose mask bit is bit `lane` of word m).
-__device__ __noinline__ void act_keys(int32_t* act_key, const int32_t* q_head, int N, int lane, uint32_t blocked_w,
+static __device__ __noinline__ void act_keys(int32_t* act_key, const int32_t* q_head, int N, int lane, uint32_t blocked_w,
                                       uint32_t slotful_w, uint32_t claimed_w, uint32_t nonempty_w, bool mass,
                                       bool only_mass_exclusion) {
 #pragma unroll 1
@@ -200,7 +192,7 @@ struct RunTiers {
 // rebuilt for the new slots (next links by atomic head exchange, then each
 // node's successor learns its predecessor). Rare, so out of line: it keeps
 // the engine loop's instruction footprint small. Returns the new length.
-__device__ __noinline__ int compact_running(RunTiers t, int R_end, int lane) {
+static __device__ __noinline__ int compact_running(RunTiers t, int R_end, int lane) {
   auto get = [&](int pos) { return pos < t.run_cap ? t.runs[pos] : t.run[pos]; };
   auto lk = [&](int pos) -> int2& { return pos < t.run_cap ? t.links[pos] : t.linkg[pos]; };
   int w = 0;
@@ -251,7 +243,7 @@ struct PqRing {
 // backward scan for the first entry that does not sort after it, then the
 // tail shifted by one (back to front). Out of line: the append / prepend
 // cases cover every victim of generated workloads.
-__device__ __noinline__ void pq_insert_middle(PqRing q, int Wp, int4 ent, bool ids_sorted, const double* arr,
+static __device__ __noinline__ void pq_insert_middle(PqRing q, int Wp, int4 ent, bool ids_sorted, const double* arr,
                                               int lane) {
   auto slot = [&](int i) {
     const int j = q.pq_h + i;

@@ -30,6 +30,16 @@ constexpr int kAdapterMask = (1 << 20) - 1;
 // iteration), w = input + output tokens.
 constexpr int kFreshBit = 1 << 30;
 
+// Engine shared-memory layout (k_engine.cuh; sized on the host in size_engine).
+// per-warp shared memory per adapter: last_used f64 + run_cnt, q_head, q_tail,
+// act_key (i32)
+constexpr int kSmemPerAdapter = 8 + 4 * 4;
+// Retire calendar: running entries are linked into bucket (retire iteration
+// mod kCalBuckets); the bucket of the current iteration holds every retiree.
+constexpr int kCalBuckets = 512;
+// Preempted-queue slots kept in shared memory (the rest in HBM).
+constexpr int kPqSmem = 64;
+
 struct DScen {
   int64_t req_begin;
   int32_t n_req;
