@@ -42,7 +42,9 @@ def main():
     base = min(a for a, _, _ in data)
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
-    cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
+    # the cubin (one per translation unit) that holds the kernel
+    cubs = [f for f in os.listdir(tmp) if f.endswith(".cubin")]
+    cub = next(f for f in cubs if fn.encode() in open(os.path.join(tmp, f), "rb").read())
     dis = subprocess.run(["nvdisasm", "-g", "-gi", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
     where = {}
     chain = []  # consecutive //## lines: one instruction's inline chain
