@@ -888,13 +888,23 @@ double mean_pair_draws(const lt_workload_batch* b) {
   return pairs ? draws / static_cast<double>(pairs) : 1e9;
 }
 
-// Arrival merge: one CUB segmented stable sort per scenario, or two global
-// radix sorts for very large batches (measured: equal or slightly slower at
-// C2's 3.6 M and C5's 9 M requests, 4 % faster at C3's 5e8-request chunks).
-// LT_MERGE=radix|segmented overrides.
+// Arrival merge: the merge tree of each scenario's per-adapter lists
+// (merge_kernel, default); LT_MERGE=segmented selects CUB's per-scenario
+// stable segmented sort, LT_MERGE=radix two global stable radix sorts. All
+// three order the arrivals identically (tested).
+int merge_mode() {
+  const char* e = std::getenv("LT_MERGE");
+  return (e && std::strcmp(e, "segmented") == 0) ? 2 : 1;
+}
+
 bool radix_merge(int64_t n_requests) {
-  if (const char* e = std::getenv("LT_MERGE")) return std::strcmp(e, "radix") == 0;
-  return n_requests >= 50000000;
+  // the merge tree is faster at every measured size (C2, C3 plans, C5 plans:
+  // 2.26 / 9.19 / 72.0 ms pre-engine with the segmented sort, 7.23 / 73.6
+  // with the radix sorts, 2.13 / 5.54 / 68.7 with the tree); the radix form
+  // stays selectable (LT_MERGE=radix)
+  (void)n_requests;
+  const char* e = std::getenv("LT_MERGE");
+  return e && std::strcmp(e, "radix") == 0;
 }
 
 // Keys seeded and drawn per chunk (the seeded states take 5 KB per key).
@@ -1612,7 +1622,7 @@ int64_t merge_requests(lt_plan& P) {
                                               P.scen_bits, st));
       perm = P.pos_a.p;
       launches += 2;  // iota, scen_key
-    } else {
+    } else if (merge_mode() == 2) {  // the per-scenario stable segmented sort (CUB)
       segments_kernel<<<static_cast<unsigned>((P.n_scen + 255) / 256), 256, 0, st>>>(
           P.scen.p, static_cast<int>(P.n_scen), P.seg_begin.p, P.seg_end.p);
       after_launch("segments_kernel", st);
@@ -1620,6 +1630,11 @@ int64_t merge_requests(lt_plan& P) {
                                                         P.sv_out.p, nr, static_cast<int>(P.n_scen), P.seg_begin.p,
                                                         P.seg_end.p, st));
       launches += 1;  // segments
+    } else {  // merge tree of the per-adapter lists, one block per scenario
+      merge_kernel<<<static_cast<unsigned>(P.n_scen), 512, 0, st>>>(P.scen.p, P.pair_begin.p, P.pair_excl.p,
+                                                                    P.st_in.p, P.sv_in.p, P.st_out.p, P.sv_out.p);
+      after_launch("merge_kernel", st);
+      launches += 1;
     }
     gather_kernel<<<gr, 256, 0, st>>>(P.scen.p, static_cast<int>(P.n_scen), P.total_req, P.adapters.p, P.keys.p,
                                       P.lens.p, P.Z.p, perm ? P.st_in.p : P.st_out.p, perm ? P.sv_in.p : P.sv_out.p,

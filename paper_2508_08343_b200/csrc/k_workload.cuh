@@ -474,6 +474,84 @@ __global__ void __launch_bounds__(256) expand_kernel(const DScen* scen, const in
   }
 }
 
+// Arrival merge by merge tree (replaces the per-scenario stable segmented
+// sort): one block per generated scenario. Its arrivals sit in pair order --
+// one list per adapter in ascending id, each list ascending in time (the
+// reference's t += E/rate), so the reference's stable_sort by (time,
+// adapter_id) (workload.cpp:204-207) is the stable merge of the lists in
+// order. Round r merges adjacent runs of 2^r lists; an element of a left run
+// lands after the right run's elements with a smaller time, an element of a
+// right run after the left run's elements with a time <= its own (ties keep
+// the lower adapter id first, within a list the draw order). Each element
+// finds its place with one binary search in the partner run, all in
+// parallel; the runs ping-pong between (t_a, v_a) and (t_b, v_b), and the
+// result ends in (t_b, v_b), the layout gather_kernel reads.
+__global__ void __launch_bounds__(512) merge_kernel(const DScen* scen, const int64_t* pair_begin,
+                                                    const unsigned long long* pair_excl, double* t_a,
+                                                    unsigned long long* v_a, double* t_b, unsigned long long* v_b) {
+  __shared__ int32_t off[kMaxAdapters + 1];
+  const DScen sc = scen[blockIdx.x];
+  if (!sc.generated || sc.status != LT_OK || sc.n_req == 0) return;
+  const int n = sc.n_req, np = sc.n_adapters;
+  const int64_t rb = sc.req_begin;
+  const int64_t p0 = pair_begin[blockIdx.x];
+  const unsigned long long e0 = pair_excl[p0];
+  for (int k = threadIdx.x; k < np; k += blockDim.x) off[k] = static_cast<int32_t>(pair_excl[p0 + k] - e0);
+  if (threadIdx.x == 0) off[np] = n;
+  __syncthreads();
+  double* st = t_a + rb;
+  unsigned long long* sv = v_a + rb;
+  double* dt = t_b + rb;
+  unsigned long long* dv = v_b + rb;
+  for (int w = 1; w < np; w *= 2) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      int lo = 0, hi = np;  // the list holding position i: last k with off[k] <= i
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (off[mid] <= i) lo = mid;
+        else hi = mid;
+      }
+      const int m = lo / w;           // its run this round
+      const int a0 = (m & ~1) * w;    // the pair of runs (A, B)
+      const int sA = off[a0], sB = off[min(a0 + w, np)], eB = off[min(a0 + 2 * w, np)];
+      const double t = st[i];
+      int pos;
+      if ((m & 1) == 0) {  // in A: after B's elements with a smaller time
+        int l = sB, h = eB;
+        while (l < h) {
+          const int mid = (l + h) >> 1;
+          if (st[mid] < t) l = mid + 1;
+          else h = mid;
+        }
+        pos = i + (l - sB);
+      } else {  // in B: after A's elements with a time <= its own
+        int l = sA, h = sB;
+        while (l < h) {
+          const int mid = (l + h) >> 1;
+          if (st[mid] <= t) l = mid + 1;
+          else h = mid;
+        }
+        pos = sA + (i - sB) + (l - sA);
+      }
+      dt[pos] = t;
+      dv[pos] = sv[i];
+    }
+    __syncthreads();
+    double* tt = st;
+    st = dt;
+    dt = tt;
+    unsigned long long* vv = sv;
+    sv = dv;
+    dv = vv;
+  }
+  if (st != t_b + rb) {  // an even number of rounds: the result is still in (t_a, v_a)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      t_b[rb + i] = st[i];
+      v_b[rb + i] = sv[i];
+    }
+  }
+}
+
 // Segment bounds of the generated scenarios (scripted / failed: empty).
 __global__ void segments_kernel(const DScen* scen, int n_scen, int* seg_begin, int* seg_end) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;

@@ -494,24 +494,26 @@ def test_parallel_host_packing_matches_serial(dev, monkeypatch):
 
 
 def test_radix_merge_matches_segmented_merge(dev, monkeypatch):
-    """The arrival merge as two global stable radix sorts (used for very large
-    batches) must order every scenario's arrivals exactly as the per-scenario
-    segmented stable sort: same request arrays, summaries and states."""
+    """The arrival merge as the merge tree (default), two global stable radix
+    sorts (very large batches) and CUB's per-scenario segmented stable sort
+    must order every scenario's arrivals identically: same request arrays,
+    summaries and states."""
     cases = [W.summary_cases(), W.full_mode_cases(), (W.c2_batch(duration_s=120.0, stride=4), lt.h100_like_config(1))]
     for b, cfg in cases:
         out = []
-        for mode in ("segmented", "radix"):
+        for mode in ("segmented", "radix", "tree"):
             monkeypatch.setenv("LT_MERGE", mode)
             g, s = dev.simulate_batch(b, cfg, want_states=True, want_digest=True)
             out.append((g, s, [dev.message(i) for i in range(len(g))]))
         monkeypatch.delenv("LT_MERGE")
-        (g1, s1, m1), (g2, s2, m2) = out
-        for f in g1.dtype.names:
-            if f not in ("device_cycles", "phase_cycles"):
-                np.testing.assert_array_equal(g1[f], g2[f], err_msg=f)
-        for k in s1:
-            np.testing.assert_array_equal(s1[k], s2[k], err_msg=k)
-        assert m1 == m2
+        (g1, s1, m1) = out[0]
+        for g2, s2, m2 in out[1:]:
+            for f in g1.dtype.names:
+                if f not in ("device_cycles", "phase_cycles"):
+                    np.testing.assert_array_equal(g1[f], g2[f], err_msg=f)
+            for k in s1:
+                np.testing.assert_array_equal(s1[k], s2[k], err_msg=k)
+            assert m1 == m2
 
 
 def _sweep_error_config():
