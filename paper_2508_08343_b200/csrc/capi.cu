@@ -18,6 +18,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <thread>
 #include <cmath>
 #include <cstdio>
@@ -44,6 +46,70 @@
 using namespace lt;
 
 namespace {
+
+// Persistent host workers for the plan-building passes (thread start-up
+// would otherwise cost more than the small batches' work): run(nt, fn)
+// calls fn(t) for t in [0, nt) on up to nt threads, the caller running t = 0.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();  // never destroyed (outlives static plans)
+    return *p;
+  }
+  static int width(int64_t work, int64_t min_per_thread) {
+    const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(hw, 16), work / min_per_thread)));
+  }
+  template <typename F>
+  void run(int nt, F&& fn) {
+    if (nt <= 1) {
+      fn(0);
+      return;
+    }
+    std::unique_lock<std::mutex> call(call_mu_);  // one parallel pass at a time
+    ensure(nt - 1);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = [&fn](int t) { fn(t); };
+      n_ = nt;
+      next_ = 1;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ == nt - 1; });
+    job_ = nullptr;
+  }
+
+ private:
+  void ensure(int k) {
+    while (static_cast<int>(threads_.size()) < k) threads_.emplace_back([this] { loop(); });
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen && next_ < n_; });
+      seen = gen_;
+      while (next_ < n_) {
+        const int t = next_++;
+        auto job = job_;
+        lk.unlock();
+        job(t);
+        lk.lock();
+        if (++done_ == n_ - 1) done_cv_.notify_one();
+      }
+    }
+  }
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  std::vector<std::thread> threads_;
+  std::function<void(int)> job_;
+  int n_ = 0, next_ = 0, done_ = 0;
+  uint64_t gen_ = 0;
+};
 
 struct CudaError {
   std::string what;
@@ -635,6 +701,90 @@ int libm_variant_for(const lt_sim_options* o) {
 }
 
 // Validates scenario `i` in reference order and fills its device record.
+// Screen of prepare_scenario's checks for plain generated scenarios (Mean
+// mode, workload-level lengths, ascending ids, valid ranks and rates, a
+// feasible slot cost), run on host threads before the serial pass: a
+// scenario that passes takes the serial pass's deferred branch in O(1)
+// (plain_scenario); anything else -- every error included, so the messages
+// stay the reference's -- takes prepare_scenario.
+struct PlainPre {
+  int32_t plain = 0;
+  int32_t G = 0;
+  int64_t capacity = 0;
+  double ideal = 0.0;
+};
+
+void prescreen_plain(const lt_plan& P, const lt_workload_batch& b, std::vector<PlainPre>& pre) {
+  const int64_t n = b.n_scenarios;
+  pre.assign(n, PlainPre{});
+  std::vector<char> len_ok(std::max<int64_t>(b.n_lengths, 1), 0);
+  for (int64_t l = 0; l < b.n_lengths; ++l) {
+    HostErr e;
+    len_ok[l] = b.lengths[l].mode == LT_MODE_MEAN && validate_lengths(b.lengths[l], b.full_lengths, "workload.lengths", &e);
+  }
+  if (!P.cfg.body_ok) return;
+  auto work = [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) {
+      const lt_scenario& s = b.scenarios[i];
+      const int G = s.slots > 0 ? s.slots : P.cfg.raw.slots;
+      if (s.n_requests >= 0 || s.n_adapters <= 0 || s.n_adapters > kMaxAdapters || !(s.duration_s > 0.0) ||
+          s.mode == LT_MODE_FULL || G < 1 || s.length_index < 0 || s.length_index >= b.n_lengths || !len_ok[s.length_index])
+        continue;
+      const lt_adapter* ad = b.adapters + s.adapter_offset;
+      bool ok = true;
+      int max_rank = 0;
+      for (int k = 0; k < s.n_adapters && ok; ++k) {
+        ok = ad[k].rank >= 0 && ad[k].rate > 0.0 && ad[k].length_index < 0 && (k == 0 || ad[k - 1].adapter_id < ad[k].adapter_id);
+        max_rank = std::max(max_rank, ad[k].rank);
+      }
+      if (!ok) continue;
+      int64_t c_slot;
+      HostErr e;
+      if (!slot_cost(P.cfg, max_rank, &c_slot, &e)) continue;
+      const int64_t capacity = P.cfg.raw.total_kv_budget - static_cast<int64_t>(G) * c_slot;
+      if (capacity <= 0) continue;
+      // ideal_throughput (metrics.cpp:36-45) in spec order, as prepare_scenario
+      const lt_length_spec& l = b.lengths[s.length_index];
+      double tokens = output_mean(l, b.full_lengths);
+      if (P.cfg.raw.ideal_includes_input) tokens += input_mean(l, b.full_lengths);
+      double ideal = 0.0;
+      for (int k = 0; k < s.n_adapters; ++k) ideal += ad[k].rate * tokens;
+      pre[i] = PlainPre{1, G, capacity, ideal};
+    }
+  };
+  const int nt = HostPool::width(n, 512);
+  HostPool::get().run(nt, [&](int t) { work(n * t / nt, n * (t + 1) / nt); });
+}
+
+// prepare_scenario's deferred branch for a screened plain scenario.
+void plain_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t i, const PlainPre& q,
+                    int32_t& last_len_index, int32_t& last_len_param) {
+  const lt_scenario& s = b.scenarios[i];
+  DScen& d = P.h_scen[i];
+  std::memset(&d, 0, sizeof(d));
+  d.G = q.G;
+  d.duration = s.duration_s;
+  d.n_adapters = s.n_adapters;
+  d.adapter_begin = static_cast<int64_t>(pr.adapters.size());
+  d.generated = 1;
+  d.ids_sorted = 1;
+  d.iter_cap = P.cfg.raw.iteration_cap;
+  d.capacity = q.capacity;
+  d.ideal = q.ideal;
+  if (s.length_index != last_len_index) {
+    last_len_index = s.length_index;
+    last_len_param = intern_len(pr, as_dlen(b.lengths[s.length_index], b.full_lengths));
+  }
+  d.length_param = last_len_param;
+  pr.deferred.push_back(Prep::Deferred{i, static_cast<int64_t>(pr.adapters.size()),
+                                       static_cast<int64_t>(pr.pair_scen.size())});
+  pr.adapters.resize(pr.adapters.size() + s.n_adapters);
+  P.adapter_ids.resize(P.adapter_ids.size() + s.n_adapters);
+  pr.pair_scen.resize(pr.pair_scen.size() + s.n_adapters);
+  pr.pair_adp.resize(pr.pair_adp.size() + s.n_adapters);
+  P.max_adapters = std::max(P.max_adapters, s.n_adapters);
+}
+
 void prepare_scenario(lt_plan& P, Prep& pr, const lt_workload_batch& b, int64_t i) {
   const lt_scenario& s = b.scenarios[i];
   DScen& d = P.h_scen[i];
@@ -1026,14 +1176,8 @@ bool pack_deferred(lt_plan& P, Prep& pr, const lt_workload_batch& b) {
   }
   const int64_t total = pr.deferred.back().a_off + b.scenarios[pr.deferred.back().i].n_adapters -
                         pr.deferred.front().a_off;
-  const int nt = total < 16384 ? 1 : static_cast<int>(std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency())));
-  if (nt <= 1) {
-    work(0, nd);
-  } else {
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t) th.emplace_back(work, nd * t / nt, nd * (t + 1) / nt);
-    for (auto& x : th) x.join();
-  }
+  const int nt = std::min<int64_t>(HostPool::width(total, 8192), std::max<int64_t>(nd, 1));
+  HostPool::get().run(nt, [&](int t) { work(nd * t / nt, nd * (t + 1) / nt); });
   return ok;
 }
 
@@ -1082,14 +1226,8 @@ void collect_keys(Prep& pr, const lt_workload_batch& b) {
       }
     }
   };
-  const int nt = base < 16384 ? 1 : static_cast<int>(std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency())));
-  if (nt <= 1) {
-    fill(0, n);
-  } else {
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t) th.emplace_back(fill, n * t / nt, n * (t + 1) / nt);
-    for (auto& x : th) x.join();
-  }
+  const int nt = std::min<int64_t>(HostPool::width(base, 8192), std::max<int64_t>(n, 1));
+  HostPool::get().run(nt, [&](int t) { fill(n * t / nt, n * (t + 1) / nt); });
   // the rest (shared seeds) deduplicated per (seed, id)
   for (int64_t i = 0; i < n; ++i) {
     const lt_scenario& s = b.scenarios[i];
@@ -1118,17 +1256,37 @@ void collect_keys(Prep& pr, const lt_workload_batch& b) {
 }
 
 // Table capacity per key: rate_max * dur_max + 8 sigma + slack draws.
+// (On host threads for large key sets: the capacities and partial sums per
+// range, then the offsets; the K0 launch waits on this.)
 int64_t size_keys(PinnedVec<DKeyNI>& keys) {
-  int64_t e_total = 0;
-  for (DKey& k : keys) {
+  const int64_t n = static_cast<int64_t>(keys.size());
+  auto cap_of = [](const DKey& k) {
     const double lam = k.rate_max * k.dur_max;
     const double capd = lam + 8.0 * std::sqrt(lam) + 32.0;
-    k.cap = static_cast<int32_t>(std::min(capd, 2.0e9));
-    k.e_off = e_total;
-    k.z_off = e_total;
-    e_total += k.cap;
-  }
-  return e_total;
+    return static_cast<int32_t>(std::min(capd, 2.0e9));
+  };
+  const int nt = HostPool::width(n, 8192);
+  std::vector<int64_t> part(nt + 1, 0);
+  auto caps = [&](int t) {
+    int64_t sum = 0;
+    for (int64_t i = n * t / nt; i < n * (t + 1) / nt; ++i) {
+      keys[i].cap = cap_of(keys[i]);
+      sum += keys[i].cap;
+    }
+    part[t + 1] = sum;
+  };
+  auto offsets = [&](int t) {
+    int64_t off = part[t];
+    for (int64_t i = n * t / nt; i < n * (t + 1) / nt; ++i) {
+      keys[i].e_off = off;
+      keys[i].z_off = off;
+      off += keys[i].cap;
+    }
+  };
+  HostPool::get().run(nt, caps);
+  for (int t = 0; t < nt; ++t) part[t + 1] += part[t];
+  HostPool::get().run(nt, offsets);
+  return part[nt];
 }
 
 // Request arrays and merge scratch for P.total_req requests of P.n_pairs
@@ -1323,27 +1481,46 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   pr.pair_adp.reserve(n_ad);
   pr.pair_begin.resize(P.n_scen);
   // pass 1 + early K0 (seed_seq and table draws; Full-mode decks follow pass 2)
+  const auto h_setup = hclk::now();
   collect_keys(pr, *b);
+  const auto h_keys = hclk::now();
   int64_t e_total = size_keys(pr.keys);
+  const auto h_size = hclk::now();
   cudaEventRecord(P.ev[0], st);
   if (!pr.keys.empty())
     P.seed_state.alloc(std::min<int64_t>(static_cast<int64_t>(pr.keys.size()), kSeedChunk) * 2 * kMtN);
   P.tab_overflow.alloc(1);
   LT_CUDA(cudaMemsetAsync(P.tab_overflow.p, 0, sizeof(int32_t), st));
   const size_t early_keys = pr.keys.size();
+  auto h_up = h_size;
   if (early_keys > 0) {
     P.keys.upload(pr.keys.data(), pr.keys.size(), st);
     P.E.alloc(std::max<int64_t>(e_total, 1));
     P.Z.alloc(std::max<int64_t>(e_total, 1));
     P.h2d_bytes += pr.keys.size() * sizeof(DKey);
+    h_up = hclk::now();
     P.launches_prep += launch_tables(P, static_cast<int>(early_keys), st);
   }
+  if (std::getenv("LT_HOST_TIMING"))
+    std::fprintf(stderr, "[lt]   K0 launch: size_keys %.2f, allocs+upload %.2f, launches %.2f ms\n", hms(h_size),
+                 hms(h_up), hms(hclk::now()));
   // pass 2: validation and packing in reference order; the adapter records
   // of plain generated scenarios are packed afterwards on several threads
+  const auto h_k0 = hclk::now();
+  std::vector<PlainPre> pre;
+  auto h_screen = h_k0, h_serial = h_k0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     pr.allow_defer = attempt == 0 && !std::getenv("LT_SERIAL_PREP");
+    const bool screen = pr.allow_defer && !std::getenv("LT_NO_PRESCREEN");
+    if (screen) prescreen_plain(P, *b, pre);
+    h_screen = hclk::now();
+    int32_t last_len_index = -1, last_len_param = -1;
     for (int64_t i = 0; i < P.n_scen; ++i) {
       pr.pair_begin[i] = static_cast<int64_t>(pr.pair_scen.size());
+      if (screen && pre[i].plain) {
+        plain_scenario(P, pr, *b, i, pre[i], last_len_index, last_len_param);
+        continue;
+      }
       prepare_scenario(P, pr, *b, i);
       if (P.errs[i].code != LT_OK) {
         // drop partially appended pairs of a failed scenario
@@ -1351,6 +1528,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
         pr.pair_adp.resize(pr.pair_begin[i]);
       }
     }
+    h_serial = hclk::now();
     if (pack_deferred(P, pr, *b)) break;
     // a key was missing: repack everything serially
     pr.deferred.clear();
@@ -1504,8 +1682,11 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   P.tables_ms = elapsed(P.ev[0], P.ev[1]);
   P.fresh = true;
   if (std::getenv("LT_HOST_TIMING"))
-    std::fprintf(stderr, "[lt] build_plan host: prep %.2f ms, +tables sync %.2f ms, total %.2f ms (%lld scenarios)\n",
-                 hms(h_prep), hms(h_tables), hms(hclk::now()), static_cast<long long>(P.n_scen));
+    std::fprintf(stderr,
+                 "[lt] build_plan host: setup %.2f, keys %.2f, K0 launch %.2f, screen %.2f, serial pass %.2f, "
+                 "packing+uploads %.2f -> prep %.2f ms, +tables sync %.2f ms, total %.2f ms (%lld scenarios)\n",
+                 hms(h_setup), hms(h_keys), hms(h_k0), hms(h_screen), hms(h_serial), hms(h_prep), hms(h_prep),
+                 hms(h_tables), hms(hclk::now()), static_cast<long long>(P.n_scen));
   return plan.release();
 }
 
