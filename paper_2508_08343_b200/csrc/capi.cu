@@ -1419,6 +1419,11 @@ void size_engine(lt_plan& P, const std::vector<double>& cost, int max_run_cap) {
   const int64_t want = std::max<int64_t>((P.n_scen + P.block / 32 - 1) / (P.block / 32),
                                          std::min<int64_t>(P.n_scen, ctx->sm_count));
   P.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(ctx->sm_count) * per_sm)));
+}
+
+// The engine workspace, once the request counts are known (size_engine ran
+// before them: it needs only the cost estimates).
+void size_workspace(lt_plan& P) {
   P.ws_stride = std::max<int64_t>(P.max_req, 1);
   {
     // Workspace per persistent warp slot (slots x longest scenario) or per
@@ -1621,6 +1626,11 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     P.pair_g = pair_group(mean_pair_draws(b));
     launch_count(P, st);
     ++P.launches_prep;
+  }
+  // the engine's order, variant and grid need only the cost estimates: sized
+  // while K0 and the counts run
+  size_engine(P, pr.cost, max_run_cap);
+  if (n_pairs > 0) {
     std::vector<unsigned long long> counts(P.n_scen);
     int32_t ovf = 0;
     LT_CUDA(cudaMemcpyAsync(counts.data(), P.scen_count.p, P.n_scen * sizeof(unsigned long long),
@@ -1674,11 +1684,9 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
       LT_CUDA(cudaMemcpyAsync(P.r_adp.p + at, adp.data() + cursor, n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
       cursor += n;
     }
-    P.h2d_bytes += cursor * 20;
-    LT_CUDA(cudaStreamSynchronize(st));
+    P.h2d_bytes += cursor * 20;  // (pageable sources: the copies are staged before the calls return)
   }
-  size_engine(P, pr.cost, max_run_cap);
-  LT_CUDA(cudaStreamSynchronize(st));
+  size_workspace(P);
   P.tables_ms = elapsed(P.ev[0], P.ev[1]);
   P.fresh = true;
   if (std::getenv("LT_HOST_TIMING"))

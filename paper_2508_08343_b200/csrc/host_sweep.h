@@ -427,6 +427,7 @@ void sweep_waves_device(lt_ctx* ctx, const SweepSetup& S, const lt_server_config
       tm.launches += merge_requests(W);
       cudaEventRecord(W.ev[3], st);
       size_engine(W, cost, 1024);
+      size_workspace(W);
       reset_state(W);
       const EngineParams E = engine_params(W);
       cudaEventRecord(W.ev[4], st);
