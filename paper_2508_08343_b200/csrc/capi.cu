@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -77,10 +78,18 @@ class HostPool {
       ++gen_;
     }
     cv_.notify_all();
-    fn(0);
+    std::exception_ptr err;
+    try {
+      fn(0);
+    } catch (...) {
+      err = std::current_exception();
+    }
     std::unique_lock<std::mutex> lk(mu_);
-    done_cv_.wait(lk, [&] { return done_ == nt - 1; });
+    done_cv_.wait(lk, [&] { return done_ == nt - 1; });  // the workers still use fn
     job_ = nullptr;
+    if (!err) err = worker_err_;
+    worker_err_ = nullptr;
+    if (err) std::rethrow_exception(err);
   }
 
  private:
@@ -97,8 +106,14 @@ class HostPool {
         const int t = next_++;
         auto job = job_;
         lk.unlock();
-        job(t);
+        std::exception_ptr err;
+        try {
+          job(t);
+        } catch (...) {
+          err = std::current_exception();
+        }
         lk.lock();
+        if (err && !worker_err_) worker_err_ = err;
         if (++done_ == n_ - 1) done_cv_.notify_one();
       }
     }
@@ -107,6 +122,7 @@ class HostPool {
   std::condition_variable cv_, done_cv_;
   std::vector<std::thread> threads_;
   std::function<void(int)> job_;
+  std::exception_ptr worker_err_;
   int n_ = 0, next_ = 0, done_ = 0;
   uint64_t gen_ = 0;
 };
