@@ -20,6 +20,7 @@ struct lt_ctx {
   std::vector<lt_ctx*> members;
   std::vector<void*> comms;  // ncclComm_t per member (LT_GATHER_NCCL)
   int32_t transport = LT_GATHER_NONE;
+  double rec_per_req = 0.0;  // ITL records per request seen by single-pass percentile runs (pool sizing)
 };
 
 // A prepared batch: everything the kernels need, resident in HBM.
@@ -75,6 +76,10 @@ struct lt_plan {
   DBuf<double> rec_d, rec_d_sorted, ttft_keys, ttft_sorted;
   DBuf<int32_t> rec_c, rec_c_sorted, pct_seg_b, pct_seg_e, pct_rseg_b, pct_rseg_e;
   DBuf<char> pct_tmp;
+  // single-pass recording pool (run_percentiles_single)
+  DBuf<double> pool_d;
+  DBuf<int32_t> pool_c, chunk_next, pool_next;
+  DBuf<int64_t> rec_total;
   // re-run state (lt_plan_run recomputes K0 tables, counts, offsets, merge)
   DBuf<int32_t> pair_scen, pair_adp, adp_count, overflow;
   DBuf<int64_t> pair_begin;

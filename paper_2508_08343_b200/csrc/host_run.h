@@ -221,10 +221,15 @@ EngineParams engine_params(const lt_plan& P) {
 
 void run_percentiles(lt_plan& P, EngineParams E);
 
+bool run_percentiles_single(lt_plan& P);
+
 void run_plan(lt_plan& P) {
   cudaStream_t st = P.st;
   untrim_plan(P);
   prepare_requests(P);
+  // percentiles in one recording engine pass when its record pool holds
+  // them (else the engine pass, then a second one sized by its counts)
+  if (P.want_pct && P.n_scen > 0 && !std::getenv("LT_PCT_TWO_PASS") && run_percentiles_single(P)) return;
   reset_state(P);
   const EngineParams E = engine_params(P);
   cudaEventRecord(P.ev[4], st);
@@ -234,6 +239,105 @@ void run_plan(lt_plan& P) {
   }
   cudaEventRecord(P.ev[5], st);
   if (P.want_pct && P.n_scen > 0) run_percentiles(P, E);
+}
+
+// TTFT/ITL p50/p99 from one engine pass of the recording build: the ITL
+// records go to a chunked pool (sized from the records per request the
+// context has seen, 8 before), are compacted per scenario and sorted. False
+// when the pool ran out (the caller falls back to two passes).
+bool run_percentiles_single(lt_plan& P) {
+  cudaStream_t st = P.st;
+  lt_ctx* ctx = P.ctx;
+  const int64_t n = P.n_scen, nr = std::max<int64_t>(P.total_req, 1);
+  const double per_req = ctx->rec_per_req > 0.0 ? 1.25 * ctx->rec_per_req : 8.0;
+  const double est = per_req * static_cast<double>(P.total_req) + static_cast<double>(n);
+  const int64_t max_chunks = (int64_t(8) << 30) / (12 * kRecChunk);  // an 8 GB pool at most
+  const int64_t chunks = std::min<int64_t>(max_chunks, 2 * n + static_cast<int64_t>(est / kRecChunk) + 1);
+  if (chunks <= n || chunks >= (int64_t(1) << 31)) return false;
+  const int64_t pool = chunks * kRecChunk;
+  P.pool_d.alloc(pool);
+  P.pool_c.alloc(pool);
+  P.chunk_next.alloc(chunks);
+  P.rec_total.alloc(std::max<int64_t>(n, 1));
+  P.pool_next.alloc(2);  // {next chunk, overflow}
+  LT_CUDA(cudaMemsetAsync(P.chunk_next.p, 0xff, chunks * sizeof(int32_t), st));
+  LT_CUDA(cudaMemsetAsync(P.rec_total.p, 0, P.rec_total.n * sizeof(int64_t), st));
+  const int32_t init[2] = {static_cast<int32_t>(n), 0};
+  LT_CUDA(cudaMemcpyAsync(P.pool_next.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  reset_state(P);
+  EngineParams E = engine_params(P);
+  E.rec_chunked = 1;
+  E.rec_pool_chunks = static_cast<int32_t>(chunks);
+  E.rec_pool_next = P.pool_next.p;
+  E.rec_overflow = P.pool_next.p + 1;
+  E.rec_chunk_next = P.chunk_next.p;
+  E.rec_total = P.rec_total.p;
+  E.rec_d = P.pool_d.p;
+  E.rec_c = P.pool_c.p;
+  cudaEventRecord(P.ev[4], st);
+  launch_engine_checked(P, E, st);
+  after_launch("engine_kernel(recording)", st);
+  metrics_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, st>>>(E.scen, E.n_scen, E.r_phase, E.r_first, E.r_arr,
+                                                                     E.r_last, E.r_out, E.r_gen, E.out);
+  after_launch("metrics_kernel", st);
+  cudaEventRecord(P.ev[5], st);
+  int32_t ovf = 0;
+  LT_CUDA(cudaMemcpyAsync(&ovf, P.pool_next.p + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  // the records' segments: exclusive scan of the counts
+  P.rec_off.alloc(std::max<int64_t>(n, 1));
+  size_t sb = 0;
+  LT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, P.rec_total.p, P.rec_off.p, static_cast<int>(n), st));
+  P.pct_tmp.alloc(static_cast<int64_t>(std::max<size_t>(sb, 1)));
+  LT_CUDA(cub::DeviceScan::ExclusiveSum(P.pct_tmp.p, sb, P.rec_total.p, P.rec_off.p, static_cast<int>(n), st));
+  int64_t last_off = 0, last_len = 0;
+  LT_CUDA(cudaMemcpyAsync(&last_off, P.rec_off.p + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaMemcpyAsync(&last_len, P.rec_total.p + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaStreamSynchronize(st));
+  if (ovf) return false;
+  const int64_t tot = last_off + last_len;
+  if (tot >= (int64_t(1) << 31)) throw CudaError{"percentiles: more than 2^31 ITL records in one plan"};
+  ctx->rec_per_req = std::max(ctx->rec_per_req, static_cast<double>(tot) / static_cast<double>(nr));
+  const int64_t nt = std::max<int64_t>(tot, 1);
+  P.rec_d.alloc(nt);
+  P.rec_c.alloc(nt);
+  P.rec_d_sorted.alloc(nt);
+  P.rec_c_sorted.alloc(nt);
+  P.pct_rseg_b.alloc(std::max<int64_t>(n, 1));
+  P.pct_rseg_e.alloc(std::max<int64_t>(n, 1));
+  rec_compact_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, st>>>(
+      static_cast<int>(n), P.chunk_next.p, P.rec_total.p, P.rec_off.p, P.pool_d.p, P.pool_c.p, P.rec_d.p, P.rec_c.p,
+      P.pct_rseg_b.p, P.pct_rseg_e.p);
+  after_launch("rec_compact_kernel", st);
+  std::vector<int32_t> tb(n), te(n);
+  for (int64_t i = 0; i < n; ++i) {
+    tb[i] = static_cast<int32_t>(P.h_scen[i].req_begin);
+    te[i] = static_cast<int32_t>(P.h_scen[i].req_begin + P.h_scen[i].n_req);
+  }
+  P.pct_seg_b.upload(tb, st);
+  P.pct_seg_e.upload(te, st);
+  P.ttft_keys.alloc(nr);
+  P.ttft_sorted.alloc(nr);
+  ttft_keys_kernel<<<static_cast<unsigned>((nr + 255) / 256), 256, 0, st>>>(P.r_arr.p, P.r_first.p, nr,
+                                                                            P.ttft_keys.p);
+  after_launch("ttft_keys_kernel", st);
+  size_t b1 = 0, b2 = 0;
+  LT_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, b1, P.ttft_keys.p, P.ttft_sorted.p, static_cast<int>(nr),
+                                             static_cast<int>(n), P.pct_seg_b.p, P.pct_seg_e.p, st));
+  LT_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, b2, P.rec_d.p, P.rec_d_sorted.p, P.rec_c.p,
+                                              P.rec_c_sorted.p, static_cast<int>(nt), static_cast<int>(n),
+                                              P.pct_rseg_b.p, P.pct_rseg_e.p, st));
+  P.pct_tmp.alloc(static_cast<int64_t>(std::max<size_t>(std::max(b1, b2), 1)));
+  LT_CUDA(cub::DeviceSegmentedSort::SortKeys(P.pct_tmp.p, b1, P.ttft_keys.p, P.ttft_sorted.p, static_cast<int>(nr),
+                                             static_cast<int>(n), P.pct_seg_b.p, P.pct_seg_e.p, st));
+  LT_CUDA(cub::DeviceSegmentedSort::SortPairs(P.pct_tmp.p, b2, P.rec_d.p, P.rec_d_sorted.p, P.rec_c.p,
+                                              P.rec_c_sorted.p, static_cast<int>(nt), static_cast<int>(n),
+                                              P.pct_rseg_b.p, P.pct_rseg_e.p, st));
+  percentile_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, st>>>(
+      P.scen.p, static_cast<int>(n), P.ttft_sorted.p, P.rec_off.p, P.rec_total.p, P.rec_d_sorted.p,
+      P.rec_c_sorted.p, P.out.p);
+  after_launch("percentile_kernel", st);
+  P.launches_run += 5;  // the recording engine, compaction, ttft keys, percentiles (metrics counted by the caller)
+  return true;
 }
 
 // TTFT/ITL p50/p99 (metrics.cpp:47-54): a second, recording engine pass sized

@@ -1329,6 +1329,29 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   double next_arr = __shfl_sync(kFull, pf_t, 0);  // arrival time of request `ingest`
   const int64_t rec_base = P.record ? P.rec_off[s] : 0;
   int64_t rec_n = 0;
+  // single-pass recording (kRep): lane 0 appends to its chunk list
+  int rc_cur = s, rc_pos = 0;
+  int64_t rc_total = 0;
+  bool rc_dead = false;
+  auto rec_put = [&](double d, int c) {
+    if (rc_dead) return;
+    if (rc_pos == kRecChunk) {
+      const int nxt = atomicAdd(P.rec_pool_next, 1);
+      if (nxt >= P.rec_pool_chunks) {
+        rc_dead = true;
+        atomicExch(P.rec_overflow, 1);
+        return;
+      }
+      P.rec_chunk_next[rc_cur] = nxt;
+      rc_cur = nxt;
+      rc_pos = 0;
+    }
+    const int64_t o = static_cast<int64_t>(rc_cur) * kRecChunk + rc_pos;
+    P.rec_d[o] = d;
+    P.rec_c[o] = c;
+    ++rc_pos;
+    ++rc_total;
+  };
   int64_t tr_base = 0;
   if (kRep && P.report) {
     tr_base = P.tr_off[s];
@@ -1477,6 +1500,34 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         P.tr_rwal[tr_base + E.iter] = make_int4(E.R, W, A, nl);
       }
     }
+    if (kRep && P.rec_chunked) {  // the same ITL records, appended by lane 0
+      if (lane == 0) rec_put(emit - E.clock, E.R - E.n_fresh - E.n_readmit);
+      if (E.n_readmit <= 32) {
+        const double dv = lane < E.n_readmit ? emit - P.r_last[E.rb + E.readmit_id] : 0.0;
+        for (int j = 0; j < E.n_readmit; ++j) {
+          const double x = __shfl_sync(kFull, dv, j);
+          if (lane == 0) rec_put(x, 1);
+        }
+      } else {
+        for (int base = r_before; base < E.R_end; base += 32) {
+          const int i = base + lane;
+          bool re = false;
+          double dv = 0.0;
+          if (i < E.R_end) {
+            const int4 e = E.run_get(i);
+            re = e.x >= 0 && !(e.z & kFreshBit);
+            if (re) dv = emit - P.r_last[E.rb + e.x];
+          }
+          unsigned m = __ballot_sync(kFull, re);
+          while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            const double x = __shfl_sync(kFull, dv, j);
+            if (lane == 0) rec_put(x, 1);
+          }
+        }
+      }
+    }
     if (LT_UNLIKELY(P.record)) {  // ITL multiset of compute_metrics (metrics.cpp:92-105)
       const int64_t r0 = rec_base + rec_n;
       if (lane == 0) {
@@ -1588,6 +1639,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
             P.rec_d[rec_base + rec_n + n] = clk - start;
             P.rec_c[rec_base + rec_n + n] = E.R;
           }
+          if (kRep && P.rec_chunked && lane == 0) rec_put(clk - start, E.R);
           if (kRep && P.report) {
             if (lane == 0) {
               P.tr_time[tr_base + E.iter + n] = start;
@@ -1657,6 +1709,10 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   o.device_cycles = clock64() - t_start;
   if (lane == 0) P.out[s] = o;
   if (kRep && P.report && lane == 0) P.sl_cnt[s] = E.sl_n;
+  if (kRep && P.rec_chunked && lane == 0) {
+    P.rec_total[s] = rc_total;
+    P.rec_chunk_next[rc_cur] = -1;
+  }
 }
 
 // Persistent kernel: each warp pulls scenarios (cost-descending order) from a

@@ -187,4 +187,31 @@ __global__ void __launch_bounds__(256) percentile_kernel(const DScen* scen, int 
   }
 }
 
+// Single-pass recording: each scenario's chunk list copied into one
+// contiguous segment at rec_off[s] (the layout the segmented sort and
+// percentile_kernel read), and its segment bounds. One warp per scenario.
+__global__ void __launch_bounds__(256) rec_compact_kernel(int n_scen, const int32_t* chunk_next,
+                                                          const int64_t* rec_total, const int64_t* rec_off,
+                                                          const double* pool_d, const int32_t* pool_c, double* rec_d,
+                                                          int32_t* rec_c, int32_t* seg_b, int32_t* seg_e) {
+  const int s = static_cast<int>((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= n_scen) return;
+  const int64_t total = rec_total[s], base = rec_off[s];
+  if (lane == 0) {
+    seg_b[s] = static_cast<int32_t>(base);
+    seg_e[s] = static_cast<int32_t>(base + total);
+  }
+  int chunk = s;
+  for (int64_t j0 = 0; j0 < total; j0 += kRecChunk) {
+    const int64_t m = total - j0 < kRecChunk ? total - j0 : kRecChunk;
+    const int64_t src = static_cast<int64_t>(chunk) * kRecChunk;
+    for (int64_t i = lane; i < m; i += 32) {
+      rec_d[base + j0 + i] = pool_d[src + i];
+      rec_c[base + j0 + i] = pool_c[src + i];
+    }
+    chunk = chunk_next[chunk];
+  }
+}
+
 }  // namespace lt

@@ -40,6 +40,9 @@ constexpr int kCalBuckets = 512;
 // Preempted-queue slots kept in shared memory (the rest in HBM).
 constexpr int kPqSmem = 64;
 
+// Records per chunk of the single-pass percentile recording pool.
+constexpr int kRecChunk = 512;
+
 struct DScen {
   int64_t req_begin;
   int32_t n_req;
@@ -158,6 +161,17 @@ struct EngineParams {
   const int64_t* sl_off;
   int2* sl_log;
   int32_t* sl_cnt;
+  // single-pass percentile recording (engine_kernel<256,1,true>): the ITL
+  // records go to chunks of kRecChunk in a pool -- scenario s starts in chunk
+  // s, further chunks come from rec_pool_next and are linked by
+  // rec_chunk_next; rec_total[s] counts them; rec_overflow is set (and the
+  // scenario stops recording) when the pool runs out
+  int32_t rec_chunked;
+  int32_t rec_pool_chunks;
+  int32_t* rec_pool_next;
+  int32_t* rec_chunk_next;
+  int64_t* rec_total;
+  int32_t* rec_overflow;
   int32_t report;            // the report pass writes the rows above
   int32_t check_invariants;  // SimOptions.check_invariants: checked engine pass
   int64_t inject_iteration;  // test hook (LT_INVARIANT_INJECT): ledger fault at this iteration, -1 none

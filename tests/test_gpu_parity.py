@@ -553,3 +553,16 @@ def test_sweep_waves_errors_and_early_exit_match_reference(dev, ref, monkeypatch
             else:
                 assert dev.message(i) == ref.message(i), i
     assert set(gp["status"]) == {0}
+
+
+def test_single_pass_percentiles_match_two_pass(dev, monkeypatch):
+    """want_percentiles in one recording engine pass (chunked record pool)
+    gives the two-pass path's TTFT/ITL p50/p99 and everything else."""
+    for b, cfg in (W.summary_cases(), (W.c2_batch(duration_s=120.0, stride=8), lt.h100_like_config(1))):
+        g1, _ = dev.simulate_batch(b, cfg, want_digest=True, want_percentiles=True)
+        monkeypatch.setenv("LT_PCT_TWO_PASS", "1")
+        g2, _ = dev.simulate_batch(b, cfg, want_digest=True, want_percentiles=True)
+        monkeypatch.delenv("LT_PCT_TWO_PASS")
+        for f in g1.dtype.names:
+            if f not in ("device_cycles", "phase_cycles"):
+                np.testing.assert_array_equal(g1[f], g2[f], err_msg=f)
