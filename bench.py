@@ -419,6 +419,10 @@ def issue_roofline(prof, iters_step: int, engine_ms: float, sm_mhz, algo_bytes: 
     return r
 
 
+COLL_DEV = "cpu"  # the device of collective tensors: cuda:LOCAL_RANK under NCCL
+SHARED = bool(os.environ.get("LT_BENCH_SHARED_GPU")) and int(os.environ.get("WORLD_SIZE", "1")) > 1
+
+
 def impl_gpu(args):
     import torch
 
@@ -427,11 +431,21 @@ def impl_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    global COLL_DEV
     dist = None
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("LT_BENCH_SHARED_GPU"):
+            # test mode of the multi-rank path on a one-GPU box: every rank on
+            # cuda:0, collectives over gloo on host tensors (never a bench line)
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+            COLL_DEV = "cpu"
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            COLL_DEV = f"cuda:{local}"
     import paper_2508_08343_b200 as lt
 
     dev = lt.device(local)
@@ -463,10 +477,10 @@ def impl_gpu(args):
     gathered = mine = None
     if world > 1:  # padded per-rank record buffer for the all-gather
         nbytes = sum(p.device_summaries()[1] for p in plans)
-        t = torch.tensor([nbytes], device=f"cuda:{local}", dtype=torch.int64)
+        t = torch.tensor([nbytes], device=COLL_DEV, dtype=torch.int64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         mine = torch.zeros(int(t.item()), dtype=torch.uint8, device=f"cuda:{local}")
-        gathered = [torch.empty_like(mine) for _ in range(world)]
+        gathered = [torch.empty_like(mine, device=COLL_DEV) for _ in range(world)]
 
     def step():
         for p in plans:
@@ -480,7 +494,7 @@ def impl_gpu(args):
                     ptr, nb = p.device_summaries()
                     mine[o:o + nb].copy_(device_view(ptr, nb, local))
                     o += nb
-                dist.all_gather(gathered, mine)
+                dist.all_gather(gathered, mine if COLL_DEV != "cpu" else mine.cpu())
 
     def collect():
         res = [p.results() for p in plans]
@@ -527,10 +541,10 @@ def impl_gpu(args):
     total_ms = sum(times)
     iters_all = iters_rank
     if dist:
-        tt = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+        tt = torch.tensor([total_ms], device=COLL_DEV, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
-        it = torch.tensor([iters_rank], device=f"cuda:{local}", dtype=torch.int64)
+        it = torch.tensor([iters_rank], device=COLL_DEV, dtype=torch.int64)
         dist.all_reduce(it, op=dist.ReduceOp.SUM)
         iters_all = int(it.item())
     value = iters_all * args.steps / (total_ms / 1000.0)
@@ -559,7 +573,8 @@ def impl_gpu(args):
                    "l2": "flushed (256 MiB write) before every timed step",
                    "parallelism": (f"scenario replicas x{world}" if args.workload in ("c1", "c2")
                                    else f"cost-balanced scenario shards over {world} GPU(s)")
-                   + (", NCCL all-gather of the per-scenario records inside the step" if world > 1 else "")},
+                   + (", NCCL all-gather of the per-scenario records inside the step" if world > 1 else "")
+                   + (" [LT_BENCH_SHARED_GPU test mode: ranks share cuda:0, gloo]" if SHARED else "")},
         "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "parity": parity,
         "clocks": clk,
     }
@@ -606,7 +621,7 @@ def e2e_simulate(args, dev, parts, dist, local, iters_all, world):
     wall = statistics.mean(walls)
     val = iters / wall
     if dist:
-        tt = torch.tensor([wall], device=f"cuda:{local}", dtype=torch.float64)
+        tt = torch.tensor([wall], device=COLL_DEV, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         val = iters_all / float(tt.item())
     e2e = {"value": val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -626,7 +641,7 @@ def e2e_simulate(args, dev, parts, dist, local, iters_all, world):
         wp = statistics.mean(pw[1:])
         pv = iters / wp
         if dist:  # whole job: every rank's iterations over the slowest rank's call
-            tt = torch.tensor([wp], device=f"cuda:{local}", dtype=torch.float64)
+            tt = torch.tensor([wp], device=COLL_DEV, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             wp = float(tt.item())
             pv = iters_all / wp
@@ -672,7 +687,7 @@ def impl_gpu_sweeps(args, dev, dist, world, rank, local):
         t0 = time.perf_counter()
         pl, fr = dev.sweep_batch(cb, cfg, grid, dur, seed, opts)
         if dist:
-            D.all_gather_records(pl, np.arange(len(pl)), len(pl), device=torch.device("cuda", local))
+            D.all_gather_records(pl, np.arange(len(pl)), len(pl), device=torch.device(COLL_DEV))
         torch.cuda.synchronize()
         walls.append(time.perf_counter() - t0)
         t = dev.timing()
@@ -681,7 +696,7 @@ def impl_gpu_sweeps(args, dev, dist, world, rank, local):
     clk = clocks.stop()
     wall = sum(walls)
     if dist:
-        tt = torch.tensor([wall], device=f"cuda:{local}", dtype=torch.float64)
+        tt = torch.tensor([wall], device=COLL_DEV, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         wall = float(tt.item())
     value = len(conds) * args.steps / wall
@@ -692,6 +707,7 @@ def impl_gpu_sweeps(args, dev, dist, world, rank, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOADS["c4"], "conditions": len(conds), "points_simulated_per_gpu": pts,
                        "engine_iterations_per_gpu": iters,
+                       **({"test_mode": "LT_BENCH_SHARED_GPU: ranks share cuda:0, gloo"} if SHARED else {}),
                        "timing": "wall time of lt_sweep_batch (the sweep's N-row waves are planned on the host per "
                                  "wave), synchronised; max over ranks"},
             "e2e": {"value": value, "unit": SWEEP_UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
