@@ -6,6 +6,25 @@
 
 namespace {
 
+// Writes back a host range that a worker thread just wrote (CLWB per 64-byte
+// line, then a store fence) so the DMA of the following upload reads memory,
+// not dirty lines in other cores' private caches: measured on the GPU box's
+// VM, 8.6 MB of keys written by 16 threads uploaded at ~7 GB/s without it
+// (0.8-1.4 ms) against ~50 GB/s from memory. The caches keep the lines.
+inline void write_back(const void* p, size_t bytes) {
+#if defined(__x86_64__)
+  if (bytes == 0) return;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(63);
+  const uintptr_t a1 = reinterpret_cast<uintptr_t>(p) + bytes;
+  if (std::getenv("LT_NO_WRITE_BACK")) return;
+  for (uintptr_t a = a0; a < a1; a += 64) asm volatile("clwb (%0)" ::"r"(a) : "memory");
+  asm volatile("sfence" ::: "memory");
+#else
+  (void)p;
+  (void)bytes;
+#endif
+}
+
 // Persistent host workers for the plan-building passes (thread start-up
 // would otherwise cost more than the small batches' work): run(nt, fn)
 // calls fn(t) for t in [0, nt) on up to nt threads, the caller running t = 0.

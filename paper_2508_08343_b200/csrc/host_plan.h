@@ -99,6 +99,7 @@ struct lt_plan {
   int64_t n_pairs = 0;
   int n_keys = 0;
   bool fresh = true;
+  bool run_fresh = false;  // the last run used the tables built with the plan
   int64_t ws_stride = 0;
   int ws_per_scenario = 0;
   int grid = 0;
@@ -734,6 +735,14 @@ bool pack_deferred(lt_plan& P, Prep& pr, const lt_workload_batch& b) {
       }
       pr.cost[df.i] = cost;
     }
+    if (d1 > d0) {  // this thread's contiguous share of the uploaded arrays
+      const int64_t a0 = pr.deferred[d0].a_off, p0 = pr.deferred[d0].p_off;
+      const int64_t na = pr.deferred[d1 - 1].a_off + b.scenarios[pr.deferred[d1 - 1].i].n_adapters - a0;
+      const int64_t np = pr.deferred[d1 - 1].p_off + b.scenarios[pr.deferred[d1 - 1].i].n_adapters - p0;
+      write_back(pr.adapters.data() + a0, na * sizeof(pr.adapters[0]));
+      write_back(pr.pair_scen.data() + p0, np * sizeof(int32_t));
+      write_back(pr.pair_adp.data() + p0, np * sizeof(int32_t));
+    }
   };
   // the load-latency cache is filled serially first (read-only in the workers)
   for (const Prep::Deferred& df : pr.deferred) {
@@ -843,11 +852,13 @@ int64_t size_keys(PinnedVec<DKeyNI>& keys) {
   };
   auto offsets = [&](int t) {
     int64_t off = part[t];
-    for (int64_t i = n * t / nt; i < n * (t + 1) / nt; ++i) {
+    const int64_t i0 = n * t / nt, i1 = n * (t + 1) / nt;
+    for (int64_t i = i0; i < i1; ++i) {
       keys[i].e_off = off;
       keys[i].z_off = off;
       off += keys[i].cap;
     }
+    write_back(keys.data() + i0, (i1 - i0) * sizeof(DKeyNI));  // uploaded next
   };
   HostPool::get().run(nt, caps);
   for (int t = 0; t < nt; ++t) part[t + 1] += part[t];
@@ -1057,20 +1068,35 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
   const auto h_keys = hclk::now();
   int64_t e_total = size_keys(pr.keys);
   const auto h_size = hclk::now();
+  cudaEvent_t dbg_k0 = nullptr;
+  if (std::getenv("LT_HOST_TIMING")) cudaEventCreate(&dbg_k0);
+  // tables_ms: ev[0] just before the first K0 launch, ev[1] after the last
+  // (in a chunk pipeline it includes waiting for the previous chunk's SMs)
   cudaEventRecord(P.ev[0], st);
+  cudaEventRecord(P.ev[1], st);
   if (!pr.keys.empty())
     P.seed_state.alloc(std::min<int64_t>(static_cast<int64_t>(pr.keys.size()), kSeedChunk) * 2 * kMtN);
   P.tab_overflow.alloc(1);
   LT_CUDA(cudaMemsetAsync(P.tab_overflow.p, 0, sizeof(int32_t), st));
   const size_t early_keys = pr.keys.size();
   auto h_up = h_size;
+  cudaEvent_t dbg_a = nullptr, dbg_b = nullptr;
+  if (dbg_k0) {
+    cudaEventCreate(&dbg_a);
+    cudaEventCreate(&dbg_b);
+    cudaEventRecord(dbg_a, st);
+  }
   if (early_keys > 0) {
     P.keys.upload(pr.keys.data(), pr.keys.size(), st);
+    if (dbg_b) cudaEventRecord(dbg_b, st);
     P.E.alloc(std::max<int64_t>(e_total, 1));
     P.Z.alloc(std::max<int64_t>(e_total, 1));
     P.h2d_bytes += pr.keys.size() * sizeof(DKey);
     h_up = hclk::now();
+    if (dbg_k0) cudaEventRecord(dbg_k0, st);
+    cudaEventRecord(P.ev[0], st);
     P.launches_prep += launch_tables(P, static_cast<int>(early_keys), st);
+    cudaEventRecord(P.ev[1], st);
   }
   if (std::getenv("LT_HOST_TIMING"))
     std::fprintf(stderr, "[lt]   K0 launch: size_keys %.2f, allocs+upload %.2f, launches %.2f ms\n", hms(h_size),
@@ -1157,6 +1183,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
       P.Z.alloc(std::max<int64_t>(e_total, 1));
       P.h2d_bytes += pr.keys.size() * sizeof(DKey);
       P.launches_prep += launch_tables(P, static_cast<int>(pr.keys.size()), st);
+      cudaEventRecord(P.ev[1], st);
     }
     relaunch = true;
     int32_t any = 0;
@@ -1175,8 +1202,14 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
       e_total += key.cap;
     }
   }
-  cudaEventRecord(P.ev[1], st);
   const auto h_tables = hclk::now();
+  if (dbg_k0) {
+    std::fprintf(stderr, "[lt]   device: keys upload %.3f ms (%zu B), K0 %.3f ms\n", elapsed(dbg_a, dbg_b),
+                 pr.keys.size() * sizeof(DKey), elapsed(dbg_k0, P.ev[1]));
+    cudaEventDestroy(dbg_a);
+    cudaEventDestroy(dbg_b);
+    cudaEventDestroy(dbg_k0);
+  }
   // count arrivals per (scenario, adapter): sizes the request arrays
   const int64_t n_pairs = static_cast<int64_t>(pr.pair_scen.size());
   P.n_pairs = n_pairs;
