@@ -1173,6 +1173,23 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     size_decks(P, pr.keys, st);
     P.launches_prep += launch_decks(P, st);
   }
+  // The arrival counts are queued right behind K0 and read back with its
+  // overflow flag in one synchronisation; the engine is sized on the host
+  // meanwhile. An overflowing table (never expected: the tables hold the
+  // Poisson bound + 8 sigma) relaunches K0 with larger tables and recounts.
+  const int64_t n_pairs = static_cast<int64_t>(pr.pair_scen.size());
+  P.n_pairs = n_pairs;
+  P.n_keys = static_cast<int>(pr.keys.size());
+  P.scen_count.alloc(std::max<int64_t>(P.n_scen, 1));
+  P.scen_off.alloc(std::max<int64_t>(P.n_scen, 1));
+  P.overflow.alloc(1);
+  if (n_pairs > 0) {
+    P.adp_count.alloc(n_pairs);
+    P.pair_g = pair_group(mean_pair_draws(b));
+  }
+  LT_CUDA(cudaStreamWaitEvent(st, P.ev_up, 0));  // the packed-scenario uploads
+  std::vector<unsigned long long> counts(std::max<int64_t>(P.n_scen, 1));
+  int32_t ovf = 0;
   for (int attempt = 0;; ++attempt) {
     if (relaunch) {
       P.seed_state.alloc(std::min<int64_t>(static_cast<int64_t>(pr.keys.size()), kSeedChunk) * 2 * kMtN);
@@ -1186,8 +1203,22 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
       cudaEventRecord(P.ev[1], st);
     }
     relaunch = true;
+    if (n_pairs > 0) {  // count arrivals per (scenario, adapter): sizes the request arrays
+      LT_CUDA(cudaMemsetAsync(P.scen_count.p, 0, P.n_scen * sizeof(unsigned long long), st));
+      LT_CUDA(cudaMemsetAsync(P.overflow.p, 0, sizeof(int32_t), st));
+      launch_count(P, st);
+      ++P.launches_prep;
+    }
+    // the engine's order, variant and grid need only the cost estimates:
+    // sized while K0 and the counts run (the pageable read-backs below block)
+    if (attempt == 0) size_engine(P, pr.cost, max_run_cap);
     int32_t any = 0;
     LT_CUDA(cudaMemcpyAsync(&any, P.tab_overflow.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    if (n_pairs > 0) {
+      LT_CUDA(cudaMemcpyAsync(counts.data(), P.scen_count.p, P.n_scen * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, st));
+      LT_CUDA(cudaMemcpyAsync(&ovf, P.overflow.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    }
     LT_CUDA(cudaStreamSynchronize(st));
     if (!any) break;
     std::vector<DKey> back(pr.keys.size());
@@ -1210,32 +1241,7 @@ lt_plan* build_plan(lt_ctx* ctx, const lt_workload_batch* b, const lt_server_con
     cudaEventDestroy(dbg_b);
     cudaEventDestroy(dbg_k0);
   }
-  // count arrivals per (scenario, adapter): sizes the request arrays
-  const int64_t n_pairs = static_cast<int64_t>(pr.pair_scen.size());
-  P.n_pairs = n_pairs;
-  P.n_keys = static_cast<int>(pr.keys.size());
-  P.scen_count.alloc(std::max<int64_t>(P.n_scen, 1));
-  P.scen_off.alloc(std::max<int64_t>(P.n_scen, 1));
-  P.overflow.alloc(1);
-  LT_CUDA(cudaStreamWaitEvent(st, P.ev_up, 0));  // the packed-scenario uploads
   if (n_pairs > 0) {
-    P.adp_count.alloc(n_pairs);
-    LT_CUDA(cudaMemsetAsync(P.scen_count.p, 0, P.n_scen * sizeof(unsigned long long), st));
-    LT_CUDA(cudaMemsetAsync(P.overflow.p, 0, sizeof(int32_t), st));
-    P.pair_g = pair_group(mean_pair_draws(b));
-    launch_count(P, st);
-    ++P.launches_prep;
-  }
-  // the engine's order, variant and grid need only the cost estimates: sized
-  // while K0 and the counts run
-  size_engine(P, pr.cost, max_run_cap);
-  if (n_pairs > 0) {
-    std::vector<unsigned long long> counts(P.n_scen);
-    int32_t ovf = 0;
-    LT_CUDA(cudaMemcpyAsync(counts.data(), P.scen_count.p, P.n_scen * sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, st));
-    LT_CUDA(cudaMemcpyAsync(&ovf, P.overflow.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    LT_CUDA(cudaStreamSynchronize(st));
     if (ovf) throw CudaError{"internal: RNG table shorter than an arrival stream"};
     for (int64_t i = 0; i < P.n_scen; ++i)
       if (P.h_scen[i].generated && P.h_scen[i].status == LT_OK) P.h_scen[i].n_req = static_cast<int32_t>(counts[i]);
