@@ -178,6 +178,7 @@ bool sweep_device_eligible(const SweepSetup& S, const Config& cfg) {
 void sweep_waves_device(lt_ctx* ctx, const SweepSetup& S, const lt_server_config* config, const lt_sim_options& so,
                         DBuf<lt_sim_summary>& d_pts, std::unordered_map<int64_t, std::string>& point_msg,
                         SweepTiming& tm) {
+  const auto t_setup = std::chrono::steady_clock::now();
   const lt_condition_batch* batch = S.batch;
   const int64_t n_cond = batch->n_conditions;
   const int n_rows = static_cast<int>(S.rows.size());
@@ -327,6 +328,9 @@ void sweep_waves_device(lt_ctx* ctx, const SweepSetup& S, const lt_server_config
   LT_CUDA(cub::DeviceSelect::Flagged(nullptr, sel_bytes, cub::CountingInputIterator<int32_t>(0), d_alive.p, d_act.p,
                                      d_num.p, static_cast<int>(std::max<int64_t>(n_cond, 1)), st));
   sel_tmp.alloc(std::max<size_t>(sel_bytes, 1));
+  if (std::getenv("LT_HOST_TIMING"))
+    std::fprintf(stderr, "[lt] sweep setup (conditions, rows, K0): %.1f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_setup).count());
   for (int ni = 0; ni < n_rows && !act.empty(); ++ni) {
     const SweepRow& r = S.rows[ni];
     size_t ci = 0;
