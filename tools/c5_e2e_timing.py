@@ -1,7 +1,7 @@
 """Host/device timeline of one C5 end-to-end call (lt_simulate_batch over
 pinned host buffers, chunked and pipelined): run with LT_HOST_TIMING=1.
 
-    LT_HOST_TIMING=1 python tools/c5_e2e_timing.py
+    LT_HOST_TIMING=1 python tools/c5_e2e_timing.py [c3|c5]
 """
 import os
 import sys
@@ -12,7 +12,7 @@ import bench  # noqa: E402
 import paper_2508_08343_b200 as lt  # noqa: E402
 
 dev = lt.device(0)
-parts = bench.sim_parts("c5", 0)
+parts = bench.sim_parts(sys.argv[1] if len(sys.argv) > 1 else "c5", 0)
 pinned = [(bench.pinned_copy(b), cfg) for _, b, cfg in parts]
 for rep in range(2):
     for (pb, _keep), cfg in pinned:
