@@ -8,6 +8,8 @@ import sys
 import time
 
 sys.path.insert(0, os.getcwd())
+import torch  # noqa: E402
+
 import bench  # noqa: E402
 import paper_2508_08343_b200 as lt  # noqa: E402
 
@@ -21,4 +23,5 @@ for rep in range(2):
         t = dev.timing()
         print(f"rep {rep}: wall {1000 * (time.perf_counter() - t0):.1f} ms plan_ms {t['plan_ms']:.1f} "
               f"engine_ms {t['engine_ms']:.1f} tables_ms {t['tables_ms']:.1f} merge_ms {t['merge_ms']:.1f} "
-              f"run_ms {t['run_ms']:.1f} h2d {t['h2d_bytes'] / 1e9:.2f} GB", file=sys.stderr, flush=True)
+              f"run_ms {t['run_ms']:.1f} h2d {t['h2d_bytes'] / 1e9:.2f} GB, device memory in use "
+              f"{(torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]) / 1e9:.1f} GB", file=sys.stderr, flush=True)
