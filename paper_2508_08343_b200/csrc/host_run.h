@@ -145,11 +145,11 @@ int64_t merge_requests(lt_plan& P) {
 
 // The report / checked engine build (engine_kernel<256,1,true>) on the plan's
 // warp layout, at most 8 warps per block.
-void launch_engine_checked(lt_plan& P, const EngineParams& E, cudaStream_t st) {
+void launch_engine_checked(lt_plan& P, const EngineParams& E, cudaStream_t st, int build = kEngineChecked) {
   const int warps = std::min(P.block / 32, 8);
-  LT_CUDA(cudaFuncSetAttribute(engine_kernel_fn(kEngineChecked), cudaFuncAttributeMaxDynamicSharedMemorySize,
+  LT_CUDA(cudaFuncSetAttribute(engine_kernel_fn(build), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                P.ctx->smem_optin));
-  launch_engine_build(kEngineChecked, static_cast<unsigned>(P.grid), static_cast<unsigned>(warps * 32),
+  launch_engine_build(build, static_cast<unsigned>(P.grid), static_cast<unsigned>(warps * 32),
                       static_cast<size_t>(P.smem_per_warp) * warps, st, E);
 }
 
@@ -276,7 +276,8 @@ bool run_percentiles_single(lt_plan& P) {
   E.rec_d = P.pool_d.p;
   E.rec_c = P.pool_c.p;
   cudaEventRecord(P.ev[4], st);
-  launch_engine_checked(P, E, st);
+  // the recording build (no report / check code) unless invariants are checked too
+  launch_engine_checked(P, E, st, E.check_invariants ? kEngineChecked : kEngineRecord);
   after_launch("engine_kernel(recording)", st);
   metrics_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, st>>>(E.scen, E.n_scen, E.r_phase, E.r_first, E.r_arr,
                                                                      E.r_last, E.r_out, E.r_gen, E.out);

@@ -1233,7 +1233,7 @@ struct WarpEngine {
   }
 };
 
-template <bool kRep, bool kQuietUnroll>
+template <bool kRep, bool kRec, bool kQuietUnroll>
 __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_warp) {
   const long long t_start = clock64();
 #ifdef LT_PHASE_PROF
@@ -1329,7 +1329,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   double next_arr = __shfl_sync(kFull, pf_t, 0);  // arrival time of request `ingest`
   const int64_t rec_base = P.record ? P.rec_off[s] : 0;
   int64_t rec_n = 0;
-  // single-pass recording (kRep): lane 0 appends to its chunk list
+  // single-pass recording (kRec): lane 0 appends to its chunk list
   int rc_cur = s, rc_pos = 0;
   int64_t rc_total = 0;
   bool rc_dead = false;
@@ -1351,6 +1351,21 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
     P.rec_c[o] = c;
     ++rc_pos;
     ++rc_total;
+  };
+  // Consecutive records of one value are kept as one record of their summed
+  // weight (the percentiles are a weighted rank select over the multiset, so
+  // this is exact): a quiet stretch's equal emit gaps cost one record. Lane 0.
+  double rl_d = 0.0;
+  int rl_w = 0;
+  auto rec_add = [&](double d, int c) {
+    if (c <= 0) return;  // (weightless records never select a percentile)
+    if (rl_w > 0 && d == rl_d && rl_w <= (1 << 30) - c) {
+      rl_w += c;
+      return;
+    }
+    if (rl_w > 0) rec_put(rl_d, rl_w);
+    rl_d = d;
+    rl_w = c;
   };
   int64_t tr_base = 0;
   if (kRep && P.report) {
@@ -1500,13 +1515,13 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         P.tr_rwal[tr_base + E.iter] = make_int4(E.R, W, A, nl);
       }
     }
-    if (kRep && P.rec_chunked) {  // the same ITL records, appended by lane 0
-      if (lane == 0) rec_put(emit - E.clock, E.R - E.n_fresh - E.n_readmit);
+    if (kRec && P.rec_chunked) {  // the same ITL records, appended by lane 0
+      if (lane == 0) rec_add(emit - E.clock, E.R - E.n_fresh - E.n_readmit);
       if (E.n_readmit <= 32) {
         const double dv = lane < E.n_readmit ? emit - P.r_last[E.rb + E.readmit_id] : 0.0;
         for (int j = 0; j < E.n_readmit; ++j) {
           const double x = __shfl_sync(kFull, dv, j);
-          if (lane == 0) rec_put(x, 1);
+          if (lane == 0) rec_add(x, 1);
         }
       } else {
         for (int base = r_before; base < E.R_end; base += 32) {
@@ -1523,7 +1538,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
             const int j = __ffs(m) - 1;
             m &= m - 1;
             const double x = __shfl_sync(kFull, dv, j);
-            if (lane == 0) rec_put(x, 1);
+            if (lane == 0) rec_add(x, 1);
           }
         }
       }
@@ -1614,7 +1629,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         const double lat_q = sched + model * adapters;  // loads == 0
         double clk = E.clock, start = E.clock;
         int n = 0, win = 0;
-        if (kQuietUnroll && !kRep && !P.record && !P.want_digest && lat_q >= 0.0) {
+        if (kQuietUnroll && !kRep && !kRec && !P.record && !P.want_digest && lat_q >= 0.0) {
           // Four iterations per loop test: the adds are the reference's, one
           // after the other; the clock only grows, so t_next above the clock
           // before the block's last add covers the block's other tests.
@@ -1639,7 +1654,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
             P.rec_d[rec_base + rec_n + n] = clk - start;
             P.rec_c[rec_base + rec_n + n] = E.R;
           }
-          if (kRep && P.rec_chunked && lane == 0) rec_put(clk - start, E.R);
+          if (kRec && P.rec_chunked && lane == 0) rec_add(clk - start, E.R);
           if (kRep && P.report) {
             if (lane == 0) {
               P.tr_time[tr_base + E.iter + n] = start;
@@ -1709,7 +1724,8 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   o.device_cycles = clock64() - t_start;
   if (lane == 0) P.out[s] = o;
   if (kRep && P.report && lane == 0) P.sl_cnt[s] = E.sl_n;
-  if (kRep && P.rec_chunked && lane == 0) {
+  if (kRec && P.rec_chunked && lane == 0) {
+    if (rl_w > 0) rec_put(rl_d, rl_w);
     P.rec_total[s] = rc_total;
     P.rec_chunk_next[rc_cur] = -1;
   }
@@ -1720,7 +1736,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
 // one 8-warp block per SM, the shortest per-engine latency (the batch's
 // longest engines set its time). kMinBlocks = 2: <= 128 registers, 16 warps
 // per SM, for batches with many rounds of engines per warp (throughput).
-template <int kThreads, int kMinBlocks, bool kRep = false>
+template <int kThreads, int kMinBlocks, bool kRep = false, bool kRec = kRep>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(EngineParams P) {
   extern __shared__ __align__(16) char smem[];
   const int warp = threadIdx.x >> 5;
@@ -1737,7 +1753,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(EnginePara
   const int first = rank * gridDim.x + blockIdx.x;
   // (one call site: engine_run is inlined once)
   for (int k = first; k < P.n_scen;) {
-    engine_run<kRep, (kThreads > 256 || kMinBlocks > 1)>(P, P.order[k], slot, mine);
+    engine_run<kRep, kRec, (kThreads > 256 || kMinBlocks > 1)>(P, P.order[k], slot, mine);
     int nk = 0;
     if ((threadIdx.x & 31) == 0) nk = atomicAdd(P.counter, 1) + gridDim.x * warps;
     k = __shfl_sync(kFull, nk, 0);
