@@ -18,6 +18,10 @@ const void* engine_kernel_fn(int build);
 void launch_engine_build(int build, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
                          const EngineParams& E);
 
+// fresh-queue chain links of the linked builds (link_kernel, engine_latency.cu)
+void link_launch(unsigned grid, size_t smem, cudaStream_t st, const DScen* scen, int n_scen, int max_adapters,
+                 const int32_t* r_in, const int32_t* r_adp, int32_t* r_link);
+
 // per-build entry points (one translation unit each)
 const void* engine_fn_latency();
 const void* engine_fn_occ16();

@@ -66,6 +66,7 @@ struct lt_plan {
   DBuf<int4> ws_run;
   DBuf<int4> ws_pq;
   DBuf<int4> ws_node;
+  DBuf<int32_t> r_link;  // chain links per request (link_kernel)
   DBuf<int32_t> ws_ov;
   DBuf<int2> ws_link;
   DBuf<lt_sim_summary> out;
@@ -881,6 +882,7 @@ void alloc_requests(lt_plan& P) {
   P.r_last.alloc(nr);
   P.r_pre.alloc(nr);
   if (P.total_req >= (int64_t(1) << 31)) throw CudaError{"batch too large: more than 2^31 requests in one plan"};
+  if (P.max_req > kMaxScenarioRequests) throw CudaError{"scenario too large: more than 2^30 - 1 requests"};
   if (P.n_pairs > 0) {
     P.pair_excl.alloc(P.n_pairs);
     P.st_in.alloc(nr);

@@ -24,6 +24,7 @@ void for_transient(lt_plan& P, F&& f) {
   f(P.ws_run);
   f(P.ws_pq);
   f(P.ws_node);
+  f(P.r_link);
   f(P.ws_ov);
   f(P.ws_link);
   f(P.pair_excl);
@@ -88,7 +89,7 @@ void prepare_requests(lt_plan& P) {
   launches += merge_requests(P);
   cudaEventRecord(P.ev[3], st);
   P.fresh = false;
-  P.launches_run = launches + 2;  // + engine, metrics (launch_engine)
+  P.launches_run = launches + 2 + (P.engine_variant == kEngineLatency);  // + (links), engine, metrics
 }
 
 // Arrival merge of the counted streams: per-pair times (expand), stable sort
@@ -145,21 +146,41 @@ int64_t merge_requests(lt_plan& P) {
 
 // The report / checked engine build (engine_kernel<256,1,true>) on the plan's
 // warp layout, at most 8 warps per block.
+// The fresh-queue chain links of the plan's requests (link_kernel), before
+// each pass of a linked engine build (latency, report, recording).
+void launch_links(lt_plan& P, cudaStream_t st) {
+  if (P.n_scen <= 0 || P.total_req <= 0) return;
+  P.r_link.alloc(P.total_req);  // (on first use: the throughput builds never read it)
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((P.n_scen + 7) / 8, int64_t(P.ctx->sm_count) * 8));
+  link_launch(grid, 8 * P.max_adapters * sizeof(int32_t), st, P.scen.p, static_cast<int>(P.n_scen), P.max_adapters,
+              P.r_in.p, P.r_adp.p, P.r_link.p);
+  after_launch("link_kernel", st);
+}
+
 void launch_engine_checked(lt_plan& P, const EngineParams& E, cudaStream_t st, int build = kEngineChecked) {
+  launch_links(P, st);
   const int warps = std::min(P.block / 32, 8);
   LT_CUDA(cudaFuncSetAttribute(engine_kernel_fn(build), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                P.ctx->smem_optin));
+  EngineParams EL = E;
+  EL.r_link = P.r_link.p;
   launch_engine_build(build, static_cast<unsigned>(P.grid), static_cast<unsigned>(warps * 32),
-                      static_cast<size_t>(P.smem_per_warp) * warps, st, E);
+                      static_cast<size_t>(P.smem_per_warp) * warps, st, EL);
 }
 
 // K1 (the engine kernel) then K2 (metrics_kernel) over the plan's scenarios.
 void launch_engine(lt_plan& P, const EngineParams& E, cudaStream_t st) {
-  if (E.check_invariants)
+  if (E.check_invariants) {
     launch_engine_checked(P, E, st);
-  else
+  } else {
+    EngineParams EL = E;
+    if (P.engine_variant == kEngineLatency) {  // (the throughput builds append at ingest)
+      launch_links(P, st);
+      EL.r_link = P.r_link.p;
+    }
     launch_engine_build(P.engine_variant, static_cast<unsigned>(P.grid), static_cast<unsigned>(P.block), P.smem, st,
-                        E);
+                        EL);
+  }
   after_launch("engine_kernel", st);
   metrics_kernel<<<static_cast<unsigned>((P.n_scen + 7) / 8), 256, 0, st>>>(
       E.scen, E.n_scen, E.r_phase, E.r_first, E.r_arr, E.r_last, E.r_out, E.r_gen, E.out);
@@ -338,7 +359,7 @@ bool run_percentiles_single(lt_plan& P) {
       P.scen.p, static_cast<int>(n), P.ttft_sorted.p, P.rec_off.p, P.rec_total.p, P.rec_d_sorted.p,
       P.rec_c_sorted.p, P.out.p);
   after_launch("percentile_kernel", st);
-  P.launches_run += 5;  // the recording engine, compaction, ttft keys, percentiles (metrics counted by the caller)
+  P.launches_run += 6;  // links, the recording engine, compaction, ttft keys, percentiles (metrics counted by the caller)
   return true;
 }
 
@@ -406,7 +427,7 @@ void run_percentiles(lt_plan& P, EngineParams E) {
       P.scen.p, static_cast<int>(n), P.ttft_sorted.p, P.rec_off.p, P.rec_len.p, P.rec_d_sorted.p,
       P.rec_c_sorted.p, P.out.p);
   after_launch("percentile_kernel", st);
-  P.launches_run += 5;  // engine + metrics (recording pass), ttft keys, percentiles
+  P.launches_run += 6;  // links + engine + metrics (recording pass), ttft keys, percentiles
 }
 
 // lt_simulate_report's second engine pass (engine_kernel<256, 1, true>),
@@ -524,7 +545,7 @@ void run_report(lt_plan& P, ReportRun& R) {
         R.emit_off.p, R.d_tr_off.p, R.tr_time.p, R.tr_lat.p, R.emit.p);
     after_launch("emit_times_kernel", st);
   }
-  P.launches_run += 7;
+  P.launches_run += 8;  // (with the chain links)
 }
 
 void fetch_results(lt_plan& P, lt_sim_summary* out, lt_request_states* states) {

@@ -441,7 +441,7 @@ void sweep_waves_device(lt_ctx* ctx, const SweepSetup& S, const lt_server_config
       wave_scatter_kernel<<<static_cast<unsigned>((W.n_scen + 255) / 256), 256, 0, st>>>(
           static_cast<int>(W.n_scen), W.out.p, d_pidx.p, d_pts.p);
       after_launch("wave_scatter_kernel", st);
-      tm.launches += 3;
+      tm.launches += 3 + (W.engine_variant == kEngineLatency);  // (links), engine, metrics, scatter
       LT_CUDA(cudaStreamSynchronize(st));
       if (!tables_timed) {
         tm.tables_ms += elapsed(W.ev[0], W.ev[1]);

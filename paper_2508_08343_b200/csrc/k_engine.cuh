@@ -328,7 +328,12 @@ struct WarpEngine {
   int lane = 0;
   double* last_used = nullptr;
   int32_t* run_cnt = nullptr;
-  // fresh queue = per-adapter FIFO chains in request-id order (+ oversized FIFO)
+  // fresh queue = per-adapter FIFO chains in request-id order (+ oversized
+  // FIFO); q_head[a] is adapter a's first request not yet admitted, and the
+  // chain is non-empty (nonempty_w) while that request has arrived (q_head in
+  // [0, ingest)). Linked builds (kLinks) take the links from link_kernel and
+  // may leave a head that has not arrived yet; the others append arrivals at
+  // q_tail (-1: empty), so their heads have always arrived.
   int32_t* q_head = nullptr;
   int32_t* q_tail = nullptr;
   int32_t* act_key = nullptr;  // scan-local: chain head if the adapter can act, else INT_MAX
@@ -373,7 +378,7 @@ struct WarpEngine {
   int4* pqs = nullptr;
   int32_t pq_h = 0, pq_cap = 1;
   bool ids_sorted = true;  // request ids follow arrival order: (arrival, id) order == id order
-  int4* node = nullptr;  // per waiting fresh request: {in, out, next-in-chain, adapter}
+  int4* node = nullptr;  // per arrived fresh request: {in, out, next chained (-1: none), adapter}
   int32_t* ov = nullptr;
 
   __device__ __forceinline__ void fail(int32_t code, int32_t kind, int64_t a, int64_t b) {
@@ -819,16 +824,6 @@ struct WarpEngine {
     return true;
   }
 
-  // admit (kv_scheduler.cpp:170-181).
-  __device__ __forceinline__ void admit(const EngineParams& P) {
-    free_slots = G - resident_count;
-    evicted_w = 0;
-    blocked_w = 0;
-    bool go = true;
-    Wp = scan(P, Wp, &go);
-    if (go) scan_fresh(P);
-  }
-
   __device__ __forceinline__ void local_best(int* bkey, int* ba) const {
     const int2 r = lane_best(act_key, N, lane);
     *bkey = r.x;
@@ -922,6 +917,7 @@ struct WarpEngine {
   // rest of the scan, so only claimed adapters' chains are walked. Oversized
   // entries (can never fit) sit in their own FIFO and are rejected up to the
   // stop point, as the reference rejects them when the scan passes them.
+  template <bool kLinks>
   __device__ __forceinline__ void scan_fresh(const EngineParams& P) {
     LT_STAT(0);
     bool mass = P.priority && free_slots == 0 && !pool_any();
@@ -993,7 +989,9 @@ struct WarpEngine {
         nd.w = a;
       } else {
         const unsigned kmin = __reduce_min_sync(kFull, static_cast<unsigned>(lk));
-        if (kmin == static_cast<unsigned>(INT_MAX)) break;
+        // (direct mode reads the raw heads, -1 sorting after every id; in the
+        // linked builds one not yet arrived sorts after every arrived one)
+        if (kLinks ? kmin >= static_cast<unsigned>(ingest) : kmin == static_cast<unsigned>(INT_MAX)) break;
         const int src = __ffs(__ballot_sync(kFull, static_cast<unsigned>(lk) == kmin)) - 1;
         id = static_cast<int>(kmin);
         a = __shfl_sync(kFull, la, src);
@@ -1049,15 +1047,17 @@ struct WarpEngine {
         run_cnt[a] += 1;
         P.r_phase[rb + id] = kRunning;
         q_head[a] = next;
-        if (next < 0) q_tail[a] = -1;
+        if (!kLinks && next < 0) q_tail[a] = -1;
       }
-      if (next < 0) mask_clear(nonempty_w, a, lane);
+      // the chain empties: no next request, or (linked builds) not arrived yet
+      const bool gone = kLinks ? (next < 0 || next >= ingest) : next < 0;
+      if (gone) mask_clear(nonempty_w, a, lane);
       --Wf;
       ++sum_m;
       // the lane set follows every chain it holds, in both modes
       if (pl_a == a) {
         if (lane_mode) pl_cl = pl_cl || claiming;
-        if (next < 0) {
+        if (gone) {
           pl_a = -1;
           pl_k = INT_MAX;
         } else {
@@ -1065,8 +1065,8 @@ struct WarpEngine {
           pl_nd = node_head(node, next);  // in flight until this lane wins again
         }
       }
-      if (next < 0) mask_clear(built_w, a, lane);
-      if (!lane_mode && !direct && mine) act_key[a] = (next < 0) ? INT_MAX : next;
+      if (gone) mask_clear(built_w, a, lane);
+      if (!lane_mode && !direct && mine) act_key[a] = gone ? INT_MAX : next;
       if (LT_UNLIKELY(claiming)) {
         const bool mass2 = P.priority && free_slots == 0 && !pool_any();
         if (mass2 != mass) {
@@ -1235,6 +1235,14 @@ struct WarpEngine {
 
 template <bool kRep, bool kRec, bool kQuietUnroll>
 __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_warp) {
+  // Linked ingest (link_kernel's links, no per-arrival append) in the latency,
+  // report and recording builds: heavy C2 engines -7 % cycles per iteration.
+  // The throughput builds keep the append (their C3 / C5 engines were 2-3 %
+  // slower with the links at the 168-register cap). Their code is sensitive
+  // to branch layout: `gone` below, written as !(next >= 0), flipped one
+  // branch of the admission path and cost C3 / C5 3.5 % with otherwise
+  // identical SASS.
+  constexpr bool kLinks = !kQuietUnroll;
   const long long t_start = clock64();
 #ifdef LT_PHASE_PROF
   long long ph[6] = {0, 0, 0, 0, 0, 0};
@@ -1297,6 +1305,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   E.pq_cap = static_cast<int32_t>(P.ws_per_scenario ? (sc.n_req > 0 ? sc.n_req : 1) : P.ws_stride);
   E.ids_sorted = sc.ids_sorted != 0;
   E.node = P.ws_node + wsb;
+  const int32_t* r_link = kLinks ? P.r_link + sc.req_begin : nullptr;
   E.ov = P.ws_ov + wsb;
   for (int a = lane; a < E.N; a += 32) {
     E.last_used[a] = 0.0;
@@ -1318,13 +1327,14 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
   __syncwarp();
   const bool capped_by_range = sc.iter_cap > 0x7ff00000LL;
   double pf_t = INFINITY;
-  int pf_a = 0, pf_in = 0, pf_out = 0;
+  int pf_a = 0, pf_in = 0, pf_out = 0, pf_lk = 0;
   if (E.n_req > 0) {
     const int jc = lane < E.n_req ? lane : E.n_req - 1;
     pf_t = lane < E.n_req ? P.r_arr[E.rb + jc] : INFINITY;
     pf_a = P.r_adp[E.rb + jc];
     pf_in = P.r_in[E.rb + jc];
     pf_out = P.r_out[E.rb + jc];
+    if constexpr (kLinks) pf_lk = r_link[jc];
   }
   double next_arr = __shfl_sync(kFull, pf_t, 0);  // arrival time of request `ingest`
   const int64_t rec_base = P.record ? P.rec_off[s] : 0;
@@ -1389,33 +1399,51 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
       const bool ok = (i < E.n_req) & (pf_t <= E.clock);
       const unsigned b = __ballot_sync(kFull, ok);
       const int n = (b == kFull) ? 32 : __ffs(~b) - 1;
-      const int a_l = pf_a, in_l = pf_in, out_l = pf_out;
-      const bool over_l = static_cast<int64_t>(in_l) + 1 > E.cap;
+      const int a_l = pf_a;
+      const bool over_l = static_cast<int64_t>(pf_in) + 1 > E.cap;
       const unsigned live = (n >= 32) ? kFull : ((1u << n) - 1);
       const unsigned overm = __ballot_sync(kFull, over_l) & live;
       if ((overm >> lane) & 1u) E.ov[E.ov_tail + __popc(overm & lanemask_lt())] = i;
       E.ov_tail += __popc(overm);
-      unsigned m = live & ~overm;
-      if ((m >> lane) & 1u) E.node[i] = make_int4(in_l, out_l, -1, a_l);
-      __syncwarp();
-      while (m) {
-        const int src = __ffs(m) - 1;
-        m &= m - 1;
-        const int a = __shfl_sync(kFull, a_l, src);
-        const int id = E.ingest + src;
-        const int t = E.q_tail[a];
-        __syncwarp();  // every lane has read q_tail[a] before lane 0 rewrites it
-        if (lane == 0) {
-          if (t < 0)
-            E.q_head[a] = id;
-          else
-            reinterpret_cast<int*>(&E.node[t])[2] = id;
-          E.q_tail[a] = id;
+      if constexpr (kLinks) {
+        const bool chained = ((live & ~overm) >> lane) & 1u;
+        const int nx = pf_lk & kLinkNone;
+        if (chained) E.node[i] = make_int4(pf_in, pf_out, nx == kLinkNone ? -1 : nx, a_l);
+        // A chain turns non-empty when its head arrives: the adapter's first
+        // chained request, or the one an admission left in q_head before it
+        // had arrived. (Two arrivals of one adapter never both qualify.)
+        const bool first = (pf_lk & kLinkFirst) != 0;
+        const bool head = chained && (first || E.q_head[a_l] == i);
+        unsigned m = __ballot_sync(kFull, head);
+        if (head && first) E.q_head[a_l] = i;
+        while (m) {
+          const int src = __ffs(m) - 1;
+          m &= m - 1;
+          mask_set(E.nonempty_w, __shfl_sync(kFull, a_l, src), lane);
         }
-        // the lane holding this chain's head node in registers sees its link
-        if (E.pl_a == a && E.pl_k == t) E.pl_nd.z = id;
-        mask_set(E.nonempty_w, a, lane);
+      } else {
+        unsigned m = live & ~overm;
+        if ((m >> lane) & 1u) E.node[i] = make_int4(pf_in, pf_out, -1, a_l);
         __syncwarp();
+        while (m) {  // append to the adapter's chain, one arrival at a time
+          const int src = __ffs(m) - 1;
+          m &= m - 1;
+          const int a = __shfl_sync(kFull, a_l, src);
+          const int id = E.ingest + src;
+          const int t = E.q_tail[a];
+          __syncwarp();  // every lane has read q_tail[a] before lane 0 rewrites it
+          if (lane == 0) {
+            if (t < 0)
+              E.q_head[a] = id;
+            else
+              reinterpret_cast<int*>(&E.node[t])[2] = id;
+            E.q_tail[a] = id;
+          }
+          // the lane holding this chain's head node in registers sees its link
+          if (E.pl_a == a && E.pl_k == t) E.pl_nd.z = id;
+          mask_set(E.nonempty_w, a, lane);
+          __syncwarp();
+        }
       }
       E.Wf += n;
       E.ingest += n;
@@ -1426,12 +1454,14 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         const int a2 = __shfl_sync(kFull, pf_a, srcl & 31);
         const int in2 = __shfl_sync(kFull, pf_in, srcl & 31);
         const int out2 = __shfl_sync(kFull, pf_out, srcl & 31);
+        const int lk2 = kLinks ? __shfl_sync(kFull, pf_lk, srcl & 31) : 0;
         const double nxt = __shfl_sync(kFull, t2, 0);  // lane 0's new head when n < 32
         if (srcl < 32) {
           pf_t = t2;
           pf_a = a2;
           pf_in = in2;
           pf_out = out2;
+          pf_lk = lk2;
         } else {
           const int j = E.ingest + lane;
           const int jc = j < E.n_req ? j : E.n_req - 1;
@@ -1439,6 +1469,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
           pf_a = P.r_adp[E.rb + jc];
           pf_in = P.r_in[E.rb + jc];
           pf_out = P.r_out[E.rb + jc];
+          if constexpr (kLinks) pf_lk = r_link[jc];
         }
         // (n == 32: lane 0 refilled from memory, wait for it)
         next_arr = (n < 32) ? nxt : __shfl_sync(kFull, pf_t, 0);
@@ -1468,7 +1499,7 @@ __device__ void engine_run(const EngineParams& P, int s, int slot, char* smem_wa
         E.Wp = E.scan(P, E.Wp, &go);
       }
       LT_PH(3);
-      if (go) E.scan_fresh(P);
+      if (go) E.template scan_fresh<kLinks>(P);
     }
     __syncwarp();
     LT_PH(4);

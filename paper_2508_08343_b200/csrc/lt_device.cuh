@@ -29,6 +29,12 @@ constexpr int kAdapterMask = (1 << 20) - 1;
 // whose start gen >= out), z = dense adapter | kFreshBit (first admission this
 // iteration), w = input + output tokens.
 constexpr int kFreshBit = 1 << 30;
+// Chain link of a request (int32, link_kernel): the low 30 bits are the
+// adapter's next chained request (kLinkNone: none); kLinkFirst marks the
+// adapter's first chained request. Oversized requests are never chained.
+constexpr int kLinkFirst = 1 << 30;
+constexpr int kLinkNone = (1 << 30) - 1;
+constexpr int kMaxScenarioRequests = kLinkNone;  // requests per scenario (link index range)
 
 // Engine shared-memory layout (k_engine.cuh; sized on the host in size_engine).
 // per-warp shared memory per adapter: last_used f64 + run_cnt, q_head, q_tail,
@@ -175,6 +181,10 @@ struct EngineParams {
   int32_t report;            // the report pass writes the rows above
   int32_t check_invariants;  // SimOptions.check_invariants: checked engine pass
   int64_t inject_iteration;  // test hook (LT_INVARIANT_INJECT): ledger fault at this iteration, -1 none
+  // chain links per request (link_kernel), linked builds only. (Last, so the
+  // fields above keep their parameter-bank offsets: the k1..k7 pairs stay
+  // 16-byte aligned for the uniform constant loads of lat_step.)
+  const int32_t* r_link;
 };
 
 }  // namespace lt
