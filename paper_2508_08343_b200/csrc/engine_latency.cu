@@ -33,33 +33,40 @@ __global__ void __launch_bounds__(256) link_kernel(const DScen* scen, int n_scen
     const int64_t rb = scen[s].req_begin, cap = scen[s].capacity;
     for (int a = lane; a < na; a += 32) last[a] = -1;
     __syncwarp();
+    // the next step's loads are issued before this step's links (the steps
+    // are a serial chain through last[], the loads are not)
+    int a_n = 0, in_n = 0;
+    if (lane < n) {
+      a_n = r_adp[rb + lane];
+      in_n = r_in[rb + lane];
+    }
     for (int base = 0; base < n; base += 32) {
       const int i = base + lane;
       const bool v = i < n;
-      int a = 0, in = 0;
-      if (v) {
-        a = r_adp[rb + i];
-        in = r_in[rb + i];
+      const int a = a_n, in = in_n;
+      if (i + 32 < n) {
+        a_n = r_adp[rb + i + 32];
+        in_n = r_in[rb + i + 32];
       }
       const bool over = v && static_cast<int64_t>(in) + 1 > cap;
       const bool chained = v && !over;
       const unsigned mm = __match_any_sync(0xffffffffu, chained ? a : -1 - lane);
       const unsigned later = mm & ~lt & ~(1u << lane);
+      int flags = 0;
       if (chained) {
-        int flags = 0;
         if (!(mm & lt)) {  // first of its adapter in this step: link from the previous tail
-          const int p = last[a];
+          const int p = last[a];  // index | its kLinkFirst flag, or -1
           if (p < 0)
             flags = kLinkFirst;
           else
-            r_link[rb + p] = i | (r_link[rb + p] & kLinkFirst);
+            r_link[rb + (p & kLinkNone)] = i | (p & kLinkFirst);
         }
         r_link[rb + i] = (later ? base + __ffs(later) - 1 : kLinkNone) | flags;
       } else if (v) {
         r_link[rb + i] = kLinkNone;
       }
       __syncwarp();
-      if (chained && !later) last[a] = i;
+      if (chained && !later) last[a] = i | flags;
       __syncwarp();
     }
   }
