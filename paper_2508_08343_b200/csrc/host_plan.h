@@ -919,7 +919,7 @@ void alloc_requests(lt_plan& P) {
 // Engine launch shape of a plan (order, variant, warps, shared memory,
 // persistent grid, workspace) from the per-scenario cost estimates and the
 // plan's request counts (max_req, total_req) and max_adapters.
-void size_engine(lt_plan& P, const std::vector<double>& cost, int max_run_cap) {
+void size_engine(lt_plan& P, const std::vector<double>& cost, int max_run_cap, bool narrow_blocks = true) {
   lt_ctx* ctx = P.ctx;
   cudaStream_t st = P.st;
   // engine order: most expensive first
@@ -956,6 +956,29 @@ void size_engine(lt_plan& P, const std::vector<double>& cost, int max_run_cap) {
     if (const char* env = std::getenv("LT_ENGINE_VARIANT")) {
       const int v = std::atoi(env);
       P.engine_variant = (v == 2 || v == 3) ? v : 1;
+    }
+    // Latency-bound batches whose work per warp slot stays under half the
+    // longest engine with half the warps per block take the smaller blocks:
+    // each warp gets a larger running-set tier in shared memory (1,024 slots
+    // at 4 warps vs 704 at 8 for 256-adapter batches) and the heaviest
+    // engines (warp 0 of each block, one per SM) share their SM with fewer
+    // others. C2 (1,024 scenarios: 0.21 of the longest engine per slot at 8
+    // warps) takes 4: engine 27.2 -> 26.9 ms (same-box A/B). Not for the
+    // sweep waves (narrow_blocks false), which are measured without it.
+    if (narrow_blocks && P.engine_variant == 1 && P.warps_per_block == 8 && P.n_scen > 0 &&
+        !std::getenv("LT_WIDE_BLOCKS")) {
+      double total = 0.0, longest = 0.0;
+      for (int64_t i = 0; i < P.n_scen; ++i) {
+        total += cost[i];
+        longest = std::max(longest, cost[i]);
+      }
+      while (P.warps_per_block > 2 &&
+             total / (static_cast<double>(ctx->sm_count) * (P.warps_per_block / 2)) <= 0.5 * longest)
+        P.warps_per_block /= 2;
+      if (std::getenv("LT_HOST_TIMING"))
+        std::fprintf(stderr, "[lt] size_engine: %lld scenarios, work per slot / longest at 8 warps %.3f -> %d warps per block\n",
+                     static_cast<long long>(P.n_scen), total / (static_cast<double>(ctx->sm_count) * 8.0) / longest,
+                     P.warps_per_block);
     }
     if (P.engine_variant == 3 && P.warps_per_block == 8) P.warps_per_block = 12;
     // per SM, below the 227 KB opt-in limit (variant 2: two blocks per SM)

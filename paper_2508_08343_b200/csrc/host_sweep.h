@@ -430,7 +430,7 @@ void sweep_waves_device(lt_ctx* ctx, const SweepSetup& S, const lt_server_config
       alloc_requests(W);
       tm.launches += merge_requests(W);
       cudaEventRecord(W.ev[3], st);
-      size_engine(W, cost, 1024);
+      size_engine(W, cost, 1024, false);  // (waves keep 8-warp blocks)
       size_workspace(W);
       reset_state(W);
       const EngineParams E = engine_params(W);
