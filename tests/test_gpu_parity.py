@@ -456,6 +456,25 @@ def test_engine_variants_match_reference(dev, ref, monkeypatch, variant):
             np.testing.assert_array_equal(gs[k], rs[k], err_msg=k)
 
 
+@pytest.mark.parametrize("wide", [False, True])
+def test_block_width_matches_reference(dev, ref, monkeypatch, wide):
+    """Latency-bound batches take 4- or 2-warp blocks by default (larger
+    running-set tiers in shared memory); LT_WIDE_BLOCKS keeps 8. The C2 grid
+    subset and a single heavy engine, both widths, against the reference."""
+    if wide:
+        monkeypatch.setenv("LT_WIDE_BLOCKS", "1")
+    full = W.c2_batch(duration_s=600.0)
+    heavy = [i for i in range(len(full.scenarios)) if full.scenarios[i]["n_adapters"] >= 200][:1]
+    one = WorkloadBatch(full.scenarios[heavy].copy(), full.adapters, full.lengths, full.full_lengths, full.requests)
+    cfg = lt.h100_like_config(1)
+    for b in (W.c2_batch(duration_s=600.0, stride=8), one):
+        g, gs = dev.simulate_batch(b, cfg, want_states=True, want_digest=True)
+        r, rs = ref.simulate(b, cfg, sim_options(None, True), want_states=True)
+        assert_summaries(g, r)
+        for k in gs:
+            np.testing.assert_array_equal(gs[k], rs[k], err_msg=k)
+
+
 def test_k0_relaunch_matches_early_launch(dev, monkeypatch):
     """K0 is launched from the first (key) pass of build_plan; the second pass
     relaunches it when a key appeared late. Forcing the relaunch (test hook)
