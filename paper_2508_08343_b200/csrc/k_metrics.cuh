@@ -46,7 +46,12 @@ __global__ void __launch_bounds__(256) metrics_kernel(const DScen* scen, int n_s
   }
   const int64_t rb = sc.req_begin;
   const double window = sc.duration;
-  double rej = 0.0, ttft = 0.0, itl = 0.0;
+  // The three ordered sums (rejected demand, TTFT, ITL), one per lane 0..2:
+  // each block's 32 terms go through shared memory and the lane adds them in
+  // request order (the reference's left-to-right sums, metrics.cpp:84-105).
+  __shared__ double terms[8][3][33];  // (33: the three lanes read different banks)
+  double (*tw)[33] = terms[(threadIdx.x >> 5) & 7];
+  double acc = 0.0;
   long long nrej = 0, nfin = 0, nttft = 0, nitl = 0;
   // the next block's loads are issued before this block's ordered sums (the
   // sums are one dependent add chain; the loads would otherwise wait on it)
@@ -85,16 +90,18 @@ __global__ void __launch_bounds__(256) metrics_kernel(const DScen* scen, int n_s
     long long g1 = has_itl ? gen - 1 : 0;
     for (int o = 16; o > 0; o >>= 1) g1 += __shfl_xor_sync(full, g1, o);
     nitl += g1;
-    const double x0 = is_rej ? static_cast<double>(outv) / window : 0.0;
-    const double x1 = has_first ? first - arr : 0.0;
-    const double x2 = has_itl ? last - first : 0.0;
+    tw[0][lane] = is_rej ? static_cast<double>(outv) / window : 0.0;
+    tw[1][lane] = has_first ? first - arr : 0.0;
+    tw[2][lane] = has_itl ? last - first : 0.0;
+    __syncwarp();
+    if (lane < 3) {
+      const double* t = tw[lane];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      rej = rej + __shfl_sync(full, x0, k);
-      ttft = ttft + __shfl_sync(full, x1, k);
-      itl = itl + __shfl_sync(full, x2, k);
+      for (int k = 0; k < 32; ++k) acc = acc + t[k];
     }
+    __syncwarp();  // read before the next block's terms overwrite them
   }
+  const double rej = __shfl_sync(full, acc, 0), ttft = __shfl_sync(full, acc, 1), itl = __shfl_sync(full, acc, 2);
   if (lane == 0) {
     lt_sim_summary& o = out[s];
     o.rejected_count = nrej;
