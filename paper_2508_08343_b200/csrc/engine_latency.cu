@@ -33,41 +33,56 @@ __global__ void __launch_bounds__(256) link_kernel(const DScen* scen, int n_scen
     const int64_t rb = scen[s].req_begin, cap = scen[s].capacity;
     for (int a = lane; a < na; a += 32) last[a] = -1;
     __syncwarp();
-    // the next step's loads are issued before this step's links (the steps
-    // are a serial chain through last[], the loads are not)
-    int a_n = 0, in_n = 0;
-    if (lane < n) {
-      a_n = r_adp[rb + lane];
-      in_n = r_in[rb + lane];
+    // Four steps (128 requests) at a time, the next four steps' loads issued
+    // before this group's links: the steps are a serial chain through last[],
+    // the loads are not (one step at a time waited on each load: 0.45 ms for
+    // C2's 15 k-request engines; one step ahead: 0.24 ms).
+    constexpr int kAhead = 4;
+    int a_n[kAhead], in_n[kAhead];
+#pragma unroll
+    for (int u = 0; u < kAhead; ++u) {
+      const int j = u * 32 + lane;
+      a_n[u] = j < n ? r_adp[rb + j] : 0;
+      in_n[u] = j < n ? r_in[rb + j] : 0;
     }
-    for (int base = 0; base < n; base += 32) {
-      const int i = base + lane;
-      const bool v = i < n;
-      const int a = a_n, in = in_n;
-      if (i + 32 < n) {
-        a_n = r_adp[rb + i + 32];
-        in_n = r_in[rb + i + 32];
+    for (int base0 = 0; base0 < n; base0 += 32 * kAhead) {
+      int a_c[kAhead], in_c[kAhead];
+#pragma unroll
+      for (int u = 0; u < kAhead; ++u) {
+        a_c[u] = a_n[u];
+        in_c[u] = in_n[u];
+        const int j = base0 + 32 * kAhead + u * 32 + lane;
+        a_n[u] = j < n ? r_adp[rb + j] : 0;
+        in_n[u] = j < n ? r_in[rb + j] : 0;
       }
-      const bool over = v && static_cast<int64_t>(in) + 1 > cap;
-      const bool chained = v && !over;
-      const unsigned mm = __match_any_sync(0xffffffffu, chained ? a : -1 - lane);
-      const unsigned later = mm & ~lt & ~(1u << lane);
-      int flags = 0;
-      if (chained) {
-        if (!(mm & lt)) {  // first of its adapter in this step: link from the previous tail
-          const int p = last[a];  // index | its kLinkFirst flag, or -1
-          if (p < 0)
-            flags = kLinkFirst;
-          else
-            r_link[rb + (p & kLinkNone)] = i | (p & kLinkFirst);
+#pragma unroll
+      for (int u = 0; u < kAhead; ++u) {
+        const int base = base0 + u * 32;
+        if (base >= n) break;
+        const int i = base + lane;
+        const bool v = i < n;
+        const int a = a_c[u], in = in_c[u];
+        const bool over = v && static_cast<int64_t>(in) + 1 > cap;
+        const bool chained = v && !over;
+        const unsigned mm = __match_any_sync(0xffffffffu, chained ? a : -1 - lane);
+        const unsigned later = mm & ~lt & ~(1u << lane);
+        int flags = 0;
+        if (chained) {
+          if (!(mm & lt)) {  // first of its adapter in this step: link from the previous tail
+            const int p = last[a];  // index | its kLinkFirst flag, or -1
+            if (p < 0)
+              flags = kLinkFirst;
+            else
+              r_link[rb + (p & kLinkNone)] = i | (p & kLinkFirst);
+          }
+          r_link[rb + i] = (later ? base + __ffs(later) - 1 : kLinkNone) | flags;
+        } else if (v) {
+          r_link[rb + i] = kLinkNone;
         }
-        r_link[rb + i] = (later ? base + __ffs(later) - 1 : kLinkNone) | flags;
-      } else if (v) {
-        r_link[rb + i] = kLinkNone;
+        __syncwarp();
+        if (chained && !later) last[a] = i | flags;
+        __syncwarp();
       }
-      __syncwarp();
-      if (chained && !later) last[a] = i | flags;
-      __syncwarp();
     }
   }
 }
