@@ -428,7 +428,7 @@ void sweep_waves_device(lt_ctx* ctx, const SweepSetup& S, const lt_server_config
       W.max_adapters = std::max(32, (r.n + 31) / 32 * 32);
       W.warps_per_block = 8;
       alloc_requests(W);
-      tm.launches += merge_requests(W);
+      tm.launches += merge_requests(W, false);  // (sized after the merge)
       cudaEventRecord(W.ev[3], st);
       size_engine(W, cost, 1024, false);  // (waves keep 8-warp blocks)
       size_workspace(W);

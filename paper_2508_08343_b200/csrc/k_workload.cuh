@@ -488,13 +488,17 @@ __global__ void __launch_bounds__(256) expand_kernel(const DScen* scen, const in
 // result ends in (t_b, v_b), the layout gather_kernel reads.
 __global__ void __launch_bounds__(512) merge_kernel(const DScen* scen, const int64_t* pair_begin,
                                                     const unsigned long long* pair_excl, double* t_a,
-                                                    unsigned long long* v_a, double* t_b, unsigned long long* v_b) {
+                                                    unsigned long long* v_a, double* t_b, unsigned long long* v_b,
+                                                    const int32_t* order) {
   __shared__ int32_t off[kMaxAdapters + 1];
-  const DScen sc = scen[blockIdx.x];
+  // (order: the engine's cost-descending scenario order when known, so the
+  // longest merges start in the first wave of blocks instead of the last)
+  const int s = order ? order[blockIdx.x] : static_cast<int>(blockIdx.x);
+  const DScen sc = scen[s];
   if (!sc.generated || sc.status != LT_OK || sc.n_req == 0) return;
   const int n = sc.n_req, np = sc.n_adapters;
   const int64_t rb = sc.req_begin;
-  const int64_t p0 = pair_begin[blockIdx.x];
+  const int64_t p0 = pair_begin[s];
   const unsigned long long e0 = pair_excl[p0];
   for (int k = threadIdx.x; k < np; k += blockDim.x) off[k] = static_cast<int32_t>(pair_excl[p0 + k] - e0);
   if (threadIdx.x == 0) off[np] = n;
