@@ -633,19 +633,21 @@ def e2e_simulate(args, dev, parts, dist, local, iters_all, world):
         # which the CPU reference pays; the same call with them, like for like:
         (pb, _keep), cfg = pinned[0]
         pw = []
-        for i in range(1 + max(1, args.e2e_steps)):
+        pct_warm = max(1, n_warm)  # (the first two calls size the record pool and its sort buffers)
+        for i in range(pct_warm + max(1, args.e2e_steps)):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             dev.simulate_batch(pb, cfg, want_percentiles=True)
             pw.append(time.perf_counter() - t0)
-        wp = statistics.mean(pw[1:])
+        wp = statistics.mean(pw[pct_warm:])
         pv = iters / wp
         if dist:  # whole job: every rank's iterations over the slowest rank's call
             tt = torch.tensor([wp], device=COLL_DEV, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             wp = float(tt.item())
             pv = iters_all / wp
-        e2e["with_percentiles"] = {"value": pv, "unit": UNIT, "ms_per_step": 1000 * wp,
+        e2e["with_percentiles"] = {"value": pv, "unit": UNIT, "ms_per_step": 1000 * wp, "warmup_calls": pct_warm,
+                                   "timed_calls": len(pw) - pct_warm,
                                    "note": "lt_simulate_batch(want_percentiles=1): the full compute_metrics incl. "
                                            "TTFT/ITL p50/p99, as the CPU reference computes; mean of warmed calls"}
     return e2e
